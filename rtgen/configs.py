@@ -1,0 +1,121 @@
+"""Concrete workloads of BASELINE.json's five configs, built
+from rtgen only.  Harness code: no method arithmetic (no features, no keys).
+
+Every function returns plain numpy arrays plus profile dicts taken from
+data/profiles.json (written by scripts/calibrate.py).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+from . import ROOT_SEED, CONFIG1_PROMPTS, arrivals, pack_texts, text, true_len
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LEX_V1 = os.path.join(ROOT, "data", "lexicon_v1.txt")
+LEX_MIN = os.path.join(ROOT, "data", "lexicon_min.txt")
+
+#: per-config base of global request ids (requests of different configs never collide)
+GID_BASE = {1: 0, 2: 0, 3: 1 << 32, 4: 2 << 32, 5: 3 << 32}
+TRACE_STRIDE = 1024  # gid = base + trace * TRACE_STRIDE + i
+
+
+def load_profiles() -> dict:
+    with open(os.path.join(ROOT, "data", "profiles.json")) as f:
+        return json.load(f)
+
+
+def paper_lms() -> list[dict]:
+    """The four LMs of the paper's v1 evaluation (DialoGPT, BlenderBot, BART, T5)."""
+    return [p for p in load_profiles()["lms"] if p["paper"]]
+
+
+def regressor(p: dict) -> np.ndarray:
+    return np.asarray([float.fromhex(h) for h in p["regressor_hex"]], dtype=np.float32)
+
+
+def read_lexicon(path: str = LEX_V1) -> bytes:
+    with open(path, "rb") as f:
+        return f.read()
+
+
+# ---------------------------------------------------------------- config 1
+#: W1 worked fixture: base weights with s = 1, u_max = 40.
+W1_REGRESSOR = np.asarray([6, 2, 1.5, 4, 3, 5, 5, 0.5], dtype=np.float32)
+#: config-1 ground-truth output lengths (tokens), fixed by this harness
+CONFIG1_TRUE_LEN = np.asarray([20, 14, 25, 30, 45, 60, 28, 22], dtype=np.uint16)
+
+
+def config1_profile() -> dict:
+    p = dict(paper_lms()[0])  # DialoGPT
+    p.update(u_max=40.0, cores=4)
+    return p
+
+
+def config1():
+    data, off = pack_texts(CONFIG1_PROMPTS)
+    n = len(CONFIG1_PROMPTS)
+    return {"data": data, "offsets": off, "arrival_us": np.zeros(n, np.int64),
+            "true_len": CONFIG1_TRUE_LEN.copy(), "trace_off": np.asarray([0, n], np.uint32),
+            "profile": config1_profile(), "regressor": W1_REGRESSOR.copy(), "lexicon": read_lexicon(LEX_MIN)}
+
+
+# ---------------------------------------------------------------- config 2
+def config2(n: int = 1 << 20, gid0: int = 0, lm: int = 0):
+    """One queue of n requests, all released at 0, one LM (DialoGPT), tight."""
+    seed = ROOT_SEED + 2
+    data, off, lat = text(seed, GID_BASE[2] + gid0, n, latent=True)
+    p = paper_lms()[lm]
+    tl = true_len(seed, GID_BASE[2] + gid0, lat, p["scale"], lm)
+    return {"data": data, "offsets": off, "arrival_us": np.zeros(n, np.int64), "true_len": tl,
+            "seg_off": np.asarray([0, n], np.uint32), "profile": dict(p), "regressor": regressor(p),
+            "lexicon": read_lexicon()}
+
+
+# ---------------------------------------------------------------- traces
+def traces(cfg: int, trace_ids, per_trace: int, lm_of, beta0=10.0, step=1.0, beta_max=150.0, tightness=1):
+    """Independent Poisson-ramp traces.  lm_of(trace_id) -> LM index.
+    Returns arrays concatenated trace by trace (arrival order within a trace)."""
+    seed = ROOT_SEED + cfg
+    lms = paper_lms()
+    datas, offs, r_all, tl_all, lm_idx = [], [], [], [], []
+    total = 0
+    for t in trace_ids:
+        g0 = GID_BASE[cfg] + int(t) * TRACE_STRIDE
+        d, o, lat = text(seed, g0, per_trace, latent=True)
+        f = lm_of(int(t))
+        datas.append(d)
+        offs.append(o[:-1].astype(np.uint64) + total)
+        total += int(o[-1])
+        r_all.append(arrivals(seed, int(t), per_trace, beta0, step, beta_max))
+        tl_all.append(true_len(seed, g0, lat, lms[f]["scale"], f))
+        lm_idx.append(f)
+    off = np.concatenate(offs + [np.asarray([total], np.uint64)])
+    if total >= 2**32:
+        raise OverflowError("trace shard text >= 4 GiB")
+    nt = len(lm_idx)
+    profiles = []
+    for p in lms:
+        q = dict(p)
+        q["tightness"] = tightness
+        profiles.append(q)
+    return {"data": np.concatenate(datas) if datas else np.zeros(0, np.uint8), "offsets": off.astype(np.uint32),
+            "arrival_us": np.concatenate(r_all), "true_len": np.concatenate(tl_all),
+            "trace_off": (np.arange(nt + 1, dtype=np.uint64) * per_trace).astype(np.uint32),
+            "trace_prof": np.asarray(lm_idx, np.uint16), "profiles": profiles,
+            "regressors": [regressor(p) for p in lms], "lexicon": read_lexicon()}
+
+
+def config3(n_traces: int = 4096, per_trace: int = 1000, first: int = 0):
+    """4096 traces x 1000 requests; 1024 consecutive traces per LM."""
+    per_lm = max(1, 4096 // 4)
+    return traces(3, range(first, first + n_traces), per_trace, lambda t: (t // per_lm) % 4)
+
+
+def config4_shard(rank: int, world: int, n_traces: int = 65536, per_trace: int = 1024):
+    """2^26 requests = 65536 traces x 1024, contiguous trace ranges per rank."""
+    lo = rank * n_traces // world
+    hi = (rank + 1) * n_traces // world
+    return traces(4, range(lo, hi), per_trace, lambda t: t % 4)
