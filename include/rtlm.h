@@ -1,0 +1,192 @@
+/*
+ * rtlm.h — C ABI of the B200-native RT-LM hot path (arXiv 2309.06619).
+ *
+ * Every compute step runs in CUDA kernels for sm_100a inside librtlm.so; the
+ * host side only validates arguments and launches.  There is no CPU fallback.
+ *
+ * Conventions (all calls):
+ *  - d_* pointers are CALLER-OWNED device memory on the context's device; the
+ *    caller keeps them alive until `stream` has executed the call.  h_* are
+ *    host pointers read synchronously during the call.  Structs passed by
+ *    pointer are copied by value at call time.
+ *  - Every call is asynchronous on `stream` (NULL = legacy default stream)
+ *    unless stated otherwise.  Argument checks are synchronous and launch
+ *    nothing on error.
+ *  - Return codes: RT_OK; RT_EINVAL (bad argument, message via rt_last_error);
+ *    RT_ELEXICON (lexicon parse error); RT_ENOMEM (workspace allocation);
+ *    RT_ECUDA (CUDA launch/runtime error, message carries the CUDA string);
+ *    RT_EOVERFLOW (a size exceeds a 32-bit index).
+ *  - Data conditions that are NOT errors: non-ASCII bytes are dropped and
+ *    counted in feat[7]; counts saturate at 65535 (sticky flag
+ *    RT_FLAG_SATURATED, read with rt_get_flags).
+ *  - One context per device, used by one host thread at a time.  Kernels are
+ *    pure functions of their inputs: same inputs -> same bits.
+ *
+ * Citations: P:a-b = PAPER.md lines (v1 P:1-912, v2 P:913-1887); S:a-b =
+ * SPEC.md lines; R-* = readings in DESIGN.md §2.
+ */
+#ifndef RTLM_H
+#define RTLM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTLM_ABI_VERSION 1
+
+typedef struct rt_ctx rt_ctx;
+typedef struct CUstream_st* rt_stream; /* == cudaStream_t */
+
+typedef enum {
+  RT_OK = 0,
+  RT_EINVAL = 1,
+  RT_ELEXICON = 2,
+  RT_ENOMEM = 3,
+  RT_ECUDA = 4,
+  RT_EOVERFLOW = 5
+} rt_status;
+
+/* Sticky context flags (rt_get_flags). */
+#define RT_FLAG_SATURATED 0x1u   /* some feature count saturated at 65535 */
+#define RT_FLAG_BAD_OFFSETS 0x2u /* offsets were not non-decreasing; affected requests scored as empty */
+
+/* Policies (A12-A14): priority key of Eq. 3 (UP/EUDF), Eq. 2
+ * (slack) and the baselines FIFO / EDF=HPF / LUF / MUF
+ * (S:301). */
+enum { RT_FIFO = 0, RT_EDF = 1, RT_LUF = 2, RT_MUF = 3, RT_SLACK = 4, RT_UP = 5 };
+
+/* Weighted-rule regression m_theta (Eq. 1):
+ * u = max(0, fma(w6,f6, ... fma(w0,f0, c))) over f = {S,Y,M,V,O,P,ntok}
+ * in binary32, index order (R-FP). */
+typedef struct {
+  float c;
+  float w[7];
+} rt_regressor;
+
+/* One LM profile (paper constants P:619-625). */
+typedef struct {
+  int64_t eta_us;   /* eta_f: latency per output token, µs */
+  int64_t mu_us;    /* mu_f / phi_f: deadline per input token, µs */
+  int64_t base_us;  /* GPU base latency per batch (R-LAT) */
+  int64_t setup_us; /* GPU batch setup (R-LAT) */
+  int64_t xi_us;    /* wait interval xi (R-XI) */
+  float lambda;     /* max uncertainty ratio inside a batch, >= 1 */
+  float alpha;      /* uncertainty weight of Eq. 3 */
+  float tau;        /* offload threshold: CPU iff u > tau (Alg. 1; Eq. 4) */
+  float u_max;      /* normaliser of alpha*u (R-NUM), > 0 */
+  int32_t C;        /* batch size C_f, 1..255 */
+  int32_t b10;      /* b in tenths (R-B): window m = b10*C/10, 10..; m <= 128 */
+  int32_t tightness;/* 1 tight, 2 loose */
+  int32_t gamma;    /* CPU slowdown (R-LAT) */
+  int32_t cores;    /* CPU cores, 0..32 (>= 1 when offload is on) */
+  int32_t policy;   /* RT_FIFO .. RT_UP */
+  int32_t consolidate; /* 1: dynamic consolidation (§IV-C); 0: fixed batch size C */
+  int32_t offload;  /* 1: strategic offloading (§IV-D) */
+  int32_t raw_numerator; /* 1: alpha*u uses raw u (R-NUM) */
+  int32_t reserved; /* must be 0 */
+} rt_profile;
+
+typedef struct {
+  int64_t sum_resp_us; /* sum over tasks of end - arrival */
+  uint32_t n;          /* tasks in the trace */
+  uint32_t misses;     /* tasks with end > arrival + D */
+} rt_trace_stats;
+
+/* ---------------------------------------------------------------- context */
+
+/* Creates a context on `device` and uploads the lexicon (SPEC S:147 format,
+ * R-LEX: sections vague/polysemy/pos/wh/coord/prep; entries are single word
+ * tokens lemmatized at load; <= 1024 distinct lemmas of <= 16 bytes).
+ * Returns RT_ELEXICON on a parse error (message via rt_last_error(*out) --
+ * *out is still created so the message can be read; destroy it). */
+rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** out);
+rt_status rt_destroy(rt_ctx* ctx);
+/* Message of the last non-OK status on this context (never NULL). */
+const char* rt_last_error(const rt_ctx* ctx);
+/* Reads and clears the sticky flags (synchronises the device). */
+rt_status rt_get_flags(rt_ctx* ctx, uint32_t* flags);
+int rt_abi_version(void);
+/* Number of distinct lexicon lemmas. */
+uint32_t rt_lexicon_size(const rt_ctx* ctx);
+
+/* ---------------------------------------------------------------- (1) score */
+
+/* RuleGen(J) (Eq. 1; Table 1; Listing 1; R-TOK,
+ * R-CLITIC, R-LEMMA, R-RULES).  Request i is bytes d_bytes[d_offsets[i] ..
+ * d_offsets[i+1]).  d_offsets: n+1 non-decreasing u32.  Output feat[i][0..7] =
+ * {S, Y, M, V, O, P, ntok, ndropped} (u16, saturating; row = 16 bytes).
+ * n == 0 is a no-op. */
+rt_status rt_score(rt_ctx* ctx, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n, uint16_t* d_feat,
+                   rt_stream stream);
+
+/* ---------------------------------------------------------------- (2) predict */
+
+/* u[i] = m_theta(feat[i]) (R-REG, R-FP).  d_feat as produced by rt_score. */
+rt_status rt_predict(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, const rt_regressor* reg, float* d_u,
+                     rt_stream stream);
+
+/* ---------------------------------------------------------------- (3) key */
+
+/* Deadline + priority key + class (R-D, R-NUM, R-OVERDUE, R-KEY; Eq. 2/3):
+ *   D_us = d_D_in ? d_D_in[i] : min(tightness*mu_us*ntok_i, 2^32-1), ntok from d_feat[i][6];
+ *   key  = cls<<63 | tier<<62 | ord(v),  cls = offload && u > tau.
+ * d_arrival_us (int64 µs, may be NULL = 0) is used by FIFO/EDF only.
+ * d_feat may be NULL iff d_D_in is given.  d_D_out may be NULL. */
+rt_status rt_key(rt_ctx* ctx, const float* d_u, const uint16_t* d_feat, const int64_t* d_arrival_us,
+                 const uint32_t* d_D_in, uint32_t n, const rt_profile* prof, uint64_t* d_key, uint32_t* d_D_out,
+                 rt_stream stream);
+
+/* Fused hot path (1)+(2)+(3) in one pass over the text: writes u and key,
+ * D_us iff d_D_out != NULL, feat iff d_feat != NULL. */
+rt_status rt_score_key(rt_ctx* ctx, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n,
+                       const rt_regressor* reg, const rt_profile* prof, const int64_t* d_arrival_us,
+                       const uint32_t* d_D_in, uint16_t* d_feat, float* d_u, uint64_t* d_key, uint32_t* d_D_out,
+                       rt_stream stream);
+
+/* ---------------------------------------------------------------- (4) schedule */
+
+/* One-pass schedule (Alg. 1 online part P:467-481; §IV-C; flush
+ * P:490-492; R-CONS, R-CARRY, R-FLUSH, R-CORE) of nq queues; queue q is
+ * elements [h_seg_off[q], h_seg_off[q+1]) (HOST array, nq+1 entries).
+ * Inputs: d_key (priority keys, e.g. from rt_score_key) and d_u.
+ * `cores` overrides prof->cores for the CPU class.
+ * Outputs (device, n = h_seg_off[nq]):
+ *   d_perm[n]      priority order per queue (global indices), stable descending key;
+ *   d_batch_of[n]  global GPU batch id (queues' batches are numbered
+ *                  consecutively in queue order), UINT32_MAX for CPU tasks;
+ *   d_slot_of[n]   position inside the batch (ascending u), 0 for CPU tasks;
+ *   d_core_of[n]   CPU core for CPU tasks, 0xFF for GPU tasks;
+ *   d_seg_batch_off[nq+1] first batch id of each queue (last = total). */
+rt_status rt_schedule(rt_ctx* ctx, const uint64_t* d_key, const float* d_u, const uint32_t* h_seg_off, uint32_t nq,
+                      const rt_profile* prof, uint32_t cores, uint32_t* d_perm, uint32_t* d_batch_of,
+                      uint8_t* d_slot_of, uint8_t* d_core_of, uint32_t* d_seg_batch_off, rt_stream stream);
+
+/* ---------------------------------------------------------------- (5) simulate */
+
+/* Discrete-event replay of nt traces (§V-A; R-REPLAY, R-LAT,
+ * R-XI).  Trace t = tasks [h_trace_off[t], h_trace_off[t+1]) (HOST array),
+ * at most 1024 tasks, in arrival order (d_arrival_us non-decreasing within
+ * the trace).  Per task: arrival (int64 µs), true output length, u, key, D_us.
+ * h_profiles[np] (host), d_trace_prof[nt] (u16 profile index; NULL = 0).
+ * Output d_stats[nt]; d_end_us[n] (nullable) receives each task's end time. */
+rt_status rt_simulate(rt_ctx* ctx, const int64_t* d_arrival_us, const uint16_t* d_true_len, const float* d_u,
+                      const uint64_t* d_key, const uint32_t* d_D_us, const uint32_t* h_trace_off, uint32_t nt,
+                      const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
+                      rt_trace_stats* d_stats, int64_t* d_end_us, rt_stream stream);
+
+/* ---------------------------------------------------------------- (6) aggregate */
+
+/* Integer sums per group (O8): d_sums[g*3 + {0,1,2}] += {sum_resp_us, n,
+ * misses} over traces with d_group_of[t] == g (NULL = group 0).  d_sums is
+ * ACCUMULATED into (zero it first); exact and order-independent, so the
+ * per-rank results can be all-reduced with SUM. */
+rt_status rt_reduce_stats(rt_ctx* ctx, const rt_trace_stats* d_stats, uint32_t nt, const uint16_t* d_group_of,
+                          uint32_t ngroups, int64_t* d_sums, rt_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTLM_H */

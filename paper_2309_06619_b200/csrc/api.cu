@@ -1,0 +1,549 @@
+// api.cu — the C ABI of include/rtlm.h: context, lexicon upload, argument
+// validation, workspace, launches.  No compute happens on the host.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+struct rt_ctx {
+  int device = 0;
+  int num_sms = 148;
+  rtlm::LexEntry* d_entries = nullptr;
+  uint16_t* d_slots = nullptr;
+  uint32_t n_entries = 0, bits = 0;
+  uint32_t* d_flags = nullptr;
+  void* ws = nullptr;
+  size_t ws_size = 0;
+  uint32_t* d_off = nullptr;  // device copy of segment / trace offsets
+  size_t off_cap = 0;
+  rt_profile* d_prof = nullptr;
+  size_t prof_cap = 0;
+  std::string err;
+};
+
+namespace {
+
+using rtlm::LexEntry;
+
+rt_status fail(rt_ctx* c, rt_status st, const std::string& msg) {
+  if (c) c->err = msg;
+  return st;
+}
+rt_status cuda_fail(rt_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, RT_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define RT_CUDA(ctx, call)                                  \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------ lexicon (host)
+bool is_w(unsigned char b) {
+  return (b >= 'a' && b <= 'z') || (b >= 'A' && b <= 'Z') || (b >= '0' && b <= '9') || b == '\'';
+}
+
+// R-LEMMA on a lowercased word (host side of the product; the device has its
+// own register-level implementation in k_score.cu).
+std::string lemma_host(const std::string& lw) {
+  const size_t n = lw.size();
+  if (lw == "n't") return "not";
+  auto tail = [&](const char* s) {
+    size_t k = std::strlen(s);
+    return n >= k && std::memcmp(lw.data() + n - k, s, k) == 0;
+  };
+  size_t strip = 0;
+  if (n >= 5 && tail("ing")) strip = 3;
+  else if (n >= 4 && tail("ed")) strip = 2;
+  else if (n >= 4 && tail("es")) strip = 2;
+  else if (n >= 3 && tail("s") && !tail("ss")) strip = 1;
+  return lw.substr(0, n - strip);
+}
+
+// true when R-CLITIC would split this W run (so it is not a single token)
+bool clitic_splits(const std::string& lw) {
+  const size_t n = lw.size();
+  auto tail = [&](const char* s) {
+    size_t k = std::strlen(s);
+    return n >= k && std::memcmp(lw.data() + n - k, s, k) == 0;
+  };
+  if (n > 3 && tail("n't")) return true;
+  if (n > 2 && (tail("'s") || tail("'m") || tail("'d"))) return true;
+  if (n > 3 && (tail("'re") || tail("'ve") || tail("'ll"))) return true;
+  return false;
+}
+
+struct HostLemma {
+  uint32_t flags = 0;
+  uint32_t tags = 0;
+  uint32_t senses = 0;
+  uint32_t id = 0;
+};
+
+const char* kTags[] = {"NOUN", "PROPN", "VERB", "ADJ", "ADV", "ADP", "PRON", "DET", "CCONJ",
+                       "SCONJ", "NUM", "PART", "INTJ", "AUX", "X", "SYM", "PUNCT"};
+
+std::string strip_ws(const std::string& s) {
+  size_t a = 0, b = s.size();
+  while (a < b && (s[a] == ' ' || s[a] == '\t' || s[a] == '\r')) ++a;
+  while (b > a && (s[b - 1] == ' ' || s[b - 1] == '\t' || s[b - 1] == '\r')) --b;
+  return s.substr(a, b - a);
+}
+
+bool parse_lexicon(const char* text, size_t len, std::vector<std::string>& lemmas, std::vector<HostLemma>& attrs,
+                   std::string& err) {
+  enum Sec { NONE, VAGUE, POLY, POS, WH, COORD, PREP } sec = NONE;
+  size_t pos = 0;
+  int line_no = 0;
+  while (pos <= len) {
+    size_t eol = pos;
+    while (eol < len && text[eol] != '\n') ++eol;
+    std::string line(text + pos, eol - pos);
+    pos = eol + 1;
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    const std::string t = strip_ws(line);
+    auto bad = [&](const std::string& m) {
+      err = "lexicon line " + std::to_string(line_no) + ": " + m;
+      return false;
+    };
+    if (t.empty() || t[0] == '#') {
+      if (eol >= len) break;
+      continue;
+    }
+    if (t.back() == ':' && t.find('\t') == std::string::npos) {
+      const std::string name = t.substr(0, t.size() - 1);
+      if (name == "vague") sec = VAGUE;
+      else if (name == "polysemy") sec = POLY;
+      else if (name == "pos") sec = POS;
+      else if (name == "wh") sec = WH;
+      else if (name == "coord") sec = COORD;
+      else if (name == "prep") sec = PREP;
+      else return bad("unknown section '" + name + "'");
+      if (eol >= len) break;
+      continue;
+    }
+    if (sec == NONE) return bad("entry before any section header");
+    const size_t tab = line.find('\t');
+    const std::string word = strip_ws(tab == std::string::npos ? line : line.substr(0, tab));
+    const std::string value = tab == std::string::npos ? std::string() : strip_ws(line.substr(tab + 1));
+    std::string lw;
+    for (unsigned char ch : word) {
+      if (!is_w(ch)) return bad("entry '" + word + "' is not a single word token");
+      lw.push_back((char)(ch | 0x20));
+    }
+    if (lw.empty() || clitic_splits(lw)) return bad("entry '" + word + "' is not a single word token");
+    const std::string lem = lemma_host(lw);
+    if (lem.empty() || lem.size() > 16) return bad("lemma of '" + word + "' longer than 16 bytes");
+    size_t k = 0;
+    while (k < lemmas.size() && lemmas[k] != lem) ++k;
+    if (k == lemmas.size()) {
+      if (lemmas.size() >= rtlm::kMaxLexEntries) return bad("more than 1024 distinct lemmas");
+      lemmas.push_back(lem);
+      HostLemma h;
+      h.id = (uint32_t)k;
+      attrs.push_back(h);
+    }
+    HostLemma& h = attrs[k];
+    switch (sec) {
+      case VAGUE:
+      case COORD:
+      case PREP:
+        if (!value.empty()) return bad("unexpected value");
+        h.flags |= sec == VAGUE ? rtlm::A_VAGUE : sec == COORD ? rtlm::A_COORD : rtlm::A_PREP;
+        break;
+      case POLY: {
+        char* end = nullptr;
+        long v = std::strtol(value.c_str(), &end, 10);
+        if (value.empty() || *end || v < 2 || v > 255) return bad("polysemy count must be an integer in [2,255]");
+        if ((uint32_t)v > h.senses) h.senses = (uint32_t)v;
+        break;
+      }
+      case POS: {
+        if (value.empty()) return bad("pos entry without tags");
+        size_t a = 0;
+        while (a <= value.size()) {
+          size_t b = value.find(',', a);
+          if (b == std::string::npos) b = value.size();
+          const std::string tag = strip_ws(value.substr(a, b - a));
+          int idx = -1;
+          for (int q = 0; q < (int)(sizeof(kTags) / sizeof(kTags[0])); ++q)
+            if (tag == kTags[q]) idx = q;
+          if (idx < 0) return bad("unknown PoS tag '" + tag + "'");
+          h.tags |= 1u << idx;
+          a = b + 1;
+        }
+        break;
+      }
+      case WH: {
+        if (value.empty()) return bad("wh entry without flags");
+        size_t a = 0;
+        while (a <= value.size()) {
+          size_t b = value.find('|', a);
+          if (b == std::string::npos) b = value.size();
+          const std::string f = strip_ws(value.substr(a, b - a));
+          if (f == "OPENER") h.flags |= rtlm::A_OPENER;
+          else if (f == "WHAT") h.flags |= rtlm::A_WHAT;
+          else if (f == "CAUSE") h.flags |= rtlm::A_CAUSE;
+          else if (f == "BROAD") h.flags |= rtlm::A_BROAD;
+          else return bad("unknown wh flag '" + f + "'");
+          a = b + 1;
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    if (eol >= len) break;
+  }
+  return true;
+}
+
+rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
+  std::vector<std::string> lemmas;
+  std::vector<HostLemma> attrs;
+  std::string err;
+  if (!parse_lexicon(text, len, lemmas, attrs, err)) return fail(c, RT_ELEXICON, err);
+  const uint32_t n = (uint32_t)lemmas.size();
+  uint32_t bits = 6;
+  while ((1u << bits) < 2 * n) ++bits;
+  std::vector<LexEntry> ent(n);
+  std::vector<uint16_t> slots(1u << bits, 0);
+  for (uint32_t k = 0; k < n; ++k) {
+    LexEntry e{};
+    for (size_t b = 0; b < lemmas[k].size(); ++b) {
+      uint64_t byte = (unsigned char)lemmas[k][b];
+      if (b < 8) e.k0 |= byte << (8 * b);
+      else e.k1 |= byte << (8 * (b - 8));
+    }
+    e.len = (uint32_t)lemmas[k].size();
+    const HostLemma& h = attrs[k];
+    uint32_t a = h.flags;
+    if (h.tags & 3u) a |= rtlm::A_NOUN;                   // NOUN or PROPN
+    if (__builtin_popcount(h.tags) >= 2) a |= rtlm::A_MULTIPOS;
+    if (h.senses >= 2) a |= (h.senses - 1) << rtlm::A_SEM_SHIFT;
+    a |= h.id << rtlm::A_ID_SHIFT;
+    e.attr = a;
+    ent[k] = e;
+    uint32_t hs = rtlm::lex_hash(e.k0, e.k1, e.len, bits);
+    while (slots[hs]) hs = (hs + 1) & ((1u << bits) - 1);
+    slots[hs] = (uint16_t)(k + 1);
+  }
+  c->n_entries = n;
+  c->bits = bits;
+  RT_CUDA(c, cudaMalloc(&c->d_entries, std::max<size_t>(1, n) * sizeof(LexEntry)));
+  RT_CUDA(c, cudaMalloc(&c->d_slots, slots.size() * sizeof(uint16_t)));
+  if (n) RT_CUDA(c, cudaMemcpy(c->d_entries, ent.data(), n * sizeof(LexEntry), cudaMemcpyHostToDevice));
+  RT_CUDA(c, cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  return RT_OK;
+}
+
+rtlm::DevLexicon dev_lex(const rt_ctx* c) { return rtlm::DevLexicon{c->d_entries, c->d_slots, c->n_entries, c->bits}; }
+
+rt_status ensure_ws(rt_ctx* c, size_t bytes) {
+  if (bytes <= c->ws_size) return RT_OK;
+  if (c->ws) cudaFree(c->ws);  // implicit device sync: no in-flight user
+  c->ws = nullptr;
+  c->ws_size = 0;
+  cudaError_t e = cudaMalloc(&c->ws, bytes);
+  if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("workspace: ") + cudaGetErrorString(e));
+  c->ws_size = bytes;
+  return RT_OK;
+}
+
+rt_status upload_offsets(rt_ctx* c, const uint32_t* h, uint32_t count, cudaStream_t s) {
+  if (count > c->off_cap) {
+    if (c->d_off) cudaFree(c->d_off);
+    c->d_off = nullptr;
+    c->off_cap = 0;
+    if (cudaMalloc(&c->d_off, (size_t)count * 4) != cudaSuccess) return fail(c, RT_ENOMEM, "offsets buffer");
+    c->off_cap = count;
+  }
+  RT_CUDA(c, cudaMemcpyAsync(c->d_off, h, (size_t)count * 4, cudaMemcpyHostToDevice, s));
+  return RT_OK;
+}
+
+rt_status check_profile(rt_ctx* c, const rt_profile* p, bool need_cores) {
+  if (!p) return fail(c, RT_EINVAL, "profile is NULL");
+  if (p->policy < RT_FIFO || p->policy > RT_UP) return fail(c, RT_EINVAL, "policy out of range");
+  if (p->C < 1 || p->C > (int)rtlm::kMaxWindow) return fail(c, RT_EINVAL, "C must be in [1,128]");
+  if (p->b10 < 10) return fail(c, RT_EINVAL, "b must be >= 1 (b10 >= 10, S:264)");
+  if ((int64_t)p->b10 * p->C / 10 > (int64_t)rtlm::kMaxWindow) return fail(c, RT_EINVAL, "window b*C must be <= 128");
+  if (!(p->lambda >= 1.0f)) return fail(c, RT_EINVAL, "lambda must be >= 1 (S:264)");
+  if (!(p->u_max > 0.0f) && !p->raw_numerator && p->policy == RT_UP) return fail(c, RT_EINVAL, "u_max must be > 0");
+  if (p->cores < 0 || p->cores > (int)rtlm::kMaxCores) return fail(c, RT_EINVAL, "cores must be in [0,32]");
+  if (need_cores && p->cores < 1) return fail(c, RT_EINVAL, "replay needs cores >= 1");
+  if (p->eta_us < 0 || p->mu_us < 0 || p->base_us < 0 || p->setup_us < 0 || p->xi_us < 0 || p->gamma < 0 ||
+      p->tightness < 0)
+    return fail(c, RT_EINVAL, "negative time coefficient");
+  if (p->reserved != 0) return fail(c, RT_EINVAL, "reserved must be 0");
+  return RT_OK;
+}
+
+cudaStream_t cs(rt_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int rt_abi_version(void) { return RTLM_ABI_VERSION; }
+
+rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** out) {
+  if (!out) return RT_EINVAL;
+  *out = nullptr;
+  rt_ctx* c = new rt_ctx();
+  *out = c;
+  c->device = device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(c, RT_EINVAL, "no such CUDA device");
+  DeviceGuard g(device);
+  RT_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  RT_CUDA(c, cudaMalloc(&c->d_flags, sizeof(uint32_t)));
+  RT_CUDA(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)));
+  if (!lexicon_text && len) return fail(c, RT_EINVAL, "lexicon_text is NULL");
+  return upload_lexicon(c, lexicon_text ? lexicon_text : "", len);
+}
+
+rt_status rt_destroy(rt_ctx* c) {
+  if (!c) return RT_OK;
+  {
+    DeviceGuard g(c->device);
+    cudaFree(c->d_entries);
+    cudaFree(c->d_slots);
+    cudaFree(c->d_flags);
+    cudaFree(c->ws);
+    cudaFree(c->d_off);
+    cudaFree(c->d_prof);
+  }
+  delete c;
+  return RT_OK;
+}
+
+const char* rt_last_error(const rt_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+uint32_t rt_lexicon_size(const rt_ctx* c) { return c ? c->n_entries : 0; }
+
+rt_status rt_get_flags(rt_ctx* c, uint32_t* flags) {
+  if (!c || !flags) return fail(c, RT_EINVAL, "null argument");
+  DeviceGuard g(c->device);
+  RT_CUDA(c, cudaDeviceSynchronize());
+  RT_CUDA(c, cudaMemcpy(flags, c->d_flags, 4, cudaMemcpyDeviceToHost));
+  RT_CUDA(c, cudaMemset(c->d_flags, 0, 4));
+  return RT_OK;
+}
+
+static rt_status score_common(rt_ctx* c, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n, int fused,
+                              const rt_regressor* reg, const rt_profile* prof, const int64_t* d_arr,
+                              const uint32_t* d_D_in, uint16_t* d_feat, float* d_u, uint64_t* d_key,
+                              uint32_t* d_D_out, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (n == 0) return RT_OK;
+  if (!d_offsets || !d_bytes) return fail(c, RT_EINVAL, "bytes/offsets are NULL");
+  if (reinterpret_cast<uintptr_t>(d_bytes) & 15u) return fail(c, RT_EINVAL, "d_bytes must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
+  if (n > 0xFFFFFFFEu) return fail(c, RT_EOVERFLOW, "n too large");
+  if (fused) {
+    if (!reg || !d_u || !d_key) return fail(c, RT_EINVAL, "regressor / u / key are required");
+    rt_status st = check_profile(c, prof, false);
+    if (st != RT_OK) return st;
+  } else if (!d_feat) {
+    return fail(c, RT_EINVAL, "d_feat is NULL");
+  }
+  DeviceGuard g(c->device);
+  rtlm::ScoreLaunch a{};
+  a.bytes = d_bytes;
+  a.offsets = d_offsets;
+  a.n = n;
+  a.lex = dev_lex(c);
+  a.fused = fused;
+  if (reg) a.reg = *reg;
+  if (prof) a.prof = *prof;
+  a.arrival = d_arr;
+  a.D_in = d_D_in;
+  a.feat = d_feat;
+  a.u = d_u;
+  a.key = d_key;
+  a.D_out = d_D_out;
+  a.flags = c->d_flags;
+  a.num_sms = c->num_sms;
+  cudaError_t e = rtlm::launch_score(a, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_score");
+  return RT_OK;
+}
+
+rt_status rt_score(rt_ctx* c, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n, uint16_t* d_feat,
+                   rt_stream stream) {
+  return score_common(c, d_bytes, d_offsets, n, 0, nullptr, nullptr, nullptr, nullptr, d_feat, nullptr, nullptr,
+                      nullptr, stream);
+}
+
+rt_status rt_score_key(rt_ctx* c, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n,
+                       const rt_regressor* reg, const rt_profile* prof, const int64_t* d_arr, const uint32_t* d_D_in,
+                       uint16_t* d_feat, float* d_u, uint64_t* d_key, uint32_t* d_D_out, rt_stream stream) {
+  return score_common(c, d_bytes, d_offsets, n, 1, reg, prof, d_arr, d_D_in, d_feat, d_u, d_key, d_D_out, stream);
+}
+
+rt_status rt_predict(rt_ctx* c, const uint16_t* d_feat, uint32_t n, const rt_regressor* reg, float* d_u,
+                     rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!n) return RT_OK;
+  if (!d_feat || !reg || !d_u) return fail(c, RT_EINVAL, "null argument");
+  if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
+  DeviceGuard g(c->device);
+  cudaError_t e = rtlm::launch_predict(d_feat, n, *reg, d_u, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_predict");
+  return RT_OK;
+}
+
+rt_status rt_key(rt_ctx* c, const float* d_u, const uint16_t* d_feat, const int64_t* d_arr, const uint32_t* d_D_in,
+                 uint32_t n, const rt_profile* prof, uint64_t* d_key, uint32_t* d_D_out, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!n) return RT_OK;
+  if (!d_u || !d_key) return fail(c, RT_EINVAL, "u / key are NULL");
+  if (!d_feat && !d_D_in) return fail(c, RT_EINVAL, "need d_feat (ntok) or d_D_in");
+  rt_status st = check_profile(c, prof, false);
+  if (st != RT_OK) return st;
+  DeviceGuard g(c->device);
+  cudaError_t e = rtlm::launch_key(d_u, d_feat, d_arr, d_D_in, n, *prof, d_key, d_D_out, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_key");
+  return RT_OK;
+}
+
+rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const uint32_t* h_seg_off, uint32_t nq,
+                      const rt_profile* prof, uint32_t cores, uint32_t* d_perm, uint32_t* d_batch_of,
+                      uint8_t* d_slot_of, uint8_t* d_core_of, uint32_t* d_seg_batch_off, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!h_seg_off) return fail(c, RT_EINVAL, "h_seg_off is NULL");
+  rt_status st = check_profile(c, prof, false);
+  if (st != RT_OK) return st;
+  if (cores > rtlm::kMaxCores) return fail(c, RT_EINVAL, "cores must be <= 32");
+  if (h_seg_off[0] != 0) return fail(c, RT_EINVAL, "h_seg_off[0] must be 0");
+  for (uint32_t q = 0; q < nq; ++q)
+    if (h_seg_off[q + 1] < h_seg_off[q]) return fail(c, RT_EINVAL, "h_seg_off must be non-decreasing");
+  const uint32_t n = h_seg_off[nq];
+  if (!d_seg_batch_off) return fail(c, RT_EINVAL, "d_seg_batch_off is NULL");
+  if (n && (!d_key || !d_u || !d_perm || !d_batch_of || !d_slot_of || !d_core_of))
+    return fail(c, RT_EINVAL, "null device buffer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = cs(stream);
+  // workspace: seg counts | big-queue sort + gather
+  size_t big_ws = 0;
+  for (uint32_t q = 0; q < nq; ++q) {
+    const uint32_t m = h_seg_off[q + 1] - h_seg_off[q];
+    if (m > rtlm::kSmallSeg) {
+      size_t need = rtlm::radix_sort_workspace(m) + ((size_t)m + 128) * 4;
+      if (need > big_ws) big_ws = need;
+    }
+  }
+  const size_t cnt_bytes = (((size_t)nq + 1) * 4 + 255) & ~size_t(255);
+  st = ensure_ws(c, cnt_bytes + big_ws);
+  if (st != RT_OK) return st;
+  st = upload_offsets(c, h_seg_off, nq + 1, s);
+  if (st != RT_OK) return st;
+  rtlm::SchedLaunch a{};
+  a.key = d_key;
+  a.u = d_u;
+  a.seg_off = c->d_off;
+  a.nq = nq;
+  a.prof = *prof;
+  a.cores = cores;
+  a.perm = d_perm;
+  a.batch_of = d_batch_of;
+  a.slot_of = d_slot_of;
+  a.core_of = d_core_of;
+  a.seg_count = static_cast<uint32_t*>(c->ws);
+  a.seg_batch_off = d_seg_batch_off;
+  char* big = static_cast<char*>(c->ws) + cnt_bytes;
+  cudaError_t e = rtlm::launch_sched_small(a, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_small");
+  const int full64 = (prof->policy == RT_FIFO || prof->policy == RT_EDF) ? 1 : 0;
+  for (uint32_t q = 0; q < nq; ++q) {
+    const uint32_t lo = h_seg_off[q], hi = h_seg_off[q + 1];
+    if (hi - lo <= rtlm::kSmallSeg) continue;
+    const size_t sort_ws = rtlm::radix_sort_workspace(hi - lo);
+    e = rtlm::radix_sort_desc(d_key + lo, lo, hi - lo, d_perm + lo, full64, big, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "radix_sort_desc");
+    e = rtlm::launch_sched_big(a, q, lo, hi, reinterpret_cast<float*>(big + sort_ws), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_big");
+  }
+  e = rtlm::launch_sched_finish(a, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_finish");
+  return RT_OK;
+}
+
+rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, const float* d_u,
+                      const uint64_t* d_key, const uint32_t* d_D, const uint32_t* h_trace_off, uint32_t nt,
+                      const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
+                      rt_trace_stats* d_stats, int64_t* d_end_us, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!nt) return RT_OK;
+  if (!h_trace_off || !h_profiles || !np || !d_stats) return fail(c, RT_EINVAL, "null argument");
+  if (!d_trace_prof && np < 1) return fail(c, RT_EINVAL, "no profile");
+  for (uint32_t k = 0; k < np; ++k) {
+    rt_status st = check_profile(c, &h_profiles[k], true);
+    if (st != RT_OK) return st;
+  }
+  if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
+  for (uint32_t t = 0; t < nt; ++t) {
+    if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
+    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
+  }
+  if (h_trace_off[nt] && (!d_arr || !d_len || !d_u || !d_key || !d_D)) return fail(c, RT_EINVAL, "null task array");
+  DeviceGuard g(c->device);
+  cudaStream_t s = cs(stream);
+  rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
+  if (st != RT_OK) return st;
+  if (np > c->prof_cap) {
+    if (c->d_prof) cudaFree(c->d_prof);
+    c->d_prof = nullptr;
+    c->prof_cap = 0;
+    if (cudaMalloc(&c->d_prof, np * sizeof(rt_profile)) != cudaSuccess) return fail(c, RT_ENOMEM, "profiles");
+    c->prof_cap = np;
+  }
+  RT_CUDA(c, cudaMemcpyAsync(c->d_prof, h_profiles, np * sizeof(rt_profile), cudaMemcpyHostToDevice, s));
+  rtlm::ReplayLaunch a{};
+  a.arrival = d_arr;
+  a.len = d_len;
+  a.u = d_u;
+  a.key = d_key;
+  a.D = d_D;
+  a.trace_off = c->d_off;
+  a.nt = nt;
+  a.profiles = c->d_prof;
+  a.trace_prof = d_trace_prof;
+  a.stats = d_stats;
+  a.end_us = d_end_us;
+  cudaError_t e = rtlm::launch_replay(a, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
+  return RT_OK;
+}
+
+rt_status rt_reduce_stats(rt_ctx* c, const rt_trace_stats* d_stats, uint32_t nt, const uint16_t* d_group_of,
+                          uint32_t ngroups, int64_t* d_sums, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!nt) return RT_OK;
+  if (!d_stats || !d_sums || !ngroups) return fail(c, RT_EINVAL, "null argument");
+  DeviceGuard g(c->device);
+  cudaError_t e = rtlm::launch_reduce_stats(d_stats, nt, d_group_of, ngroups, d_sums, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_reduce_stats");
+  return RT_OK;
+}
+
+}  // extern "C"

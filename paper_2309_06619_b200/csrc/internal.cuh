@@ -1,0 +1,128 @@
+// internal.cuh — shared definitions of librtlm.so (product code only; the
+// oracle in oracle/ shares nothing with this file).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rtlm.h"
+
+namespace rtlm {
+
+// ---------------------------------------------------------------- lexicon
+// Device lexicon: open-addressing table of lemma keys (<= 16 bytes, zero
+// padded, little-endian in two u64) -> packed attributes.
+enum : uint32_t {
+  A_VAGUE = 1u << 0,
+  A_PREP = 1u << 1,
+  A_COORD = 1u << 2,
+  A_NOUN = 1u << 3,
+  A_OPENER = 1u << 4,
+  A_WHAT = 1u << 5,
+  A_CAUSE = 1u << 6,
+  A_BROAD = 1u << 7,
+  A_MULTIPOS = 1u << 8,
+};
+constexpr int A_SEM_SHIFT = 9;    // bits 9..16: senses - 1 (0..254)
+constexpr uint32_t A_SEM_MASK = 0xFFu;
+constexpr int A_ID_SHIFT = 17;    // bits 17..31: entry id (noun id)
+constexpr uint32_t kMaxLexEntries = 1024;
+
+struct LexEntry {
+  uint64_t k0, k1;
+  uint32_t attr, len;
+};
+
+struct DevLexicon {
+  const LexEntry* entries;  // n_entries
+  const uint16_t* slots;    // 1 << bits; 0 = empty, else entry index + 1
+  uint32_t n_entries;
+  uint32_t bits;
+};
+
+__host__ __device__ __forceinline__ uint32_t lex_hash(uint64_t k0, uint64_t k1, uint32_t len, uint32_t bits) {
+  uint64_t h = (k0 * 0x9E3779B97F4A7C15ull) ^ ((k1 + len) * 0xC2B2AE3D27D4EB4Full);
+  h ^= h >> 31;
+  return (uint32_t)((h * 0xD6E8FEB86659FD93ull) >> (64 - bits));
+}
+
+// ---------------------------------------------------------------- keys
+__host__ __device__ __forceinline__ uint32_t ord32_bits(uint32_t b) {
+  if (b == 0x80000000u) b = 0;  // -0 -> +0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+constexpr uint32_t kNoBatch = 0xFFFFFFFFu;
+constexpr uint32_t kSmallSeg = 2048;     // queues up to this size are scheduled inside one CTA
+constexpr uint32_t kMaxWindow = 128;     // m = b10*C/10 <= 128
+constexpr uint32_t kMaxTrace = 1024;     // tasks per replayed trace
+constexpr uint32_t kMaxCores = 32;
+
+// ---------------------------------------------------------------- launchers
+struct ScoreLaunch {
+  const uint8_t* bytes;
+  const uint32_t* offsets;
+  uint32_t n;
+  DevLexicon lex;
+  int fused;  // 0: feat only; 1: + u, key (and D, feat if non-null)
+  rt_regressor reg;
+  rt_profile prof;
+  const int64_t* arrival;
+  const uint32_t* D_in;
+  uint16_t* feat;
+  float* u;
+  uint64_t* key;
+  uint32_t* D_out;
+  uint32_t* flags;
+  int num_sms;
+};
+cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s);
+cudaError_t launch_predict(const uint16_t* feat, uint32_t n, const rt_regressor& reg, float* u, cudaStream_t s);
+cudaError_t launch_key(const float* u, const uint16_t* feat, const int64_t* arrival, const uint32_t* D_in,
+                       uint32_t n, const rt_profile& p, uint64_t* key, uint32_t* D_out, cudaStream_t s);
+
+// Radix sort (stable, descending 64-bit keys) of one range; values = global
+// element indices.  Workspace sized by radix_sort_workspace(n).
+size_t radix_sort_workspace(uint32_t n);
+cudaError_t radix_sort_desc(const uint64_t* keys_in, uint32_t base_index, uint32_t n, uint32_t* perm_out,
+                            int full64, void* workspace, cudaStream_t s);
+
+struct SchedLaunch {
+  const uint64_t* key;
+  const float* u;
+  const uint32_t* seg_off;   // device copy, nq + 1
+  uint32_t nq;
+  rt_profile prof;
+  uint32_t cores;
+  uint32_t* perm;
+  uint32_t* batch_of;
+  uint8_t* slot_of;
+  uint8_t* core_of;
+  uint32_t* seg_count;       // device, nq (local batch counts)
+  uint32_t* seg_batch_off;   // device, nq + 1
+};
+// small queues (all segments with n <= kSmallSeg; others skipped)
+cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s);
+// one large queue [lo, hi) whose perm is already sorted in a.perm
+cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, float* u_sorted_ws,
+                             cudaStream_t s);
+cudaError_t launch_sched_finish(const SchedLaunch& a, cudaStream_t s);
+
+struct ReplayLaunch {
+  const int64_t* arrival;
+  const uint16_t* len;
+  const float* u;
+  const uint64_t* key;
+  const uint32_t* D;
+  const uint32_t* trace_off;  // device, nt + 1
+  uint32_t nt;
+  const rt_profile* profiles; // device
+  const uint16_t* trace_prof;
+  rt_trace_stats* stats;
+  int64_t* end_us;
+};
+cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* group_of, uint32_t ngroups,
+                                int64_t* sums, cudaStream_t s);
+
+}  // namespace rtlm

@@ -1,0 +1,294 @@
+// k_replay.cu — K5: discrete-event replay of independent arrival traces
+// (§8(a) row a7) and K6: integer statistics reduction (row a8).
+//
+// One warp (one CTA) per trace of <= 1024 tasks (R-REPLAY; §V-A).
+// Priorities are static per task (Eq. 3 depends on d - r, not on the clock,
+// P:377), so the trace's keys are sorted once in shared memory and every
+// "ready" set is a 1024-bit bitmap over key rank, one 32-bit word per lane:
+// the top-m ready tasks are the first m set bits (popc + warp scan), the
+// highest-key CPU task is the first set bit, and a second bitmap over arrival
+// index gives the oldest waiting task for the xi flush (R-XI).  Batches are
+// consolidated with the same O6 round as rt_schedule (R-CONS) and timed with
+// the latency model R-LAT in int64 microseconds (R-TIME).
+#include "internal.cuh"
+
+namespace rtlm {
+namespace {
+
+struct ReplaySmem {
+  // s_r aliases s_key: keys are only needed until the ranks are known
+  union {
+    uint64_t key[kMaxTrace];
+    int64_t r[kMaxTrace];
+  };
+  uint16_t sidx[kMaxTrace];  // rank -> arrival index
+  uint16_t rank[kMaxTrace];  // arrival index -> rank
+  uint16_t len[kMaxTrace];
+  float u[kMaxTrace];
+  uint32_t D[kMaxTrace];
+  uint32_t ready_gpu[32], ready_cpu[32], wait_arr[32];
+  int64_t core_free[kMaxCores];
+  uint32_t W[kMaxWindow], S[kMaxWindow];
+  float Wu[kMaxWindow], Su[kMaxWindow];
+};
+
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  ReplaySmem& sm = *reinterpret_cast<ReplaySmem*>(smem_raw);
+  const uint32_t lane = threadIdx.x;
+  const uint32_t t = blockIdx.x;
+  const uint32_t lo = a.trace_off[t], n = a.trace_off[t + 1] - lo;
+  const rt_profile p = a.profiles[a.trace_prof ? a.trace_prof[t] : 0];
+  if (n == 0) {
+    if (lane == 0) a.stats[t] = rt_trace_stats{0, 0u, 0u};
+    return;
+  }
+  // ---- key rank: bitonic sort of (key desc, arrival index asc)
+  uint32_t npow = 32;
+  while (npow < n) npow <<= 1;
+  for (uint32_t i = lane; i < npow; i += 32) {
+    sm.key[i] = i < n ? a.key[lo + i] : 0ull;
+    sm.sidx[i] = i < n ? (uint16_t)i : (uint16_t)0xFFFF;
+  }
+  __syncwarp();
+  for (uint32_t k = 2; k <= npow; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < npow; i += 32) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t ki = sm.key[i], kl = sm.key[l];
+          const uint32_t ii = sm.sidx[i], il = sm.sidx[l];
+          const bool l_first = kl > ki || (kl == ki && il < ii);
+          const bool i_first = ki > kl || (ki == kl && ii < il);
+          if ((i & k) == 0 ? l_first : i_first) {
+            sm.key[i] = kl; sm.key[l] = ki;
+            sm.sidx[i] = (uint16_t)il; sm.sidx[l] = (uint16_t)ii;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  uint32_t ncpu_l = 0;
+  for (uint32_t j = lane; j < n; j += 32) {
+    sm.rank[sm.sidx[j]] = (uint16_t)j;
+    ncpu_l += (uint32_t)(sm.key[j] >> 63);
+  }
+  const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);  // CPU class = ranks [0, ncpu)
+  __syncwarp();
+  for (uint32_t i = lane; i < n; i += 32) {
+    sm.r[i] = a.arrival[lo + i];
+    sm.len[i] = a.len[lo + i];
+    sm.u[i] = a.u[lo + i];
+    sm.D[i] = a.D[lo + i];
+  }
+  sm.ready_gpu[lane] = 0; sm.ready_cpu[lane] = 0; sm.wait_arr[lane] = 0;
+  sm.core_free[lane] = 0;
+  __syncwarp();
+
+  const uint32_t C = (uint32_t)p.C, m = (uint32_t)p.b10 * C / 10u, cores = (uint32_t)p.cores;
+  const int64_t gpu_fixed = p.setup_us + p.base_us;
+  int64_t now = sm.r[0], gpu_free = 0;
+  uint32_t next = 0, done = 0;
+  int64_t resp = 0;     // per-lane partial sums
+  uint32_t misses = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+
+  for (;;) {
+    // ---- admit arrivals <= now (arrival order is non-decreasing)
+    while (next < n) {
+      const uint32_t i = next + lane;
+      const bool arr = i < n && sm.r[i] <= now;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
+      const uint32_t cnt = __popc(bal);  // a prefix of ones
+      if (arr) {
+        const uint32_t rk = sm.rank[i];
+        if (rk < ncpu) {
+          atomicOr(&sm.ready_cpu[rk >> 5], 1u << (rk & 31));
+        } else {
+          atomicOr(&sm.ready_gpu[rk >> 5], 1u << (rk & 31));
+          atomicOr(&sm.wait_arr[i >> 5], 1u << (i & 31));
+        }
+      }
+      next += cnt;
+      if (cnt < 32) break;
+    }
+    __syncwarp();
+    // ---- CPU cores: highest-key ready CPU task -> lowest-index free core
+    for (;;) {
+      const uint32_t wcpu = sm.ready_cpu[lane];
+      const uint32_t any = __ballot_sync(0xFFFFFFFFu, wcpu != 0);
+      if (!any) break;
+      const uint32_t fm = __ballot_sync(0xFFFFFFFFu, lane < cores && sm.core_free[lane] <= now);
+      if (!fm) break;
+      const uint32_t c = __ffs(fm) - 1, wl = __ffs(any) - 1;
+      const uint32_t word = __shfl_sync(0xFFFFFFFFu, wcpu, wl);
+      const uint32_t rk = wl * 32 + (__ffs(word) - 1);
+      const uint32_t i = sm.sidx[rk];
+      const int64_t end = now + (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)sm.len[i]);
+      if (lane == 0) {
+        sm.core_free[c] = end;
+        sm.ready_cpu[wl] = word & (word - 1u);
+        resp += end - sm.r[i];
+        misses += end > sm.r[i] + (int64_t)sm.D[i];
+        if (a.end_us) a.end_us[lo + i] = end;
+      }
+      ++done;
+      __syncwarp();
+    }
+    // ---- GPU dispatch
+    bool waiting = false;
+    int64_t oldest_r = 0;
+    if (gpu_free <= now) {
+      uint32_t gw = sm.ready_gpu[lane];
+      const uint32_t cl = __popc(gw);
+      const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, cl);
+      if (total) {
+        const uint32_t aw = sm.wait_arr[lane];
+        const uint32_t anyw = __ballot_sync(0xFFFFFFFFu, aw != 0);
+        const uint32_t owl = __ffs(anyw) - 1;
+        const uint32_t oword = __shfl_sync(0xFFFFFFFFu, aw, owl);
+        const uint32_t oldest = owl * 32 + (__ffs(oword) - 1);
+        oldest_r = sm.r[oldest];
+        const bool flush = (oldest_r <= now - p.xi_us) || next == n;
+        const uint32_t full = p.consolidate ? m : C;
+        const uint32_t take = total >= full ? full : (flush ? total : 0u);
+        if (!take) {
+          waiting = true;
+        } else {
+          // first `take` set bits in rank order -> W
+          uint32_t excl = cl;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            uint32_t v = __shfl_up_sync(0xFFFFFFFFu, excl, o);
+            if (lane >= (uint32_t)o) excl += v;
+          }
+          excl -= cl;
+          if (excl < take) {
+            uint32_t k = min(cl, take - excl);
+            for (uint32_t e = 0; e < k; ++e) {
+              const uint32_t b = __ffs(gw) - 1;
+              gw &= gw - 1u;
+              sm.W[excl + e] = lane * 32 + b;
+            }
+          }
+          __syncwarp();
+          uint32_t cnt;
+          const uint32_t* B;
+          if (p.consolidate) {
+            for (uint32_t e = lane; e < take; e += 32) sm.Wu[e] = sm.u[sm.sidx[sm.W[e]]];
+            __syncwarp();
+            for (uint32_t e = lane; e < take; e += 32) {  // sort window by (u, rank)
+              const float ue = sm.Wu[e];
+              const uint32_t re = sm.W[e];
+              uint32_t pos = 0;
+              for (uint32_t x = 0; x < take; ++x) {
+                const float ux = sm.Wu[x];
+                pos += (ux < ue) || (ux == ue && sm.W[x] < re);
+              }
+              sm.S[pos] = re;
+              sm.Su[pos] = ue;
+            }
+            __syncwarp();
+            const uint32_t lim = min(C, take);
+            cnt = lim;
+            for (uint32_t base = 1; base < lim; base += 32) {
+              const uint32_t ii = base + lane;
+              const bool bad = ii < lim && !(sm.Su[ii] <= __fmul_rn(p.lambda, sm.Su[ii - 1]));
+              const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+              if (bal) {
+                cnt = base + __ffs(bal) - 1;
+                break;
+              }
+            }
+            B = sm.S;
+          } else {
+            cnt = take;
+            B = sm.W;
+          }
+          uint32_t ml = 0;
+          for (uint32_t e = lane; e < cnt; e += 32) ml = max(ml, (uint32_t)sm.len[sm.sidx[B[e]]]);
+          ml = __reduce_max_sync(0xFFFFFFFFu, ml);
+          const int64_t end = now + gpu_fixed + p.eta_us * (int64_t)ml;
+          for (uint32_t e = lane; e < cnt; e += 32) {
+            const uint32_t rk = B[e];
+            const uint32_t i = sm.sidx[rk];
+            atomicAnd(&sm.ready_gpu[rk >> 5], ~(1u << (rk & 31)));
+            atomicAnd(&sm.wait_arr[i >> 5], ~(1u << (i & 31)));
+            resp += end - sm.r[i];
+            misses += end > sm.r[i] + (int64_t)sm.D[i];
+            if (a.end_us) a.end_us[lo + i] = end;
+          }
+          done += cnt;
+          gpu_free = end;
+          __syncwarp();
+        }
+      }
+    }
+    if (done >= n) break;
+    // ---- next event time
+    int64_t nxt = INT64_MAX;
+    if (next < n) nxt = sm.r[next];
+    if (gpu_free > now) nxt = min(nxt, gpu_free);
+    const bool cpu_waiting = __ballot_sync(0xFFFFFFFFu, sm.ready_cpu[lane] != 0) != 0;
+    if (cpu_waiting) {
+      int64_t cf = (lane < cores && sm.core_free[lane] > now) ? sm.core_free[lane] : INT64_MAX;
+      nxt = min(nxt, warp_min64(cf));
+    }
+    if (waiting) nxt = min(nxt, oldest_r + p.xi_us);
+    if (nxt == INT64_MAX) break;  // unreachable with valid inputs (cores >= 1)
+    now = nxt;
+    (void)lt;
+  }
+  const int64_t sr = warp_sum64(resp);
+  const uint32_t ms = __reduce_add_sync(0xFFFFFFFFu, misses);
+  if (lane == 0) a.stats[t] = rt_trace_stats{sr, n, ms};
+}
+
+__global__ void k_reduce_stats(const rt_trace_stats* __restrict__ st, uint32_t nt, const uint16_t* __restrict__ grp,
+                               uint32_t ngroups, int64_t* __restrict__ sums) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const uint32_t g = grp ? grp[t] : 0u;
+    if (g >= ngroups) continue;
+    unsigned long long* s = reinterpret_cast<unsigned long long*>(sums + (size_t)g * 3);
+    atomicAdd(s + 0, (unsigned long long)st[t].sum_resp_us);
+    atomicAdd(s + 1, (unsigned long long)st[t].n);
+    atomicAdd(s + 2, (unsigned long long)st[t].misses);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
+  if (!a.nt) return cudaSuccess;
+  const size_t smem = sizeof(ReplaySmem);
+  cudaError_t e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_replay<<<a.nt, 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* grp, uint32_t ngroups,
+                                int64_t* sums, cudaStream_t s) {
+  if (!nt) return cudaSuccess;
+  uint32_t blocks = (nt + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  k_reduce_stats<<<blocks, 256, 0, s>>>(st, nt, grp, ngroups, sums);
+  return cudaGetLastError();
+}
+
+}  // namespace rtlm

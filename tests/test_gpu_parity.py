@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bar (north_star): features, keys, orders, batch/core
+assignments, end times and miss counts bit-exact; u bit-exact too (same fp32
+operation sequence; the 1e-5 relative tolerance of north_star is asserted as
+the outer bound).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import rtgen
+from rtgen import configs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2309_06619_b200 as rt  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+U32 = np.uint32
+
+
+def dev(a):
+    a = np.ascontiguousarray(a)
+    view = {np.dtype(np.uint32): np.int32, np.dtype(np.uint16): np.int16, np.dtype(np.uint64): np.int64}
+    if a.dtype in view:
+        a = a.view(view[a.dtype])
+    return torch.from_numpy(a).to(DEV)
+
+
+def host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+@pytest.fixture(scope="module")
+def ctx_v1():
+    return rt.Context(configs.read_lexicon(), 0)
+
+
+@pytest.fixture(scope="module")
+def ctx_min():
+    return rt.Context(configs.read_lexicon(configs.LEX_MIN), 0)
+
+
+@pytest.fixture(scope="module")
+def lex_v1():
+    return oracle.Lexicon(configs.read_lexicon())
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+def edge_texts():
+    rng = np.random.default_rng(11)
+    t = ["", " ", "?", "a", "n't", "don't", "DON'T STOP!!", "What's", "x" * 40, "stuffing" * 3, "'s's's",
+         "Why art? How art? Tell art?", "a, b, c, d", "a,, b", "cats, and dogs", "bats's", "flies'",
+         "\t\n\x0b\x0c\r", "caf\xe9 na\xefve", "abcdefghijklmnopqrsing", "abcdefghijklmnopqing", "abcdefghijklmnoping",
+         "abcdefghijklmnopqrs's", "history" * 3 + "'s", "John saw a boy in the park with a telescope.",
+         "What are the causes and consequences of poverty in developing countries?"]
+    for _ in range(300):  # random bytes over the whole 0..255 range
+        t.append(bytes(rng.integers(0, 256, size=int(rng.integers(0, 60)), dtype=np.uint8)))
+    for _ in range(300):  # random printable soup with apostrophes and punctuation
+        alphabet = np.frombuffer(b"abcdeSTUVW'0123 ,.?!;-\t", dtype=np.uint8)
+        t.append(bytes(rng.choice(alphabet, size=int(rng.integers(0, 80)))))
+    t.append("stuff " * 9000)            # > 32 KB staging tile: slow path
+    t.append("and " * 70000)             # u16 saturation of ntok
+    return t
+
+
+@pytest.mark.parametrize("lexname", ["v1", "min"])
+def test_score_edge_cases(lexname, ctx_v1, ctx_min):
+    ctx = ctx_v1 if lexname == "v1" else ctx_min
+    lex = oracle.Lexicon(configs.read_lexicon() if lexname == "v1" else configs.read_lexicon(configs.LEX_MIN))
+    data, off = rtgen.pack_texts(edge_texts())
+    feat = ctx.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got = host(feat, np.uint16)
+    want = oracle.rule_gen(lex, data, off)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), bytes(data[off[i]:off[i + 1]])[:60], got[i].tolist(), want[i].tolist())
+                           for i in bad[:5]]
+    assert ctx.flags() & 1  # saturation was flagged
+
+
+def _score_all(ctx, lex, d, prof, reg, arrival=None):
+    out = ctx.score_key(dev(d["data"]), dev(d["offsets"]), reg, prof,
+                        arrival=None if arrival is None else dev(arrival), want_feat=True)
+    torch.cuda.synchronize()
+    f = oracle.rule_gen(lex, d["data"], d["offsets"])
+    u = oracle.predict(f, reg)
+    k, D = oracle.key(u, f, prof, r_us=arrival)
+    return out, f, u, k, D
+
+
+def test_score_key_parity_ragged(ctx_v1, lex_v1):
+    """50 001 requests: many tiles plus a ragged tail."""
+    d = configs.config2(n=50001, gid0=777)
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, d["profile"], d["regressor"])
+    assert (host(out["feat"], np.uint16) == f).all()
+    gu = out["u"].cpu().numpy()
+    assert np.all(np.abs(gu - u) <= 1e-5 * np.abs(u))
+    assert (gu.view(U32) == u.view(U32)).all()
+    assert (host(out["key"], np.uint64) == k).all()
+    assert (host(out["D"], U32) == D).all()
+    # unfused calls agree with the fused one
+    feat = ctx_v1.score(dev(d["data"]), dev(d["offsets"]))
+    u2 = ctx_v1.predict(feat, d["regressor"])
+    k2, D2 = ctx_v1.key(u2, d["profile"], feat=feat)
+    torch.cuda.synchronize()
+    assert (host(feat, np.uint16) == f).all()
+    assert (u2.cpu().numpy().view(U32) == u.view(U32)).all()
+    assert (host(k2, np.uint64) == k).all() and (host(D2, U32) == D).all()
+
+
+@pytest.mark.parametrize("policy", ["FIFO", "EDF", "LUF", "MUF", "SLACK", "UP"])
+@pytest.mark.parametrize("variant", ["plain", "loose_raw_nooffload"])
+def test_key_policies(ctx_v1, lex_v1, policy, variant):
+    d = configs.traces(3, range(2), 1000, lambda t: t % 4)
+    prof = dict(d["profiles"][0], policy=policy)
+    if variant != "plain":
+        prof.update(tightness=2, raw_numerator=1, offload=0, alpha=0.3)
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressors"][0], arrival=d["arrival_us"])
+    assert (host(out["key"], np.uint64) == k).all()
+    assert (host(out["D"], U32) == D).all()
+
+
+def _check_schedule(g, s, nseg):
+    assert (host(g["perm"], U32) == s["perm"]).all(), "perm"
+    assert (host(g["batch_of"], U32) == s["batch_of"]).all(), "batch_of"
+    assert (g["slot_of"].cpu().numpy() == s["slot_of"]).all(), "slot_of"
+    assert (g["core_of"].cpu().numpy() == s["core_of"]).all(), "core_of"
+    assert (host(g["seg_batch_off"], U32) == s["seg_batch_off"]).all(), "seg_batch_off"
+
+
+@pytest.mark.parametrize("C,b10,lam,cores", [(11, 18, 1.5, 4), (33, 18, 1.5, 4), (4, 10, 1.0, 1), (24, 30, 2.0, 32),
+                                             (1, 10, 1.5, 7)])
+def test_schedule_many_small_queues(ctx_v1, lex_v1, C, b10, lam, cores):
+    rng = np.random.default_rng(C * 100 + b10)
+    sizes = [0, 1, 2, 2048, 37] + [int(x) for x in rng.integers(0, 700, 60)]
+    seg = np.concatenate([[0], np.cumsum(sizes)]).astype(U32)
+    d = configs.config2(n=int(seg[-1]), gid0=5000 + C)
+    prof = dict(d["profile"], C=C, b10=b10, **{"lambda": lam}, cores=cores)
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressor"])
+    g = ctx_v1.schedule(out["key"], out["u"], seg, prof)
+    torch.cuda.synchronize()
+    s = oracle.schedule(k, u, seg, prof)
+    _check_schedule(g, s, len(sizes))
+
+
+@pytest.mark.parametrize("n", [2049, 30000])
+def test_schedule_big_queue(ctx_v1, lex_v1, n):
+    d = configs.config2(n=n, gid0=90000)
+    for pol in ["UP", "FIFO"]:
+        prof = dict(d["profile"], policy=pol)
+        out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressor"], arrival=np.zeros(n, np.int64))
+        seg = np.asarray([0, 1000, 1000 + n, 1000 + n], U32) if False else np.asarray([0, n], U32)
+        g = ctx_v1.schedule(out["key"], out["u"], seg, prof)
+        torch.cuda.synchronize()
+        s = oracle.schedule(k, u, seg, prof)
+        _check_schedule(g, s, 1)
+
+
+def test_schedule_mixed_big_and_small(ctx_v1, lex_v1):
+    sizes = [100, 5000, 0, 3000, 7]
+    seg = np.concatenate([[0], np.cumsum(sizes)]).astype(U32)
+    d = configs.config2(n=int(seg[-1]), gid0=123456)
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, d["profile"], d["regressor"])
+    g = ctx_v1.schedule(out["key"], out["u"], seg, d["profile"])
+    torch.cuda.synchronize()
+    _check_schedule(g, oracle.schedule(k, u, seg, d["profile"]), len(sizes))
+
+
+def _replay_case(ctx, lex, d, overrides, want_end=True):
+    nt = len(d["trace_off"]) - 1
+    profs = [dict(p, **overrides) for p in d["profiles"]]
+    u = np.zeros(len(d["arrival_us"]), np.float32)
+    k = np.zeros(len(u), np.uint64)
+    D = np.zeros(len(u), U32)
+    f = oracle.rule_gen(lex, d["data"], d["offsets"])
+    gpu_u, gpu_k, gpu_D = [], [], []
+    for t in range(nt):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        p = profs[int(d["trace_prof"][t])]
+        reg = d["regressors"][int(d["trace_prof"][t])]
+        u[lo:hi] = oracle.predict(f[lo:hi], reg)
+        k[lo:hi], D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], p, r_us=d["arrival_us"][lo:hi])
+    st, end = oracle.simulate(d["arrival_us"], d["true_len"], u, k, D, d["trace_off"], profs, d["trace_prof"],
+                              want_end=want_end)
+    gs, gend = ctx.simulate(dev(d["arrival_us"]), dev(d["true_len"]), dev(u), dev(k), dev(D), d["trace_off"], profs,
+                            dev(d["trace_prof"]), want_end=want_end)
+    torch.cuda.synchronize()
+    g = rt.decode_stats(gs)
+    assert (g == st).all(), [(i, g[i], st[i]) for i in np.nonzero(g != st)[0][:3]]
+    if want_end:
+        assert (gend.cpu().numpy() == end).all()
+    return st
+
+
+@pytest.mark.parametrize("ov", [{}, {"consolidate": 0}, {"offload": 0}, {"policy": "FIFO", "consolidate": 0,
+                                                                          "offload": 0},
+                                {"policy": "LUF"}, {"policy": "MUF"}, {"policy": "EDF"}, {"tightness": 2},
+                                {"b10": 30, "lambda": 1.1}, {"cores": 1}, {"xi_us": 0}])
+def test_replay_parity(ctx_v1, lex_v1, ov):
+    d = configs.traces(3, range(40, 56), 1000, lambda t: t % 4)
+    _replay_case(ctx_v1, lex_v1, d, ov)
+
+
+def test_replay_sizes_and_heavy_load(ctx_v1, lex_v1):
+    # trace sizes 1 and 1024 and a 16x arrival-rate overload
+    d = configs.traces(5, range(8), 1024, lambda t: t % 4, beta0=160, step=16, beta_max=2400)
+    _replay_case(ctx_v1, lex_v1, d, {})
+    d1 = configs.traces(5, range(3), 1, lambda t: t % 4)
+    _replay_case(ctx_v1, lex_v1, d1, {})
+
+
+def test_reduce_stats(ctx_v1):
+    rng = np.random.default_rng(3)
+    nt = 5000
+    raw = np.zeros((nt, 2), np.int64)
+    raw[:, 0] = rng.integers(0, 2**40, nt)
+    n = rng.integers(0, 1025, nt).astype(np.uint64)
+    m = rng.integers(0, 1025, nt).astype(np.uint64)
+    raw[:, 1] = (n | (m << np.uint64(32))).view(np.int64)
+    grp = rng.integers(0, 7, nt).astype(np.uint16)
+    sums = ctx_v1.reduce_stats(dev(raw), dev(grp), 7)
+    torch.cuda.synchronize()
+    for gi in range(7):
+        sel = grp == gi
+        assert sums[gi, 0].item() == int(raw[sel, 0].sum())
+        assert sums[gi, 1].item() == int(n[sel].sum()) and sums[gi, 2].item() == int(m[sel].sum())
+
+
+def test_errors(ctx_v1):
+    with pytest.raises(rt.RtlmError, match="RT_ELEXICON"):
+        rt.Context("bogus:\nx\n", 0)
+    p = dict(configs.paper_lms()[0], **{"lambda": 0.5})
+    u = torch.zeros(4, device=DEV)
+    with pytest.raises(rt.RtlmError, match="lambda"):
+        ctx_v1.key(u, p, D_in=torch.zeros(4, dtype=torch.int32, device=DEV))
+    p = dict(configs.paper_lms()[0], C=200)
+    with pytest.raises(rt.RtlmError, match="RT_EINVAL"):
+        ctx_v1.key(u, p, D_in=torch.zeros(4, dtype=torch.int32, device=DEV))
+
+
+@pytest.mark.slow
+def test_config2_full_size(ctx_v1, lex_v1):
+    """BASELINE configs[1] at full size (2^20 requests, one queue), in the bench's
+    launch configuration: score_key + schedule, everything compared with the oracle."""
+    d = configs.config2()
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, d["profile"], d["regressor"])
+    assert (host(out["feat"], np.uint16) == f).all()
+    assert (out["u"].cpu().numpy().view(U32) == u.view(U32)).all()
+    assert (host(out["key"], np.uint64) == k).all()
+    seg = np.asarray([0, len(u)], U32)
+    g = ctx_v1.schedule(out["key"], out["u"], seg, d["profile"])
+    torch.cuda.synchronize()
+    _check_schedule(g, oracle.schedule(k, u, seg, d["profile"]), 1)
