@@ -1,0 +1,392 @@
+#!/usr/bin/env python3
+"""Benchmark of the RT-LM hot path on B200 (BASELINE.json metric:
+"M requests scored+scheduled/s and traces/s at 1/2/4/8 B200; % of HBM peak").
+
+One STEP = one pass of the hot path over one batch of synthetic input:
+  * value (requests leg, BASELINE configs[1] = config 2): one queue of 2^20
+    requests per GPU -> rt_score_key (a1-a4: features, u, key) -> rt_schedule
+    (a5-a6: order, consolidation, CPU cores).  value = requests/s (whole job).
+  * traces leg (configs[2] = config 3): 4096 Poisson traces x 1000 requests per
+    GPU -> rt_score_key per LM (a1-a4) -> rt_simulate (a5 in-kernel sort, a6
+    consolidation rounds, a7 replay) -> rt_reduce_stats + NCCL all-reduce (a8).
+    Reported as traces/s in "traces".
+Under torchrun each rank runs its own queue / trace shard (replicas / weak
+scaling; the only collective is the int64 stats all-reduce).
+
+L2 hygiene: the inputs of one requests step are ~100 MB (< 126 MB L2), so a
+256 MB buffer is written between timed steps (outside the events).  Timing:
+CUDA events on the launching stream around every step, summed; max over ranks.
+
+--impl reference: the CPU oracle (oracle/, single thread) on a bounded sample
+of the same workload, same metric/unit (the task's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "M requests scored+scheduled/s"
+UNIT = "Mreq/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 20, help="requests per GPU queue (config 2)")
+    ap.add_argument("--traces", type=int, default=4096, help="traces per GPU (config 3)")
+    ap.add_argument("--per-trace", type=int, default=1000)
+    ap.add_argument("--no-traces", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ native arm
+def native(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_06619_b200 as rt
+    from rtgen import configs
+
+    rank, world, local = dist_env()
+    if args.gpus > 1 or world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- inputs (config 2 queue, this rank's gid range)
+    d2 = configs.config2(n=args.n, gid0=rank * args.n)
+    prof = d2["profile"]
+    reg = d2["regressor"]
+    ctx = rt.Context(d2["lexicon"], local)
+    h_bytes = torch.from_numpy(d2["data"]).pin_memory()
+    h_off = torch.from_numpy(d2["offsets"].view(np.int32)).pin_memory()
+    data = h_bytes.to(dev)
+    off = h_off.to(dev)
+    n = args.n
+    total_bytes = int(d2["offsets"][-1])
+    seg = np.asarray([0, n], np.uint32)
+    outs = {"u": torch.empty(n, dtype=torch.float32, device=dev), "key": torch.empty(n, dtype=torch.int64, device=dev)}
+    souts = {"perm": torch.empty(n, dtype=torch.int32, device=dev), "batch_of": torch.empty(n, dtype=torch.int32, device=dev),
+             "slot_of": torch.empty(n, dtype=torch.uint8, device=dev), "core_of": torch.empty(n, dtype=torch.uint8, device=dev),
+             "seg_batch_off": torch.empty(2, dtype=torch.int32, device=dev)}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        ctx.score_key(data, off, reg, prof, want_D=False, out=outs)
+        ev_mid.record(stream)
+        ctx.schedule(outs["key"], outs["u"], seg, prof, out=souts)
+
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_mid = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    t_step, t_score = [], []
+    launches0 = rt.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            ev_a.record(stream)
+            step()
+            ev_b.record(stream)
+            ev_b.synchronize()
+            t_step.append(ev_a.elapsed_time(ev_b))
+            t_score.append(ev_a.elapsed_time(ev_mid))
+        torch.cuda.synchronize()
+        barrier()
+    launches = rt.launch_count() - launches0
+    clocks = clk.summary()
+    sum_ms = max_over_ranks(sum(t_step))
+    score_ms = sum(t_score) / len(t_score)
+    value = world * n * args.steps / (sum_ms / 1e3) / 1e6
+
+    # ---------------- e2e: pinned host -> device, the public calls, device -> host result
+    h_batch = torch.empty(n, dtype=torch.int32).pin_memory()
+    h_slot = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_core = torch.empty(n, dtype=torch.uint8).pin_memory()
+    e2e_ms = []
+    torch.cuda.synchronize()
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        ev_a.record(stream)
+        data.copy_(h_bytes, non_blocking=True)
+        off.copy_(h_off, non_blocking=True)
+        step()
+        h_batch.copy_(souts["batch_of"], non_blocking=True)
+        h_slot.copy_(souts["slot_of"], non_blocking=True)
+        h_core.copy_(souts["core_of"], non_blocking=True)
+        ev_b.record(stream)
+        ev_b.synchronize()
+        e2e_ms.append(ev_a.elapsed_time(ev_b))
+    e2e_sum = max_over_ranks(sum(e2e_ms))
+    e2e_value = world * n * args.steps / (e2e_sum / 1e3) / 1e6
+
+    # ---------------- roofline of the scoring kernel (k_score: the HBM-bound pass)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    alg_bytes = total_bytes + 4 * (n + 1) + 12 * n  # text + offsets + u (4 B) + key (8 B)
+    achieved = alg_bytes / (score_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_score (rt_score_key)", "achieved": round(achieved, 1),
+                "peak": peak_gbs, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
+                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(score_ms, 5),
+                "step_share": round(score_ms / (sum(t_step) / len(t_step)), 4)}
+
+    # ---------------- traces leg (config 3 per GPU)
+    traces = None
+    if not args.no_traces:
+        traces = traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush)
+
+    # ---------------- cpu baseline (oracle, rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_requests_timing(d2, 1 << 18)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(sum_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8+f32", "data": "synthetic",
+            "config": {"workload": "config2: one 2^20-request queue per GPU (DialoGPT profile, all r=0), "
+                                   "score+key+schedule", "requests_per_gpu": n, "bytes_per_gpu": total_bytes,
+                       "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}"},
+            "stage_ms": {"score_key": round(score_ms, 4),
+                         "schedule": round(sum(t_step) / len(t_step) - score_ms, 4)},
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": total_bytes + 4 * (n + 1),
+                    "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_sum / args.steps, 4)},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "clocks": clocks,
+        }
+        if traces is not None:
+            line["traces"] = traces
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):
+    import torch
+    import torch.distributed as dist
+    nt = args.traces
+    per_lm = max(1, nt // 4)
+    first = rank * nt
+    d = configs.traces(3, range(first, first + nt), args.per_trace, lambda t: ((t % nt) // per_lm) % 4)
+    n = len(d["arrival_us"])
+    data = torch.from_numpy(d["data"]).to(dev)
+    off_np = d["offsets"]
+    off = torch.from_numpy(off_np.view(np.int32)).to(dev)
+    arr = torch.from_numpy(d["arrival_us"]).to(dev)
+    tl = torch.from_numpy(d["true_len"].view(np.int16)).to(dev)
+    tp = torch.from_numpy(d["trace_prof"].view(np.int16)).to(dev)
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    key = torch.empty(n, dtype=torch.int64, device=dev)
+    D = torch.empty(n, dtype=torch.int32, device=dev)
+    stats = torch.empty((nt, 2), dtype=torch.int64, device=dev)
+    sums = torch.zeros((4, 3), dtype=torch.int64, device=dev)
+    # contiguous request ranges per LM (traces t*per_lm .. ) -> one score_key launch per LM
+    groups = []
+    for f in range(4):
+        sel = np.nonzero(d["trace_prof"] == f)[0]
+        if len(sel) == 0:
+            continue
+        t0, t1 = int(sel[0]), int(sel[-1]) + 1
+        r0, r1 = int(d["trace_off"][t0]), int(d["trace_off"][t1])
+        sub_off = torch.from_numpy((off_np[r0:r1 + 1] - off_np[r0]).astype(np.uint32).view(np.int32)).to(dev)
+        b0 = int(off_np[r0])
+        align = b0 & ~15
+        groups.append((f, r0, r1, b0, align, sub_off))
+    # score_key requires 16-byte-aligned text: re-base each group's bytes into its own aligned buffer
+    gdata = [data[b0:int(off_np[r1])].clone() for (f, r0, r1, b0, align, so) in groups]
+    grp_of = torch.from_numpy(d["trace_prof"].view(np.int16)).to(dev)
+
+    def step():
+        for (f, r0, r1, b0, align, so), gd in zip(groups, gdata):
+            ctx.score_key(gd, so, d["regressors"][f], d["profiles"][f], arrival=arr[r0:r1],
+                          out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
+        ctx.simulate(arr, tl, u, key, D, d["trace_off"], d["profiles"], tp, stats=stats)
+        sums.zero_()
+        ctx.reduce_stats(stats, grp_of, 4, sums=sums)
+        if world > 1:
+            dist.all_reduce(sums)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev_a.record(stream)
+        step()
+        ev_b.record(stream)
+        ev_b.synchronize()
+        ts.append(ev_a.elapsed_time(ev_b))
+    tsum = max_over_ranks(sum(ts))
+    s = sums.cpu().numpy()
+    mean_resp = [float(s[f, 0]) / max(1, s[f, 1]) / 1e6 for f in range(4)]
+    miss = [float(s[f, 2]) / max(1, s[f, 1]) for f in range(4)]
+    return {"metric": "traces/s", "value": round(world * nt * args.steps / (tsum / 1e3), 1), "unit": "traces/s",
+            "requests_per_s": round(world * n * args.steps / (tsum / 1e3), 1),
+            "ms_per_step": round(tsum / args.steps, 4),
+            "workload": f"config3: {nt} Poisson-ramp traces x {args.per_trace} requests per GPU, 4 LMs, tight, UP+C+O",
+            "mean_response_s_per_lm": [round(x, 4) for x in mean_resp], "miss_ratio_per_lm": [round(x, 4) for x in miss]}
+
+
+def oracle_requests_timing(d2, n_sample: int):
+    """The oracle (single thread, as it stands) on a bounded sample of config 2."""
+    import oracle
+    t0 = time.time()
+    lex = oracle.Lexicon(d2["lexicon"])
+    m = min(n_sample, len(d2["offsets"]) - 1)
+    off = d2["offsets"][: m + 1]
+    data = d2["data"][: int(off[-1])]
+    t1 = time.time()
+    f = oracle.rule_gen(lex, data, off)
+    u = oracle.predict(f, d2["regressor"])
+    k, D = oracle.key(u, f, d2["profile"])
+    oracle.schedule(k, u, np.asarray([0, m], np.uint32), d2["profile"])
+    t2 = time.time()
+    return {"value": round(m / (t2 - t1) / 1e6, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"config 2 prefix queue of {m} requests (score+key+schedule), single thread",
+            "seconds": round(t2 - t1, 3), "lexicon_load_s": round(t1 - t0, 4)}
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from rtgen import configs
+    m = 1 << 17
+    d2 = configs.config2(n=m, gid0=0)
+    lex = oracle.Lexicon(d2["lexicon"])
+    seg = np.asarray([0, m], np.uint32)
+
+    def step():
+        f = oracle.rule_gen(lex, d2["data"], d2["offsets"])
+        u = oracle.predict(f, d2["regressor"])
+        k, D = oracle.key(u, f, d2["profile"])
+        oracle.schedule(k, u, seg, d2["profile"])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.time()
+    for _ in range(args.steps):
+        step()
+    dt = time.time() - t0
+    value = m * args.steps / dt / 1e6
+    sample = f"config 2 prefix queue of {m} requests per step (score+key+schedule), single thread"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8+f32", "data": "synthetic",
+        "config": {"workload": "config2 (oracle sample)", "requests_per_step": m},
+        "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference(args)
+    else:
+        native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -109,6 +109,8 @@ const char* rt_last_error(const rt_ctx* ctx);
 /* Reads and clears the sticky flags (synchronises the device). */
 rt_status rt_get_flags(rt_ctx* ctx, uint32_t* flags);
 int rt_abi_version(void);
+/* Total CUDA kernel launches issued by this library in this process (all contexts). */
+uint64_t rt_launch_count(void);
 /* Number of distinct lexicon lemmas. */
 uint32_t rt_lexicon_size(const rt_ctx* ctx);
 

@@ -24,7 +24,7 @@ INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5}
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
-           "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats"]
+           "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
     L.rt_get_flags.restype = I32
     L.rt_get_flags.argtypes = [V, ctypes.POINTER(U32)]
     L.rt_abi_version.restype = I32
+    L.rt_launch_count.restype = ctypes.c_uint64
     L.rt_lexicon_size.restype = U32
     L.rt_lexicon_size.argtypes = [V]
     L.rt_score.restype = I32
@@ -112,6 +113,11 @@ def load_library(path: str = LIB_PATH):
     L.rt_reduce_stats.argtypes = [V, P, U32, P, U32, P, V]
     _lib = L
     return L
+
+
+def launch_count() -> int:
+    """Kernel launches issued by librtlm.so so far (this process)."""
+    return int(load_library().rt_launch_count())
 
 
 def _torch():

@@ -1,5 +1,6 @@
 // api.cu — the C ABI of include/rtlm.h: context, lexicon upload, argument
 // validation, workspace, launches.  No compute happens on the host.
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -22,6 +23,11 @@ struct rt_ctx {
   size_t prof_cap = 0;
   std::string err;
 };
+
+namespace rtlm {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(unsigned k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace rtlm
 
 namespace {
 
@@ -302,6 +308,8 @@ cudaStream_t cs(rt_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 extern "C" {
 
 int rt_abi_version(void) { return RTLM_ABI_VERSION; }
+
+uint64_t rt_launch_count(void) { return rtlm::g_launches.load(); }
 
 rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** out) {
   if (!out) return RT_EINVAL;

@@ -59,6 +59,8 @@ constexpr uint32_t kMaxTrace = 1024;     // tasks per replayed trace
 constexpr uint32_t kMaxCores = 32;
 
 // ---------------------------------------------------------------- launchers
+// Every kernel launch of the library is counted (rt_launch_count).
+void note_launch(unsigned k = 1);
 struct ScoreLaunch {
   const uint8_t* bytes;
   const uint32_t* offsets;

@@ -279,6 +279,7 @@ cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_replay<<<a.nt, 32, smem, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -288,6 +289,7 @@ cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uin
   uint32_t blocks = (nt + 255) / 256;
   if (blocks > 1184) blocks = 1184;
   k_reduce_stats<<<blocks, 256, 0, s>>>(st, nt, grp, ngroups, sums);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -279,6 +279,7 @@ __global__ void k_batch_fix(uint32_t* __restrict__ batch_of, const uint32_t* __r
 cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s) {
   if (!a.nq) return cudaSuccess;
   k_sched_small<<<a.nq, kSmallThreads, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -290,12 +291,17 @@ cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
   cudaMemsetAsync(ncpu, 0, sizeof(uint32_t), s);
   k_gather<<<(n + 255) / 256, 256, 0, s>>>(a.perm, a.u, a.key, lo, n, u_sorted, ncpu);
   k_sched_big<<<1, 64, 0, s>>>(a, q, lo, n, u_sorted, ncpu);
+  note_launch(2);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sched_finish(const SchedLaunch& a, cudaStream_t s) {
   k_seg_scan<<<1, 1024, 0, s>>>(a.seg_count, a.nq, a.seg_batch_off);
-  if (a.nq > 1) k_batch_fix<<<1184, 256, 0, s>>>(a.batch_of, a.seg_off, a.nq, a.seg_batch_off);
+  note_launch();
+  if (a.nq > 1) {
+    k_batch_fix<<<1184, 256, 0, s>>>(a.batch_of, a.seg_off, a.nq, a.seg_batch_off);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

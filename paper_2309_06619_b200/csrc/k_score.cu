@@ -358,12 +358,14 @@ cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   uint32_t grid = (uint32_t)(a.num_sms * per_sm);
   if (grid > ntiles) grid = ntiles;
   k_score<<<grid, kThreads, smem, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_predict(const uint16_t* feat, uint32_t n, const rt_regressor& reg, float* u, cudaStream_t s) {
   if (!n) return cudaSuccess;
   k_predict<<<(n + 255) / 256, 256, 0, s>>>(feat, n, reg, u);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -371,6 +373,7 @@ cudaError_t launch_key(const float* u, const uint16_t* feat, const int64_t* arr,
                        const rt_profile& p, uint64_t* key, uint32_t* D_out, cudaStream_t s) {
   if (!n) return cudaSuccess;
   k_key<<<(n + 255) / 256, 256, 0, s>>>(u, feat, arr, D_in, n, p, key, D_out);
+  note_launch();
   return cudaGetLastError();
 }
 

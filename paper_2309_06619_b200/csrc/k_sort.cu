@@ -135,6 +135,7 @@ cudaError_t radix_sort_desc(const uint64_t* keys_in, uint32_t base_index, uint32
     k_hist<<<ntiles, kThreads, 0, s>>>(ksrc, n, shift, ntiles, hist);
     k_scan<<<1, 1024, 0, s>>>(hist, 256 * ntiles);
     k_scatter<<<ntiles, kThreads, 0, s>>>(ksrc, vsrc, base_index, n, shift, ntiles, hist, kdst, vdst);
+    note_launch(3);
     ksrc = kdst;
     vsrc = vdst;
   }

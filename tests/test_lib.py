@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "rtlm.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:rt_status|const char\*|int|uint32_t)\s+(rt_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:rt_status|const char\*|int|uint32_t|uint64_t)\s+(rt_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_header_symbols():
