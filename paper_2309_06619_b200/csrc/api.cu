@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/rtlm.h: context, lexicon upload, argument
 // validation, workspace, launches.  No compute happens on the host.
 #include <atomic>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -21,6 +22,8 @@ struct rt_ctx {
   size_t off_cap = 0;
   rt_profile* d_prof = nullptr;
   size_t prof_cap = 0;
+  cudaStream_t aux = nullptr;  // internal fork stream (CPU-class list scheduling)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
 };
 
@@ -325,6 +328,9 @@ rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** o
   RT_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   RT_CUDA(c, cudaMalloc(&c->d_flags, sizeof(uint32_t)));
   RT_CUDA(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)));
+  RT_CUDA(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   if (!lexicon_text && len) return fail(c, RT_EINVAL, "lexicon_text is NULL");
   return upload_lexicon(c, lexicon_text ? lexicon_text : "", len);
 }
@@ -339,6 +345,9 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->ws);
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->aux) cudaStreamDestroy(c->aux);
   }
   delete c;
   return RT_OK;
@@ -456,7 +465,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   for (uint32_t q = 0; q < nq; ++q) {
     const uint32_t m = h_seg_off[q + 1] - h_seg_off[q];
     if (m > rtlm::kSmallSeg) {
-      size_t need = rtlm::radix_sort_workspace(m) + ((size_t)m + 128) * 4;
+      size_t need = std::max(rtlm::radix_sort_workspace(m), rtlm::ff_workspace(m, rtlm::ff_levels(m)));
       if (need > big_ws) big_ws = need;
     }
   }
@@ -485,11 +494,10 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   for (uint32_t q = 0; q < nq; ++q) {
     const uint32_t lo = h_seg_off[q], hi = h_seg_off[q + 1];
     if (hi - lo <= rtlm::kSmallSeg) continue;
-    const size_t sort_ws = rtlm::radix_sort_workspace(hi - lo);
     e = rtlm::radix_sort_desc(d_key + lo, lo, hi - lo, d_perm + lo, full64, big, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "radix_sort_desc");
-    e = rtlm::launch_sched_big(a, q, lo, hi, reinterpret_cast<float*>(big + sort_ws), s);
-    if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_big");
+    e = rtlm::launch_ff(a, q, lo, hi, big, s, c->aux, c->ev_fork, c->ev_join);
+    if (e != cudaSuccess) return cuda_fail(c, e, "k_ff");
   }
   e = rtlm::launch_sched_finish(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_finish");

@@ -1,0 +1,766 @@
+// k_ff.cu — parallel exact one-pass consolidation of ONE large queue
+// (§8(a) row a6, Alg. 1 P:467-481 with R-CONS/R-CARRY/R-FLUSH), DESIGN.md §7.
+//
+// Reformulation (proved in DESIGN.md §7 "K4-FF"):  let S be the GPU-class
+// stream in priority order, x ≺ y the window order (u, then rank), K = m - C.
+// While windows are full, the carry after every cut-free round equals
+// topK_≺(consumed prefix), so every element becomes *ready* exactly when it
+// is evicted from a streaming top-K heap: the ready sequence Rseq (one element
+// per consumed position) is computed in parallel (chunk top-K summaries, a
+// scan of summaries, per-chunk heap replays).  O6 then equals the "R-process"
+// on Rseq: A = L ∪ next (C - |L|) ready elements; emit the λ-prefix of sorted
+// A (<= C); L = rest.  From an empty L (an "∅-point" z) the next round is the
+// aligned chunk Rseq[z, z+C): if it passes the λ chain the process is at ∅
+// again at z + C.  So the trajectory is ∅-runs of aligned chunks separated by
+// "excursions" that start at failing chunks.  We evaluate pass(j) for every j,
+// simulate the excursion from every failing position in parallel, link
+// failing positions into a successor forest, find the trajectory's path by
+// pointer doubling, and emit ∅-run chunks and path excursions in parallel.
+// The last partial windows (stream exhausted) are finished by one warp (tail).
+#include "internal.cuh"
+
+namespace rtlm {
+namespace {
+
+constexpr uint32_t KS = 128;         // row stride of K-lists (K <= 127)
+constexpr uint32_t B1 = 1024;        // heap-replay chunk
+constexpr uint32_t kEnd = 0xFFFFFFFFu;
+constexpr uint64_t kInf = 0xFFFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ float kk_u(uint64_t k) { return __uint_as_float((uint32_t)(k >> 32) & 0x7FFFFFFFu); }
+__device__ __forceinline__ uint32_t kk_p(uint64_t k) { return (uint32_t)k; }
+
+struct FF {
+  // inputs
+  const uint32_t* perm;   // queue-relative priority order (global indices), CPU class first
+  const float* u;
+  const uint64_t* key;
+  uint32_t n;             // queue length
+  uint32_t K, C, m;
+  float lambda;
+  // device scalars
+  uint32_t* scal;         // [0] ncpu, [1] G, [2] NR, [3] nfail, [4] nruns, [5] total batches, [6] path_len
+  // buffers
+  uint64_t* kk;           // G
+  uint64_t* rseq;         // NR
+  uint64_t* summ;         // nc1 * KS
+  uint64_t* heapH;        // nc1 * KS  (exclusive prefix top-K per chunk)
+  uint64_t* hfinal;       // KS
+  uint32_t* passbm;       // bitmap, bit j = pass(j)
+  uint32_t* failpos;      // nfail (sorted)
+  uint32_t* exE;          // excursion end ∅-point (kEnd = reached the stream end)
+  uint32_t* exR;          // rounds inside the excursion
+  uint32_t* nxt;          // levels * (nfail + 1)
+  uint32_t* wr;           // levels * (nfail + 1)
+  uint32_t* runz;         // per fail i (and start node nfail): ∅-point after the excursion
+  uint32_t* runn;         // chunks of the ∅-run
+  uint32_t* path_node;    // path nodes (unordered)
+  uint32_t* path_off;     // batch offset at the node's excursion start
+  uint32_t* run_z;        // sorted ∅-runs: start
+  uint32_t* run_n;        // chunks
+  uint32_t* run_b;        // first batch id
+  uint32_t levels;
+  uint32_t* batch_of;
+  uint8_t* slot_of;
+  uint8_t* core_of;
+  uint32_t* seg_count_q;  // &seg_count[q]
+};
+
+// ------------------------------------------------------------ 1. gather
+__global__ void k_ff_gather(FF f) {
+  const uint32_t ncpu = f.scal[0], G = f.n - ncpu;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < G; p += gridDim.x * blockDim.x) {
+    const float uu = f.u[f.perm[ncpu + p]];
+    f.kk[p] = ((uint64_t)ord32_bits(__float_as_uint(uu)) << 32) | p;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    f.scal[1] = G;
+    f.scal[2] = G > f.K ? G - f.K : 0u;
+  }
+}
+
+// count the CPU class (a prefix of the sorted queue)
+__global__ void k_ff_ncpu(FF f) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < f.n; j += gridDim.x * blockDim.x) {
+    const bool cpu = (f.key[f.perm[j]] >> 63) != 0;
+    const bool next_gpu = (j + 1 == f.n) || ((f.key[f.perm[j + 1]] >> 63) == 0);
+    if (cpu && next_gpu) f.scal[0] = j + 1;
+  }
+}
+
+// ------------------------------------------------------------ 2. ready sequence
+// 2a: top-K (descending) of every chunk of B1 positions
+__global__ void __launch_bounds__(256) k_ff_topk(FF f) {
+  __shared__ uint64_t s[B1];
+  const uint32_t G = f.scal[1];
+  const uint32_t c = blockIdx.x, p0 = c * B1;
+  if (p0 >= G) return;
+  for (uint32_t i = threadIdx.x; i < B1; i += 256) s[i] = p0 + i < G ? f.kk[p0 + i] : 0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= B1; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < B1; i += 256) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t a = s[i], b = s[l];
+          const bool desc = (i & k) == 0;
+          if (desc ? (a < b) : (a > b)) { s[i] = b; s[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (uint32_t i = threadIdx.x; i < KS; i += 256) f.summ[(size_t)c * KS + i] = i < f.K ? s[i] : 0ull;
+}
+
+// merge two descending K-lists (smem) into their top-K (smem out); one warp.
+// Real keys are unique; zero padding may collide only with zeros.
+__device__ void merge_topk(const uint64_t* A, const uint64_t* B, uint64_t* O, uint32_t K) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t i = lane; i < K; i += 32) {
+    const uint64_t a = A[i];
+    uint32_t lo = 0, hi = K;  // #(B > a)
+    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (B[md] > a) lo = md + 1; else hi = md; }
+    if (i + lo < K) O[i + lo] = a;
+    const uint64_t b = B[i];
+    lo = 0; hi = K;           // #(A > b)
+    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (A[md] > b) lo = md + 1; else hi = md; }
+    if (i + lo < K) O[i + lo] = b;
+  }
+  __syncwarp();
+}
+
+// 2b: exclusive prefix top-K over chunks (one CTA of 32 warps)
+__global__ void __launch_bounds__(1024) k_ff_scan(FF f, uint64_t* loc) {
+  extern __shared__ __align__(16) uint64_t buf_raw[];
+  uint64_t (*buf)[3][KS] = reinterpret_cast<uint64_t (*)[3][KS]>(buf_raw);
+  const uint32_t G = f.scal[1];
+  const uint32_t nc = (G + B1 - 1) / B1;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u, K = f.K;
+  const uint32_t gs = (nc + 31) / 32;
+  const uint32_t c0 = w * gs, c1 = min(nc, c0 + gs);
+  uint64_t* acc = buf[w][0];
+  uint64_t* tmp = buf[w][1];
+  uint64_t* nx = buf[w][2];
+  for (uint32_t i = lane; i < KS; i += 32) acc[i] = 0ull;
+  __syncwarp();
+  // level 1: inclusive running top-K inside the group
+  for (uint32_t c = c0; c < c1; ++c) {
+    for (uint32_t i = lane; i < KS; i += 32) tmp[i] = f.summ[(size_t)c * KS + i];
+    __syncwarp();
+    for (uint32_t i = lane; i < KS; i += 32) nx[i] = 0ull;
+    __syncwarp();
+    merge_topk(acc, tmp, nx, K);
+    for (uint32_t i = lane; i < KS; i += 32) { acc[i] = nx[i]; loc[(size_t)c * KS + i] = nx[i]; }
+    __syncwarp();
+  }
+  __syncthreads();
+  // level 2: warp 0 computes the exclusive prefix of group totals into buf[g][0]
+  if (w == 0) {
+    uint64_t* run = buf[0][1];
+    uint64_t* t2 = buf[0][2];
+    for (uint32_t i = lane; i < KS; i += 32) run[i] = 0ull;
+    __syncwarp();
+    for (uint32_t g = 0; g < 32; ++g) {
+      const uint32_t gc0 = g * gs, gc1 = min(nc, gc0 + gs);
+      // group g's exclusive prefix = run; stash into heapH of its first chunk (if any)
+      if (gc0 < gc1)
+        for (uint32_t i = lane; i < KS; i += 32) f.heapH[(size_t)gc0 * KS + i] = run[i];
+      __syncwarp();
+      if (gc0 < gc1) {
+        // run = merge(run, loc[last of group])
+        uint64_t* lastl = buf[1][0];  // scratch (warp 1 finished level 1)
+        for (uint32_t i = lane; i < KS; i += 32) lastl[i] = loc[(size_t)(gc1 - 1) * KS + i];
+        __syncwarp();
+        for (uint32_t i = lane; i < KS; i += 32) t2[i] = 0ull;
+        __syncwarp();
+        merge_topk(run, lastl, t2, K);
+        for (uint32_t i = lane; i < KS; i += 32) run[i] = t2[i];
+        __syncwarp();
+      }
+    }
+    // the overall top-K = final heap (elements never ready)
+    for (uint32_t i = lane; i < KS; i += 32) f.hfinal[i] = run[i];
+  }
+  __syncthreads();
+  // level 3: H[c] = merge(groupprefix, loc[c-1]) for c > c0 in the group
+  if (c0 < c1) {
+    uint64_t* gp = buf[w][0];
+    for (uint32_t i = lane; i < KS; i += 32) gp[i] = f.heapH[(size_t)c0 * KS + i];
+    __syncwarp();
+    for (uint32_t c = c0 + 1; c < c1; ++c) {
+      for (uint32_t i = lane; i < KS; i += 32) { tmp[i] = loc[(size_t)(c - 1) * KS + i]; nx[i] = 0ull; }
+      __syncwarp();
+      merge_topk(gp, tmp, nx, K);
+      for (uint32_t i = lane; i < KS; i += 32) f.heapH[(size_t)c * KS + i] = nx[i];
+      __syncwarp();
+    }
+  }
+}
+
+// 2c: per-chunk streaming heap replay -> Rseq (evictions).  Heap slots s =
+// t*32 + lane, ascending; unused slots (>= K) hold +inf.
+template <int SPL>
+__global__ void __launch_bounds__(128) k_ff_replay(FF f) {
+  const uint32_t G = f.scal[1], K = f.K;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  const uint32_t p0 = warp * B1;
+  if (p0 >= G) return;
+  const uint32_t p1 = min(G, p0 + B1);
+  uint64_t h[SPL];
+#pragma unroll
+  for (int t = 0; t < SPL; ++t) {
+    const uint32_t s = t * 32 + lane;
+    h[t] = s < K ? f.heapH[(size_t)warp * KS + (K - 1 - s)] : kInf;
+  }
+  for (uint32_t pb = p0; pb < p1; pb += 32) {
+    const uint64_t mine = pb + lane < p1 ? f.kk[pb + lane] : 0ull;
+    const uint32_t cnt = min(32u, p1 - pb);
+    uint64_t outv = 0;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint64_t x = __shfl_sync(0xFFFFFFFFu, mine, i);
+      uint32_t c = 0;
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) c += __popc(__ballot_sync(0xFFFFFFFFu, h[t] < x));
+      const uint64_t h0 = __shfl_sync(0xFFFFFFFFu, h[0], 0);
+      // shift slots [1, c) down by one, x into slot c-1
+      uint64_t nh[SPL];
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) {
+        uint64_t up = __shfl_down_sync(0xFFFFFFFFu, h[t], 1);
+        const uint64_t wrap = (t + 1 < SPL) ? __shfl_sync(0xFFFFFFFFu, h[t + 1 < SPL ? t + 1 : t], 0) : kInf;
+        if (lane == 31) up = wrap;
+        const uint32_t sl = t * 32 + lane;
+        nh[t] = (sl + 1 < c) ? up : ((sl + 1 == c) ? x : h[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < SPL; ++t) h[t] = nh[t];
+      if (lane == i) outv = c ? h0 : x;  // evicted element of position pb + i
+    }
+    const uint32_t q = pb + lane;
+    if (lane < cnt && q >= K) f.rseq[q - K] = outv;
+  }
+}
+
+// K == 0: every element is ready at its own position
+__global__ void k_ff_copy(FF f) {
+  const uint32_t G = f.scal[1];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < G; p += gridDim.x * blockDim.x) f.rseq[p] = f.kk[p];
+  if (blockIdx.x == 0 && threadIdx.x == 0) f.hfinal[0] = 0ull;
+}
+
+// ------------------------------------------------------------ 3. pass(j)
+// pass(j): sorted Rseq[j, j+C) has every adjacent ratio <= lambda.
+__global__ void __launch_bounds__(256) k_ff_pass(FF f) {
+  __shared__ uint64_t t[256 + kMaxWindow];
+  const uint32_t NR = f.scal[2], C = f.C;
+  const uint32_t j0 = blockIdx.x * 256u;
+  const uint32_t j = j0 + threadIdx.x;
+  const uint32_t nwords = (NR + 31) / 32 + 1;
+  if (j0 >= nwords * 32) return;  // block-uniform
+  for (uint32_t i = threadIdx.x; i < 256 + C; i += 256) t[i] = j0 + i < NR ? f.rseq[j0 + i] : 0ull;
+  __syncthreads();
+  bool ok = false;
+  if (j + C <= NR) {
+    ok = true;
+    // every element but the minimum must be <= lambda * (its predecessor in the window)
+    const uint64_t* w = t + threadIdx.x;
+    for (uint32_t a = 0; a < C; ++a) {
+      const uint64_t xa = w[a];
+      uint64_t pred = 0;
+      for (uint32_t b = 0; b < C; ++b) {
+        const uint64_t xb = w[b];
+        pred = (xb < xa && xb > pred) ? xb : pred;
+      }
+      ok &= (pred == 0) || (kk_u(xa) <= __fmul_rn(f.lambda, kk_u(pred)));
+    }
+  }
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
+  if ((threadIdx.x & 31u) == 0 && j < nwords * 32) f.passbm[j >> 5] = bal;
+}
+
+__device__ __forceinline__ bool pass_at(const uint32_t* bm, uint32_t j) { return (bm[j >> 5] >> (j & 31u)) & 1u; }
+
+// compact failing positions (j + C <= NR and !pass)
+__global__ void k_ff_failcount(FF f, uint32_t* blocksum) {
+  const uint32_t NR = f.scal[2], C = f.C;
+  const uint32_t lim = NR >= C ? NR - C + 1 : 0u;  // positions with a full chunk
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool fl = j < lim && !pass_at(f.passbm, j);
+  const uint32_t c = __syncthreads_count(fl);
+  if (threadIdx.x == 0) blocksum[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(1024) k_ff_blockscan(uint32_t* blocksum, uint32_t nb, uint32_t* total) {
+  __shared__ uint32_t part[1024];
+  const uint32_t per = (nb + 1023) / 1024;
+  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, nb);
+  uint32_t s = 0;
+  for (uint32_t i = lo; i < hi; ++i) s += blocksum[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    uint32_t v = threadIdx.x >= (uint32_t)d ? part[threadIdx.x - d] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+  for (uint32_t i = lo; i < hi; ++i) {
+    uint32_t v = blocksum[i];
+    blocksum[i] = run;
+    run += v;
+  }
+  if (threadIdx.x == 1023) *total = part[1023];
+}
+
+__global__ void k_ff_failwrite(FF f, const uint32_t* blockoff) {
+  __shared__ uint32_t wsum[32];
+  const uint32_t NR = f.scal[2], C = f.C;
+  const uint32_t lim = NR >= C ? NR - C + 1 : 0u;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool fl = j < lim && !pass_at(f.passbm, j);
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, fl);
+  if (lane == 0) wsum[w] = __popc(bal);
+  __syncthreads();
+  uint32_t base = blockoff[blockIdx.x];
+  for (uint32_t i = 0; i < w; ++i) base += wsum[i];
+  if (fl) f.failpos[base + __popc(bal & ((1u << lane) - 1u))] = j;
+}
+
+// ------------------------------------------------------------ 4. R-process warp
+// One round on state (L: ascending kk in smem, lc; j).  A = L ∪ Rseq[j, j+need).
+// Emits via callback; returns cnt.  Requires j + need <= NR (full round) unless
+// `partial` (tail), where A = L ∪ Rseq[j, NR) ∪ extra.
+struct Warp3 {
+  uint64_t* L;  // capacity kMaxWindow
+  uint64_t* A;
+  uint64_t* S;
+};
+
+template <class Emit>
+__device__ __forceinline__ uint32_t r_round(const FF& f, Warp3 w, uint32_t& lc, uint32_t& j, uint32_t na,
+                                            Emit emit) {
+  // na = |A| = lc + new elements (taken from Rseq[j, j + na - lc))
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t need = na - lc;
+  for (uint32_t i = lane; i < na; i += 32) w.A[i] = i < lc ? w.L[i] : f.rseq[j + (i - lc)];
+  __syncwarp();
+  for (uint32_t i = lane; i < na; i += 32) {
+    const uint64_t x = w.A[i];
+    uint32_t pos = 0;
+    for (uint32_t b = 0; b < na; ++b) pos += w.A[b] < x;
+    w.S[pos] = x;
+  }
+  __syncwarp();
+  const uint32_t lim = min(f.C, na);
+  uint32_t cnt = lim;
+  for (uint32_t base = 1; base < lim; base += 32) {
+    const uint32_t i = base + lane;
+    const bool bad = i < lim && !(kk_u(w.S[i]) <= __fmul_rn(f.lambda, kk_u(w.S[i - 1])));
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+    if (bal) { cnt = base + __ffs(bal) - 1; break; }
+  }
+  for (uint32_t i = lane; i < cnt; i += 32) emit(w.S[i], i);
+  for (uint32_t i = lane; i < na - cnt; i += 32) w.L[i] = w.S[cnt + i];
+  lc = na - cnt;
+  j += need;
+  __syncwarp();
+  return cnt;
+}
+
+// ------------------------------------------------------------ 5. excursions
+// For every failing position: run from (∅, f) until L is empty again (exE, exR),
+// or until a full round is impossible (exE = kEnd).
+__global__ void __launch_bounds__(128) k_ff_excursion(FF f) {
+  __shared__ uint64_t sm[4][3][kMaxWindow];
+  const uint32_t wl = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nfail = f.scal[3], NR = f.scal[2];
+  if (gw >= nfail) return;
+  Warp3 w{sm[wl][0], sm[wl][1], sm[wl][2]};
+  uint32_t lc = 0, j = f.failpos[gw], r = 0;
+  for (;;) {
+    const uint32_t need = f.C - lc;
+    if (j + need > NR) { r = r; break; }
+    r_round(f, w, lc, j, f.C, [](uint64_t, uint32_t) {});
+    ++r;
+    if (lc == 0) break;
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    f.exE[gw] = lc == 0 ? j : kEnd;
+    f.exR[gw] = r;
+  }
+}
+
+// ∅-run from z: chunks at z + tC while pass; returns (first fail index or kEnd, #chunks)
+__device__ void run_from(const FF& f, uint32_t z, uint32_t& fail_idx, uint32_t& nch) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t NR = f.scal[2], C = f.C, nfail = f.scal[3];
+  uint32_t t = 0;
+  for (;;) {
+    const uint32_t jj = z + (t + lane) * C;
+    const bool full = jj + C <= NR;
+    const bool fail = full && !pass_at(f.passbm, jj);
+    const uint32_t bf = __ballot_sync(0xFFFFFFFFu, fail);
+    const uint32_t bn = __ballot_sync(0xFFFFFFFFu, !full);
+    if (bf | bn) {
+      const uint32_t first_f = bf ? __ffs(bf) - 1 : 32u;
+      const uint32_t first_n = bn ? __ffs(bn) - 1 : 32u;
+      if (first_f < first_n) {
+        nch = t + first_f;
+        const uint32_t pos = z + nch * C;
+        // binary search pos in failpos
+        uint32_t lo = 0, hi = nfail;
+        while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.failpos[md] < pos) lo = md + 1; else hi = md; }
+        fail_idx = lo;
+      } else {
+        nch = t + first_n;
+        fail_idx = kEnd;
+      }
+      return;
+    }
+    t += 32;
+  }
+}
+
+// successor of every node: node i < nfail = failing position; node nfail = start (∅ at 0)
+__global__ void __launch_bounds__(128) k_ff_link(FF f) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nfail = f.scal[3];
+  if (gw > nfail) return;
+  uint32_t z, r0;
+  if (gw == nfail) { z = 0; r0 = 0; }
+  else { z = f.exE[gw]; r0 = f.exR[gw]; }
+  uint32_t fi = kEnd, nch = 0;
+  if (z != kEnd) run_from(f, z, fi, nch);
+  if ((threadIdx.x & 31u) == 0) {
+    f.nxt[gw] = fi;
+    f.wr[gw] = r0 + nch;
+    f.runz[gw] = z;
+    f.runn[gw] = nch;
+  }
+}
+
+// pointer doubling level k from k-1
+__global__ void k_ff_double(FF f, uint32_t k) {
+  const uint32_t nn = f.scal[3] + 1;
+  const uint32_t* n0 = f.nxt + (size_t)(k - 1) * nn;
+  const uint32_t* w0 = f.wr + (size_t)(k - 1) * nn;
+  uint32_t* n1 = f.nxt + (size_t)k * nn;
+  uint32_t* w1 = f.wr + (size_t)k * nn;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+    const uint32_t a = n0[i];
+    if (a == kEnd) { n1[i] = kEnd; w1[i] = w0[i]; }
+    else { n1[i] = n0[a]; w1[i] = w0[i] + w0[a]; }
+  }
+}
+
+// expand the path from the start node (levels high -> low), one CTA
+__global__ void __launch_bounds__(1024) k_ff_expand(FF f) {
+  __shared__ uint32_t cnt;
+  const uint32_t nn = f.scal[3] + 1;
+  if (threadIdx.x == 0) {
+    cnt = 1;
+    f.path_node[0] = nn - 1;
+    f.path_off[0] = 0;
+  }
+  __syncthreads();
+  for (int k = (int)f.levels - 1; k >= 0; --k) {
+    const uint32_t cur = cnt;
+    __syncthreads();
+    const uint32_t* nk = f.nxt + (size_t)k * nn;
+    const uint32_t* wk = f.wr + (size_t)k * nn;
+    for (uint32_t i = threadIdx.x; i < cur; i += blockDim.x) {
+      const uint32_t x = f.path_node[i];
+      const uint32_t y = nk[x];
+      if (y != kEnd) {
+        const uint32_t slot = atomicAdd(&cnt, 1u);
+        f.path_node[slot] = y;
+        f.path_off[slot] = f.path_off[i] + wk[x];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) f.scal[6] = cnt;
+}
+
+// ∅-run table in path-list order: run_z (start), run_b (first batch id),
+// run_n = exclusive prefix of chunk counts; total chunks -> scal[4].  One CTA.
+__global__ void __launch_bounds__(1024) k_ff_runs(FF f) {
+  __shared__ uint32_t part[1024];
+  const uint32_t np = f.scal[6], nfail = f.scal[3];
+  const uint32_t per = (np + 1023) / 1024;
+  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, np);
+  uint32_t sum = 0;
+  for (uint32_t i = lo; i < hi; ++i) sum += f.runn[f.path_node[i]];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    uint32_t v = threadIdx.x >= (uint32_t)d ? part[threadIdx.x - d] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t x = f.path_node[i];
+    f.run_z[i] = f.runz[x];
+    f.run_b[i] = f.path_off[i] + (x == nfail ? 0u : f.exR[x]);
+    f.run_n[i] = run;
+    run += f.runn[x];
+  }
+  if (threadIdx.x == 1023) f.scal[4] = part[1023];
+}
+
+// emit the ∅-run chunks: one thread per (chunk, element)
+__global__ void k_ff_emit_runs(FF f) {
+  const uint32_t np = f.scal[6], T = f.scal[4], C = f.C, ncpu = f.scal[0];
+  const uint64_t total = (uint64_t)T * C;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t ch = (uint32_t)(g / C), i = (uint32_t)(g % C);
+    uint32_t lo = 0, hi = np;  // last path index with run_n <= ch
+    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.run_n[md] <= ch) lo = md + 1; else hi = md; }
+    const uint32_t r = lo - 1;
+    const uint32_t t = ch - f.run_n[r];
+    const uint32_t s0 = f.run_z[r] + t * C;
+    const uint64_t x = f.rseq[s0 + i];
+    uint32_t slot = 0;
+    for (uint32_t b = 0; b < C; ++b) slot += f.rseq[s0 + b] < x;
+    const uint32_t gi = f.perm[ncpu + kk_p(x)];
+    f.batch_of[gi] = f.run_b[r] + t;
+    f.slot_of[gi] = (uint8_t)slot;
+    f.core_of[gi] = 0xFF;
+  }
+}
+
+// re-run every path excursion and emit its batches
+__global__ void __launch_bounds__(128) k_ff_emit_exc(FF f) {
+  __shared__ uint64_t sm[4][3][kMaxWindow];
+  const uint32_t wl = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2], ncpu = f.scal[0];
+  if (gw >= np) return;
+  const uint32_t x = f.path_node[gw];
+  if (x == nfail) return;  // start node: no excursion
+  Warp3 w{sm[wl][0], sm[wl][1], sm[wl][2]};
+  uint32_t lc = 0, j = f.failpos[x], b = f.path_off[gw];
+  for (;;) {
+    const uint32_t need = f.C - lc;
+    if (j + need > NR) break;
+    const uint32_t bb = b;
+    r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) {
+      const uint32_t g = f.perm[ncpu + kk_p(e)];
+      f.batch_of[g] = bb;
+      f.slot_of[g] = (uint8_t)slot;
+      f.core_of[g] = 0xFF;
+    });
+    ++b;
+    if (lc == 0) break;
+  }
+}
+
+// tail: find the path end, rebuild its final state, finish with partial windows
+__global__ void __launch_bounds__(32) k_ff_tail(FF f) {
+  __shared__ uint64_t L[2 * kMaxWindow], A[2 * kMaxWindow], S[2 * kMaxWindow];
+  __shared__ uint32_t s_last, s_off;
+  const uint32_t lane = threadIdx.x;
+  const uint32_t NR = f.scal[2], nfail = f.scal[3], np = f.scal[6], ncpu = f.scal[0], G = f.scal[1];
+  if (lane == 0) {
+    s_last = kEnd;
+    s_off = 0;
+  }
+  __syncwarp();
+  // the path node whose successor is END
+  for (uint32_t i = lane; i < np; i += 32) {
+    const uint32_t x = f.path_node[i];
+    if (f.nxt[x] == kEnd) { s_last = x; s_off = f.path_off[i]; }
+  }
+  __syncwarp();
+  uint32_t lc = 0, j = 0, b = 0;
+  const uint32_t x = s_last;
+  if (G > f.K && x != kEnd) {
+    b = s_off;
+    const uint32_t ex_end = (x == nfail) ? 0u : f.exE[x];
+    if (x != nfail && ex_end == kEnd) {
+      // the excursion itself reaches the stream end: replay it to get (L, j)
+      Warp3 w{L, A, S};
+      j = f.failpos[x];
+      for (;;) {
+        const uint32_t need = f.C - lc;
+        if (j + need > NR) break;
+        const uint32_t bb = b;
+        r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) {
+          const uint32_t g = f.perm[ncpu + kk_p(e)];
+          f.batch_of[g] = bb; f.slot_of[g] = (uint8_t)slot; f.core_of[g] = 0xFF;
+        });
+        ++b;
+      }
+    } else {
+      b = s_off + f.wr[x];  // excursion + ∅-run rounds (level 0)
+      j = f.runz[x] + f.runn[x] * f.C;
+      lc = 0;
+    }
+  }
+  // remaining: L ∪ Rseq[j, NR) ∪ final heap (non-zero)
+  uint32_t na = lc;
+  for (uint32_t i = lane; i < NR - j; i += 32) A[lc + i] = f.rseq[j + i];
+  for (uint32_t i = lane; i < lc; i += 32) A[i] = L[i];
+  na += NR - j;
+  __syncwarp();
+  // final heap entries (exactly min(K, G) real ones)
+  const uint32_t nh = min(f.K, G);
+  for (uint32_t i = lane; i < nh; i += 32) A[na + i] = f.hfinal[i];
+  na += nh;
+  __syncwarp();
+  while (na) {
+    for (uint32_t i = lane; i < na; i += 32) {
+      const uint64_t v = A[i];
+      uint32_t pos = 0;
+      for (uint32_t q = 0; q < na; ++q) pos += A[q] < v;
+      S[pos] = v;
+    }
+    __syncwarp();
+    const uint32_t lim = min(f.C, na);
+    uint32_t cnt = lim;
+    for (uint32_t base = 1; base < lim; base += 32) {
+      const uint32_t i = base + lane;
+      const bool bad = i < lim && !(kk_u(S[i]) <= __fmul_rn(f.lambda, kk_u(S[i - 1])));
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+      if (bal) { cnt = base + __ffs(bal) - 1; break; }
+    }
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const uint32_t g = f.perm[ncpu + kk_p(S[i])];
+      f.batch_of[g] = b; f.slot_of[g] = (uint8_t)i; f.core_of[g] = 0xFF;
+    }
+    for (uint32_t i = lane; i < na - cnt; i += 32) A[i] = S[cnt + i];
+    na -= cnt;
+    ++b;
+    __syncwarp();
+  }
+  if (lane == 0) *f.seg_count_q = b;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host side
+size_t ff_workspace(uint32_t n, uint32_t levels) {
+  const size_t nc1 = (n + B1 - 1) / B1 + 1;
+  size_t s = 0;
+  auto add = [&](size_t bytes) { s += (bytes + 255) & ~size_t(255); };
+  add(64);                       // scal
+  add((size_t)n * 8);            // kk
+  add((size_t)n * 8);            // rseq
+  add(nc1 * KS * 8 * 3);         // summ, heapH, loc
+  add(KS * 8);                   // hfinal
+  add(((size_t)n / 32 + 2) * 4); // passbm
+  add((size_t)n * 4 * 3);        // failpos, exE, exR
+  add((size_t)(n + 1) * 4 * levels * 2);  // nxt, wr
+  add((size_t)(n + 1) * 4 * 2);  // runz, runn
+  add((size_t)(n + 1) * 4 * 2);  // path_node, path_off
+  add((size_t)(n + 1) * 4 * 3);  // run_z, run_n, run_b
+  add(((size_t)n / 256 + 2) * 4);  // fail block sums
+  return s;
+}
+
+uint32_t ff_levels(uint32_t n) {
+  uint32_t l = 1;
+  while ((1ull << l) < (uint64_t)n + 2) ++l;
+  return l + 1;
+}
+
+cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, void* ws, cudaStream_t s,
+                      cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+  const uint32_t n = hi - lo;
+  const uint32_t levels = ff_levels(n);
+  FF f{};
+  f.perm = a.perm + lo;
+  f.u = a.u;
+  f.key = a.key;
+  f.n = n;
+  f.C = (uint32_t)a.prof.C;
+  f.m = (uint32_t)a.prof.b10 * f.C / 10u;
+  f.K = f.m - f.C;
+  f.lambda = a.prof.lambda;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
+  const size_t nc1 = (n + B1 - 1) / B1 + 1;
+  f.scal = reinterpret_cast<uint32_t*>(take(64));
+  f.kk = reinterpret_cast<uint64_t*>(take((size_t)n * 8));
+  f.rseq = reinterpret_cast<uint64_t*>(take((size_t)n * 8));
+  f.summ = reinterpret_cast<uint64_t*>(take(nc1 * KS * 8 * 3));
+  f.heapH = f.summ + nc1 * KS;
+  uint64_t* loc = f.summ + 2 * nc1 * KS;
+  f.hfinal = reinterpret_cast<uint64_t*>(take(KS * 8));
+  f.passbm = reinterpret_cast<uint32_t*>(take(((size_t)n / 32 + 2) * 4));
+  f.failpos = reinterpret_cast<uint32_t*>(take((size_t)n * 4 * 3));
+  f.exE = f.failpos + n;
+  f.exR = f.failpos + 2 * (size_t)n;
+  f.nxt = reinterpret_cast<uint32_t*>(take((size_t)(n + 1) * 4 * levels * 2));
+  f.wr = f.nxt + (size_t)(n + 1) * levels;
+  f.runz = reinterpret_cast<uint32_t*>(take((size_t)(n + 1) * 4 * 2));
+  f.runn = f.runz + (n + 1);
+  f.path_node = reinterpret_cast<uint32_t*>(take((size_t)(n + 1) * 4 * 2));
+  f.path_off = f.path_node + (n + 1);
+  f.run_z = reinterpret_cast<uint32_t*>(take((size_t)(n + 1) * 4 * 3));
+  f.run_n = f.run_z + (n + 1);
+  f.run_b = f.run_z + 2 * (size_t)(n + 1);
+  uint32_t* blocksum = reinterpret_cast<uint32_t*>(take(((size_t)n / 256 + 2) * 4));
+  f.levels = levels;
+  f.batch_of = a.batch_of;
+  f.slot_of = a.slot_of;
+  f.core_of = a.core_of;
+  f.seg_count_q = a.seg_count + q;
+
+  cudaMemsetAsync(f.scal, 0, 64, s);
+  const uint32_t g1 = (n + 255) / 256;
+  k_ff_ncpu<<<g1, 256, 0, s>>>(f);
+  note_launch();
+  // CPU class (serial list scheduling) runs concurrently on the aux stream
+  cudaEventRecord(ev_fork, s);
+  cudaStreamWaitEvent(aux, ev_fork, 0);
+  cudaError_t e = launch_cpu_big(a, lo, n, f.scal, aux);
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(ev_join, aux);
+  k_ff_gather<<<g1, 256, 0, s>>>(f);
+  note_launch();
+  if (f.K == 0) {
+    k_ff_copy<<<g1, 256, 0, s>>>(f);
+    note_launch();
+  } else {
+    const uint32_t nc = (n + B1 - 1) / B1;
+    k_ff_topk<<<nc, 256, 0, s>>>(f);
+    const int scan_smem = 32 * 3 * KS * 8;
+    cudaFuncSetAttribute(k_ff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, scan_smem);
+    k_ff_scan<<<1, 1024, scan_smem, s>>>(f, loc);
+    const uint32_t rg = (nc * 32 + 127) / 128;
+    if (f.K <= 32) k_ff_replay<1><<<rg, 128, 0, s>>>(f);
+    else if (f.K <= 64) k_ff_replay<2><<<rg, 128, 0, s>>>(f);
+    else k_ff_replay<4><<<rg, 128, 0, s>>>(f);
+    note_launch(3);
+  }
+  const uint32_t npass = ((n + 31) / 32 + 1) * 32;
+  k_ff_pass<<<(npass + 255) / 256, 256, 0, s>>>(f);
+  const uint32_t fb = (n + 255) / 256;
+  k_ff_failcount<<<fb, 256, 0, s>>>(f, blocksum);
+  k_ff_blockscan<<<1, 1024, 0, s>>>(blocksum, fb, f.scal + 3);
+  k_ff_failwrite<<<fb, 256, 0, s>>>(f, blocksum);
+  const uint32_t gw = ((n + 1) * 32 + 127) / 128;
+  k_ff_excursion<<<gw, 128, 0, s>>>(f);
+  k_ff_link<<<gw, 128, 0, s>>>(f);
+  note_launch(6);
+  for (uint32_t k = 1; k < levels; ++k) {
+    k_ff_double<<<(n + 256) / 256, 256, 0, s>>>(f, k);
+    note_launch();
+  }
+  k_ff_expand<<<1, 1024, 0, s>>>(f);
+  k_ff_runs<<<1, 1024, 0, s>>>(f);
+  k_ff_emit_runs<<<1184, 256, 0, s>>>(f);
+  k_ff_emit_exc<<<gw, 128, 0, s>>>(f);
+  k_ff_tail<<<1, 32, 0, s>>>(f);
+  note_launch(5);
+  cudaStreamWaitEvent(s, ev_join, 0);
+  return cudaGetLastError();
+}
+
+}  // namespace rtlm

@@ -234,6 +234,52 @@ __global__ void __launch_bounds__(64) k_sched_big(SchedLaunch a, uint32_t q, uin
   }
 }
 
+// CPU class of a large queue: preds computed in parallel into shared memory,
+// the list-scheduling recurrence run by one thread, outputs written in parallel.
+constexpr uint32_t kCpuChunk = 4096;
+template <int MAXC>
+__global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p) {
+  __shared__ int64_t s_pred[kCpuChunk];
+  __shared__ uint8_t s_core[kCpuChunk];
+  const uint32_t ncpu = *ncpu_p;
+  const uint32_t* perm = a.perm + lo;
+  const float eta = __ll2float_rn(a.prof.eta_us);
+  const uint32_t cores = a.cores;
+  int64_t fr[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) fr[c] = 0;
+  for (uint32_t j0 = 0; j0 < ncpu; j0 += kCpuChunk) {
+    const uint32_t cnt = min(kCpuChunk, ncpu - j0);
+    for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
+      const float eu = __fmul_rn(eta, a.u[perm[j0 + k]]);
+      s_pred[k] = (int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t k = 0; k < cnt; ++k) {
+        int best = 0;
+        int64_t bv = fr[0];
+#pragma unroll
+        for (int c = 1; c < MAXC; ++c)
+          if (c < (int)cores && fr[c] < bv) { bv = fr[c]; best = c; }
+        const int64_t pr = s_pred[k];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c)
+          if (c == best) fr[c] += pr;
+        s_core[k] = (uint8_t)best;
+      }
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
+      const uint32_t i = perm[j0 + k];
+      a.core_of[i] = cores ? s_core[k] : (uint8_t)0xFF;
+      a.batch_of[i] = kNoBatch;
+      a.slot_of[i] = 0;
+    }
+    __syncthreads();
+  }
+}
+
 // seg_batch_off = exclusive scan of seg_count (one CTA)
 __global__ void __launch_bounds__(1024) k_seg_scan(const uint32_t* __restrict__ cnt, uint32_t nq,
                                                     uint32_t* __restrict__ off) {
@@ -292,6 +338,15 @@ cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
   k_gather<<<(n + 255) / 256, 256, 0, s>>>(a.perm, a.u, a.key, lo, n, u_sorted, ncpu);
   k_sched_big<<<1, 64, 0, s>>>(a, q, lo, n, u_sorted, ncpu);
   note_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu, cudaStream_t s) {
+  (void)n;
+  if (a.cores <= 4) k_cpu_big<4><<<1, 256, 0, s>>>(a, lo, ncpu);
+  else if (a.cores <= 8) k_cpu_big<8><<<1, 256, 0, s>>>(a, lo, ncpu);
+  else k_cpu_big<32><<<1, 256, 0, s>>>(a, lo, ncpu);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -165,6 +165,33 @@ def test_schedule_big_queue(ctx_v1, lex_v1, n):
         _check_schedule(g, s, 1)
 
 
+@pytest.mark.parametrize("C,b10,lam,cores", [(11, 18, 1.5, 4), (33, 18, 1.5, 4), (11, 10, 1.5, 4), (33, 30, 1.5, 2),
+                                             (5, 20, 1.0, 1), (24, 13, 3.0, 8), (1, 10, 1.5, 4), (11, 18, 1.05, 32)])
+def test_schedule_big_queue_params(ctx_v1, lex_v1, C, b10, lam, cores):
+    """The parallel consolidation path (queues > 2048) against O6 for window
+    shapes K = m - C from 0 to 66 and lambda from 1.0 (cuts everywhere) to 3.0."""
+    n = 20011
+    d = configs.config2(n=n, gid0=424242 + C)
+    prof = dict(d["profile"], C=C, b10=b10, **{"lambda": lam}, cores=cores)
+    out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressor"])
+    seg = np.asarray([0, n], U32)
+    g = ctx_v1.schedule(out["key"], out["u"], seg, prof)
+    torch.cuda.synchronize()
+    _check_schedule(g, oracle.schedule(k, u, seg, prof), 1)
+
+
+def test_schedule_big_queue_no_offload_and_tiny_gpu_class(ctx_v1, lex_v1):
+    """All-GPU queue, and a queue whose GPU class is smaller than the carry K."""
+    n = 5000
+    d = configs.config2(n=n, gid0=777777)
+    for prof in [dict(d["profile"], offload=0), dict(d["profile"], tau=6.0, C=33, b10=30)]:
+        out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressor"])
+        seg = np.asarray([0, n], U32)
+        g = ctx_v1.schedule(out["key"], out["u"], seg, prof)
+        torch.cuda.synchronize()
+        _check_schedule(g, oracle.schedule(k, u, seg, prof), 1)
+
+
 def test_schedule_mixed_big_and_small(ctx_v1, lex_v1):
     sizes = [100, 5000, 0, 3000, 7]
     seg = np.concatenate([[0], np.cumsum(sizes)]).astype(U32)
