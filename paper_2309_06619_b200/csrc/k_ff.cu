@@ -60,11 +60,19 @@ struct FF {
   uint32_t* run_n;        // chunks
   uint32_t* run_b;        // first batch id
   uint32_t levels;
+  uint32_t* batch_p;      // G: batch id by stream position p (scattered to global indices at the end)
+  uint8_t* slot_p;        // G
   uint32_t* batch_of;
   uint8_t* slot_of;
   uint8_t* core_of;
   uint32_t* seg_count_q;  // &seg_count[q]
 };
+
+__device__ __forceinline__ void put(const FF& f, uint64_t x, uint32_t b, uint32_t slot) {
+  const uint32_t p = (uint32_t)x;
+  f.batch_p[p] = b;
+  f.slot_p[p] = (uint8_t)slot;
+}
 
 // ------------------------------------------------------------ 1. gather
 __global__ void k_ff_gather(FF f) {
@@ -369,6 +377,116 @@ __device__ __forceinline__ uint32_t r_round(const FF& f, Warp3 w, uint32_t& lc, 
   return cnt;
 }
 
+
+// ------------------------------------------------------------ 4b. register rounds (C <= 32)
+// Lane i holds A[i]; Rseq is streamed through a per-warp shared ring that is
+// filled three 32-entry blocks ahead with register-staged loads, so a round
+// never waits on L2.
+constexpr uint32_t kRing = 512;
+
+struct RegWarp {
+  uint64_t* ring;   // kRing entries
+  uint64_t* S;      // 32 entries
+  uint32_t filled;  // ring holds rseq[q] for q < filled (and >= filled - kRing)
+  uint32_t issue;   // next rseq index to load into the pipeline
+  uint64_t pf0, pf1, pf2;
+};
+
+__device__ __forceinline__ uint64_t ld_rseq(const FF& f, uint32_t q, uint32_t NR) {
+  return q < NR ? f.rseq[q] : kInf;
+}
+
+__device__ __forceinline__ void ring_init(const FF& f, RegWarp& w, uint32_t j, uint32_t NR) {
+  const uint32_t lane = threadIdx.x & 31u;
+  w.filled = j;
+  w.pf0 = ld_rseq(f, j + lane, NR);
+  w.pf1 = ld_rseq(f, j + 32 + lane, NR);
+  w.pf2 = ld_rseq(f, j + 64 + lane, NR);
+  w.issue = j + 96;
+}
+
+__device__ __forceinline__ void ring_step(const FF& f, RegWarp& w, uint32_t NR) {
+  const uint32_t lane = threadIdx.x & 31u;
+  w.ring[(w.filled + lane) & (kRing - 1)] = w.pf0;
+  w.filled += 32;
+  w.pf0 = w.pf1;
+  w.pf1 = w.pf2;
+  w.pf2 = ld_rseq(f, w.issue + lane, NR);
+  w.issue += 32;
+}
+
+// one round; state lv (lane < lc holds L sorted), lc, j.  Returns cnt.
+template <class Emit>
+__device__ __forceinline__ uint32_t reg_round(const FF& f, RegWarp& w, uint64_t& lv, uint32_t& lc, uint32_t& j,
+                                              uint32_t NR, Emit emit) {
+  const uint32_t lane = threadIdx.x & 31u, C = f.C;
+  while (w.filled < j + C) ring_step(f, w, NR);
+  if (w.filled < j + C + 64) ring_step(f, w, NR);  // stay ahead
+  __syncwarp();
+  const uint64_t x = lane < lc ? lv : (lane < C ? w.ring[(j + lane - lc) & (kRing - 1)] : kInf);
+  uint32_t rank = 0;
+  for (uint32_t k = 0; k < C; ++k) rank += __shfl_sync(0xFFFFFFFFu, x, k) < x;
+  if (lane < C) w.S[rank] = x;
+  __syncwarp();
+  const uint64_t sv = lane < C ? w.S[lane] : kInf;
+  const uint64_t pv = __shfl_up_sync(0xFFFFFFFFu, sv, 1);
+  const bool bad = lane >= 1 && lane < C && !(kk_u(sv) <= __fmul_rn(f.lambda, kk_u(pv)));
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+  const uint32_t cnt = bal ? __ffs(bal) - 1 : C;
+  if (lane < cnt) emit(sv, lane);
+  const uint32_t src = min(lane + cnt, 31u);
+  lv = __shfl_sync(0xFFFFFFFFu, sv, src);
+  j += C - lc;
+  lc = C - cnt;
+  __syncwarp();
+  return cnt;
+}
+
+__global__ void __launch_bounds__(128) k_ff_excursion_reg(FF f) {
+  __shared__ uint64_t ring[4][kRing];
+  __shared__ uint64_t Sb[4][32];
+  const uint32_t wl = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nfail = f.scal[3], NR = f.scal[2];
+  if (gw >= nfail) return;
+  uint32_t j = f.failpos[gw], lc = 0, r = 0;
+  RegWarp w{ring[wl], Sb[wl], 0, 0, 0, 0, 0};
+  ring_init(f, w, j, NR);
+  uint64_t lv = kInf;
+  for (;;) {
+    if (j + (f.C - lc) > NR) break;
+    reg_round(f, w, lv, lc, j, NR, [](uint64_t, uint32_t) {});
+    ++r;
+    if (lc == 0) break;
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    f.exE[gw] = lc == 0 ? j : kEnd;
+    f.exR[gw] = r;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_ff_emit_exc_reg(FF f) {
+  __shared__ uint64_t ring[4][kRing];
+  __shared__ uint64_t Sb[4][32];
+  const uint32_t wl = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2];
+  if (gw >= np) return;
+  const uint32_t x = f.path_node[gw];
+  if (x == nfail) return;
+  uint32_t j = f.failpos[x], lc = 0, b = f.path_off[gw];
+  RegWarp w{ring[wl], Sb[wl], 0, 0, 0, 0, 0};
+  ring_init(f, w, j, NR);
+  uint64_t lv = kInf;
+  for (;;) {
+    if (j + (f.C - lc) > NR) break;
+    const uint32_t bb = b;
+    reg_round(f, w, lv, lc, j, NR, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
+    ++b;
+    if (lc == 0) break;
+  }
+}
+
 // ------------------------------------------------------------ 5. excursions
 // For every failing position: run from (∅, f) until L is empty again (exE, exR),
 // or until a full round is impossible (exE = kEnd).
@@ -527,10 +645,8 @@ __global__ void k_ff_emit_runs(FF f) {
     const uint64_t x = f.rseq[s0 + i];
     uint32_t slot = 0;
     for (uint32_t b = 0; b < C; ++b) slot += f.rseq[s0 + b] < x;
-    const uint32_t gi = f.perm[ncpu + kk_p(x)];
-    f.batch_of[gi] = f.run_b[r] + t;
-    f.slot_of[gi] = (uint8_t)slot;
-    f.core_of[gi] = 0xFF;
+    put(f, x, f.run_b[r] + t, slot);
+    (void)ncpu;
   }
 }
 
@@ -549,15 +665,11 @@ __global__ void __launch_bounds__(128) k_ff_emit_exc(FF f) {
     const uint32_t need = f.C - lc;
     if (j + need > NR) break;
     const uint32_t bb = b;
-    r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) {
-      const uint32_t g = f.perm[ncpu + kk_p(e)];
-      f.batch_of[g] = bb;
-      f.slot_of[g] = (uint8_t)slot;
-      f.core_of[g] = 0xFF;
-    });
+    r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
     ++b;
     if (lc == 0) break;
   }
+  (void)ncpu;
 }
 
 // tail: find the path end, rebuild its final state, finish with partial windows
@@ -590,10 +702,7 @@ __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
         const uint32_t need = f.C - lc;
         if (j + need > NR) break;
         const uint32_t bb = b;
-        r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) {
-          const uint32_t g = f.perm[ncpu + kk_p(e)];
-          f.batch_of[g] = bb; f.slot_of[g] = (uint8_t)slot; f.core_of[g] = 0xFF;
-        });
+        r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
         ++b;
       }
     } else {
@@ -629,16 +738,25 @@ __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
       if (bal) { cnt = base + __ffs(bal) - 1; break; }
     }
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t g = f.perm[ncpu + kk_p(S[i])];
-      f.batch_of[g] = b; f.slot_of[g] = (uint8_t)i; f.core_of[g] = 0xFF;
-    }
+    for (uint32_t i = lane; i < cnt; i += 32) put(f, S[i], b, i);
     for (uint32_t i = lane; i < na - cnt; i += 32) A[i] = S[cnt + i];
     na -= cnt;
     ++b;
     __syncwarp();
   }
   if (lane == 0) *f.seg_count_q = b;
+  (void)ncpu;
+}
+
+// scatter the per-position results to global element indices
+__global__ void k_ff_scatter(FF f) {
+  const uint32_t ncpu = f.scal[0], G = f.scal[1];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < G; p += gridDim.x * blockDim.x) {
+    const uint32_t g = f.perm[ncpu + p];
+    f.batch_of[g] = f.batch_p[p];
+    f.slot_of[g] = f.slot_p[p];
+    f.core_of[g] = 0xFF;
+  }
 }
 
 }  // namespace
@@ -660,6 +778,7 @@ size_t ff_workspace(uint32_t n, uint32_t levels) {
   add((size_t)(n + 1) * 4 * 2);  // path_node, path_off
   add((size_t)(n + 1) * 4 * 3);  // run_z, run_n, run_b
   add(((size_t)n / 256 + 2) * 4);  // fail block sums
+  add((size_t)n * 5);              // batch_p, slot_p
   return s;
 }
 
@@ -706,6 +825,8 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
   f.run_n = f.run_z + (n + 1);
   f.run_b = f.run_z + 2 * (size_t)(n + 1);
   uint32_t* blocksum = reinterpret_cast<uint32_t*>(take(((size_t)n / 256 + 2) * 4));
+  f.batch_p = reinterpret_cast<uint32_t*>(take((size_t)n * 5));
+  f.slot_p = reinterpret_cast<uint8_t*>(f.batch_p + n);
   f.levels = levels;
   f.batch_of = a.batch_of;
   f.slot_of = a.slot_of;
@@ -746,7 +867,8 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
   k_ff_blockscan<<<1, 1024, 0, s>>>(blocksum, fb, f.scal + 3);
   k_ff_failwrite<<<fb, 256, 0, s>>>(f, blocksum);
   const uint32_t gw = ((n + 1) * 32 + 127) / 128;
-  k_ff_excursion<<<gw, 128, 0, s>>>(f);
+  if (f.C <= 32) k_ff_excursion_reg<<<gw, 128, 0, s>>>(f);
+  else k_ff_excursion<<<gw, 128, 0, s>>>(f);
   k_ff_link<<<gw, 128, 0, s>>>(f);
   note_launch(6);
   for (uint32_t k = 1; k < levels; ++k) {
@@ -756,9 +878,11 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
   k_ff_expand<<<1, 1024, 0, s>>>(f);
   k_ff_runs<<<1, 1024, 0, s>>>(f);
   k_ff_emit_runs<<<1184, 256, 0, s>>>(f);
-  k_ff_emit_exc<<<gw, 128, 0, s>>>(f);
+  if (f.C <= 32) k_ff_emit_exc_reg<<<gw, 128, 0, s>>>(f);
+  else k_ff_emit_exc<<<gw, 128, 0, s>>>(f);
   k_ff_tail<<<1, 32, 0, s>>>(f);
-  note_launch(5);
+  k_ff_scatter<<<g1, 256, 0, s>>>(f);
+  note_launch(6);
   cudaStreamWaitEvent(s, ev_join, 0);
   return cudaGetLastError();
 }

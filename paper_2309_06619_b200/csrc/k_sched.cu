@@ -234,8 +234,12 @@ __global__ void __launch_bounds__(64) k_sched_big(SchedLaunch a, uint32_t q, uin
   }
 }
 
-// CPU class of a large queue: preds computed in parallel into shared memory,
-// the list-scheduling recurrence run by one thread, outputs written in parallel.
+// CPU class of a large queue: predicted latencies computed in parallel into
+// shared memory, the list-scheduling recurrence (R-CORE) run by one thread on
+// a sorted state, outputs written in parallel.  State: the core clocks as
+// keys (t << 5 | core) kept sorted, so the earliest-free core with the lowest
+// index is key[0] and a job is an add plus a sorted insert of key[0] + (p << 5)
+// (exact while t < 2^58 µs).
 constexpr uint32_t kCpuChunk = 4096;
 template <int MAXC>
 __global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p) {
@@ -245,34 +249,40 @@ __global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, con
   const uint32_t* perm = a.perm + lo;
   const float eta = __ll2float_rn(a.prof.eta_us);
   const uint32_t cores = a.cores;
-  int64_t fr[MAXC];
+  uint64_t k[MAXC];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) fr[c] = 0;
+  for (int c = 0; c < MAXC; ++c) k[c] = c < (int)cores ? (uint64_t)c : ~0ull;  // unused cores never chosen
   for (uint32_t j0 = 0; j0 < ncpu; j0 += kCpuChunk) {
     const uint32_t cnt = min(kCpuChunk, ncpu - j0);
-    for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
-      const float eu = __fmul_rn(eta, a.u[perm[j0 + k]]);
-      s_pred[k] = (int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu));
+    for (uint32_t q = threadIdx.x; q < cnt; q += 256) {
+      const float eu = __fmul_rn(eta, a.u[perm[j0 + q]]);
+      s_pred[q] = ((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu))) << 5;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (uint32_t k = 0; k < cnt; ++k) {
-        int best = 0;
-        int64_t bv = fr[0];
+    if (threadIdx.x == 0 && cores) {
+#pragma unroll 4
+      for (uint32_t q = 0; q < cnt; ++q) {
+        const uint64_t v = k[0] + (uint64_t)s_pred[q];
+        s_core[q] = (uint8_t)(k[0] & 31u);
+        // remove k[0], insert v: lt[c] = v < k[c] (old keys, monotone in c)
+        bool lt[MAXC];
 #pragma unroll
-        for (int c = 1; c < MAXC; ++c)
-          if (c < (int)cores && fr[c] < bv) { bv = fr[c]; best = c; }
-        const int64_t pr = s_pred[k];
+        for (int c = 1; c < MAXC; ++c) lt[c] = v < k[c];
+        uint64_t nk[MAXC];
 #pragma unroll
-        for (int c = 0; c < MAXC; ++c)
-          if (c == best) fr[c] += pr;
-        s_core[k] = (uint8_t)best;
+        for (int c = 0; c < MAXC; ++c) {
+          const bool take_next = (c + 1 < MAXC) && !lt[c + 1 < MAXC ? c + 1 : 0];
+          const bool keep = (c >= 1) && lt[c >= 1 ? c : 1];
+          nk[c] = take_next ? k[c + 1 < MAXC ? c + 1 : c] : (keep ? k[c] : v);
+        }
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
       }
     }
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
-      const uint32_t i = perm[j0 + k];
-      a.core_of[i] = cores ? s_core[k] : (uint8_t)0xFF;
+    for (uint32_t q = threadIdx.x; q < cnt; q += 256) {
+      const uint32_t i = perm[j0 + q];
+      a.core_of[i] = cores ? s_core[q] : (uint8_t)0xFF;
       a.batch_of[i] = kNoBatch;
       a.slot_of[i] = 0;
     }
