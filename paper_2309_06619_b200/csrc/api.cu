@@ -465,7 +465,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   for (uint32_t q = 0; q < nq; ++q) {
     const uint32_t m = h_seg_off[q + 1] - h_seg_off[q];
     if (m > rtlm::kSmallSeg) {
-      size_t need = std::max(rtlm::radix_sort_workspace(m), rtlm::ff_workspace(m, rtlm::ff_levels(m)));
+      size_t need = std::max(rtlm::radix_sort_workspace(m), rtlm::ff_workspace(m, rtlm::ff_levels(m), (uint32_t)prof->C));
       if (need > big_ws) big_ws = need;
     }
   }

@@ -112,7 +112,7 @@ cudaError_t launch_sched_finish(const SchedLaunch& a, cudaStream_t s);
 // CPU class of a large queue [lo, lo+n) (ncpu read from device memory)
 cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu_dev, cudaStream_t s);
 // GPU class of a large queue: parallel exact consolidation (k_ff.cu)
-size_t ff_workspace(uint32_t n, uint32_t levels);
+size_t ff_workspace(uint32_t n, uint32_t levels, uint32_t C);
 uint32_t ff_levels(uint32_t n);
 cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, void* ws, cudaStream_t s,
                       cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);

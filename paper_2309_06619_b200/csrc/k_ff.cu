@@ -39,7 +39,7 @@ struct FF {
   uint32_t K, C, m;
   float lambda;
   // device scalars
-  uint32_t* scal;         // [0] ncpu, [1] G, [2] NR, [3] nfail, [4] nruns, [5] total batches, [6] path_len
+  uint32_t* scal;         // [0] ncpu [1] G [2] NR [3] nfail [4] stretch elements [5] - [6] path_len [7] #descriptors
   // buffers
   uint64_t* kk;           // G
   uint64_t* rseq;         // NR
@@ -60,6 +60,13 @@ struct FF {
   uint32_t* run_n;        // chunks
   uint32_t* run_b;        // first batch id
   uint32_t levels;
+  float* vt;              // C x vstride: u(max) of Rseq[j, j+c) if that chunk passes its λ chain, else +inf
+  uint32_t vstride;
+  uint32_t* ds_j;         // stretch descriptors (emission): start, chunk size, rounds, first batch
+  uint32_t* ds_c;
+  uint32_t* ds_r;
+  uint32_t* ds_b;
+  uint32_t* ds_pre;       // exclusive prefix of ds_r * ds_c
   uint32_t* batch_p;      // G: batch id by stream position p (scattered to global indices at the end)
   uint8_t* slot_p;        // G
   uint32_t* batch_of;
@@ -256,33 +263,47 @@ __global__ void k_ff_copy(FF f) {
   if (blockIdx.x == 0 && threadIdx.x == 0) f.hfinal[0] = 0ull;
 }
 
-// ------------------------------------------------------------ 3. pass(j)
-// pass(j): sorted Rseq[j, j+C) has every adjacent ratio <= lambda.
-__global__ void __launch_bounds__(256) k_ff_pass(FF f) {
+// ------------------------------------------------------------ 3. chunk tables
+// For every start j and chunk size c = 1..C: vt[c-1][j] = u(max of Rseq[j, j+c))
+// if the sorted chunk passes the λ chain (every adjacent ratio <= λ), else
+// +inf (also +inf when j + c > NR).  Incremental insertion keeps the count of
+// failing adjacent pairs.  pass(j) = vt[C-1][j] < inf.
+__device__ __forceinline__ bool ratio_bad(uint64_t lo, uint64_t hi, float lam) {
+  return !(kk_u(hi) <= __fmul_rn(lam, kk_u(lo)));
+}
+
+__global__ void __launch_bounds__(256) k_ff_vtab(FF f) {
   __shared__ uint64_t t[256 + kMaxWindow];
   const uint32_t NR = f.scal[2], C = f.C;
   const uint32_t j0 = blockIdx.x * 256u;
-  const uint32_t j = j0 + threadIdx.x;
   const uint32_t nwords = (NR + 31) / 32 + 1;
   if (j0 >= nwords * 32) return;  // block-uniform
+  const uint32_t j = j0 + threadIdx.x;
   for (uint32_t i = threadIdx.x; i < 256 + C; i += 256) t[i] = j0 + i < NR ? f.rseq[j0 + i] : 0ull;
   __syncthreads();
-  bool ok = false;
-  if (j + C <= NR) {
-    ok = true;
-    // every element but the minimum must be <= lambda * (its predecessor in the window)
-    const uint64_t* w = t + threadIdx.x;
-    for (uint32_t a = 0; a < C; ++a) {
-      const uint64_t xa = w[a];
-      uint64_t pred = 0;
-      for (uint32_t b = 0; b < C; ++b) {
-        const uint64_t xb = w[b];
-        pred = (xb < xa && xb > pred) ? xb : pred;
+  const uint64_t* w = t + threadIdx.x;
+  const float lam = f.lambda;
+  int bad = 0;
+  uint64_t mx = 0;
+  bool passC = false;
+  for (uint32_t c = 1; c <= C; ++c) {
+    const bool full = j + c <= NR;
+    if (full) {
+      const uint64_t x = w[c - 1];
+      uint64_t pred = 0, succ = kInf;
+      for (uint32_t b = 0; b + 1 < c; ++b) {
+        const uint64_t y = w[b];
+        pred = (y < x && y > pred) ? y : pred;
+        succ = (y > x && y < succ) ? y : succ;
       }
-      ok &= (pred == 0) || (kk_u(xa) <= __fmul_rn(f.lambda, kk_u(pred)));
+      const bool hp = pred != 0, hs = succ != kInf;
+      bad += (hp && ratio_bad(pred, x, lam)) + (hs && ratio_bad(x, succ, lam)) - (hp && hs && ratio_bad(pred, succ, lam));
+      mx = x > mx ? x : mx;
     }
+    if (j < NR) f.vt[(size_t)(c - 1) * f.vstride + j] = (full && bad == 0) ? kk_u(mx) : __int_as_float(0x7f800000);
+    if (c == C) passC = full && bad == 0;
   }
-  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, passC);
   if ((threadIdx.x & 31u) == 0 && j < nwords * 32) f.passbm[j >> 5] = bal;
 }
 
@@ -298,6 +319,7 @@ __global__ void k_ff_failcount(FF f, uint32_t* blocksum) {
   if (threadIdx.x == 0) blocksum[blockIdx.x] = c;
 }
 
+// exclusive scan of nb counters by one CTA; total -> *total
 __global__ void __launch_bounds__(1024) k_ff_blockscan(uint32_t* blocksum, uint32_t nb, uint32_t* total) {
   __shared__ uint32_t part[1024];
   const uint32_t per = (nb + 1023) / 1024;
@@ -336,10 +358,29 @@ __global__ void k_ff_failwrite(FF f, const uint32_t* blockoff) {
   if (fl) f.failpos[base + __popc(bal & ((1u << lane) - 1u))] = j;
 }
 
-// ------------------------------------------------------------ 4. R-process warp
-// One round on state (L: ascending kk in smem, lc; j).  A = L ∪ Rseq[j, j+need).
-// Emits via callback; returns cnt.  Requires j + need <= NR (full round) unless
-// `partial` (tail), where A = L ∪ Rseq[j, NR) ∪ extra.
+// ------------------------------------------------------------ 4. trajectories
+// A trajectory of the R-process alternates GENERAL rounds (O6 round on
+// A = L ∪ next C-|L| ready elements) and STEADY stretches: with ℓ = |L| and
+// c = C - ℓ, a round at j is steady (emits exactly the chunk Rseq[j, j+c),
+// leaves L unchanged) iff the chunk passes its λ chain and
+// u(min L) > λ·u(max chunk) -- i.e. !(u0 <= λ·vt[c-1][j]) with u0 = u(min L)
+// (+inf when L is empty).  ffwd() checks 32 consecutive rounds per warp step.
+__device__ __forceinline__ uint32_t ffwd(const FF& f, uint32_t lc, float u0, uint32_t& j, uint32_t NR) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t c = f.C - lc;
+  uint32_t total = 0;
+  for (;;) {
+    const uint32_t jk = j + lane * c;
+    const bool ok = (jk + c <= NR) && !(u0 <= __fmul_rn(f.lambda, f.vt[(size_t)(c - 1) * f.vstride + jk]));
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
+    const uint32_t k = (bal == 0xFFFFFFFFu) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+    j += k * c;
+    total += k;
+    if (k < 32) return total;
+  }
+}
+
+// ---- general rounds, shared-memory version (any C <= 128)
 struct Warp3 {
   uint64_t* L;  // capacity kMaxWindow
   uint64_t* A;
@@ -349,7 +390,6 @@ struct Warp3 {
 template <class Emit>
 __device__ __forceinline__ uint32_t r_round(const FF& f, Warp3 w, uint32_t& lc, uint32_t& j, uint32_t na,
                                             Emit emit) {
-  // na = |A| = lc + new elements (taken from Rseq[j, j + na - lc))
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t need = na - lc;
   for (uint32_t i = lane; i < na; i += 32) w.A[i] = i < lc ? w.L[i] : f.rseq[j + (i - lc)];
@@ -365,7 +405,7 @@ __device__ __forceinline__ uint32_t r_round(const FF& f, Warp3 w, uint32_t& lc, 
   uint32_t cnt = lim;
   for (uint32_t base = 1; base < lim; base += 32) {
     const uint32_t i = base + lane;
-    const bool bad = i < lim && !(kk_u(w.S[i]) <= __fmul_rn(f.lambda, kk_u(w.S[i - 1])));
+    const bool bad = i < lim && ratio_bad(w.S[i - 1], w.S[i], f.lambda);
     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
     if (bal) { cnt = base + __ffs(bal) - 1; break; }
   }
@@ -377,168 +417,139 @@ __device__ __forceinline__ uint32_t r_round(const FF& f, Warp3 w, uint32_t& lc, 
   return cnt;
 }
 
-
-// ------------------------------------------------------------ 4b. register rounds (C <= 32)
-// Lane i holds A[i]; Rseq is streamed through a per-warp shared ring that is
-// filled three 32-entry blocks ahead with register-staged loads, so a round
-// never waits on L2.
-constexpr uint32_t kRing = 512;
-
-struct RegWarp {
-  uint64_t* ring;   // kRing entries
-  uint64_t* S;      // 32 entries
-  uint32_t filled;  // ring holds rseq[q] for q < filled (and >= filled - kRing)
-  uint32_t issue;   // next rseq index to load into the pipeline
-  uint64_t pf0, pf1, pf2;
+struct SmemTraj {
+  Warp3 w;
+  uint32_t lc = 0;
+  __device__ void init(const FF&, uint32_t, uint32_t) { lc = 0; }
+  __device__ float u0() const { return lc ? kk_u(w.L[0]) : __int_as_float(0x7f800000); }
+  template <class Emit>
+  __device__ uint32_t round(const FF& f, uint32_t& j, uint32_t, Emit emit) { return r_round(f, w, lc, j, f.C, emit); }
 };
 
-__device__ __forceinline__ uint64_t ld_rseq(const FF& f, uint32_t q, uint32_t NR) {
-  return q < NR ? f.rseq[q] : kInf;
+// ---- general rounds, register version (C <= 32): lane i holds A[i]; Rseq is
+// streamed through a per-warp shared ring filled three 32-entry blocks ahead.
+constexpr uint32_t kRing = 512;
+
+__device__ __forceinline__ uint64_t ld_rseq(const FF& f, uint32_t q, uint32_t NR) { return q < NR ? f.rseq[q] : kInf; }
+
+struct RegTraj {
+  uint64_t* ring;
+  uint64_t* S;
+  uint32_t filled, issue;
+  uint64_t pf0, pf1, pf2;
+  uint64_t lv;
+  uint32_t lc;
+  __device__ void init(const FF& f, uint32_t j, uint32_t NR) {
+    const uint32_t lane = threadIdx.x & 31u;
+    filled = j;
+    pf0 = ld_rseq(f, j + lane, NR);
+    pf1 = ld_rseq(f, j + 32 + lane, NR);
+    pf2 = ld_rseq(f, j + 64 + lane, NR);
+    issue = j + 96;
+    lv = kInf;
+    lc = 0;
+  }
+  __device__ void step(const FF& f, uint32_t NR) {
+    const uint32_t lane = threadIdx.x & 31u;
+    ring[(filled + lane) & (kRing - 1)] = pf0;
+    filled += 32;
+    pf0 = pf1;
+    pf1 = pf2;
+    pf2 = ld_rseq(f, issue + lane, NR);
+    issue += 32;
+  }
+  __device__ float u0() const {
+    const uint64_t l0 = __shfl_sync(0xFFFFFFFFu, lv, 0);
+    return lc ? kk_u(l0) : __int_as_float(0x7f800000);
+  }
+  template <class Emit>
+  __device__ uint32_t round(const FF& f, uint32_t& j, uint32_t NR, Emit emit) {
+    const uint32_t lane = threadIdx.x & 31u, C = f.C;
+    if (j > filled) {  // jumped past the prefetched range: restart the pipeline at j
+      const uint64_t keep = lv;
+      const uint32_t klc = lc;
+      init(f, j, NR);
+      lv = keep;
+      lc = klc;
+    }
+    while (filled < j + C) step(f, NR);
+    if (filled < j + C + 64) step(f, NR);
+    __syncwarp();
+    const uint64_t x = lane < lc ? lv : (lane < C ? ring[(j + lane - lc) & (kRing - 1)] : kInf);
+    uint32_t rank = 0;
+    for (uint32_t k = 0; k < C; ++k) rank += __shfl_sync(0xFFFFFFFFu, x, k) < x;
+    if (lane < C) S[rank] = x;
+    __syncwarp();
+    const uint64_t sv = lane < C ? S[lane] : kInf;
+    const uint64_t pv = __shfl_up_sync(0xFFFFFFFFu, sv, 1);
+    const bool bad = lane >= 1 && lane < C && ratio_bad(pv, sv, f.lambda);
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+    const uint32_t cnt = bal ? __ffs(bal) - 1 : C;
+    if (lane < cnt) emit(sv, lane);
+    lv = __shfl_sync(0xFFFFFFFFu, sv, min(lane + cnt, 31u));
+    j += C - lc;
+    lc = C - cnt;
+    __syncwarp();
+    return cnt;
+  }
+};
+
+__device__ __forceinline__ void tr_setup(SmemTraj& t, uint64_t* base) {
+  t.w = Warp3{base, base + kMaxWindow, base + 2 * kMaxWindow};
+}
+__device__ __forceinline__ void tr_setup(RegTraj& t, uint64_t* base) {
+  t.ring = base;
+  t.S = base + kRing;
 }
 
-__device__ __forceinline__ void ring_init(const FF& f, RegWarp& w, uint32_t j, uint32_t NR) {
-  const uint32_t lane = threadIdx.x & 31u;
-  w.filled = j;
-  w.pf0 = ld_rseq(f, j + lane, NR);
-  w.pf1 = ld_rseq(f, j + 32 + lane, NR);
-  w.pf2 = ld_rseq(f, j + 64 + lane, NR);
-  w.issue = j + 96;
-}
-
-__device__ __forceinline__ void ring_step(const FF& f, RegWarp& w, uint32_t NR) {
-  const uint32_t lane = threadIdx.x & 31u;
-  w.ring[(w.filled + lane) & (kRing - 1)] = w.pf0;
-  w.filled += 32;
-  w.pf0 = w.pf1;
-  w.pf1 = w.pf2;
-  w.pf2 = ld_rseq(f, w.issue + lane, NR);
-  w.issue += 32;
-}
-
-// one round; state lv (lane < lc holds L sorted), lc, j.  Returns cnt.
-template <class Emit>
-__device__ __forceinline__ uint32_t reg_round(const FF& f, RegWarp& w, uint64_t& lv, uint32_t& lc, uint32_t& j,
-                                              uint32_t NR, Emit emit) {
-  const uint32_t lane = threadIdx.x & 31u, C = f.C;
-  while (w.filled < j + C) ring_step(f, w, NR);
-  if (w.filled < j + C + 64) ring_step(f, w, NR);  // stay ahead
-  __syncwarp();
-  const uint64_t x = lane < lc ? lv : (lane < C ? w.ring[(j + lane - lc) & (kRing - 1)] : kInf);
-  uint32_t rank = 0;
-  for (uint32_t k = 0; k < C; ++k) rank += __shfl_sync(0xFFFFFFFFu, x, k) < x;
-  if (lane < C) w.S[rank] = x;
-  __syncwarp();
-  const uint64_t sv = lane < C ? w.S[lane] : kInf;
-  const uint64_t pv = __shfl_up_sync(0xFFFFFFFFu, sv, 1);
-  const bool bad = lane >= 1 && lane < C && !(kk_u(sv) <= __fmul_rn(f.lambda, kk_u(pv)));
-  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
-  const uint32_t cnt = bal ? __ffs(bal) - 1 : C;
-  if (lane < cnt) emit(sv, lane);
-  const uint32_t src = min(lane + cnt, 31u);
-  lv = __shfl_sync(0xFFFFFFFFu, sv, src);
-  j += C - lc;
-  lc = C - cnt;
-  __syncwarp();
-  return cnt;
-}
-
-__global__ void __launch_bounds__(128) k_ff_excursion_reg(FF f) {
-  __shared__ uint64_t ring[4][kRing];
-  __shared__ uint64_t Sb[4][32];
-  const uint32_t wl = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nfail = f.scal[3], NR = f.scal[2];
-  if (gw >= nfail) return;
-  uint32_t j = f.failpos[gw], lc = 0, r = 0;
-  RegWarp w{ring[wl], Sb[wl], 0, 0, 0, 0, 0};
-  ring_init(f, w, j, NR);
-  uint64_t lv = kInf;
+// Run the trajectory from (∅, j) through its first general round until L is
+// empty again (returns true, j = ∅-point) or no full round fits (false).
+// Steady stretches are reported to `stretch(j0, c, rounds)`, general rounds
+// emit through `emit`; r counts rounds.
+template <class T, class Emit, class Stretch>
+__device__ bool excursion(const FF& f, T& tr, uint32_t& j, uint32_t& r, uint32_t NR, Emit emit, Stretch stretch) {
   for (;;) {
-    if (j + (f.C - lc) > NR) break;
-    reg_round(f, w, lv, lc, j, NR, [](uint64_t, uint32_t) {});
+    if (j + (f.C - tr.lc) > NR) return false;
+    tr.round(f, j, NR, emit);
     ++r;
-    if (lc == 0) break;
-  }
-  if ((threadIdx.x & 31u) == 0) {
-    f.exE[gw] = lc == 0 ? j : kEnd;
-    f.exR[gw] = r;
-  }
-}
-
-__global__ void __launch_bounds__(128) k_ff_emit_exc_reg(FF f) {
-  __shared__ uint64_t ring[4][kRing];
-  __shared__ uint64_t Sb[4][32];
-  const uint32_t wl = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2];
-  if (gw >= np) return;
-  const uint32_t x = f.path_node[gw];
-  if (x == nfail) return;
-  uint32_t j = f.failpos[x], lc = 0, b = f.path_off[gw];
-  RegWarp w{ring[wl], Sb[wl], 0, 0, 0, 0, 0};
-  ring_init(f, w, j, NR);
-  uint64_t lv = kInf;
-  for (;;) {
-    if (j + (f.C - lc) > NR) break;
-    const uint32_t bb = b;
-    reg_round(f, w, lv, lc, j, NR, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
-    ++b;
-    if (lc == 0) break;
+    if (tr.lc == 0) return true;
+    const uint32_t j0 = j;
+    const uint32_t k = ffwd(f, tr.lc, tr.u0(), j, NR);
+    if (k) stretch(j0, f.C - tr.lc, k);
+    r += k;
   }
 }
 
 // ------------------------------------------------------------ 5. excursions
-// For every failing position: run from (∅, f) until L is empty again (exE, exR),
-// or until a full round is impossible (exE = kEnd).
+template <class T>
 __global__ void __launch_bounds__(128) k_ff_excursion(FF f) {
-  __shared__ uint64_t sm[4][3][kMaxWindow];
+  __shared__ uint64_t sm[4][3 * kMaxWindow + kRing];
   const uint32_t wl = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nfail = f.scal[3], NR = f.scal[2];
   if (gw >= nfail) return;
-  Warp3 w{sm[wl][0], sm[wl][1], sm[wl][2]};
-  uint32_t lc = 0, j = f.failpos[gw], r = 0;
-  for (;;) {
-    const uint32_t need = f.C - lc;
-    if (j + need > NR) { r = r; break; }
-    r_round(f, w, lc, j, f.C, [](uint64_t, uint32_t) {});
-    ++r;
-    if (lc == 0) break;
-  }
+  uint32_t j = f.failpos[gw], r = 0;
+  T tr;
+  tr_setup(tr, sm[wl]);
+  tr.init(f, j, NR);
+  const bool back = excursion(f, tr, j, r, NR, [](uint64_t, uint32_t) {}, [](uint32_t, uint32_t, uint32_t) {});
   if ((threadIdx.x & 31u) == 0) {
-    f.exE[gw] = lc == 0 ? j : kEnd;
+    f.exE[gw] = back ? j : kEnd;
     f.exR[gw] = r;
   }
 }
 
 // ∅-run from z: chunks at z + tC while pass; returns (first fail index or kEnd, #chunks)
 __device__ void run_from(const FF& f, uint32_t z, uint32_t& fail_idx, uint32_t& nch) {
-  const uint32_t lane = threadIdx.x & 31u;
   const uint32_t NR = f.scal[2], C = f.C, nfail = f.scal[3];
-  uint32_t t = 0;
-  for (;;) {
-    const uint32_t jj = z + (t + lane) * C;
-    const bool full = jj + C <= NR;
-    const bool fail = full && !pass_at(f.passbm, jj);
-    const uint32_t bf = __ballot_sync(0xFFFFFFFFu, fail);
-    const uint32_t bn = __ballot_sync(0xFFFFFFFFu, !full);
-    if (bf | bn) {
-      const uint32_t first_f = bf ? __ffs(bf) - 1 : 32u;
-      const uint32_t first_n = bn ? __ffs(bn) - 1 : 32u;
-      if (first_f < first_n) {
-        nch = t + first_f;
-        const uint32_t pos = z + nch * C;
-        // binary search pos in failpos
-        uint32_t lo = 0, hi = nfail;
-        while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.failpos[md] < pos) lo = md + 1; else hi = md; }
-        fail_idx = lo;
-      } else {
-        nch = t + first_n;
-        fail_idx = kEnd;
-      }
-      return;
-    }
-    t += 32;
+  uint32_t jj = z;
+  nch = ffwd(f, 0, __int_as_float(0x7f800000), jj, NR);
+  if (jj + C <= NR) {
+    uint32_t lo = 0, hi = nfail;  // jj is a failing position
+    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.failpos[md] < jj) lo = md + 1; else hi = md; }
+    fail_idx = lo;
+  } else {
+    fail_idx = kEnd;
   }
 }
 
@@ -574,7 +585,8 @@ __global__ void k_ff_double(FF f, uint32_t k) {
   }
 }
 
-// expand the path from the start node (levels high -> low), one CTA
+// expand the path from the start node (levels high -> low), one CTA; also
+// emits one stretch descriptor per path node for its ∅-run
 __global__ void __launch_bounds__(1024) k_ff_expand(FF f) {
   __shared__ uint32_t cnt;
   const uint32_t nn = f.scal[3] + 1;
@@ -600,90 +612,56 @@ __global__ void __launch_bounds__(1024) k_ff_expand(FF f) {
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) f.scal[6] = cnt;
-}
-
-// ∅-run table in path-list order: run_z (start), run_b (first batch id),
-// run_n = exclusive prefix of chunk counts; total chunks -> scal[4].  One CTA.
-__global__ void __launch_bounds__(1024) k_ff_runs(FF f) {
-  __shared__ uint32_t part[1024];
-  const uint32_t np = f.scal[6], nfail = f.scal[3];
-  const uint32_t per = (np + 1023) / 1024;
-  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, np);
-  uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; ++i) sum += f.runn[f.path_node[i]];
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  for (int d = 1; d < 1024; d <<= 1) {
-    uint32_t v = threadIdx.x >= (uint32_t)d ? part[threadIdx.x - d] : 0u;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
-  for (uint32_t i = lo; i < hi; ++i) {
+  const uint32_t np = cnt;
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
     const uint32_t x = f.path_node[i];
-    f.run_z[i] = f.runz[x];
-    f.run_b[i] = f.path_off[i] + (x == nfail ? 0u : f.exR[x]);
-    f.run_n[i] = run;
-    run += f.runn[x];
+    if (f.runz[x] != kEnd && f.runn[x]) {
+      const uint32_t d = atomicAdd(&f.scal[7], 1u);
+      f.ds_j[d] = f.runz[x];
+      f.ds_c[d] = f.C;
+      f.ds_r[d] = f.runn[x];
+      f.ds_b[d] = f.path_off[i] + (x == nn - 1 ? 0u : f.exR[x]);
+    }
   }
-  if (threadIdx.x == 1023) f.scal[4] = part[1023];
+  if (threadIdx.x == 0) f.scal[6] = np;
 }
 
-// emit the ∅-run chunks: one thread per (chunk, element)
-__global__ void k_ff_emit_runs(FF f) {
-  const uint32_t np = f.scal[6], T = f.scal[4], C = f.C, ncpu = f.scal[0];
-  const uint64_t total = (uint64_t)T * C;
-  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t ch = (uint32_t)(g / C), i = (uint32_t)(g % C);
-    uint32_t lo = 0, hi = np;  // last path index with run_n <= ch
-    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.run_n[md] <= ch) lo = md + 1; else hi = md; }
-    const uint32_t r = lo - 1;
-    const uint32_t t = ch - f.run_n[r];
-    const uint32_t s0 = f.run_z[r] + t * C;
-    const uint64_t x = f.rseq[s0 + i];
-    uint32_t slot = 0;
-    for (uint32_t b = 0; b < C; ++b) slot += f.rseq[s0 + b] < x;
-    put(f, x, f.run_b[r] + t, slot);
-    (void)ncpu;
-  }
-}
-
-// re-run every path excursion and emit its batches
+// re-run every path excursion: general rounds emit, steady stretches -> descriptors
+template <class T>
 __global__ void __launch_bounds__(128) k_ff_emit_exc(FF f) {
-  __shared__ uint64_t sm[4][3][kMaxWindow];
+  __shared__ uint64_t sm[4][3 * kMaxWindow + kRing];
   const uint32_t wl = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2], ncpu = f.scal[0];
+  const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2];
   if (gw >= np) return;
   const uint32_t x = f.path_node[gw];
   if (x == nfail) return;  // start node: no excursion
-  Warp3 w{sm[wl][0], sm[wl][1], sm[wl][2]};
-  uint32_t lc = 0, j = f.failpos[x], b = f.path_off[gw];
-  for (;;) {
-    const uint32_t need = f.C - lc;
-    if (j + need > NR) break;
-    const uint32_t bb = b;
-    r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
-    ++b;
-    if (lc == 0) break;
-  }
-  (void)ncpu;
+  uint32_t j = f.failpos[x], r = 0;
+  const uint32_t b0 = f.path_off[gw];
+  T tr;
+  tr_setup(tr, sm[wl]);
+  tr.init(f, j, NR);
+  const uint32_t lane = threadIdx.x & 31u;
+  excursion(f, tr, j, r, NR, [&](uint64_t e, uint32_t slot) { put(f, e, b0 + r, slot); },
+            [&](uint32_t j0, uint32_t c, uint32_t k) {
+              if (lane == 0) {
+                const uint32_t d = atomicAdd(&f.scal[7], 1u);
+                f.ds_j[d] = j0; f.ds_c[d] = c; f.ds_r[d] = k; f.ds_b[d] = b0 + r;
+              }
+            });
 }
 
-// tail: find the path end, rebuild its final state, finish with partial windows
+// tail: rebuild the path end state, finish with partial windows
 __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
   __shared__ uint64_t L[2 * kMaxWindow], A[2 * kMaxWindow], S[2 * kMaxWindow];
   __shared__ uint32_t s_last, s_off;
   const uint32_t lane = threadIdx.x;
-  const uint32_t NR = f.scal[2], nfail = f.scal[3], np = f.scal[6], ncpu = f.scal[0], G = f.scal[1];
+  const uint32_t NR = f.scal[2], nfail = f.scal[3], np = f.scal[6], G = f.scal[1];
   if (lane == 0) {
     s_last = kEnd;
     s_off = 0;
   }
   __syncwarp();
-  // the path node whose successor is END
   for (uint32_t i = lane; i < np; i += 32) {
     const uint32_t x = f.path_node[i];
     if (f.nxt[x] == kEnd) { s_last = x; s_off = f.path_off[i]; }
@@ -692,32 +670,28 @@ __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
   uint32_t lc = 0, j = 0, b = 0;
   const uint32_t x = s_last;
   if (G > f.K && x != kEnd) {
-    b = s_off;
     const uint32_t ex_end = (x == nfail) ? 0u : f.exE[x];
     if (x != nfail && ex_end == kEnd) {
-      // the excursion itself reaches the stream end: replay it to get (L, j)
-      Warp3 w{L, A, S};
+      // the path's last excursion reaches the stream end: replay it for (L, j)
+      SmemTraj tr;
+      tr.w = Warp3{L, A, S};
       j = f.failpos[x];
-      for (;;) {
-        const uint32_t need = f.C - lc;
-        if (j + need > NR) break;
-        const uint32_t bb = b;
-        r_round(f, w, lc, j, f.C, [&](uint64_t e, uint32_t slot) { put(f, e, bb, slot); });
-        ++b;
-      }
+      tr.init(f, j, NR);
+      uint32_t r = 0;
+      excursion(f, tr, j, r, NR, [](uint64_t, uint32_t) {}, [](uint32_t, uint32_t, uint32_t) {});
+      lc = tr.lc;
+      b = s_off + r;
     } else {
       b = s_off + f.wr[x];  // excursion + ∅-run rounds (level 0)
       j = f.runz[x] + f.runn[x] * f.C;
       lc = 0;
     }
   }
-  // remaining: L ∪ Rseq[j, NR) ∪ final heap (non-zero)
-  uint32_t na = lc;
+  // remaining: L ∪ Rseq[j, NR) ∪ final heap
   for (uint32_t i = lane; i < NR - j; i += 32) A[lc + i] = f.rseq[j + i];
   for (uint32_t i = lane; i < lc; i += 32) A[i] = L[i];
-  na += NR - j;
+  uint32_t na = lc + (NR - j);
   __syncwarp();
-  // final heap entries (exactly min(K, G) real ones)
   const uint32_t nh = min(f.K, G);
   for (uint32_t i = lane; i < nh; i += 32) A[na + i] = f.hfinal[i];
   na += nh;
@@ -734,7 +708,7 @@ __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
     uint32_t cnt = lim;
     for (uint32_t base = 1; base < lim; base += 32) {
       const uint32_t i = base + lane;
-      const bool bad = i < lim && !(kk_u(S[i]) <= __fmul_rn(f.lambda, kk_u(S[i - 1])));
+      const bool bad = i < lim && ratio_bad(S[i - 1], S[i], f.lambda);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
       if (bal) { cnt = base + __ffs(bal) - 1; break; }
     }
@@ -745,7 +719,47 @@ __global__ void __launch_bounds__(32) k_ff_tail(FF f) {
     __syncwarp();
   }
   if (lane == 0) *f.seg_count_q = b;
-  (void)ncpu;
+}
+
+// exclusive prefix of descriptor element counts (one CTA); total -> scal[4]
+__global__ void __launch_bounds__(1024) k_ff_dscan(FF f) {
+  __shared__ uint32_t part[1024];
+  const uint32_t nd = f.scal[7];
+  const uint32_t per = (nd + 1023) / 1024;
+  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, nd);
+  uint32_t s = 0;
+  for (uint32_t i = lo; i < hi; ++i) s += f.ds_r[i] * f.ds_c[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    uint32_t v = threadIdx.x >= (uint32_t)d ? part[threadIdx.x - d] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+  for (uint32_t i = lo; i < hi; ++i) {
+    f.ds_pre[i] = run;
+    run += f.ds_r[i] * f.ds_c[i];
+  }
+  if (threadIdx.x == 1023) f.scal[4] = part[1023];
+}
+
+// emit every element of every steady stretch / ∅-run (thread per element)
+__global__ void k_ff_emit_stretch(FF f) {
+  const uint32_t nd = f.scal[7], T = f.scal[4];
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < T; g += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nd;  // last descriptor with ds_pre <= g
+    while (lo < hi) { uint32_t md = (lo + hi) >> 1; if (f.ds_pre[md] <= g) lo = md + 1; else hi = md; }
+    const uint32_t d = lo - 1;
+    const uint32_t c = f.ds_c[d], idx = g - f.ds_pre[d];
+    const uint32_t t = idx / c, i = idx % c;
+    const uint32_t s0 = f.ds_j[d] + t * c;
+    const uint64_t x = f.rseq[s0 + i];
+    uint32_t slot = 0;
+    for (uint32_t b = 0; b < c; ++b) slot += f.rseq[s0 + b] < x;
+    put(f, x, f.ds_b[d] + t, slot);
+  }
 }
 
 // scatter the per-position results to global element indices
@@ -762,7 +776,7 @@ __global__ void k_ff_scatter(FF f) {
 }  // namespace
 
 // ------------------------------------------------------------ host side
-size_t ff_workspace(uint32_t n, uint32_t levels) {
+size_t ff_workspace(uint32_t n, uint32_t levels, uint32_t C) {
   const size_t nc1 = (n + B1 - 1) / B1 + 1;
   size_t s = 0;
   auto add = [&](size_t bytes) { s += (bytes + 255) & ~size_t(255); };
@@ -779,6 +793,8 @@ size_t ff_workspace(uint32_t n, uint32_t levels) {
   add((size_t)(n + 1) * 4 * 3);  // run_z, run_n, run_b
   add(((size_t)n / 256 + 2) * 4);  // fail block sums
   add((size_t)n * 5);              // batch_p, slot_p
+  add((size_t)n * 4 * C);          // vt
+  add((size_t)(n + 1) * 4 * 5);    // descriptors
   return s;
 }
 
@@ -827,6 +843,13 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
   uint32_t* blocksum = reinterpret_cast<uint32_t*>(take(((size_t)n / 256 + 2) * 4));
   f.batch_p = reinterpret_cast<uint32_t*>(take((size_t)n * 5));
   f.slot_p = reinterpret_cast<uint8_t*>(f.batch_p + n);
+  f.vt = reinterpret_cast<float*>(take((size_t)n * 4 * f.C));
+  f.vstride = n;
+  f.ds_j = reinterpret_cast<uint32_t*>(take((size_t)(n + 1) * 4 * 5));
+  f.ds_c = f.ds_j + (n + 1);
+  f.ds_r = f.ds_j + 2 * (size_t)(n + 1);
+  f.ds_b = f.ds_j + 3 * (size_t)(n + 1);
+  f.ds_pre = f.ds_j + 4 * (size_t)(n + 1);
   f.levels = levels;
   f.batch_of = a.batch_of;
   f.slot_of = a.slot_of;
@@ -861,14 +884,14 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
     note_launch(3);
   }
   const uint32_t npass = ((n + 31) / 32 + 1) * 32;
-  k_ff_pass<<<(npass + 255) / 256, 256, 0, s>>>(f);
+  k_ff_vtab<<<(npass + 255) / 256, 256, 0, s>>>(f);
   const uint32_t fb = (n + 255) / 256;
   k_ff_failcount<<<fb, 256, 0, s>>>(f, blocksum);
   k_ff_blockscan<<<1, 1024, 0, s>>>(blocksum, fb, f.scal + 3);
   k_ff_failwrite<<<fb, 256, 0, s>>>(f, blocksum);
   const uint32_t gw = ((n + 1) * 32 + 127) / 128;
-  if (f.C <= 32) k_ff_excursion_reg<<<gw, 128, 0, s>>>(f);
-  else k_ff_excursion<<<gw, 128, 0, s>>>(f);
+  if (f.C <= 32) k_ff_excursion<RegTraj><<<gw, 128, 0, s>>>(f);
+  else k_ff_excursion<SmemTraj><<<gw, 128, 0, s>>>(f);
   k_ff_link<<<gw, 128, 0, s>>>(f);
   note_launch(6);
   for (uint32_t k = 1; k < levels; ++k) {
@@ -876,11 +899,11 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
     note_launch();
   }
   k_ff_expand<<<1, 1024, 0, s>>>(f);
-  k_ff_runs<<<1, 1024, 0, s>>>(f);
-  k_ff_emit_runs<<<1184, 256, 0, s>>>(f);
-  if (f.C <= 32) k_ff_emit_exc_reg<<<gw, 128, 0, s>>>(f);
-  else k_ff_emit_exc<<<gw, 128, 0, s>>>(f);
+  if (f.C <= 32) k_ff_emit_exc<RegTraj><<<gw, 128, 0, s>>>(f);
+  else k_ff_emit_exc<SmemTraj><<<gw, 128, 0, s>>>(f);
   k_ff_tail<<<1, 32, 0, s>>>(f);
+  k_ff_dscan<<<1, 1024, 0, s>>>(f);
+  k_ff_emit_stretch<<<1184, 256, 0, s>>>(f);
   k_ff_scatter<<<g1, 256, 0, s>>>(f);
   note_launch(6);
   cudaStreamWaitEvent(s, ev_join, 0);
