@@ -55,10 +55,8 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    return rank, world, local
+    from paper_2309_06619_b200 import dist as rdist
+    return rdist.env()
 
 
 # ------------------------------------------------------------------ clocks
@@ -257,7 +255,7 @@ def native(args):
 
 def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):
     import torch
-    import torch.distributed as dist
+    from paper_2309_06619_b200 import dist as rdist
     nt = args.traces
     per_lm = max(1, nt // 4)
     first = rank * nt
@@ -297,8 +295,7 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
         ctx.simulate(arr, tl, u, key, D, d["trace_off"], d["profiles"], tp, stats=stats)
         sums.zero_()
         ctx.reduce_stats(stats, grp_of, 4, sums=sums)
-        if world > 1:
-            dist.all_reduce(sums)
+        rdist.allreduce_sums(sums)
 
     for _ in range(args.warmup):
         step()

@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, con
   const uint32_t* perm = a.perm + lo;
   const float eta = __ll2float_rn(a.prof.eta_us);
   const uint32_t cores = a.cores;
-  uint64_t k[MAXC];
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t k[MAXC];  // identical in every lane of warp 0
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) k[c] = c < (int)cores ? (uint64_t)c : ~0ull;  // unused cores never chosen
   for (uint32_t j0 = 0; j0 < ncpu; j0 += kCpuChunk) {
@@ -259,24 +260,60 @@ __global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, con
       s_pred[q] = ((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu))) << 5;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && cores) {
-#pragma unroll 4
-      for (uint32_t q = 0; q < cnt; ++q) {
-        const uint64_t v = k[0] + (uint64_t)s_pred[q];
-        s_core[q] = (uint8_t)(k[0] & 31u);
-        // remove k[0], insert v: lt[c] = v < k[c] (old keys, monotone in c)
-        bool lt[MAXC];
+    if (threadIdx.x < 32 && cores) {
+      // warp 0 runs the recurrence redundantly in every lane; 32 predictions
+      // are fetched per step and broadcast with shuffles (off the critical path)
+      int64_t nextp = lane < cnt ? s_pred[lane] : 0;
+      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
+        const int64_t mine = nextp;
+        nextp = (q0 + 32 + lane < cnt) ? s_pred[q0 + 32 + lane] : 0;
+        const uint32_t m = min(32u, cnt - q0);
+        uint32_t mycore = 0;
+        if (MAXC == 4) {
+          // four sorted keys: v = k0 + p; three compares; selects.  Predictions
+          // are read 8 at a time (broadcast loads hoisted off the chain).
+          uint64_t k0 = k[0], k1 = k[1], k2 = k[MAXC > 2 ? 2 : 1], k3 = k[MAXC > 3 ? 3 : 1];
+          for (uint32_t i0 = 0; i0 < m; i0 += 8) {
+            uint64_t pp[8];
 #pragma unroll
-        for (int c = 1; c < MAXC; ++c) lt[c] = v < k[c];
-        uint64_t nk[MAXC];
+            for (int t = 0; t < 8; ++t) pp[t] = (uint64_t)s_pred[q0 + min(i0 + t, m - 1)];
 #pragma unroll
-        for (int c = 0; c < MAXC; ++c) {
-          const bool take_next = (c + 1 < MAXC) && !lt[c + 1 < MAXC ? c + 1 : 0];
-          const bool keep = (c >= 1) && lt[c >= 1 ? c : 1];
-          nk[c] = take_next ? k[c + 1 < MAXC ? c + 1 : c] : (keep ? k[c] : v);
+            for (int t = 0; t < 8; ++t) {
+              if (i0 + t < m) {
+                if (lane == i0 + t) mycore = (uint32_t)k0 & 31u;
+                const uint64_t v = k0 + pp[t];
+                const bool c1 = v < k1, c2 = v < k2, c3 = v < k3;
+                const uint64_t n0 = c1 ? v : k1;
+                const uint64_t n1 = c1 ? k1 : (c2 ? v : k2);
+                const uint64_t n2 = c2 ? k2 : (c3 ? v : k3);
+                const uint64_t n3 = c3 ? k3 : v;
+                k0 = n0; k1 = n1; k2 = n2; k3 = n3;
+              }
+            }
+          }
+          k[0] = k0; k[1] = k1;
+          if (MAXC > 2) k[MAXC > 2 ? 2 : 1] = k2;
+          if (MAXC > 3) k[MAXC > 3 ? 3 : 1] = k3;
+        } else {
+          for (uint32_t i = 0; i < m; ++i) {
+            const uint64_t p = (uint64_t)__shfl_sync(0xFFFFFFFFu, mine, i);
+            const uint64_t v = k[0] + p;
+            if (lane == i) mycore = (uint32_t)(k[0] & 31u);
+            bool lt[MAXC];
+#pragma unroll
+            for (int c = 1; c < MAXC; ++c) lt[c] = v < k[c];
+            uint64_t nk[MAXC];
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {
+              const bool take_next = (c + 1 < MAXC) && !lt[c + 1 < MAXC ? c + 1 : 0];
+              const bool keep = (c >= 1) && lt[c >= 1 ? c : 1];
+              nk[c] = take_next ? k[c + 1 < MAXC ? c + 1 : c] : (keep ? k[c] : v);
+            }
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
+          }
         }
-#pragma unroll
-        for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
+        if (lane < m) s_core[q0 + lane] = (uint8_t)mycore;
       }
     }
     __syncthreads();

@@ -86,6 +86,22 @@ __device__ __forceinline__ uint32_t probe(const Lex& L, uint64_t k0, uint64_t k1
   }
 }
 
+// entry index + 1 of a lemma (0 = not in the lexicon)
+__device__ __forceinline__ uint32_t probe_idx(const Lex& L, uint64_t k0, uint64_t k1, uint32_t len) {
+  const uint32_t mask = (1u << L.bits) - 1u;
+  uint32_t h = lex_hash(k0, k1, len, L.bits);
+  for (;;) {
+    const uint32_t s = L.slots[h];
+    if (!s) return 0;
+    const LexEntry& e = L.e[s - 1];
+    if (e.k0 == k0 && e.k1 == k1 && e.len == len) return s;
+    h = (h + 1u) & mask;
+  }
+}
+
+// 12-bit prefilter index of a lemma from its first two bytes (b1 = 0 if the lemma has one byte)
+__host__ __device__ __forceinline__ uint32_t pref_idx(uint32_t b0, uint32_t b1) { return ((b0 << 5) ^ b1) & 0xFFFu; }
+
 __device__ __forceinline__ uint64_t mask_bytes(uint32_t nbytes) {  // nbytes in 0..8
   return nbytes >= 8 ? ~0ull : ((1ull << (8 * nbytes)) - 1ull);
 }
@@ -107,6 +123,29 @@ __device__ __forceinline__ uint32_t word_attr(const Lex& L, uint32_t len, uint64
   uint64_t m0 = k0 & mask_bytes(ll < 8 ? ll : 8);
   uint64_t m1 = ll > 8 ? (k1 & mask_bytes(ll - 8)) : 0ull;
   return probe(L, m0, m1, ll);
+}
+
+// Entry index + 1 of a word token (R-LEMMA), with the 2-byte prefilter.
+__device__ __forceinline__ uint32_t word_idx(const Lex& L, const uint32_t* pref, uint32_t len, uint64_t k0,
+                                             uint64_t k1, uint32_t s3) {
+  const uint32_t b1 = s3 & 0xFFu, b2 = (s3 >> 8) & 0xFFu, b3 = (s3 >> 16) & 0xFFu;
+  if (len == 3 && s3 == (('n' << 16) | ('\'' << 8) | 't')) {  // n't -> not
+    const uint32_t pi = pref_idx('n', 'o');
+    if (!((pref[pi >> 5] >> (pi & 31u)) & 1u)) return 0;
+    return probe_idx(L, (uint64_t)'n' | ((uint64_t)'o' << 8) | ((uint64_t)'t' << 16), 0ull, 3);
+  }
+  uint32_t strip = 0;
+  if (len >= 5 && b3 == 'i' && b2 == 'n' && b1 == 'g') strip = 3;
+  else if (len >= 4 && b2 == 'e' && b1 == 'd') strip = 2;
+  else if (len >= 4 && b2 == 'e' && b1 == 's') strip = 2;
+  else if (len >= 3 && b1 == 's' && b2 != 's') strip = 1;
+  const uint32_t ll = len - strip;
+  if (ll == 0 || ll > 16) return 0;
+  const uint32_t pi = pref_idx((uint32_t)(k0 & 0xFFu), ll >= 2 ? (uint32_t)((k0 >> 8) & 0xFFu) : 0u);
+  if (!((pref[pi >> 5] >> (pi & 31u)) & 1u)) return 0;
+  const uint64_t m0 = k0 & mask_bytes(ll < 8 ? ll : 8);
+  const uint64_t m1 = ll > 8 ? (k1 & mask_bytes(ll - 8)) : 0ull;
+  return probe_idx(L, m0, m1, ll);
 }
 
 // ------------------------------------------------------------ rule FSM
@@ -185,6 +224,28 @@ struct Rules {
     prev = T_OTHER;
   }
 
+  // add this thread's partial counters of one request into the tile accumulators
+  __device__ __forceinline__ void flush(uint32_t* acc9) {
+    const uint32_t v[9] = {S, Y, M, V, O, P, ntok, nd, nq};
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if (v[i]) atomicAdd(&acc9[i], v[i]);
+  }
+
+  // token record of the two-phase path: kind in bits 0..2, entry+1 in bits 3..15
+  __device__ __forceinline__ void on_record(uint32_t rec, const Lex& L) {
+    const uint32_t kind = rec & 7u;
+    if (kind == 1u) {
+      const uint32_t e = rec >> 3;
+      on_word(e ? L.e[e - 1].attr : 0u);
+    } else if (kind == 7u) {
+      ++nd;
+    } else if (kind != 0u) {
+      const uint32_t c = kind == 2u ? ',' : kind == 3u ? '.' : kind == 4u ? '?' : kind == 5u ? '!' : '#';
+      on_punct(c);
+    }
+  }
+
   // end of a W run: one clitic split (R-CLITIC), then word tokens
   __device__ __forceinline__ void end_run(const Lex& L) {
     const uint32_t n = wlen;
@@ -222,6 +283,17 @@ struct Rules {
     if (c == ' ' || (c - 9u) < 5u) return;        // S
     if (c - 0x21u < 0x5Eu) on_punct(c);           // P
     else ++nd;                                    // X: dropped, counted
+  }
+
+  static __device__ __forceinline__ void finish_acc(const uint32_t* a9, uint32_t f[8], bool& sat) {
+    unsigned long long Pt = (unsigned long long)a9[5] + (a9[8] > 1 ? a9[8] - 1 : 0);
+    uint64_t raw[8] = {a9[0], a9[1], a9[2], a9[3], a9[4], Pt, a9[6], a9[7]};
+    sat = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sat |= raw[k] > 65535ull;
+      f[k] = raw[k] > 65535ull ? 65535u : (uint32_t)raw[k];
+    }
   }
 
   __device__ __forceinline__ void finish(const Lex& L, uint32_t f[8], bool& sat) {
@@ -320,6 +392,330 @@ __global__ void __launch_bounds__(kThreads) k_score(ScoreLaunch a) {
   }
 }
 
+
+// ============================================================ K1 v2 (two-phase)
+// Phase 1 (byte-parallel): each thread classifies 128 staged bytes with a
+// bank-replicated class table (W / punctuation / dropped -> one bit each),
+// run starts are derived from the word masks (a run never crosses a request
+// start), a block scan gives every thread its record range, and every token
+// becomes a 16-bit record (kind + lexicon entry) -- words through the lemma,
+// a 2-byte prefilter and at most one hash probe.  Phase 2: one lane per
+// request walks its records with the rule FSM (R-RULES) and runs the fused
+// epilogue.  Tiles whose text or token count does not fit fall back to the
+// per-lane byte FSM over global memory (same rules, same results).
+constexpr uint32_t kT2 = 256;                 // threads = requests per tile
+constexpr uint32_t kStage2 = 32768;           // staged bytes per tile
+constexpr uint32_t kPer = kStage2 / kT2;      // bytes per thread in phase 1 (128)
+constexpr uint32_t kMaxRec = 8192;            // token records per tile
+constexpr uint32_t kW2 = kStage2 / 32;        // mask words per tile
+
+constexpr uint32_t kQ = 1024;                 // run queue entries per warp (reuses the class table)
+
+struct Smem2 {
+  uint32_t lut[256 * 32];        // class table replicated per lane: W 0x1, P 0x100, X 0x10000;
+                                 // reused as per-warp run queues in phase 1c
+  uint8_t pad0[16];              // zeros in front of stage (tail reads may start before 0)
+  uint8_t stage[kStage2 + 64];
+  uint32_t wmask[kW2 + 1];       // word bytes
+  uint32_t emask[kW2 + 1];       // punctuation / dropped bytes
+  uint32_t rmask[kW2 + 1];       // run starts
+  uint32_t marks[kW2 + 1];       // request starts
+  uint16_t rec[kMaxRec];
+  uint32_t rstart[kT2 + 1];      // first record of each request of the tile (+ total)
+  uint32_t tbase[kT2 + 1];
+  uint32_t wsum[kT2 / 32];
+  uint32_t pref[128];
+  uint32_t flag;
+};
+
+__device__ __forceinline__ uint32_t class_bits(uint32_t b) {
+  const uint32_t lc = b | 0x20u;
+  const bool w = (lc - 'a' < 26u) || (b - '0' < 10u) || b == '\'';
+  const bool sp = b == ' ' || (b - 9u) < 5u;
+  const bool p = !w && (b - 0x21u < 0x5Eu);
+  return w ? 0x1u : (p ? 0x100u : (sp ? 0u : 0x10000u));
+}
+
+__device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const uint32_t f[8]) {
+  if (!a.fused || a.feat) {
+    uint4 pk = make_uint4(f[0] | (f[1] << 16), f[2] | (f[3] << 16), f[4] | (f[5] << 16), f[6] | (f[7] << 16));
+    *reinterpret_cast<uint4*>(a.feat + (size_t)r * 8) = pk;
+  }
+  if (a.fused) {
+    const float u = regress(f, a.reg);
+    const uint32_t D = a.D_in ? a.D_in[r] : deadline_us(f[6], a.prof);
+    const int64_t arr = a.arrival ? a.arrival[r] : 0;
+    a.u[r] = u;
+    a.key[r] = priority_key(u, D, arr, a.prof);
+    if (a.D_out) a.D_out[r] = D;
+  }
+}
+
+// number of records produced by events at positions < p (p <= span)
+__device__ __forceinline__ uint32_t rec_index(const Smem2& S, uint32_t p, uint32_t total, uint32_t span) {
+  if (p >= span) return total;
+  const uint32_t t = p / kPer;
+  uint32_t idx = S.tbase[t];
+  const uint32_t w0 = t * (kPer / 32), wp = p >> 5;
+  for (uint32_t w = w0; w < wp; ++w) idx += __popc(S.emask[w]) + 2u * __popc(S.rmask[w]);
+  const uint32_t below = (p & 31u) ? ((1u << (p & 31u)) - 1u) : 0u;
+  idx += __popc(S.emask[wp] & below) + 2u * __popc(S.rmask[wp] & below);
+  return idx;
+}
+
+__global__ void __launch_bounds__(kT2, 2) k_score2(ScoreLaunch a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
+  uint8_t* tail_mem = smem_raw + ((sizeof(Smem2) + 15) & ~size_t(15));
+  LexEntry* s_ent = reinterpret_cast<LexEntry*>(tail_mem);
+  const uint32_t ent_bytes = a.lex.n_entries * (uint32_t)sizeof(LexEntry);
+  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + ((ent_bytes + 15u) & ~15u));
+  const uint32_t nslots = 1u << a.lex.bits;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  // ---- per-CTA tables
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.lex.entries);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_ent);
+    for (uint32_t i = tid; i < ent_bytes / 4; i += kT2) dst[i] = src[i];
+    for (uint32_t i = tid; i < nslots; i += kT2) s_slots[i] = a.lex.slots[i];
+    for (uint32_t i = tid; i < 128; i += kT2) S.pref[i] = 0;
+    for (uint32_t i = tid; i < 16; i += kT2) S.pad0[i] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < a.lex.n_entries; i += kT2) {
+    const LexEntry e = a.lex.entries[i];
+    const uint32_t pi = pref_idx((uint32_t)(e.k0 & 0xFFu), e.len >= 2 ? (uint32_t)((e.k0 >> 8) & 0xFFu) : 0u);
+    atomicOr(&S.pref[pi >> 5], 1u << (pi & 31u));
+  }
+  const Lex L{s_ent, s_slots, a.lex.bits};
+  const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
+  const uint32_t ntiles = (a.n + kT2 - 1) / kT2;
+
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t r0 = tile * kT2;
+    const uint32_t r1 = min(r0 + kT2, a.n);
+    const uint32_t b0 = a.offsets[r0];
+    uint32_t b1 = a.offsets[r1];
+    if (b1 < b0) b1 = b0;
+    const uint32_t base = b0 & ~15u;
+    const uint32_t span = b1 - base;
+    const uint32_t r = r0 + tid;
+    uint32_t s_r = 0, e_r = 0;
+    if (r < r1) {
+      s_r = a.offsets[r];
+      e_r = a.offsets[r + 1];
+      if (e_r < s_r) { atomicOr(a.flags, RT_FLAG_BAD_OFFSETS); e_r = s_r; }
+    }
+    __syncthreads();  // previous tile done with shared buffers (and tables ready)
+    bool fast = span <= kStage2;
+    bool in_order = true;
+    for (uint32_t i = tid; i < 256 * 32; i += kT2) S.lut[i] = class_bits(i >> 5);
+    if (fast) {
+      // ---- stage [base, base + span) and clear the masks
+      for (uint32_t off = tid * 16u; off < span; off += kT2 * 16u) {
+        const uint32_t g = base + off;
+        if (g + 16u <= total_bytes) *reinterpret_cast<uint4*>(S.stage + off) = ld_nc_v4(a.bytes + g);
+        else
+          for (uint32_t j = 0; j < 16u; ++j) S.stage[off + j] = g + j < total_bytes ? a.bytes[g + j] : 0;
+      }
+      for (uint32_t w = tid; w <= kW2; w += kT2) S.marks[w] = 0;
+      if (tid == 0) S.flag = 0;
+      __syncthreads();
+      if (r < r1 && s_r - base < span) atomicOr(&S.marks[(s_r - base) >> 5], 1u << ((s_r - base) & 31u));
+      // requests must be in byte order inside the tile for the record ranges
+      if (r < r1 && r > r0 && s_r < a.offsets[r - 1]) atomicOr(&S.flag, 2u);
+      // ---- phase 1a: classify kPer bytes per thread
+      const uint32_t p0 = tid * kPer;
+#pragma unroll 1
+      for (uint32_t w = 0; w < kPer / 32; ++w) {
+        const uint32_t pos = p0 + w * 32;
+        uint32_t W = 0, E = 0;
+        if (pos < span) {
+          const uint4 q0 = *reinterpret_cast<const uint4*>(S.stage + pos);
+          const uint4 q1 = *reinterpret_cast<const uint4*>(S.stage + pos + 16);
+          const uint32_t words[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc += S.lut[((words[g] >> (8 * i)) & 0xFFu) * 32u + lane] << i;
+            W |= (acc & 0xFu) << (4 * g);
+            E |= (((acc >> 8) | (acc >> 16)) & 0xFu) << (4 * g);
+          }
+          const uint32_t valid = span - pos >= 32 ? 0xFFFFFFFFu : ((1u << (span - pos)) - 1u);
+          W &= valid;
+          E &= valid;
+        }
+        S.wmask[(p0 >> 5) + w] = W;
+        S.emask[(p0 >> 5) + w] = E;
+      }
+      __syncthreads();
+      // ---- phase 1b: run starts and record counts
+      uint32_t cnt = 0;
+#pragma unroll 1
+      for (uint32_t w = 0; w < kPer / 32; ++w) {
+        const uint32_t wi = (p0 >> 5) + w;
+        const uint32_t W = S.wmask[wi];
+        const uint32_t prev = wi ? (S.wmask[wi - 1] >> 31) : 0u;
+        const uint32_t R = (W & ~((W << 1) | prev)) | (W & S.marks[wi]);
+        S.rmask[wi] = R;
+        cnt += __popc(S.emask[wi]) + 2u * __popc(R);
+      }
+      // block exclusive scan of cnt
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+      }
+      if (lane == 31) S.wsum[wid] = incl;
+      __syncthreads();
+      uint32_t wbase = 0;
+      for (uint32_t k = 0; k < wid; ++k) wbase += S.wsum[k];
+      S.tbase[tid] = wbase + incl - cnt;
+      uint32_t total = 0;
+      for (uint32_t k = 0; k < kT2 / 32; ++k) total += S.wsum[k];
+      if (tid == 0) S.tbase[kT2] = total;
+      in_order = !(S.flag & 2u);
+      fast = total <= kMaxRec && in_order;
+      if (fast) {
+        // ---- phase 1c (i): lanes walk their events; punctuation / dropped bytes
+        // become records, runs go to the warp's queue as (position, record index)
+        __syncthreads();  // class table no longer needed: reuse as run queues
+        uint32_t* q = S.lut + wid * kQ;
+        uint32_t k = wbase + incl - cnt;
+        uint32_t nq_local = 0;
+#pragma unroll 1
+        for (uint32_t w = 0; w < kPer / 32; ++w) {
+          const uint32_t wi = (p0 >> 5) + w;
+          const uint32_t R = S.rmask[wi];
+          uint32_t ev = R | S.emask[wi];
+          nq_local += __popc(R);
+          while (ev) {
+            const uint32_t bit = __ffs(ev) - 1;
+            ev &= ev - 1u;
+            if ((R >> bit) & 1u) { k += 2; continue; }
+            const uint32_t c = S.stage[wi * 32 + bit];
+            uint32_t kind = 7u;  // dropped byte
+            if (c - 0x21u < 0x5Eu) kind = c == ',' ? 2u : c == '.' ? 3u : c == '?' ? 4u : c == '!' ? 5u : 6u;
+            S.rec[k++] = (uint16_t)kind;
+          }
+        }
+        // queue slots: exclusive scan of run counts inside the warp
+        uint32_t qincl = nq_local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, qincl, o);
+          if (lane >= (uint32_t)o) qincl += v;
+        }
+        const uint32_t qtot = __shfl_sync(0xFFFFFFFFu, qincl, 31);
+        if (qtot > kQ) {
+          if (lane == 0) atomicOr(&S.flag, 4u);  // queue overflow: whole tile falls back
+        } else {
+          uint32_t slot = qincl - nq_local;
+          k = wbase + incl - cnt;
+#pragma unroll 1
+          for (uint32_t w = 0; w < kPer / 32; ++w) {
+            const uint32_t wi = (p0 >> 5) + w;
+            const uint32_t R = S.rmask[wi];
+            uint32_t ev = R | S.emask[wi];
+            while (ev) {
+              const uint32_t bit = __ffs(ev) - 1;
+              ev &= ev - 1u;
+              if ((R >> bit) & 1u) {
+                q[slot++] = (wi * 32 + bit) | (k << 15);
+                k += 2;
+              } else {
+                ++k;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        // ---- phase 1c (ii): the warp processes its runs 32 at a time
+        const uint32_t* st32 = reinterpret_cast<const uint32_t*>(S.stage);
+        for (uint32_t e = lane; e < (qtot > kQ ? 0u : qtot); e += 32) {
+          const uint32_t ent = q[e];
+          const uint32_t x = ent & 0x7FFFu, kk = ent >> 15;
+          // run length: up to the first non-word byte or the next request start
+          uint32_t n = 1;
+          {
+            uint32_t qq = x + 1;
+            for (;;) {
+              if (qq >= span) break;
+              const uint32_t qw = qq >> 5, qb = qq & 31u;
+              const uint32_t stop = (~S.wmask[qw] | S.marks[qw]) >> qb;
+              if (stop) { n += __ffs(stop) - 1; break; }
+              n += 32 - qb;
+              qq += 32 - qb;
+            }
+          }
+          // first 16 bytes (lowercased; bytes past the run are masked by length)
+          const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
+          const uint32_t w0 = st32[a0], w1 = st32[a0 + 1], w2 = st32[a0 + 2], w3 = st32[a0 + 3], w4 = st32[a0 + 4];
+          const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
+          const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
+          const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
+          const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
+          // last (up to) 6 bytes, newest in the low byte: byte-reverse of the 8 bytes ending at x + n
+          const int32_t tb = (int32_t)(x + n) - 8;  // may be negative: stage has a zero pad in front
+          const uint32_t ta = (uint32_t)(tb + 16) >> 2, tsh = ((uint32_t)(tb + 16) & 3u) * 8u;
+          const uint32_t* pz = reinterpret_cast<const uint32_t*>(S.pad0);
+          const uint32_t v0 = pz[ta], v1 = pz[ta + 1], v2 = pz[ta + 2];
+          const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
+          uint64_t tail = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
+          tail = (tail | 0x2020202020202020ull) & mask_bytes(n < 6 ? n : 6);
+          const uint32_t t3 = (uint32_t)(tail & 0xFFFFFFu), t2 = (uint32_t)(tail & 0xFFFFu);
+          uint32_t cut = 0;
+          if (n > 3 && t3 == (('n' << 16) | ('\'' << 8) | 't')) cut = 3;
+          else if (n > 2 && (t2 == (('\'' << 8) | 's') || t2 == (('\'' << 8) | 'm') || t2 == (('\'' << 8) | 'd')))
+            cut = 2;
+          else if (n > 3 && (t3 == (('\'' << 16) | ('r' << 8) | 'e') || t3 == (('\'' << 16) | ('v' << 8) | 'e') ||
+                             t3 == (('\'' << 16) | ('l' << 8) | 'l')))
+            cut = 3;
+          if (!cut) {
+            S.rec[kk] = (uint16_t)(1u | (word_idx(L, S.pref, n, k0, k1, t3) << 3));
+            S.rec[kk + 1] = 0;
+          } else {
+            const uint32_t ns = n - cut;
+            S.rec[kk] = (uint16_t)(1u | (word_idx(L, S.pref, ns, k0, k1, (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu)) << 3));
+            const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
+            S.rec[kk + 1] = (uint16_t)(1u | (word_idx(L, S.pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu)) << 3));
+          }
+        }
+      }
+      __syncthreads();
+      fast = fast && !(S.flag & 4u);
+      __syncthreads();
+      if (fast && r < r1) {
+        // ---- phase 2: rule FSM over this request's records
+        const uint32_t total2 = S.tbase[kT2];
+        const uint32_t i0 = rec_index(S, s_r - base, total2, span);
+        const uint32_t i1 = rec_index(S, e_r - base, total2, span);
+        Rules R;
+        R.init();
+        for (uint32_t i = i0; i < i1; ++i) R.on_record(S.rec[i], L);
+        uint32_t f[8];
+        bool sat;
+        R.finish(L, f, sat);
+        if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+        epilogue(a, r, f);
+      }
+    }
+    if (!fast && r < r1) {
+      // ---- fallback: per-lane byte FSM over global memory
+      Rules R;
+      R.init();
+      for (uint32_t i = s_r; i < e_r; ++i) R.byte(__ldg(a.bytes + i), L);
+      uint32_t f[8];
+      bool sat;
+      R.finish(L, f, sat);
+      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+      epilogue(a, r, f);
+    }
+  }
+}
+
 __global__ void k_predict(const uint16_t* __restrict__ feat, uint32_t n, rt_regressor reg, float* __restrict__ u) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -347,17 +743,18 @@ size_t score_smem_bytes(const DevLexicon& lex) {
 
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  const size_t smem = score_smem_bytes(a.lex);
-  cudaError_t e = cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = ((sizeof(Smem2) + 15) & ~size_t(15)) + ((a.lex.n_entries * sizeof(LexEntry) + 15) & ~size_t(15)) +
+                      (((size_t(1) << a.lex.bits) * 2 + 15) & ~size_t(15));
+  cudaError_t e = cudaFuncSetAttribute(k_score2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score2, kT2, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const uint32_t ntiles = (a.n + kThreads - 1) / kThreads;
+  const uint32_t ntiles = (a.n + kT2 - 1) / kT2;
   uint32_t grid = (uint32_t)(a.num_sms * per_sm);
   if (grid > ntiles) grid = ntiles;
-  k_score<<<grid, kThreads, smem, s>>>(a);
+  k_score2<<<grid, kT2, smem, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

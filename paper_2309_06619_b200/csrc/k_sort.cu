@@ -31,29 +31,32 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
     if (i < n) atomicAdd(&h[(uint32_t)(~keys[i] >> shift) & 0xFFu], 1u);
   }
   __syncthreads();
-  hist[threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  hist[blockIdx.x * 256u + threadIdx.x] = h[threadIdx.x];  // tile-major
 }
 
-// exclusive scan of 256 * ntiles counters by one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ hist, uint32_t total) {
-  __shared__ uint32_t part[1024];
-  const uint32_t per = (total + 1023) / 1024;
-  const uint32_t lo = threadIdx.x * per, hi = min(lo + per, total);
+// exclusive scan of the tile-major histogram in digit-major order: thread d
+// owns digit d (coalesced across threads), sums its column, a block scan over
+// digits gives the digit bases, a second pass writes the running offsets.
+__global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ hist, uint32_t ntiles) {
+  __shared__ uint32_t wsum[8];
+  const uint32_t d = threadIdx.x, lane = d & 31u, w = d >> 5;
   uint32_t s = 0;
-  for (uint32_t i = lo; i < hi; ++i) s += hist[i];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  // Hillis-Steele inclusive scan over 1024 partials
-  for (int d = 1; d < 1024; d <<= 1) {
-    uint32_t v = threadIdx.x >= (uint32_t)d ? part[threadIdx.x - d] : 0u;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
+#pragma unroll 8
+  for (uint32_t t = 0; t < ntiles; ++t) s += hist[t * 256u + d];
+  uint32_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
   }
-  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
-  for (uint32_t i = lo; i < hi; ++i) {
-    uint32_t v = hist[i];
-    hist[i] = run;
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t run = incl - s;
+  for (uint32_t k = 0; k < w; ++k) run += wsum[k];
+#pragma unroll 8
+  for (uint32_t t = 0; t < ntiles; ++t) {
+    const uint32_t v = hist[t * 256u + d];
+    hist[t * 256u + d] = run;
     run += v;
   }
 }
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
   __shared__ uint32_t s_base[256];           // running output position per digit
   __shared__ uint16_t s_cnt[kWarps][256];    // per-warp digit counts of the current round
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  s_base[threadIdx.x] = hist[threadIdx.x * ntiles + blockIdx.x];
+  s_base[threadIdx.x] = hist[blockIdx.x * 256u + threadIdx.x];
   const uint32_t t0 = blockIdx.x * kTile;
   const uint32_t lt = (1u << lane) - 1u;
   for (int k = 0; k < kItems; ++k) {
@@ -133,7 +136,7 @@ cudaError_t radix_sort_desc(const uint64_t* keys_in, uint32_t base_index, uint32
     // values ping-pong between perm_out and v2 so that the last pass writes perm_out
     uint32_t* vdst = ((nsh - 1 - j) & 1) ? v2 : perm_out;
     k_hist<<<ntiles, kThreads, 0, s>>>(ksrc, n, shift, ntiles, hist);
-    k_scan<<<1, 1024, 0, s>>>(hist, 256 * ntiles);
+    k_scan<<<1, 256, 0, s>>>(hist, ntiles);
     k_scatter<<<ntiles, kThreads, 0, s>>>(ksrc, vsrc, base_index, n, shift, ntiles, hist, kdst, vdst);
     note_launch(3);
     ksrc = kdst;
