@@ -241,90 +241,134 @@ __global__ void __launch_bounds__(64) k_sched_big(SchedLaunch a, uint32_t q, uin
 // index is key[0] and a job is an add plus a sorted insert of key[0] + (p << 5)
 // (exact while t < 2^58 µs).
 constexpr uint32_t kCpuChunk = 4096;
+
+// one job of list scheduling on the sorted keys: remove k[0], insert k[0] + p
+template <int MAXC>
+__device__ __forceinline__ void list_step(uint64_t (&k)[MAXC], uint64_t p) {
+  const uint64_t v = k[0] + p;
+  bool lt[MAXC];
+#pragma unroll
+  for (int c = 1; c < MAXC; ++c) lt[c] = v < k[c];
+  uint64_t nk[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const bool take_next = (c + 1 < MAXC) && !lt[c + 1 < MAXC ? c + 1 : 0];
+    const bool keep = (c >= 1) && lt[c >= 1 ? c : 1];
+    nk[c] = take_next ? k[c + 1 < MAXC ? c + 1 : c] : (keep ? k[c] : v);
+  }
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
+}
+template <int MAXC>
+__device__ __forceinline__ void cpu_chunk_serial(uint64_t (&k)[MAXC], const int64_t* pred, uint8_t* core,
+                                                 uint32_t cnt, bool small) {
+  if (small) {
+    // keys relative to the smallest one: d_c = k_c - k_0 (u32), base = k_0.
+    // A job: insert p into (d1, d2, d3) by min/max, rebase by the new minimum.
+    uint64_t base = k[0];
+    uint32_t d1 = (uint32_t)(k[1] - base), d2 = (uint32_t)(k[MAXC > 2 ? 2 : 1] - base),
+             d3 = (uint32_t)(k[MAXC > 3 ? 3 : 1] - base);
+    uint32_t q = 0;
+    for (; q + 8 <= cnt; q += 8) {
+      uint32_t pp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) pp[t] = (uint32_t)pred[q + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        core[q + t] = (uint8_t)(base & 31u);
+        const uint32_t v = pp[t];
+        const uint32_t e0 = min(d1, v), e1 = min(max(d1, v), d2), e2 = min(max(d2, v), d3), e3 = max(d3, v);
+        base += e0;
+        d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
+      }
+    }
+    for (; q < cnt; ++q) {
+      core[q] = (uint8_t)(base & 31u);
+      const uint32_t v = (uint32_t)pred[q];
+      const uint32_t e0 = min(d1, v), e1 = min(max(d1, v), d2), e2 = min(max(d2, v), d3), e3 = max(d3, v);
+      base += e0;
+      d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
+    }
+    k[0] = base;
+    k[1] = base + d1;
+    if (MAXC > 2) k[MAXC > 2 ? 2 : 1] = base + d2;
+    if (MAXC > 3) k[MAXC > 3 ? 3 : 1] = base + d3;
+  } else {
+    uint32_t q = 0;
+    for (; q + 8 <= cnt; q += 8) {
+      uint64_t pp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) pp[t] = (uint64_t)pred[q + t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        core[q + t] = (uint8_t)(k[0] & 31u);
+        list_step<MAXC>(k, pp[t]);
+      }
+    }
+    for (; q < cnt; ++q) {
+      core[q] = (uint8_t)(k[0] & 31u);
+      list_step<MAXC>(k, (uint64_t)pred[q]);
+    }
+  }
+}
+
+// CPU class of a large queue.  Warp 0 (one lane) runs the list-scheduling
+// recurrence on chunk c while warps 1..7 compute the predicted latencies of
+// chunk c+1 and write the assignments of chunk c-1 (double-buffered).
 template <int MAXC>
 __global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p) {
-  __shared__ int64_t s_pred[kCpuChunk];
-  __shared__ uint8_t s_core[kCpuChunk];
+  extern __shared__ __align__(16) uint8_t cpu_smem[];
+  int64_t* s_pred = reinterpret_cast<int64_t*>(cpu_smem);                 // [2][kCpuChunk]
+  uint8_t* s_core = cpu_smem + 2 * kCpuChunk * sizeof(int64_t);           // [2][kCpuChunk]
+  __shared__ int s_small[2];
   const uint32_t ncpu = *ncpu_p;
   const uint32_t* perm = a.perm + lo;
   const float eta = __ll2float_rn(a.prof.eta_us);
   const uint32_t cores = a.cores;
-  const uint32_t lane = threadIdx.x & 31u;
-  uint64_t k[MAXC];  // identical in every lane of warp 0
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) k[c] = c < (int)cores ? (uint64_t)c : ~0ull;  // unused cores never chosen
-  for (uint32_t j0 = 0; j0 < ncpu; j0 += kCpuChunk) {
-    const uint32_t cnt = min(kCpuChunk, ncpu - j0);
-    for (uint32_t q = threadIdx.x; q < cnt; q += 256) {
+  const uint32_t nchunks = (ncpu + kCpuChunk - 1) / kCpuChunk;
+  auto fill = [&](uint32_t c, uint32_t t0, uint32_t nt) {  // predictions of chunk c by threads t0..t0+nt-1
+    const uint32_t j0 = c * kCpuChunk, cnt = min(kCpuChunk, ncpu - j0);
+    int64_t* pb = s_pred + (c & 1) * kCpuChunk;
+    bool big = false;
+    for (uint32_t q = threadIdx.x - t0; q < cnt; q += nt) {
       const float eu = __fmul_rn(eta, a.u[perm[j0 + q]]);
-      s_pred[q] = ((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu))) << 5;
+      const int64_t pr = ((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu))) << 5;
+      pb[q] = pr;
+      big |= (uint64_t)pr >= 0xFFFFFFFFull;
     }
-    __syncthreads();
-    if (threadIdx.x < 32 && cores) {
-      // warp 0 runs the recurrence redundantly in every lane; 32 predictions
-      // are fetched per step and broadcast with shuffles (off the critical path)
-      int64_t nextp = lane < cnt ? s_pred[lane] : 0;
-      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
-        const int64_t mine = nextp;
-        nextp = (q0 + 32 + lane < cnt) ? s_pred[q0 + 32 + lane] : 0;
-        const uint32_t m = min(32u, cnt - q0);
-        uint32_t mycore = 0;
-        if (MAXC == 4) {
-          // four sorted keys: v = k0 + p; three compares; selects.  Predictions
-          // are read 8 at a time (broadcast loads hoisted off the chain).
-          uint64_t k0 = k[0], k1 = k[1], k2 = k[MAXC > 2 ? 2 : 1], k3 = k[MAXC > 3 ? 3 : 1];
-          for (uint32_t i0 = 0; i0 < m; i0 += 8) {
-            uint64_t pp[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) pp[t] = (uint64_t)s_pred[q0 + min(i0 + t, m - 1)];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              if (i0 + t < m) {
-                if (lane == i0 + t) mycore = (uint32_t)k0 & 31u;
-                const uint64_t v = k0 + pp[t];
-                const bool c1 = v < k1, c2 = v < k2, c3 = v < k3;
-                const uint64_t n0 = c1 ? v : k1;
-                const uint64_t n1 = c1 ? k1 : (c2 ? v : k2);
-                const uint64_t n2 = c2 ? k2 : (c3 ? v : k3);
-                const uint64_t n3 = c3 ? k3 : v;
-                k0 = n0; k1 = n1; k2 = n2; k3 = n3;
-              }
-            }
-          }
-          k[0] = k0; k[1] = k1;
-          if (MAXC > 2) k[MAXC > 2 ? 2 : 1] = k2;
-          if (MAXC > 3) k[MAXC > 3 ? 3 : 1] = k3;
-        } else {
-          for (uint32_t i = 0; i < m; ++i) {
-            const uint64_t p = (uint64_t)__shfl_sync(0xFFFFFFFFu, mine, i);
-            const uint64_t v = k[0] + p;
-            if (lane == i) mycore = (uint32_t)(k[0] & 31u);
-            bool lt[MAXC];
-#pragma unroll
-            for (int c = 1; c < MAXC; ++c) lt[c] = v < k[c];
-            uint64_t nk[MAXC];
-#pragma unroll
-            for (int c = 0; c < MAXC; ++c) {
-              const bool take_next = (c + 1 < MAXC) && !lt[c + 1 < MAXC ? c + 1 : 0];
-              const bool keep = (c >= 1) && lt[c >= 1 ? c : 1];
-              nk[c] = take_next ? k[c + 1 < MAXC ? c + 1 : c] : (keep ? k[c] : v);
-            }
-#pragma unroll
-            for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
-          }
-        }
-        if (lane < m) s_core[q0 + lane] = (uint8_t)mycore;
-      }
-    }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < cnt; q += 256) {
+    if (big) s_small[c & 1] = 0;
+  };
+  auto drain = [&](uint32_t c, uint32_t t0, uint32_t nt) {  // write assignments of chunk c
+    const uint32_t j0 = c * kCpuChunk, cnt = min(kCpuChunk, ncpu - j0);
+    const uint8_t* cb = s_core + (c & 1) * kCpuChunk;
+    for (uint32_t q = threadIdx.x - t0; q < cnt; q += nt) {
       const uint32_t i = perm[j0 + q];
-      a.core_of[i] = cores ? s_core[q] : (uint8_t)0xFF;
+      a.core_of[i] = cores ? cb[q] : (uint8_t)0xFF;
       a.batch_of[i] = kNoBatch;
       a.slot_of[i] = 0;
     }
+  };
+  uint64_t k[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) k[c] = c < (int)cores ? (uint64_t)c : ~0ull;  // unused cores never chosen
+  if (threadIdx.x < 2) s_small[threadIdx.x] = (MAXC == 4 && cores == 4) ? 1 : 0;
+  __syncthreads();
+  if (nchunks) fill(0, 0, 256);
+  __syncthreads();
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0 && cores)
+        cpu_chunk_serial<MAXC>(k, s_pred + (c & 1) * kCpuChunk, s_core + (c & 1) * kCpuChunk,
+                               min(kCpuChunk, ncpu - c * kCpuChunk), s_small[c & 1] != 0);
+    } else {
+      if (threadIdx.x == 32) s_small[(c + 1) & 1] = (MAXC == 4 && cores == 4) ? 1 : 0;
+      asm volatile("bar.sync 1, 224;");
+      if (c + 1 < nchunks) fill(c + 1, 32, 224);
+      if (c >= 1) drain(c - 1, 32, 224);
+    }
     __syncthreads();
   }
+  if (nchunks) drain(nchunks - 1, 0, 256);
 }
 
 // seg_batch_off = exclusive scan of seg_count (one CTA)
@@ -390,9 +434,17 @@ cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
 
 cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu, cudaStream_t s) {
   (void)n;
-  if (a.cores <= 4) k_cpu_big<4><<<1, 256, 0, s>>>(a, lo, ncpu);
-  else if (a.cores <= 8) k_cpu_big<8><<<1, 256, 0, s>>>(a, lo, ncpu);
-  else k_cpu_big<32><<<1, 256, 0, s>>>(a, lo, ncpu);
+  const int smem = 2 * kCpuChunk * (sizeof(int64_t) + 1);
+  if (a.cores <= 4) {
+    cudaFuncSetAttribute(k_cpu_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_big<4><<<1, 256, smem, s>>>(a, lo, ncpu);
+  } else if (a.cores <= 8) {
+    cudaFuncSetAttribute(k_cpu_big<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_big<8><<<1, 256, smem, s>>>(a, lo, ncpu);
+  } else {
+    cudaFuncSetAttribute(k_cpu_big<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_big<32><<<1, 256, smem, s>>>(a, lo, ncpu);
+  }
   note_launch();
   return cudaGetLastError();
 }
