@@ -287,3 +287,33 @@ def test_config2_full_size(ctx_v1, lex_v1):
     g = ctx_v1.schedule(out["key"], out["u"], seg, d["profile"])
     torch.cuda.synchronize()
     _check_schedule(g, oracle.schedule(k, u, seg, d["profile"]), 1)
+
+
+def test_config4_shape_parity(ctx_v1, lex_v1):
+    """BASELINE configs[3] shape: traces of 1024 requests (65 536 per job, 8 192
+    per rank); a sample of one rank's shard replayed against the oracle."""
+    d = configs.config4_shard(rank=3, world=8, n_traces=65536, per_trace=1024)
+    sub = {k: d[k] for k in ("profiles", "regressors", "lexicon")}
+    # take the first 24 traces of the shard (bytes/offsets sliced consistently)
+    nt = 24
+    lo_req, hi_req = 0, int(d["trace_off"][nt])
+    b0, b1 = int(d["offsets"][lo_req]), int(d["offsets"][hi_req])
+    sub.update(data=d["data"][b0:b1], offsets=(d["offsets"][:hi_req + 1] - b0).astype(np.uint32),
+               arrival_us=d["arrival_us"][:hi_req], true_len=d["true_len"][:hi_req],
+               trace_off=d["trace_off"][:nt + 1], trace_prof=d["trace_prof"][:nt])
+    _replay_case(ctx_v1, lex_v1, sub, {})
+
+
+@pytest.mark.parametrize("point", [
+    {"policy": "FIFO", "consolidate": 0, "offload": 0}, {"policy": "EDF", "consolidate": 0, "offload": 0},
+    {"policy": "LUF", "consolidate": 0, "offload": 0}, {"policy": "MUF", "consolidate": 0, "offload": 0},
+    {"policy": "UP", "consolidate": 0, "offload": 0}, {"policy": "UP", "consolidate": 1, "offload": 0},
+    {"policy": "UP", "alpha": 0.0}, {"policy": "UP", "alpha": 2.0}, {"policy": "UP", "b10": 10},
+    {"policy": "UP", "b10": 30}, {"tightness": 2}])
+@pytest.mark.parametrize("mult", [0.25, 4.0, 32.0])
+def test_config5_sweep_points(ctx_v1, lex_v1, point, mult):
+    """BASELINE configs[4]: arrival-rate multipliers x policy / consolidation /
+    offload / alpha / b / tightness points."""
+    d = configs.traces(5, range(int(mult * 100), int(mult * 100) + 8), 1000, lambda t: t % 4,
+                       beta0=10 * mult, step=1 * mult, beta_max=150 * mult)
+    _replay_case(ctx_v1, lex_v1, d, point)
