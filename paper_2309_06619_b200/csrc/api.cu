@@ -465,7 +465,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   for (uint32_t q = 0; q < nq; ++q) {
     const uint32_t m = h_seg_off[q + 1] - h_seg_off[q];
     if (m > rtlm::kSmallSeg) {
-      size_t need = std::max(rtlm::radix_sort_workspace(m), rtlm::ff_workspace(m, rtlm::ff_levels(m), (uint32_t)prof->C));
+      size_t need = rtlm::big_queue_workspace(m, (uint32_t)prof->C);
       if (need > big_ws) big_ws = need;
     }
   }
@@ -494,10 +494,8 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   for (uint32_t q = 0; q < nq; ++q) {
     const uint32_t lo = h_seg_off[q], hi = h_seg_off[q + 1];
     if (hi - lo <= rtlm::kSmallSeg) continue;
-    e = rtlm::radix_sort_desc(d_key + lo, lo, hi - lo, d_perm + lo, full64, big, s);
-    if (e != cudaSuccess) return cuda_fail(c, e, "radix_sort_desc");
-    e = rtlm::launch_ff(a, q, lo, hi, big, s, c->aux, c->ev_fork, c->ev_join);
-    if (e != cudaSuccess) return cuda_fail(c, e, "k_ff");
+    e = rtlm::launch_big_queue(a, q, lo, hi, full64, big, s, c->aux, c->ev_fork, c->ev_join);
+    if (e != cudaSuccess) return cuda_fail(c, e, "big queue schedule");
   }
   e = rtlm::launch_sched_finish(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_finish");

@@ -88,6 +88,11 @@ cudaError_t launch_key(const float* u, const uint16_t* feat, const int64_t* arri
 size_t radix_sort_workspace(uint32_t n);
 cudaError_t radix_sort_desc(const uint64_t* keys_in, uint32_t base_index, uint32_t n, uint32_t* perm_out,
                             int full64, void* workspace, cudaStream_t s);
+cudaError_t radix_sort_desc2(const uint64_t* keys_in, const uint32_t* vals_in, uint32_t base_index, uint32_t n,
+                             const uint32_t* n_dev, uint32_t* perm_out, int full64, void* workspace, cudaStream_t s);
+// stable split by class bit: CPU-class keys/indices (ck, cv), GPU-class (gk, gv); counts[0..1] on device
+cudaError_t split_by_class(const uint64_t* key, uint32_t base, uint32_t n, uint32_t* bsum, uint32_t* counts,
+                           uint64_t* ck, uint32_t* cv, uint64_t* gk, uint32_t* gv, cudaStream_t s);
 
 struct SchedLaunch {
   const uint64_t* key;
@@ -105,17 +110,19 @@ struct SchedLaunch {
 };
 // small queues (all segments with n <= kSmallSeg; others skipped)
 cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s);
-// one large queue [lo, hi) whose perm is already sorted in a.perm
-cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, float* u_sorted_ws,
-                             cudaStream_t s);
 cudaError_t launch_sched_finish(const SchedLaunch& a, cudaStream_t s);
 // CPU class of a large queue [lo, lo+n) (ncpu read from device memory)
-cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu_dev, cudaStream_t s);
+size_t cpu_big_workspace(uint32_t n);
+cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu_dev, void* ws,
+                           cudaStream_t s);
 // GPU class of a large queue: parallel exact consolidation (k_ff.cu)
 size_t ff_workspace(uint32_t n, uint32_t levels, uint32_t C);
 uint32_t ff_levels(uint32_t n);
-cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, void* ws, cudaStream_t s,
-                      cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);
+// one large queue: class split, CPU-class sort + list scheduling on `aux`,
+// GPU-class sort + consolidation on `s` (joined before return)
+size_t big_queue_workspace(uint32_t n, uint32_t C);
+cudaError_t launch_big_queue(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, int full64, void* ws,
+                             cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join);
 
 struct ReplayLaunch {
   const int64_t* arrival;

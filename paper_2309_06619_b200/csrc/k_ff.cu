@@ -17,6 +17,8 @@
 // failing positions into a successor forest, find the trajectory's path by
 // pointer doubling, and emit ∅-run chunks and path excursions in parallel.
 // The last partial windows (stream exhausted) are finished by one warp (tail).
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace rtlm {
@@ -32,7 +34,9 @@ __device__ __forceinline__ uint32_t kk_p(uint64_t k) { return (uint32_t)k; }
 
 struct FF {
   // inputs
-  const uint32_t* perm;   // queue-relative priority order (global indices), CPU class first
+  uint32_t* perm;         // queue-relative priority order output (global indices), CPU class first
+  const uint32_t* gperm;  // GPU class in priority order (global indices)
+  const uint32_t* ncpu_dev;
   const float* u;
   const uint64_t* key;
   uint32_t n;             // queue length
@@ -83,23 +87,16 @@ __device__ __forceinline__ void put(const FF& f, uint64_t x, uint32_t b, uint32_
 
 // ------------------------------------------------------------ 1. gather
 __global__ void k_ff_gather(FF f) {
-  const uint32_t ncpu = f.scal[0], G = f.n - ncpu;
+  const uint32_t ncpu = *f.ncpu_dev, G = f.n - ncpu;
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < G; p += gridDim.x * blockDim.x) {
-    const float uu = f.u[f.perm[ncpu + p]];
-    f.kk[p] = ((uint64_t)ord32_bits(__float_as_uint(uu)) << 32) | p;
+    const uint32_t g = f.gperm[p];
+    f.perm[ncpu + p] = g;  // the API's priority order (GPU class after the CPU class)
+    f.kk[p] = ((uint64_t)ord32_bits(__float_as_uint(f.u[g])) << 32) | p;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    f.scal[0] = ncpu;
     f.scal[1] = G;
     f.scal[2] = G > f.K ? G - f.K : 0u;
-  }
-}
-
-// count the CPU class (a prefix of the sorted queue)
-__global__ void k_ff_ncpu(FF f) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < f.n; j += gridDim.x * blockDim.x) {
-    const bool cpu = (f.key[f.perm[j]] >> 63) != 0;
-    const bool next_gpu = (j + 1 == f.n) || ((f.key[f.perm[j + 1]] >> 63) == 0);
-    if (cpu && next_gpu) f.scal[0] = j + 1;
   }
 }
 
@@ -764,9 +761,9 @@ __global__ void k_ff_emit_stretch(FF f) {
 
 // scatter the per-position results to global element indices
 __global__ void k_ff_scatter(FF f) {
-  const uint32_t ncpu = f.scal[0], G = f.scal[1];
+  const uint32_t G = f.scal[1];
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < G; p += gridDim.x * blockDim.x) {
-    const uint32_t g = f.perm[ncpu + p];
+    const uint32_t g = f.gperm[p];
     f.batch_of[g] = f.batch_p[p];
     f.slot_of[g] = f.slot_p[p];
     f.core_of[g] = 0xFF;
@@ -804,12 +801,14 @@ uint32_t ff_levels(uint32_t n) {
   return l + 1;
 }
 
-cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, void* ws, cudaStream_t s,
-                      cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+static cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, const uint32_t* gperm,
+                             const uint32_t* ncpu_dev, void* ws, cudaStream_t s) {
   const uint32_t n = hi - lo;
   const uint32_t levels = ff_levels(n);
   FF f{};
   f.perm = a.perm + lo;
+  f.gperm = gperm;
+  f.ncpu_dev = ncpu_dev;
   f.u = a.u;
   f.key = a.key;
   f.n = n;
@@ -858,14 +857,6 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
 
   cudaMemsetAsync(f.scal, 0, 64, s);
   const uint32_t g1 = (n + 255) / 256;
-  k_ff_ncpu<<<g1, 256, 0, s>>>(f);
-  note_launch();
-  // CPU class (serial list scheduling) runs concurrently on the aux stream
-  cudaEventRecord(ev_fork, s);
-  cudaStreamWaitEvent(aux, ev_fork, 0);
-  cudaError_t e = launch_cpu_big(a, lo, n, f.scal, aux);
-  if (e != cudaSuccess) return e;
-  cudaEventRecord(ev_join, aux);
   k_ff_gather<<<g1, 256, 0, s>>>(f);
   note_launch();
   if (f.K == 0) {
@@ -906,6 +897,46 @@ cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi
   k_ff_emit_stretch<<<1184, 256, 0, s>>>(f);
   k_ff_scatter<<<g1, 256, 0, s>>>(f);
   note_launch(6);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ one large queue
+size_t big_queue_workspace(uint32_t n, uint32_t C) {
+  const size_t split = (((size_t)n / 256 + 2) * 4 + 64 + (size_t)n * 12 * 2 + (size_t)n * 4 + 8 * 256);
+  const size_t sortw = radix_sort_workspace(n);
+  size_t ffw = ff_workspace(n, ff_levels(n), C);
+  return split + std::max(sortw, cpu_big_workspace(n)) + (ffw > sortw ? ffw : sortw) + 5 * 256;
+}
+
+cudaError_t launch_big_queue(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, int full64, void* ws,
+                             cudaStream_t s, cudaStream_t aux, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+  const uint32_t n = hi - lo;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
+  uint32_t* bsum = reinterpret_cast<uint32_t*>(take(((size_t)n / 256 + 2) * 4));
+  uint32_t* counts = reinterpret_cast<uint32_t*>(take(64));  // [0] CPU class, [1] GPU class
+  uint64_t* ck = reinterpret_cast<uint64_t*>(take((size_t)n * 8));
+  uint32_t* cv = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+  uint64_t* gk = reinterpret_cast<uint64_t*>(take((size_t)n * 8));
+  uint32_t* gv = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+  uint32_t* gperm = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+  void* cpu_ws = take(std::max(radix_sort_workspace(n), cpu_big_workspace(n)));
+  void* main_ws = p;  // GPU-class sort, then the consolidation pipeline
+  cudaError_t e = split_by_class(a.key + lo, lo, n, bsum, counts, ck, cv, gk, gv, s);
+  if (e != cudaSuccess) return e;
+  // CPU class: sort + list scheduling on the forked stream
+  cudaEventRecord(ev_fork, s);
+  cudaStreamWaitEvent(aux, ev_fork, 0);
+  e = radix_sort_desc2(ck, cv, 0, n, counts + 0, a.perm + lo, full64, cpu_ws, aux);
+  if (e != cudaSuccess) return e;
+  e = launch_cpu_big(a, lo, n, counts + 0, cpu_ws, aux);  // the CPU-class sort is done with cpu_ws
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(ev_join, aux);
+  // GPU class: sort + parallel consolidation on the caller's stream
+  e = radix_sort_desc2(gk, gv, 0, n, counts + 1, gperm, full64, main_ws, s);
+  if (e != cudaSuccess) return e;
+  e = launch_ff(a, q, lo, hi, gperm, counts + 0, main_ws, s);
+  if (e != cudaSuccess) return e;
   cudaStreamWaitEvent(s, ev_join, 0);
   return cudaGetLastError();
 }

@@ -199,48 +199,127 @@ __global__ void __launch_bounds__(kSmallThreads) k_sched_small(SchedLaunch a) {
   }
 }
 
-// gather u in priority order; count the CPU class (keys are sorted, so the CPU
-// class is a prefix)
-__global__ void k_gather(const uint32_t* __restrict__ perm, const float* __restrict__ u,
-                         const uint64_t* __restrict__ key, uint32_t lo, uint32_t n, float* __restrict__ u_sorted,
-                         uint32_t* __restrict__ ncpu) {
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t i = perm[lo + j];
-  u_sorted[j] = u[i];
-  const bool cpu = (key[i] >> 63) != 0;
-  const bool next_gpu = (j + 1 == n) || ((key[perm[lo + j + 1]] >> 63) == 0);
-  if (cpu && next_gpu) *ncpu = j + 1;
-}
+// CPU class of a large queue (R-CORE), in three launches:
+//  k_cpu_pred   (grid)  predicted latency of the j-th CPU task in priority
+//                       order, p_j = gamma * (base + ceil(eta * u)); batch/slot
+//                       outputs; per-chunk maxima of p;
+//  k_cpu_chain  (1 CTA) the list-scheduling recurrence, one thread, chunks of
+//                       the p stream staged in shared memory by cp.async;
+//  k_cpu_scatter(grid)  core_of[perm[j]] = chosen core.
+// State: the core clocks as keys (t << 5 | core) kept sorted, so the
+// earliest-free core with the lowest index is key[0] and a job is an add plus
+// a sorted insert of key[0] + (p << 5) (exact while t < 2^58 µs).  When the
+// spread of the keys and every p of a chunk are < 2^32 (checked per chunk)
+// the keys are kept as u32 offsets from a 64-bit base.
+constexpr uint32_t kCpuChunk = 4096;
 
-__global__ void __launch_bounds__(64) k_sched_big(SchedLaunch a, uint32_t q, uint32_t lo, uint32_t n,
-                                                   const float* __restrict__ u_sorted,
-                                                   const uint32_t* __restrict__ ncpu_p) {
-  __shared__ uint32_t W[kMaxWindow], S[kMaxWindow];
-  __shared__ float Wu[kMaxWindow], Su[kMaxWindow];
+__global__ void __launch_bounds__(256) k_cpu_pred(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p,
+                                                  uint64_t* __restrict__ pred, uint64_t* __restrict__ chunk_max) {
+  __shared__ uint64_t wmax[8];
   const uint32_t ncpu = *ncpu_p;
+  const uint32_t j0 = blockIdx.x * kCpuChunk;
+  if (j0 >= ncpu) return;
   const uint32_t* perm = a.perm + lo;
-  auto get_u = [&](uint32_t j) { return u_sorted[j]; };
-  auto get_idx = [&](uint32_t j) { return perm[j]; };
-  const uint32_t warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    if ((threadIdx.x & 31u) == 0)
-      cpu_class(0, ncpu, a.cores, a.prof, get_u, get_idx, a.batch_of, a.slot_of, a.core_of);
-  } else {
-    const uint32_t m = (uint32_t)a.prof.b10 * (uint32_t)a.prof.C / 10u;
-    uint32_t nb = consolidate_warp(ncpu, n, m, (uint32_t)a.prof.C, a.prof.lambda, get_u, get_idx, W, Wu, S, Su,
-                                   a.batch_of, a.slot_of, a.core_of);
-    if ((threadIdx.x & 31u) == 0) a.seg_count[q] = nb;
+  const float eta = __ll2float_rn(a.prof.eta_us);
+  uint64_t mx = 0;
+#pragma unroll 4
+  for (uint32_t k = 0; k < kCpuChunk / 256; ++k) {
+    const uint32_t j = j0 + k * 256 + threadIdx.x;
+    if (j < ncpu) {
+      const uint32_t i = perm[j];
+      const float eu = __fmul_rn(eta, a.u[i]);
+      const uint64_t pr = (uint64_t)((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu)));
+      pred[j] = pr;
+      mx = max(mx, pr);
+      a.batch_of[i] = kNoBatch;
+      a.slot_of[i] = 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  if ((threadIdx.x & 31u) == 0) wmax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < 8; ++w) t = max(t, wmax[w]);
+    chunk_max[blockIdx.x] = t;
   }
 }
 
-// CPU class of a large queue: predicted latencies computed in parallel into
-// shared memory, the list-scheduling recurrence (R-CORE) run by one thread on
-// a sorted state, outputs written in parallel.  State: the core clocks as
-// keys (t << 5 | core) kept sorted, so the earliest-free core with the lowest
-// index is key[0] and a job is an add plus a sorted insert of key[0] + (p << 5)
-// (exact while t < 2^58 µs).
-constexpr uint32_t kCpuChunk = 4096;
+// one chunk on u32 offsets from the smallest key: d1 <= d2 <= d3 relative to
+// base = key[0]; a job inserts p into (d1, d2, d3) by min/max and rebases by
+// the new minimum, so every offset stays <= max(spread, max p) < 2^32.
+__device__ __forceinline__ void chain4_u32(uint64_t& base, uint32_t& d1, uint32_t& d2, uint32_t& d3,
+                                           const uint64_t* __restrict__ p, uint8_t* __restrict__ out, uint32_t cnt) {
+  uint32_t q = 0;
+  for (; q + 8 <= cnt; q += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      const uint4 w = *reinterpret_cast<const uint4*>(p + q + t);
+      v[t] = w.x << 5;
+      v[t + 1] = w.z << 5;
+    }
+    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      // low byte of the key = core index (bits 0-4) + clock bits, masked later
+      const uint32_t lb = (uint32_t)base & 0xFFu;
+      if (t < 4) o0 |= lb << (8 * t); else o1 |= lb << (8 * (t - 4));
+      const uint32_t x = v[t];
+      const uint32_t e0 = min(d1, x), e1 = min(max(d1, x), d2), e2 = min(max(d2, x), d3), e3 = max(d3, x);
+      base += e0;
+      d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
+    }
+    *reinterpret_cast<uint2*>(out + q) = make_uint2(o0, o1);
+  }
+  for (; q < cnt; ++q) {
+    out[q] = (uint8_t)base;
+    const uint32_t x = (uint32_t)p[q] << 5;
+    const uint32_t e0 = min(d1, x), e1 = min(max(d1, x), d2), e2 = min(max(d2, x), d3), e3 = max(d3, x);
+    base += e0;
+    d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
+  }
+}
+
+// one chunk on absolute u32 clocks a_c = (t_c - t_base) << 2 | core (4 cores):
+// a job is w = a0 + (p << 2) and a sorted insert of w into (a1, a2, a3) --
+// two dependent operations per job.  Every 8 jobs the clocks are rebased by
+// the minimum; the caller checks (spread + 9 max p) * 4 + 3 < 2^32, which
+// bounds every clock between rebases.
+__device__ __forceinline__ void chain4_abs(uint64_t& tb, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3,
+                                           const uint64_t* __restrict__ p, uint8_t* __restrict__ out, uint32_t cnt) {
+  uint32_t q = 0;
+  for (; q + 8 <= cnt; q += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      const uint4 w = *reinterpret_cast<const uint4*>(p + q + t);
+      v[t] = w.x;
+      v[t + 1] = w.z;
+    }
+    uint32_t c[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      c[t] = a0;
+      const uint32_t w = a0 + (v[t] << 2);
+      const uint32_t n0 = min(a1, w), n1 = min(max(a1, w), a2), n2 = min(max(a2, w), a3), n3 = max(a3, w);
+      a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+    }
+    const uint32_t o0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
+    const uint32_t o1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
+    *reinterpret_cast<uint2*>(out + q) = make_uint2(o0 & 0x03030303u, o1 & 0x03030303u);
+    const uint32_t m = a0 & ~3u;
+    tb += m >> 2;
+    a0 -= m; a1 -= m; a2 -= m; a3 -= m;
+  }
+  for (; q < cnt; ++q) {
+    out[q] = (uint8_t)(a0 & 3u);
+    const uint32_t w = a0 + ((uint32_t)p[q] << 2);
+    const uint32_t n0 = min(a1, w), n1 = min(max(a1, w), a2), n2 = min(max(a2, w), a3), n3 = max(a3, w);
+    a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+  }
+}
 
 // one job of list scheduling on the sorted keys: remove k[0], insert k[0] + p
 template <int MAXC>
@@ -259,116 +338,91 @@ __device__ __forceinline__ void list_step(uint64_t (&k)[MAXC], uint64_t p) {
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) k[c] = nk[c];
 }
+
 template <int MAXC>
-__device__ __forceinline__ void cpu_chunk_serial(uint64_t (&k)[MAXC], const int64_t* pred, uint8_t* core,
-                                                 uint32_t cnt, bool small) {
-  if (small) {
-    // keys relative to the smallest one: d_c = k_c - k_0 (u32), base = k_0.
-    // A job: insert p into (d1, d2, d3) by min/max, rebase by the new minimum.
-    uint64_t base = k[0];
-    uint32_t d1 = (uint32_t)(k[1] - base), d2 = (uint32_t)(k[MAXC > 2 ? 2 : 1] - base),
-             d3 = (uint32_t)(k[MAXC > 3 ? 3 : 1] - base);
-    uint32_t q = 0;
-    for (; q + 8 <= cnt; q += 8) {
-      uint32_t pp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) pp[t] = (uint32_t)pred[q + t];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        core[q + t] = (uint8_t)(base & 31u);
-        const uint32_t v = pp[t];
-        const uint32_t e0 = min(d1, v), e1 = min(max(d1, v), d2), e2 = min(max(d2, v), d3), e3 = max(d3, v);
-        base += e0;
-        d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
-      }
-    }
-    for (; q < cnt; ++q) {
-      core[q] = (uint8_t)(base & 31u);
-      const uint32_t v = (uint32_t)pred[q];
-      const uint32_t e0 = min(d1, v), e1 = min(max(d1, v), d2), e2 = min(max(d2, v), d3), e3 = max(d3, v);
-      base += e0;
-      d1 = e1 - e0; d2 = e2 - e0; d3 = e3 - e0;
-    }
-    k[0] = base;
-    k[1] = base + d1;
-    if (MAXC > 2) k[MAXC > 2 ? 2 : 1] = base + d2;
-    if (MAXC > 3) k[MAXC > 3 ? 3 : 1] = base + d3;
-  } else {
-    uint32_t q = 0;
-    for (; q + 8 <= cnt; q += 8) {
-      uint64_t pp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) pp[t] = (uint64_t)pred[q + t];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        core[q + t] = (uint8_t)(k[0] & 31u);
-        list_step<MAXC>(k, pp[t]);
-      }
-    }
-    for (; q < cnt; ++q) {
-      core[q] = (uint8_t)(k[0] & 31u);
-      list_step<MAXC>(k, (uint64_t)pred[q]);
-    }
+__device__ __forceinline__ void chain_u64(uint64_t (&k)[MAXC], const uint64_t* __restrict__ p, uint8_t* __restrict__ out,
+                                          uint32_t cnt) {
+  for (uint32_t q = 0; q < cnt; ++q) {
+    out[q] = (uint8_t)k[0];
+    list_step<MAXC>(k, p[q] << 5);
   }
 }
 
-// CPU class of a large queue.  Warp 0 (one lane) runs the list-scheduling
-// recurrence on chunk c while warps 1..7 compute the predicted latencies of
-// chunk c+1 and write the assignments of chunk c-1 (double-buffered).
+// warps 1..3 stage chunk c+1 of p (cp.async) and write out the cores of chunk
+// c-1 while lane 0 of warp 0 runs chunk c
 template <int MAXC>
-__global__ void __launch_bounds__(256) k_cpu_big(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p) {
-  extern __shared__ __align__(16) uint8_t cpu_smem[];
-  int64_t* s_pred = reinterpret_cast<int64_t*>(cpu_smem);                 // [2][kCpuChunk]
-  uint8_t* s_core = cpu_smem + 2 * kCpuChunk * sizeof(int64_t);           // [2][kCpuChunk]
-  __shared__ int s_small[2];
+__global__ void __launch_bounds__(128) k_cpu_chain(uint32_t cores, const uint32_t* __restrict__ ncpu_p,
+                                                   const uint64_t* __restrict__ pred,
+                                                   const uint64_t* __restrict__ chunk_max, uint8_t* __restrict__ csel) {
+  extern __shared__ __align__(16) uint8_t chain_smem[];
+  uint64_t* s_p = reinterpret_cast<uint64_t*>(chain_smem);               // [2][kCpuChunk]
+  uint8_t* s_o = chain_smem + 2 * kCpuChunk * sizeof(uint64_t);          // [2][kCpuChunk]
   const uint32_t ncpu = *ncpu_p;
-  const uint32_t* perm = a.perm + lo;
-  const float eta = __ll2float_rn(a.prof.eta_us);
-  const uint32_t cores = a.cores;
   const uint32_t nchunks = (ncpu + kCpuChunk - 1) / kCpuChunk;
-  auto fill = [&](uint32_t c, uint32_t t0, uint32_t nt) {  // predictions of chunk c by threads t0..t0+nt-1
+  auto stage = [&](uint32_t c, uint32_t t) {  // threads t = 0..95 of warps 1..3
     const uint32_t j0 = c * kCpuChunk, cnt = min(kCpuChunk, ncpu - j0);
-    int64_t* pb = s_pred + (c & 1) * kCpuChunk;
-    bool big = false;
-    for (uint32_t q = threadIdx.x - t0; q < cnt; q += nt) {
-      const float eu = __fmul_rn(eta, a.u[perm[j0 + q]]);
-      const int64_t pr = ((int64_t)a.prof.gamma * (a.prof.base_us + (int64_t)ceilf(eu))) << 5;
-      pb[q] = pr;
-      big |= (uint64_t)pr >= 0xFFFFFFFFull;
+    const uint32_t nv = (cnt + 1) / 2;  // 16-byte vectors (pred is padded to even length)
+    uint64_t* dst = s_p + (c & 1) * kCpuChunk;
+    for (uint32_t v = t; v < nv; v += 96) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 2 * v);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(pred + j0 + 2 * v) : "memory");
     }
-    if (big) s_small[c & 1] = 0;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   };
-  auto drain = [&](uint32_t c, uint32_t t0, uint32_t nt) {  // write assignments of chunk c
+  auto drain = [&](uint32_t c, uint32_t t, uint32_t nt) {
     const uint32_t j0 = c * kCpuChunk, cnt = min(kCpuChunk, ncpu - j0);
-    const uint8_t* cb = s_core + (c & 1) * kCpuChunk;
-    for (uint32_t q = threadIdx.x - t0; q < cnt; q += nt) {
-      const uint32_t i = perm[j0 + q];
-      a.core_of[i] = cores ? cb[q] : (uint8_t)0xFF;
-      a.batch_of[i] = kNoBatch;
-      a.slot_of[i] = 0;
-    }
+    const uint8_t* src = s_o + (c & 1) * kCpuChunk;
+    for (uint32_t q = t; q < cnt; q += nt) csel[j0 + q] = src[q];
   };
   uint64_t k[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) k[c] = c < (int)cores ? (uint64_t)c : ~0ull;  // unused cores never chosen
-  if (threadIdx.x < 2) s_small[threadIdx.x] = (MAXC == 4 && cores == 4) ? 1 : 0;
-  __syncthreads();
-  if (nchunks) fill(0, 0, 256);
+  if (nchunks && threadIdx.x >= 32) stage(0, threadIdx.x - 32);
   __syncthreads();
   for (uint32_t c = 0; c < nchunks; ++c) {
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0 && cores)
-        cpu_chunk_serial<MAXC>(k, s_pred + (c & 1) * kCpuChunk, s_core + (c & 1) * kCpuChunk,
-                               min(kCpuChunk, ncpu - c * kCpuChunk), s_small[c & 1] != 0);
-    } else {
-      if (threadIdx.x == 32) s_small[(c + 1) & 1] = (MAXC == 4 && cores == 4) ? 1 : 0;
-      asm volatile("bar.sync 1, 224;");
-      if (c + 1 < nchunks) fill(c + 1, 32, 224);
-      if (c >= 1) drain(c - 1, 32, 224);
+    if (threadIdx.x == 0) {
+      const uint32_t cnt = min(kCpuChunk, ncpu - c * kCpuChunk);
+      const uint64_t* pp = s_p + (c & 1) * kCpuChunk;
+      uint8_t* oo = s_o + (c & 1) * kCpuChunk;
+      const uint64_t spread_t = (k[MAXC - 1] >> 5) - (k[0] >> 5), pm = chunk_max[c];
+      if (MAXC == 4 && cores == 4 && spread_t < (1ull << 28) && pm < (1ull << 28) &&
+          ((spread_t + 9 * pm) << 2) + 3 < 0xFFFFFFFFull) {
+        uint64_t tb = k[0] >> 5;
+        uint32_t a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = (uint32_t)(((k[i % MAXC] >> 5) - tb) << 2) | (uint32_t)(k[i % MAXC] & 3u);
+        chain4_abs(tb, a[0], a[1], a[2], a[3], pp, oo, cnt);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) k[i % MAXC] = ((tb + (a[i] >> 2)) << 5) | (a[i] & 3u);
+      } else if (MAXC == 4 && cores == 4 && k[MAXC - 1] - k[0] < 0xFFFFFFFFull && pm < (1ull << 27)) {
+        uint64_t base = k[0];
+        uint32_t d1 = (uint32_t)(k[1 % MAXC] - base), d2 = (uint32_t)(k[2 % MAXC] - base),
+                 d3 = (uint32_t)(k[3 % MAXC] - base);
+        chain4_u32(base, d1, d2, d3, pp, oo, cnt);
+        k[0] = base;
+        k[1 % MAXC] = base + d1;
+        k[2 % MAXC] = base + d2;
+        k[3 % MAXC] = base + d3;
+      } else {
+        chain_u64<MAXC>(k, pp, oo, cnt);
+      }
+    } else if (threadIdx.x >= 32) {
+      if (c + 1 < nchunks) stage(c + 1, threadIdx.x - 32);
+      if (c >= 1) drain(c - 1, threadIdx.x - 32, 96);
     }
     __syncthreads();
   }
-  if (nchunks) drain(nchunks - 1, 0, 256);
+  if (nchunks) drain(nchunks - 1, threadIdx.x, 128);
+}
+
+__global__ void k_cpu_scatter(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p,
+                              const uint8_t* __restrict__ csel) {
+  const uint32_t ncpu = *ncpu_p;
+  const uint32_t* perm = a.perm + lo;
+  const bool any = a.cores != 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < ncpu; j += gridDim.x * blockDim.x)
+    a.core_of[perm[j]] = any ? (uint8_t)(csel[j] & 31u) : (uint8_t)0xFF;
 }
 
 // seg_batch_off = exclusive scan of seg_count (one CTA)
@@ -420,32 +474,35 @@ cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_sched_big(const SchedLaunch& a, uint32_t q, uint32_t lo, uint32_t hi, float* ws,
-                             cudaStream_t s) {
-  const uint32_t n = hi - lo;
-  float* u_sorted = ws;
-  uint32_t* ncpu = reinterpret_cast<uint32_t*>(ws + ((n + 63) & ~63u));
-  cudaMemsetAsync(ncpu, 0, sizeof(uint32_t), s);
-  k_gather<<<(n + 255) / 256, 256, 0, s>>>(a.perm, a.u, a.key, lo, n, u_sorted, ncpu);
-  k_sched_big<<<1, 64, 0, s>>>(a, q, lo, n, u_sorted, ncpu);
-  note_launch(2);
-  return cudaGetLastError();
+size_t cpu_big_workspace(uint32_t n) {
+  const size_t nch = (size_t)n / kCpuChunk + 2;
+  return (((size_t)n + 2) * 8 + 255 & ~size_t(255)) + (nch * 8 + 255 & ~size_t(255)) + ((size_t)n + 255 & ~size_t(255));
 }
 
-cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu, cudaStream_t s) {
-  (void)n;
-  const int smem = 2 * kCpuChunk * (sizeof(int64_t) + 1);
+cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const uint32_t* ncpu, void* ws,
+                           cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  char* w = static_cast<char*>(ws);
+  uint64_t* pred = reinterpret_cast<uint64_t*>(w);
+  w += ((size_t)n + 2) * 8 + 255 & ~size_t(255);
+  uint64_t* chunk_max = reinterpret_cast<uint64_t*>(w);
+  w += ((size_t)n / kCpuChunk + 2) * 8 + 255 & ~size_t(255);
+  uint8_t* csel = reinterpret_cast<uint8_t*>(w);
+  const uint32_t nch = (n + kCpuChunk - 1) / kCpuChunk;
+  k_cpu_pred<<<nch, 256, 0, s>>>(a, lo, ncpu, pred, chunk_max);
+  const int smem = 2 * kCpuChunk * (sizeof(uint64_t) + 1);
   if (a.cores <= 4) {
-    cudaFuncSetAttribute(k_cpu_big<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_cpu_big<4><<<1, 256, smem, s>>>(a, lo, ncpu);
+    cudaFuncSetAttribute(k_cpu_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_chain<4><<<1, 128, smem, s>>>(a.cores, ncpu, pred, chunk_max, csel);
   } else if (a.cores <= 8) {
-    cudaFuncSetAttribute(k_cpu_big<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_cpu_big<8><<<1, 256, smem, s>>>(a, lo, ncpu);
+    cudaFuncSetAttribute(k_cpu_chain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_chain<8><<<1, 128, smem, s>>>(a.cores, ncpu, pred, chunk_max, csel);
   } else {
-    cudaFuncSetAttribute(k_cpu_big<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_cpu_big<32><<<1, 256, smem, s>>>(a, lo, ncpu);
+    cudaFuncSetAttribute(k_cpu_chain<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_cpu_chain<32><<<1, 128, smem, s>>>(a.cores, ncpu, pred, chunk_max, csel);
   }
-  note_launch();
+  k_cpu_scatter<<<(n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184, 256, 0, s>>>(a, lo, ncpu, csel);
+  note_launch(3);
   return cudaGetLastError();
 }
 
