@@ -326,8 +326,8 @@ rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** o
   if (device < 0 || device >= ndev) return fail(c, RT_EINVAL, "no such CUDA device");
   DeviceGuard g(device);
   RT_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-  RT_CUDA(c, cudaMalloc(&c->d_flags, sizeof(uint32_t)));
-  RT_CUDA(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)));
+  RT_CUDA(c, cudaMalloc(&c->d_flags, 4 * sizeof(uint32_t)));  // [0] flags, [2] scoring work counter
+  RT_CUDA(c, cudaMemset(c->d_flags, 0, 4 * sizeof(uint32_t)));
   RT_CUDA(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -399,6 +399,7 @@ static rt_status score_common(rt_ctx* c, const uint8_t* d_bytes, const uint32_t*
   a.key = d_key;
   a.D_out = d_D_out;
   a.flags = c->d_flags;
+  a.work = c->d_flags + 2;
   a.num_sms = c->num_sms;
   cudaError_t e = rtlm::launch_score(a, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_score");

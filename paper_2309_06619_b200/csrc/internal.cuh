@@ -76,6 +76,7 @@ struct ScoreLaunch {
   uint64_t* key;
   uint32_t* D_out;
   uint32_t* flags;
+  uint32_t* work;  // device counter (scoring work queue), zeroed by the launcher
   int num_sms;
 };
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s);

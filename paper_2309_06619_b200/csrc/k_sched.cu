@@ -212,18 +212,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_sched_small(SchedLaunch a) {
 // spread of the keys and every p of a chunk are < 2^32 (checked per chunk)
 // the keys are kept as u32 offsets from a 64-bit base.
 constexpr uint32_t kCpuChunk = 4096;
+constexpr uint32_t kPredBlock = 1024;  // k_cpu_pred elements per CTA (max of p per CTA)
 
 __global__ void __launch_bounds__(256) k_cpu_pred(SchedLaunch a, uint32_t lo, const uint32_t* __restrict__ ncpu_p,
                                                   uint64_t* __restrict__ pred, uint64_t* __restrict__ chunk_max) {
   __shared__ uint64_t wmax[8];
   const uint32_t ncpu = *ncpu_p;
-  const uint32_t j0 = blockIdx.x * kCpuChunk;
+  const uint32_t j0 = blockIdx.x * kPredBlock;
   if (j0 >= ncpu) return;
   const uint32_t* perm = a.perm + lo;
   const float eta = __ll2float_rn(a.prof.eta_us);
   uint64_t mx = 0;
-#pragma unroll 4
-  for (uint32_t k = 0; k < kCpuChunk / 256; ++k) {
+#pragma unroll
+  for (uint32_t k = 0; k < kPredBlock / 256; ++k) {
     const uint32_t j = j0 + k * 256 + threadIdx.x;
     if (j < ncpu) {
       const uint32_t i = perm[j];
@@ -283,10 +284,36 @@ __device__ __forceinline__ void chain4_u32(uint64_t& base, uint32_t& d1, uint32_
 }
 
 // one chunk on absolute u32 clocks a_c = (t_c - t_base) << 2 | core (4 cores):
-// a job is w = a0 + (p << 2) and a sorted insert of w into (a1, a2, a3) --
-// two dependent operations per job.  Every 8 jobs the clocks are rebased by
-// the minimum; the caller checks (spread + 9 max p) * 4 + 3 < 2^32, which
-// bounds every clock between rebases.
+// a job is w = a0 + (p << 2) and a sorted insert of w into (a1, a2, a3).
+// Nearly every job lands on the end of the order (a job outlasts the other
+// cores' remaining work), so jobs are taken 4 at a time on the assumption
+// that all four append: then job k runs on the core of a_k, w_k = a_k +
+// (p_k << 2) and the new state is (w1..w4) -- four independent adds checked
+// by w1 > a3, w2 > w1, w3 > w2, w4 > w3.  If the check fails the 4 jobs are
+// redone one by one (sorted insert by min/max).  Every 8 jobs the clocks are
+// rebased by the minimum; the caller checks (spread + 9 max p) * 4 + 3 < 2^32,
+// which bounds every clock between rebases.
+__device__ __forceinline__ void insert4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3, uint32_t x) {
+  const uint32_t w = a0 + (x << 2);
+  const uint32_t n0 = min(a1, w), n1 = min(max(a1, w), a2), n2 = min(max(a2, w), a3), n3 = max(a3, w);
+  a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+}
+
+__device__ __forceinline__ void block4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3, const uint32_t* v,
+                                       uint32_t* c) {
+  const uint32_t w1 = a0 + (v[0] << 2), w2 = a1 + (v[1] << 2), w3 = a2 + (v[2] << 2), w4 = a3 + (v[3] << 2);
+  if ((w1 > a3) & (w2 > w1) & (w3 > w2) & (w4 > w3)) {
+    c[0] = a0; c[1] = a1; c[2] = a2; c[3] = a3;
+    a0 = w1; a1 = w2; a2 = w3; a3 = w4;
+  } else {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      c[t] = a0;
+      insert4(a0, a1, a2, a3, v[t]);
+    }
+  }
+}
+
 __device__ __forceinline__ void chain4_abs(uint64_t& tb, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3,
                                            const uint64_t* __restrict__ p, uint8_t* __restrict__ out, uint32_t cnt) {
   uint32_t q = 0;
@@ -299,13 +326,8 @@ __device__ __forceinline__ void chain4_abs(uint64_t& tb, uint32_t& a0, uint32_t&
       v[t + 1] = w.z;
     }
     uint32_t c[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      c[t] = a0;
-      const uint32_t w = a0 + (v[t] << 2);
-      const uint32_t n0 = min(a1, w), n1 = min(max(a1, w), a2), n2 = min(max(a2, w), a3), n3 = max(a3, w);
-      a0 = n0; a1 = n1; a2 = n2; a3 = n3;
-    }
+    block4(a0, a1, a2, a3, v, c);
+    block4(a0, a1, a2, a3, v + 4, c + 4);
     const uint32_t o0 = __byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410);
     const uint32_t o1 = __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410);
     *reinterpret_cast<uint2*>(out + q) = make_uint2(o0 & 0x03030303u, o1 & 0x03030303u);
@@ -315,9 +337,7 @@ __device__ __forceinline__ void chain4_abs(uint64_t& tb, uint32_t& a0, uint32_t&
   }
   for (; q < cnt; ++q) {
     out[q] = (uint8_t)(a0 & 3u);
-    const uint32_t w = a0 + ((uint32_t)p[q] << 2);
-    const uint32_t n0 = min(a1, w), n1 = min(max(a1, w), a2), n2 = min(max(a2, w), a3), n3 = max(a3, w);
-    a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+    insert4(a0, a1, a2, a3, (uint32_t)p[q]);
   }
 }
 
@@ -357,10 +377,16 @@ __global__ void __launch_bounds__(128) k_cpu_chain(uint32_t cores, const uint32_
   extern __shared__ __align__(16) uint8_t chain_smem[];
   uint64_t* s_p = reinterpret_cast<uint64_t*>(chain_smem);               // [2][kCpuChunk]
   uint8_t* s_o = chain_smem + 2 * kCpuChunk * sizeof(uint64_t);          // [2][kCpuChunk]
+  __shared__ uint64_t s_pm[2];                                            // max p of the staged chunk
   const uint32_t ncpu = *ncpu_p;
   const uint32_t nchunks = (ncpu + kCpuChunk - 1) / kCpuChunk;
   auto stage = [&](uint32_t c, uint32_t t) {  // threads t = 0..95 of warps 1..3
     const uint32_t j0 = c * kCpuChunk, cnt = min(kCpuChunk, ncpu - j0);
+    if (t == 0) {
+      uint64_t pm = 0;
+      for (uint32_t b = j0 / kPredBlock; b * kPredBlock < j0 + cnt; ++b) pm = max(pm, chunk_max[b]);
+      s_pm[c & 1] = pm;
+    }
     const uint32_t nv = (cnt + 1) / 2;  // 16-byte vectors (pred is padded to even length)
     uint64_t* dst = s_p + (c & 1) * kCpuChunk;
     for (uint32_t v = t; v < nv; v += 96) {
@@ -385,7 +411,8 @@ __global__ void __launch_bounds__(128) k_cpu_chain(uint32_t cores, const uint32_
       const uint32_t cnt = min(kCpuChunk, ncpu - c * kCpuChunk);
       const uint64_t* pp = s_p + (c & 1) * kCpuChunk;
       uint8_t* oo = s_o + (c & 1) * kCpuChunk;
-      const uint64_t spread_t = (k[MAXC - 1] >> 5) - (k[0] >> 5), pm = chunk_max[c];
+      const uint64_t pm = s_pm[c & 1];
+      const uint64_t spread_t = (k[MAXC - 1] >> 5) - (k[0] >> 5);
       if (MAXC == 4 && cores == 4 && spread_t < (1ull << 28) && pm < (1ull << 28) &&
           ((spread_t + 9 * pm) << 2) + 3 < 0xFFFFFFFFull) {
         uint64_t tb = k[0] >> 5;
@@ -475,7 +502,7 @@ cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s) {
 }
 
 size_t cpu_big_workspace(uint32_t n) {
-  const size_t nch = (size_t)n / kCpuChunk + 2;
+  const size_t nch = (size_t)n / kPredBlock + 2;
   return (((size_t)n + 2) * 8 + 255 & ~size_t(255)) + (nch * 8 + 255 & ~size_t(255)) + ((size_t)n + 255 & ~size_t(255));
 }
 
@@ -486,9 +513,9 @@ cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const 
   uint64_t* pred = reinterpret_cast<uint64_t*>(w);
   w += ((size_t)n + 2) * 8 + 255 & ~size_t(255);
   uint64_t* chunk_max = reinterpret_cast<uint64_t*>(w);
-  w += ((size_t)n / kCpuChunk + 2) * 8 + 255 & ~size_t(255);
+  w += ((size_t)n / kPredBlock + 2) * 8 + 255 & ~size_t(255);
   uint8_t* csel = reinterpret_cast<uint8_t*>(w);
-  const uint32_t nch = (n + kCpuChunk - 1) / kCpuChunk;
+  const uint32_t nch = (n + kPredBlock - 1) / kPredBlock;
   k_cpu_pred<<<nch, 256, 0, s>>>(a, lo, ncpu, pred, chunk_max);
   const int smem = 2 * kCpuChunk * (sizeof(uint64_t) + 1);
   if (a.cores <= 4) {

@@ -716,6 +716,487 @@ __global__ void __launch_bounds__(kT2, 2) k_score2(ScoreLaunch a) {
   }
 }
 
+// ============================================================ K1 v4 (warp streams)
+// One warp owns 32 consecutive requests (taken from a global work counter) and
+// streams their bytes in 512-byte chunks; no CTA-wide barriers.
+//  (1) classify: each lane classifies its 16 staged bytes through a per-lane
+//      replicated class table -> word / punctuation / dropped bit masks;
+//  (2) events: word-run starts (a run never crosses a request start) and
+//      punctuation bytes, compacted in byte order; a run reaching the chunk end
+//      is carried into the next chunk;
+//  (3) tokens: lane per event -- punctuation kind, or the run's clitic split
+//      (R-CLITIC), lemma (R-LEMMA) and lexicon probe -> 1 or 2 tokens written
+//      in order into a small ring;
+//  (4) rules (R-RULES, in the oracle's sentence formulation O2): lane per
+//      token.  Every rule is a predicate on the token, its three predecessors
+//      and "last earlier token with property X" positions (request start,
+//      sentence end, word, first word, noun, first noun, second distinct
+//      noun, punctuation) obtained with ballots, so the counters become
+//      per-token contributions summed per request (segmented warp scan).
+// Warps whose offsets are not non-decreasing use the per-lane byte FSM.
+constexpr uint32_t kT4 = 768;                 // threads per CTA (24 warps)
+constexpr uint32_t kW4 = kT4 / 32;
+constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
+constexpr uint32_t kRing = 128;               // token ring per warp
+
+enum : uint32_t { K_W = 1, K_COMMA = 2, K_END = 3, K_Q = 4, K_OTH = 5 };
+
+struct __align__(16) WarpBuf {
+  uint32_t stage[4 + kChunk / 4 + 8];  // 16 B pad | chunk | 32 B pad
+  uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
+  uint16_t ev[kChunk + 1];
+  uint32_t rs[32];                     // request starts (absolute byte offsets)
+  uint32_t t_attr[kRing];
+  uint8_t t_meta[kRing];               // kind | req << 3
+  uint32_t acc[32][9];                 // S Y M V O P ntok nd nq
+};
+
+struct Smem4 {
+  uint32_t lut[256 * 32];              // class bits per byte, replicated per lane: W 0x1, P 0x100, X 0x10000
+  uint32_t pref[128];
+  WarpBuf w[kW4];
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() { uint32_t m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
+__device__ __forceinline__ uint32_t lanemask_le() { uint32_t m; asm("mov.u32 %0, %%lanemask_le;" : "=r"(m)); return m; }
+
+// last position (global token index) among lanes whose bit is set in m, else carry
+__device__ __forceinline__ int32_t last_pos(uint32_t m, int32_t tb, int32_t carry) {
+  return m ? tb + 31 - (int32_t)__clz(m) : carry;
+}
+
+// request index of absolute byte position pos: last i < cnt with rs[i] <= pos
+__device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uint32_t pos) {
+  uint32_t lo = 0;
+#pragma unroll
+  for (uint32_t st = 16; st; st >>= 1)
+    if (lo + st < cnt && rs[lo + st] <= pos) lo += st;
+  return lo;
+}
+
+// Word token(s) of a run of n bytes whose first 16 bytes (lowercased) are k0/k1
+// and whose last bytes (newest low) are `tail`; returns the token count.
+__device__ __forceinline__ uint32_t run_tokens(const Lex& L, const uint32_t* pref, uint32_t n, uint64_t k0,
+                                               uint64_t k1, uint64_t tail, uint32_t& attr0, uint32_t& attr1) {
+  tail = (tail | 0x2020202020202020ull) & mask_bytes(n < 6 ? n : 6);
+  const uint32_t t3 = (uint32_t)(tail & 0xFFFFFFu), t2 = (uint32_t)(tail & 0xFFFFu);
+  uint32_t cut = 0;
+  if (n > 3 && t3 == (('n' << 16) | ('\'' << 8) | 't')) cut = 3;
+  else if (n > 2 && (t2 == (('\'' << 8) | 's') || t2 == (('\'' << 8) | 'm') || t2 == (('\'' << 8) | 'd')))
+    cut = 2;
+  else if (n > 3 && (t3 == (('\'' << 16) | ('r' << 8) | 'e') || t3 == (('\'' << 16) | ('v' << 8) | 'e') ||
+                     t3 == (('\'' << 16) | ('l' << 8) | 'l')))
+    cut = 3;
+  if (!cut) {
+    const uint32_t e = word_idx(L, pref, n, k0, k1, t3);
+    attr0 = e ? L.e[e - 1].attr : 0u;
+    return 1;
+  }
+  const uint32_t e0 = word_idx(L, pref, n - cut, k0, k1, (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu));
+  const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
+  const uint32_t e1 = word_idx(L, pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu));
+  attr0 = e0 ? L.e[e0 - 1].attr : 0u;
+  attr1 = e1 ? L.e[e1 - 1].attr : 0u;
+  return 2;
+}
+
+struct Carry {
+  int32_t rs, end, word, fw, noun, fn, d, punct;
+  uint32_t fn_id, word_broad, punct_comma, punct_link;
+  uint32_t prev_req;  // request of the last token (0xFFFFFFFF: none)
+};
+
+// rules over tokens [tb, tend) of the ring (tend - tb <= 32)
+__device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, int32_t tend, uint32_t lane) {
+  const int32_t T = tb + (int32_t)lane;
+  const bool valid = T < tend;
+  uint32_t meta = 0, attr = 0;
+  if (valid) { meta = B.t_meta[T & (kRing - 1)]; attr = B.t_attr[T & (kRing - 1)]; }
+  const uint32_t kind = meta & 7u, req = meta >> 3;
+  // three predecessors (same request only)
+  uint32_t pk[4], pa[4];
+#pragma unroll
+  for (int k = 1; k <= 3; ++k) {
+    pk[k] = 0; pa[k] = 0;
+    if (valid && T - k >= 0) {
+      const uint32_t m = B.t_meta[(T - k) & (kRing - 1)];
+      if ((m >> 3) == req) { pk[k] = m & 7u; pa[k] = B.t_attr[(T - k) & (kRing - 1)]; }
+    }
+  }
+  const bool isW = valid && kind == K_W, isComma = valid && kind == K_COMMA;
+  const bool isQ = valid && kind == K_Q, isEnd = valid && (kind == K_END || kind == K_Q);
+  const bool isP = valid && kind >= K_COMMA;
+  const uint32_t prev_req_lane = __shfl_up_sync(0xFFFFFFFFu, req, 1);
+  const bool isRS = valid && (lane == 0 ? req != cy.prev_req : req != prev_req_lane);
+  const uint32_t lt = lanemask_lt(), le = lanemask_le();
+  const int32_t rstart = last_pos(__ballot_sync(0xFFFFFFFFu, isRS) & le, tb, cy.rs);
+  const uint32_t b_end = __ballot_sync(0xFFFFFFFFu, isEnd);
+  const int32_t lend = last_pos(b_end & lt, tb, cy.end);
+  const int32_t sst = max(lend + 1, rstart);  // sentence start
+  const uint32_t b_w = __ballot_sync(0xFFFFFFFFu, isW);
+  const int32_t lword = last_pos(b_w & lt, tb, cy.word);
+  const bool firstW = isW && lword < sst;
+  const uint32_t b_fw = __ballot_sync(0xFFFFFFFFu, firstW);
+  const int32_t f = last_pos(b_fw & le, tb, cy.fw);
+  const bool isN = isW && (attr & A_NOUN);
+  const uint32_t nid = attr >> A_ID_SHIFT;
+  const uint32_t b_n = __ballot_sync(0xFFFFFFFFu, isN);
+  const int32_t lnoun = last_pos(b_n & lt, tb, cy.noun);
+  const bool firstN = isN && lnoun < sst;
+  const uint32_t b_fn = __ballot_sync(0xFFFFFFFFu, firstN);
+  const int32_t fn = last_pos(b_fn & le, tb, cy.fn);
+  const uint32_t fn_id_l = __shfl_sync(0xFFFFFFFFu, nid, (uint32_t)max(fn - tb, 0) & 31u);
+  const uint32_t fn_id = fn >= tb ? fn_id_l : cy.fn_id;
+  const bool isD = isN && fn >= sst && nid != fn_id;
+  const uint32_t b_d = __ballot_sync(0xFFFFFFFFu, isD);
+  const int32_t ld = last_pos(b_d & lt, tb, cy.d);
+  // structural: PREP after a second distinct noun of the sentence
+  const uint32_t cS = (isW && (attr & A_PREP) && ld >= sst) ? 1u : 0u;
+  // open-endedness
+  uint32_t cO = (firstW && (attr & A_OPENER)) ? 1u : 0u;
+  if (isW && !firstW && f >= sst && (attr & A_CAUSE)) {
+    const int32_t dd = T - f;
+    if (dd >= 1 && dd <= 3) {
+      const uint32_t af = pa[dd == 1 ? 1 : dd == 2 ? 2 : 3];
+      bool earlier = false;  // a CAUSE word between f and T
+      if (dd >= 2 && pk[1] == K_W && (pa[1] & A_CAUSE)) earlier = true;
+      if (dd >= 3 && pk[2] == K_W && (pa[2] & A_CAUSE)) earlier = true;
+      if ((af & A_WHAT) && !earlier) cO = 1u;
+    }
+  }
+  const uint32_t broad_l = __shfl_sync(0xFFFFFFFFu, (attr & A_BROAD) ? 1u : 0u, (uint32_t)max(lword - tb, 0) & 31u);
+  const uint32_t lw_broad = lword >= tb ? broad_l : cy.word_broad;
+  if (isQ && lword >= sst && lw_broad) cO += 1u;
+  // content spans: coordinator between words (counted at the word after it)
+  uint32_t cP = 0;
+  if (isW && pk[1] == K_W && (pa[1] & A_COORD) && (pk[2] == K_W || (pk[2] == K_COMMA && pk[3] == K_W))) cP = 1u;
+  // comma chains: link = previous punctuation is a comma with >= 1 word between
+  const uint32_t b_p = __ballot_sync(0xFFFFFFFFu, isP);
+  const int32_t lp = last_pos(b_p & lt, tb, cy.punct);
+  const uint32_t lpl = (uint32_t)max(lp - tb, 0) & 31u;
+  const uint32_t lp_comma_l = __shfl_sync(0xFFFFFFFFu, isComma ? 1u : 0u, lpl);
+  const uint32_t lp_comma = lp >= tb ? lp_comma_l : cy.punct_comma;
+  const bool link = isComma && lp >= rstart && lp_comma && lp <= T - 2;
+  const uint32_t lp_link_l = __shfl_sync(0xFFFFFFFFu, link ? 1u : 0u, lpl);
+  const uint32_t lp_link = lp >= tb ? lp_link_l : cy.punct_link;
+  if (link && !lp_link) cP += 1u;
+  // per-token contributions, packed: ntok 0-6, V 7-13, Y 14-20, S 21-27, O 28-34, P 35-41, nq 42-48, M 49-63
+  uint64_t v = 0;
+  if (valid) {
+    v = 1ull;
+    if (isW) {
+      v |= (uint64_t)(attr & A_VAGUE) << 7;
+      v |= (uint64_t)((attr >> 8) & 1u) << 14;
+      v |= (uint64_t)((attr >> A_SEM_SHIFT) & A_SEM_MASK) << 49;
+    }
+    v |= (uint64_t)cS << 21;
+    v |= (uint64_t)cO << 28;
+    v |= (uint64_t)cP << 35;
+    v |= (uint64_t)(isQ ? 1u : 0u) << 42;
+  }
+  // segmented sum by request (requests are contiguous and increasing)
+  const uint32_t b_head = __ballot_sync(0xFFFFFFFFu, valid && (lane == 0 || req != prev_req_lane));
+  const int32_t head = 31 - (int32_t)__clz(b_head & le);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if ((int32_t)lane - o >= head) v += up;
+  }
+  const uint32_t next_req = __shfl_down_sync(0xFFFFFFFFu, req, 1);
+  const bool next_valid = __shfl_down_sync(0xFFFFFFFFu, valid ? 1u : 0u, 1) != 0u;
+  if (valid && (lane == 31 || !next_valid || next_req != req)) {
+    uint32_t* a = B.acc[req];
+    a[6] += (uint32_t)(v & 0x7F);
+    a[3] += (uint32_t)((v >> 7) & 0x7F);
+    a[1] += (uint32_t)((v >> 14) & 0x7F);
+    a[0] += (uint32_t)((v >> 21) & 0x7F);
+    a[4] += (uint32_t)((v >> 28) & 0x7F);
+    a[5] += (uint32_t)((v >> 35) & 0x7F);
+    a[8] += (uint32_t)((v >> 42) & 0x7F);
+    a[2] = min(a[2] + (uint32_t)(v >> 49), 0xFFFFFFu);
+  }
+  // carries for the next batch
+  const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+  if (vm) {
+    const int32_t lastT = tb + 31 - (int32_t)__clz(vm);
+    cy.prev_req = __shfl_sync(0xFFFFFFFFu, req, (uint32_t)(lastT - tb));
+    cy.rs = last_pos(__ballot_sync(0xFFFFFFFFu, isRS), tb, cy.rs);
+    cy.end = last_pos(b_end, tb, cy.end);
+    if (b_w) cy.word_broad = __shfl_sync(0xFFFFFFFFu, (attr & A_BROAD) ? 1u : 0u, 31 - __clz(b_w));
+    cy.word = last_pos(b_w, tb, cy.word);
+    cy.fw = last_pos(b_fw, tb, cy.fw);
+    cy.noun = last_pos(b_n, tb, cy.noun);
+    if (b_fn) cy.fn_id = __shfl_sync(0xFFFFFFFFu, nid, 31 - __clz(b_fn));
+    cy.fn = last_pos(b_fn, tb, cy.fn);
+    cy.d = last_pos(b_d, tb, cy.d);
+    if (b_p) {
+      const uint32_t L = 31 - __clz(b_p);
+      cy.punct_comma = __shfl_sync(0xFFFFFFFFu, isComma ? 1u : 0u, L);
+      cy.punct_link = __shfl_sync(0xFFFFFFFFu, link ? 1u : 0u, L);
+    }
+    cy.punct = last_pos(b_p, tb, cy.punct);
+  }
+}
+
+__global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem4& S = *reinterpret_cast<Smem4*>(smem_raw);
+  uint8_t* tail_mem = smem_raw + ((sizeof(Smem4) + 15) & ~size_t(15));
+  LexEntry* s_ent = reinterpret_cast<LexEntry*>(tail_mem);
+  const uint32_t ent_bytes = a.lex.n_entries * (uint32_t)sizeof(LexEntry);
+  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + ((ent_bytes + 15u) & ~15u));
+  const uint32_t nslots = 1u << a.lex.bits;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.lex.entries);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_ent);
+    for (uint32_t i = tid; i < ent_bytes / 4; i += kT4) dst[i] = src[i];
+    for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
+    for (uint32_t i = tid; i < 128; i += kT4) S.pref[i] = 0;
+    for (uint32_t i = tid; i < 256 * 32; i += kT4) S.lut[i] = class_bits(i >> 5);
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < a.lex.n_entries; i += kT4) {
+    const LexEntry e = a.lex.entries[i];
+    const uint32_t pi = pref_idx((uint32_t)(e.k0 & 0xFFu), e.len >= 2 ? (uint32_t)((e.k0 >> 8) & 0xFFu) : 0u);
+    atomicOr(&S.pref[pi >> 5], 1u << (pi & 31u));
+  }
+  __syncthreads();
+  const Lex L{s_ent, s_slots, a.lex.bits};
+  WarpBuf& B = S.w[wid];
+  const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
+  const uint32_t ntasks = (a.n + 31) / 32;
+  const uint8_t* st8 = reinterpret_cast<const uint8_t*>(B.stage);
+  if (lane < 4) B.stage[lane] = 0;
+
+  for (;;) {
+    uint32_t task = 0;
+    if (lane == 0) task = atomicAdd(work, 1u);
+    task = __shfl_sync(0xFFFFFFFFu, task, 0);
+    if (task >= ntasks) break;
+    const uint32_t r0 = task * 32, rcnt = min(32u, a.n - r0);
+    const uint32_t r = r0 + lane;
+    const bool rv = lane < rcnt;
+    const uint32_t s_r = rv ? a.offsets[r] : 0u;
+    const uint32_t e_r = rv ? a.offsets[r + 1] : 0u;
+    const bool bad = rv && e_r < s_r;
+    if (__any_sync(0xFFFFFFFFu, bad)) {
+      // offsets not non-decreasing: per-lane byte FSM (requests with e < s are empty)
+      if (bad) atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
+      if (rv) {
+        Rules R;
+        R.init();
+        for (uint32_t i = s_r; i < (bad ? s_r : e_r); ++i) R.byte(__ldg(a.bytes + i), L);
+        uint32_t f[8];
+        bool sat;
+        R.finish(L, f, sat);
+        if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+        epilogue(a, r, f);
+      }
+      continue;
+    }
+    const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
+    const uint32_t B1 = __shfl_sync(0xFFFFFFFFu, e_r, rcnt - 1);
+    B.rs[lane] = s_r;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) B.acc[lane][k] = 0;
+    Carry cy{-1, -1, -1, -1, -1, -1, -1, -1, 0u, 0u, 0u, 0u, 0xFFFFFFFFu};
+    int32_t tokbase = 0;
+    uint32_t prevW = 0;                 // W bit of the byte before the chunk
+    int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
+    const uint32_t base = B0 & ~15u;
+    __syncwarp();
+    for (uint32_t cb = base; cb < B1; cb += kChunk) {
+      // ---- (1) stage + classify 16 bytes per lane
+      const uint32_t g = cb + lane * 16u;
+      uint4 q;
+      if (g + 16u <= total_bytes) q = ld_nc_v4(a.bytes + g);
+      else {
+        uint32_t w4[4] = {0, 0, 0, 0};
+        for (uint32_t j = 0; j < 16u; ++j)
+          if (g + j < total_bytes) w4[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
+        q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
+      *reinterpret_cast<uint4*>(&B.stage[4 + lane * 4]) = q;
+      if (lane < kChunk / 32 + 1) B.mk[lane] = 0;
+      __syncwarp();
+      if (rv && s_r >= cb && s_r < cb + kChunk && s_r < B1)
+        atomicOr(&B.mk[(s_r - cb) >> 5], 1u << ((s_r - cb) & 31u));
+      uint32_t accA = 0, accB = 0;
+      {
+        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t byte = (wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu;
+            const uint32_t c = S.lut[byte * 32u + lane] << i;
+            if (j == 0) accA += c; else accB += c;
+          }
+      }
+      // in-range bytes of this lane: [B0, B1)
+      uint32_t vmask = 0xFFFFu;
+      if (g < B0) vmask &= B0 - g >= 16u ? 0u : (0xFFFFu << (B0 - g)) & 0xFFFFu;
+      if (g + 16u > B1) vmask &= B1 <= g ? 0u : (0xFFFFu >> (g + 16u - B1));
+      const uint32_t W16 = ((accA & 0xFFu) | ((accB & 0xFFu) << 8)) & vmask;
+      const uint32_t P16 = (((accA >> 8) & 0xFFu) | (((accB >> 8) & 0xFFu) << 8)) & vmask;
+      const uint32_t X16 = (((accA >> 16) & 0xFFu) | (((accB >> 16) & 0xFFu) << 8)) & vmask;
+      const uint32_t Wn = __shfl_down_sync(0xFFFFFFFFu, W16, 1);
+      if (!(lane & 1u)) B.wm[lane >> 1] = W16 | (Wn << 16);
+      if (lane == 0) B.wm[kChunk / 32] = 0;
+      __syncwarp();
+      // ---- (2) events
+      const uint32_t mk16 = (B.mk[lane >> 1] >> (16u * (lane & 1u))) & 0xFFFFu;
+      const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W16, 1);
+      const uint32_t pw = lane ? (Wp >> 15) & 1u : prevW;
+      uint32_t R16 = (W16 & ~((W16 << 1) | pw)) | (W16 & mk16);
+      // a run reaching the chunk end continues in the next chunk
+      const bool last_chunk = cb + kChunk >= B1;
+      const bool defer = !last_chunk && ((__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u);
+      const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R16 != 0u);
+      bool pend_here = false;  // the carried run ends in this chunk
+      int32_t new_pend = -1;
+      if (defer) {
+        if (b_r) {
+          const uint32_t L2 = 31 - __clz(b_r);
+          const uint32_t top = __shfl_sync(0xFFFFFFFFu, R16, L2);
+          const uint32_t bit = 31 - __clz(top);
+          new_pend = (int32_t)(cb + L2 * 16u + bit);
+          if (lane == L2) R16 &= ~(1u << bit);
+          pend_here = pend_start >= 0;
+        }  // else: the carried run spans the whole chunk
+      } else {
+        pend_here = pend_start >= 0;
+      }
+      const uint32_t E16 = R16 | P16;
+      const uint32_t cnt = __popc(E16);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      const uint32_t ph = pend_here ? 1u : 0u;
+      const uint32_t nev = __shfl_sync(0xFFFFFFFFu, incl, 31) + ph;
+      {
+        uint32_t k = incl - cnt + ph;
+        uint32_t e = E16;
+        while (e) {
+          const uint32_t bit = __ffs(e) - 1;
+          e &= e - 1u;
+          B.ev[k++] = (uint16_t)(lane * 16u + bit);
+        }
+      }
+      if (lane == 0 && ph) B.ev[0] = 0xFFFFu;
+      __syncwarp();
+      // ---- (3) tokens, 32 events at a time, then (4) rules
+      for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
+        const uint32_t k = e0 + lane;
+        uint32_t ntk = 0, at0 = 0, at1 = 0, kind = K_W, rq = 0;
+        if (k < nev) {
+          const uint32_t p = B.ev[k];
+          if (p == 0xFFFFu) {
+            // carried run: [pend_start, stop) with stop the first non-word byte or request start here
+            const uint32_t ps = (uint32_t)pend_start;
+            uint32_t stop = 0;
+            for (uint32_t w = 0;; ++w) {
+              const uint32_t sm = ~B.wm[w] | B.mk[w];
+              if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
+            }
+            const uint32_t n = cb + stop - ps;
+            uint64_t k0 = 0, k1 = 0, tl = 0;
+            for (uint32_t j = 0; j < 16u && j < n; ++j) {
+              const uint64_t c = (uint64_t)(__ldg(a.bytes + ps + j) | 0x20u);
+              if (j < 8) k0 |= c << (8 * j); else k1 |= c << (8 * (j - 8));
+            }
+            for (uint32_t j = 0; j < 6u && j < n; ++j) tl |= (uint64_t)__ldg(a.bytes + ps + n - 1 - j) << (8 * j);
+            ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
+            rq = req_of(B.rs, rcnt, ps);
+          } else {
+            const uint32_t c = st8[16 + p];
+            rq = req_of(B.rs, rcnt, cb + p);
+            if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
+              // run length: up to the first non-word byte or request start
+              uint32_t n = 1, qq = p + 1;
+              for (;;) {
+                const uint32_t qw = qq >> 5, qb = qq & 31u;
+                const uint32_t stop = (~B.wm[qw] | B.mk[qw]) >> qb;
+                if (stop) { n += __ffs(stop) - 1; break; }
+                n += 32 - qb;
+                qq += 32 - qb;
+              }
+              const uint32_t x = 16 + p;
+              const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
+              const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
+                             w4 = B.stage[a0 + 4];
+              const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
+              const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
+              const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
+              const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
+              const uint32_t tb8 = x + n - 8;  // >= 8
+              const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
+              const uint32_t v0 = B.stage[ta], v1 = B.stage[ta + 1], v2 = B.stage[ta + 2];
+              const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
+              const uint64_t tl = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
+              ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
+            } else {
+              ntk = 1;
+              kind = c == ',' ? K_COMMA : (c == '.' || c == '!') ? K_END : c == '?' ? K_Q : K_OTH;
+            }
+          }
+        }
+        uint32_t ti = ntk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ti, o);
+          if (lane >= (uint32_t)o) ti += t;
+        }
+        const uint32_t nt = __shfl_sync(0xFFFFFFFFu, ti, 31);
+        if (ntk) {
+          const uint32_t t0 = (uint32_t)tokbase + ti - ntk;
+          B.t_meta[t0 & (kRing - 1)] = (uint8_t)(kind | (rq << 3));
+          B.t_attr[t0 & (kRing - 1)] = at0;
+          if (ntk == 2) {
+            B.t_meta[(t0 + 1) & (kRing - 1)] = (uint8_t)(K_W | (rq << 3));
+            B.t_attr[(t0 + 1) & (kRing - 1)] = at1;
+          }
+        }
+        __syncwarp();
+        for (uint32_t t = 0; t < nt; t += 32)
+          rules_batch(B, cy, tokbase + (int32_t)t, tokbase + (int32_t)nt, lane);
+        tokbase += (int32_t)nt;
+        __syncwarp();
+      }
+      // dropped bytes (rare): count per request
+      if (__any_sync(0xFFFFFFFFu, X16 != 0u)) {
+        uint32_t xm = X16;
+        while (xm) {
+          const uint32_t bit = __ffs(xm) - 1;
+          xm &= xm - 1u;
+          atomicAdd(&B.acc[req_of(B.rs, rcnt, g + bit)][7], 1u);
+        }
+      }
+      if (pend_here) pend_start = -1;
+      if (defer && b_r) pend_start = new_pend;
+      prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
+      __syncwarp();
+    }
+    // ---- epilogue: lane = request
+    if (rv) {
+      const uint32_t* ac = B.acc[lane];
+      uint32_t a9[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) a9[k] = ac[k];
+      uint32_t f[8];
+      bool sat;
+      Rules::finish_acc(a9, f, sat);
+      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+      epilogue(a, r, f);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_predict(const uint16_t* __restrict__ feat, uint32_t n, rt_regressor reg, float* __restrict__ u) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -743,18 +1224,16 @@ size_t score_smem_bytes(const DevLexicon& lex) {
 
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  const size_t smem = ((sizeof(Smem2) + 15) & ~size_t(15)) + ((a.lex.n_entries * sizeof(LexEntry) + 15) & ~size_t(15)) +
+  const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + ((a.lex.n_entries * sizeof(LexEntry) + 15) & ~size_t(15)) +
                       (((size_t(1) << a.lex.bits) * 2 + 15) & ~size_t(15));
-  cudaError_t e = cudaFuncSetAttribute(k_score2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_score4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score2, kT2, smem);
+  e = cudaMemsetAsync(a.work, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const uint32_t ntiles = (a.n + kT2 - 1) / kT2;
-  uint32_t grid = (uint32_t)(a.num_sms * per_sm);
-  if (grid > ntiles) grid = ntiles;
-  k_score2<<<grid, kT2, smem, s>>>(a);
+  const uint32_t ntasks = (a.n + 31) / 32;
+  uint32_t grid = (uint32_t)a.num_sms;
+  if (grid * kW4 > ntasks) grid = (ntasks + kW4 - 1) / kW4;
+  k_score4<<<grid, kT4, smem, s>>>(a, a.work);
   note_launch();
   return cudaGetLastError();
 }

@@ -18,34 +18,52 @@ constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr uint32_t kTile = kThreads * kItems;  // 4096 keys
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxPass = 8;
+constexpr uint32_t kFlagA = 1u << 30;  // tile aggregate published
+constexpr uint32_t kFlagP = 2u << 30;  // inclusive prefix published
+constexpr uint32_t kCountMask = (1u << 30) - 1u;
 
-__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ keys, uint32_t n, int shift,
-                                                    uint32_t ntiles, uint32_t* __restrict__ hist,
-                                                    const uint32_t* __restrict__ n_dev) {
-  __shared__ uint32_t h[256];
+struct Passes {
+  int n;
+  int shift[kMaxPass];
+};
+
+__device__ __forceinline__ uint32_t digit_of(uint64_t key, int shift) { return (uint32_t)(~key >> shift) & 0xFFu; }
+
+// global digit histograms of every pass in one read of the keys
+__global__ void __launch_bounds__(kThreads) k_ghist(const uint64_t* __restrict__ keys, uint32_t n,
+                                                     const uint32_t* __restrict__ n_dev, Passes ps,
+                                                     uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kMaxPass][256];
   if (n_dev) n = min(n, *n_dev);
-  h[threadIdx.x] = 0;
+  for (int p = 0; p < kMaxPass; ++p) h[p][threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t t0 = blockIdx.x * kTile;
-#pragma unroll 4
-  for (int k = 0; k < kItems; ++k) {
-    uint32_t i = t0 + k * kThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(uint32_t)(~keys[i] >> shift) & 0xFFu], 1u);
+  for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+    const uint64_t k = keys[i];
+#pragma unroll
+    for (int p = 0; p < kMaxPass; ++p)
+      if (p < ps.n) atomicAdd(&h[p][digit_of(k, ps.shift[p])], 1u);
   }
   __syncthreads();
-  hist[blockIdx.x * 256u + threadIdx.x] = h[threadIdx.x];  // tile-major
+  for (int p = 0; p < ps.n; ++p) {
+    const uint32_t c = h[p][threadIdx.x];
+    if (c) atomicAdd(&ghist[p * 256 + threadIdx.x], c);
+  }
 }
 
-// exclusive scan of the tile-major histogram in digit-major order: thread d
-// owns digit d (coalesced across threads), sums its column, a block scan over
-// digits gives the digit bases, a second pass writes the running offsets.
-__global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ hist, uint32_t ntiles) {
-  __shared__ uint32_t wsum[8];
-  const uint32_t d = threadIdx.x, lane = d & 31u, w = d >> 5;
-  uint32_t s = 0;
-#pragma unroll 8
-  for (uint32_t t = 0; t < ntiles; ++t) s += hist[t * 256u + d];
-  uint32_t incl = s;
+__device__ __forceinline__ void st_relaxed(uint32_t* a, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+// exclusive block scan over 256 threads (one value each)
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* wsum) {
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  uint32_t incl = x;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -53,57 +71,105 @@ __global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ hist, uint3
   }
   if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  uint32_t run = incl - s;
+  uint32_t run = incl - x;
   for (uint32_t k = 0; k < w; ++k) run += wsum[k];
-#pragma unroll 8
-  for (uint32_t t = 0; t < ntiles; ++t) {
-    const uint32_t v = hist[t * 256u + d];
-    hist[t * 256u + d] = run;
-    run += v;
-  }
+  return run;
 }
 
-__global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                       uint32_t base_index, uint32_t n, int shift, uint32_t ntiles,
-                                                       const uint32_t* __restrict__ hist, uint64_t* __restrict__ kout,
-                                                       uint32_t* __restrict__ vout, const uint32_t* __restrict__ n_dev) {
+// One stable counting pass ("onesweep"): a tile ranks its keys per warp with
+// __match_any_sync, publishes its digit counts, looks back over the earlier
+// tiles' published counts (decoupled look-back, tiles taken in launch order
+// from an atomic counter), reorders the tile in shared memory by digit and
+// writes runs of equal digits contiguously.
+__global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t* __restrict__ kin,
+                                                        const uint32_t* __restrict__ vin, uint32_t base_index,
+                                                        uint32_t n, const uint32_t* __restrict__ n_dev, int shift,
+                                                        const uint32_t* __restrict__ ghist, uint32_t* status,
+                                                        uint32_t* counter, uint64_t* __restrict__ kout,
+                                                        uint32_t* __restrict__ vout) {
+  extern __shared__ __align__(16) uint8_t sort_smem[];
+  uint64_t* s_k = reinterpret_cast<uint64_t*>(sort_smem);               // [kTile]
+  uint32_t* s_v = reinterpret_cast<uint32_t*>(sort_smem + kTile * 8);   // [kTile]
+  __shared__ uint32_t s_wcnt[kWarps][256];
+  __shared__ uint32_t s_loc[256], s_glob[256], s_wsum[2][8];
+  __shared__ uint32_t s_tile;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(counter, 1u);
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) s_wcnt[k][tid] = 0;
   if (n_dev) n = min(n, *n_dev);
-  __shared__ uint32_t s_base[256];           // running output position per digit
-  __shared__ uint16_t s_cnt[kWarps][256];    // per-warp digit counts of the current round
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  s_base[threadIdx.x] = hist[blockIdx.x * 256u + threadIdx.x];
-  const uint32_t t0 = blockIdx.x * kTile;
+  __syncthreads();
+  const uint32_t tile = s_tile, t0 = tile * kTile;
+  if (t0 >= n) return;
+  uint64_t key[kItems];
+  uint32_t val[kItems], dg[kItems], rk[kItems];
+  const uint32_t wb = t0 + w * (kTile / kWarps);
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const uint32_t i = wb + r * 32 + lane;
+    const bool ok = i < n;
+    key[r] = ok ? kin[i] : 0ull;
+    val[r] = ok ? (vin ? vin[i] : base_index + i) : 0u;
+    dg[r] = ok ? digit_of(key[r], shift) : 256u;
+  }
   const uint32_t lt = (1u << lane) - 1u;
-  for (int k = 0; k < kItems; ++k) {
-    for (int w = 0; w < kWarps; ++w) s_cnt[w][threadIdx.x] = 0;
-    __syncthreads();
-    const uint32_t i = t0 + k * kThreads + threadIdx.x;
-    const bool valid = i < n;
-    uint64_t key = valid ? kin[i] : 0ull;
-    uint32_t val = valid ? (vin ? vin[i] : base_index + i) : 0u;
-    uint32_t d = valid ? ((uint32_t)(~key >> shift) & 0xFFu) : 256u;
-    uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-    uint32_t rank = __popc(peers & lt);
-    if (valid && rank == 0) s_cnt[warp][d] = (uint16_t)__popc(peers);
-    __syncthreads();
-    // per digit: exclusive prefix over warps (thread = digit)
-    {
-      uint32_t run = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        uint32_t c = s_cnt[w][threadIdx.x];
-        s_cnt[w][threadIdx.x] = (uint16_t)run;
-        run += c;
-      }
-      __syncthreads();
-      if (valid) {
-        uint32_t pos = s_base[d] + s_cnt[warp][d] + rank;
-        kout[pos] = key;
-        vout[pos] = val;
-      }
-      __syncthreads();
-      s_base[threadIdx.x] += run;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const uint32_t d = dg[r];
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    const uint32_t before = d < 256u ? s_wcnt[w][d] : 0u;
+    rk[r] = before + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256u && (peers & lt) == 0u) s_wcnt[w][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // thread = digit: tile count, per-warp exclusive prefix
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) {
+    const uint32_t c = s_wcnt[k][tid];
+    s_wcnt[k][tid] = tot;
+    tot += c;
+  }
+  uint32_t* st = status + (size_t)tile * 256u + tid;
+  if (tile == 0) st_relaxed(st, kFlagP | tot);
+  else st_relaxed(st, kFlagA | tot);
+  const uint32_t gbase = block_excl_scan256(ghist[tid], s_wsum[0]);
+  const uint32_t lbase = block_excl_scan256(tot, s_wsum[1]);
+  uint32_t excl = 0;
+  if (tile > 0) {
+    uint32_t p = tile - 1;
+    for (;;) {
+      uint32_t v;
+      do { v = ld_relaxed(status + (size_t)p * 256u + tid); } while ((v & ~kCountMask) == 0u);
+      excl += v & kCountMask;
+      if ((v & kFlagP) || p == 0) break;
+      --p;
     }
-    __syncthreads();
+    st_relaxed(st, kFlagP | (excl + tot));
+  }
+  s_loc[tid] = lbase;
+  s_glob[tid] = gbase + excl;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const uint32_t d = dg[r];
+    if (d < 256u) {
+      const uint32_t lp = s_loc[d] + s_wcnt[w][d] + rk[r];
+      s_k[lp] = key[r];
+      s_v[lp] = val[r];
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = min(kTile, n - t0);
+#pragma unroll 4
+  for (uint32_t i = tid; i < cnt; i += kThreads) {
+    const uint64_t k = s_k[i];
+    const uint32_t d = digit_of(k, shift);
+    const uint32_t pos = s_glob[d] + (i - s_loc[d]);
+    kout[pos] = k;
+    vout[pos] = s_v[i];
   }
 }
 
@@ -176,11 +242,15 @@ cudaError_t split_by_class(const uint64_t* key, uint32_t base, uint32_t n, uint3
   return cudaGetLastError();
 }
 
+static size_t status_words(uint32_t n) {
+  const size_t ntiles = (n + kTile - 1) / kTile;
+  return (size_t)kMaxPass * 256 + kMaxPass + (size_t)kMaxPass * ntiles * 256;  // ghist, counters, status
+}
+
 size_t radix_sort_workspace(uint32_t n) {
-  size_t ntiles = (n + kTile - 1) / kTile;
   size_t a = ((size_t)n * 8 + 255) & ~size_t(255);
   size_t b = ((size_t)n * 4 + 255) & ~size_t(255);
-  return 2 * a + b + ((256 * ntiles * 4 + 255) & ~size_t(255));
+  return 2 * a + b + ((status_words(n) * 4 + 255) & ~size_t(255));
 }
 
 // keys_in: n keys; perm_out: n global indices (base_index + i) sorted by key desc.
@@ -201,24 +271,31 @@ cudaError_t radix_sort_desc2(const uint64_t* keys_in, const uint32_t* vals_in, u
   uint64_t* k1 = reinterpret_cast<uint64_t*>(p);
   uint64_t* k2 = reinterpret_cast<uint64_t*>(p + a);
   uint32_t* v2 = reinterpret_cast<uint32_t*>(p + 2 * a);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p + 2 * a + b);
+  uint32_t* ghist = reinterpret_cast<uint32_t*>(p + 2 * a + b);
+  uint32_t* counters = ghist + kMaxPass * 256;
+  uint32_t* status = counters + kMaxPass;
+  Passes ps;
   const int shifts_f[5] = {0, 8, 16, 24, 56};
-  const int nsh = full64 ? 8 : 5;
+  ps.n = full64 ? 8 : 5;
+  for (int j = 0; j < kMaxPass; ++j) ps.shift[j] = j < ps.n ? (full64 ? 8 * j : shifts_f[j]) : 0;
+  cudaMemsetAsync(ghist, 0, status_words(n) * 4, s);
+  const uint32_t gh_blocks = ntiles < 592 ? ntiles : 592;
+  k_ghist<<<gh_blocks, kThreads, 0, s>>>(keys_in, n, n_dev, ps, ghist);
+  const int smem = kTile * 12;
+  cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // ping-pong: pass j reads (ksrc, vsrc) writes (kdst, vdst); last pass writes perm_out
   const uint64_t* ksrc = keys_in;
   const uint32_t* vsrc = vals_in;  // null = identity (base_index + i)
-  for (int j = 0; j < nsh; ++j) {
-    const int shift = full64 ? 8 * j : shifts_f[j];
+  for (int j = 0; j < ps.n; ++j) {
     uint64_t* kdst = (j & 1) ? k2 : k1;
     // values ping-pong between perm_out and v2 so that the last pass writes perm_out
-    uint32_t* vdst = ((nsh - 1 - j) & 1) ? v2 : perm_out;
-    k_hist<<<ntiles, kThreads, 0, s>>>(ksrc, n, shift, ntiles, hist, n_dev);
-    k_scan<<<1, 256, 0, s>>>(hist, ntiles);
-    k_scatter<<<ntiles, kThreads, 0, s>>>(ksrc, vsrc, base_index, n, shift, ntiles, hist, kdst, vdst, n_dev);
-    note_launch(3);
+    uint32_t* vdst = ((ps.n - 1 - j) & 1) ? v2 : perm_out;
+    k_onesweep<<<ntiles, kThreads, smem, s>>>(ksrc, vsrc, base_index, n, n_dev, ps.shift[j], ghist + j * 256,
+                                              status + (size_t)j * ntiles * 256, counters + j, kdst, vdst);
     ksrc = kdst;
     vsrc = vdst;
   }
+  note_launch(1 + ps.n);
   return cudaGetLastError();
 }
 
