@@ -230,7 +230,7 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
   if (!parse_lexicon(text, len, lemmas, attrs, err)) return fail(c, RT_ELEXICON, err);
   const uint32_t n = (uint32_t)lemmas.size();
   uint32_t bits = 6;
-  while ((1u << bits) < 2 * n) ++bits;
+  while ((1u << bits) < 4 * n) ++bits;  // load factor <= 1/4
   std::vector<LexEntry> ent(n);
   std::vector<uint16_t> slots(1u << bits, 0);
   for (uint32_t k = 0; k < n; ++k) {

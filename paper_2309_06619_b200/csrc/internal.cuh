@@ -41,9 +41,13 @@ struct DevLexicon {
 };
 
 __host__ __device__ __forceinline__ uint32_t lex_hash(uint64_t k0, uint64_t k1, uint32_t len, uint32_t bits) {
-  uint64_t h = (k0 * 0x9E3779B97F4A7C15ull) ^ ((k1 + len) * 0xC2B2AE3D27D4EB4Full);
-  h ^= h >> 31;
-  return (uint32_t)((h * 0xD6E8FEB86659FD93ull) >> (64 - bits));
+  // 32-bit multiply-xor hash of the (<= 16-byte) key (bits >= 6)
+  uint32_t h = (uint32_t)k0 * 0x9E3779B1u;
+  h ^= ((uint32_t)(k0 >> 32) + len) * 0x85EBCA77u;
+  h ^= ((uint32_t)k1 ^ (uint32_t)(k1 >> 32)) * 0xC2B2AE3Du;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  return h >> (32 - bits);
 }
 
 // ---------------------------------------------------------------- keys

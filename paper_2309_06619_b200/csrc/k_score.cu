@@ -742,7 +742,7 @@ constexpr uint32_t kRing = 128;               // token ring per warp
 enum : uint32_t { K_W = 1, K_COMMA = 2, K_END = 3, K_Q = 4, K_OTH = 5 };
 
 struct __align__(16) WarpBuf {
-  uint32_t stage[4 + kChunk / 4 + 8];  // 16 B pad | chunk | 32 B pad
+  uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
   uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
   uint16_t ev[kChunk + 1];
   uint32_t rs[32];                     // request starts (absolute byte offsets)
@@ -798,6 +798,24 @@ __device__ __forceinline__ uint32_t run_tokens(const Lex& L, const uint32_t* pre
   attr0 = e0 ? L.e[e0 - 1].attr : 0u;
   attr1 = e1 ? L.e[e1 - 1].attr : 0u;
   return 2;
+}
+
+// word token(s) of the run of n bytes at stage byte x
+__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L,
+                                              const uint32_t* pref, uint32_t& at0, uint32_t& at1) {
+  const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
+  const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
+                 w4 = B.stage[a0 + 4];
+  const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
+  const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
+  const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
+  const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
+  const uint32_t tb8 = x + n - 8;  // >= 8
+  const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
+  const uint32_t v0 = B.stage[ta], v1 = B.stage[ta + 1], v2 = B.stage[ta + 2];
+  const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
+  const uint64_t tl = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
+  return run_tokens(L, pref, n, k0, k1, tl, at0, at1);
 }
 
 struct Carry {
@@ -1005,6 +1023,8 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     uint32_t prevW = 0;                 // W bit of the byte before the chunk
     int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
     const uint32_t base = B0 & ~15u;
+    uint4 qprev = make_uint4(0, 0, 0, 0);
+    int32_t tokdone = 0;                // tokens already through the rules
     __syncwarp();
     for (uint32_t cb = base; cb < B1; cb += kChunk) {
       // ---- (1) stage + classify 16 bytes per lane
@@ -1017,7 +1037,9 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
           if (g + j < total_bytes) w4[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
         q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
-      *reinterpret_cast<uint4*>(&B.stage[4 + lane * 4]) = q;
+      *reinterpret_cast<uint4*>(&B.stage[4 + lane * 4]) = qprev;
+      *reinterpret_cast<uint4*>(&B.stage[4 + kChunk / 4 + lane * 4]) = q;
+      qprev = q;
       if (lane < kChunk / 32 + 1) B.mk[lane] = 0;
       __syncwarp();
       if (rv && s_r >= cb && s_r < cb + kChunk && s_r < B1)
@@ -1104,16 +1126,20 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
             }
             const uint32_t n = cb + stop - ps;
-            uint64_t k0 = 0, k1 = 0, tl = 0;
-            for (uint32_t j = 0; j < 16u && j < n; ++j) {
-              const uint64_t c = (uint64_t)(__ldg(a.bytes + ps + j) | 0x20u);
-              if (j < 8) k0 |= c << (8 * j); else k1 |= c << (8 * (j - 8));
+            if (ps + kChunk >= cb) {
+              ntk = stage_run(B, 16 + kChunk + ps - cb, n, L, S.pref, at0, at1);
+            } else {  // run longer than a chunk: bytes from global memory
+              uint64_t k0 = 0, k1 = 0, tl = 0;
+              for (uint32_t j = 0; j < 16u && j < n; ++j) {
+                const uint64_t c = (uint64_t)(__ldg(a.bytes + ps + j) | 0x20u);
+                if (j < 8) k0 |= c << (8 * j); else k1 |= c << (8 * (j - 8));
+              }
+              for (uint32_t j = 0; j < 6u && j < n; ++j) tl |= (uint64_t)__ldg(a.bytes + ps + n - 1 - j) << (8 * j);
+              ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
             }
-            for (uint32_t j = 0; j < 6u && j < n; ++j) tl |= (uint64_t)__ldg(a.bytes + ps + n - 1 - j) << (8 * j);
-            ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
             rq = req_of(B.rs, rcnt, ps);
           } else {
-            const uint32_t c = st8[16 + p];
+            const uint32_t c = st8[16 + kChunk + p];
             rq = req_of(B.rs, rcnt, cb + p);
             if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
               // run length: up to the first non-word byte or request start
@@ -1125,20 +1151,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
                 n += 32 - qb;
                 qq += 32 - qb;
               }
-              const uint32_t x = 16 + p;
-              const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
-              const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
-                             w4 = B.stage[a0 + 4];
-              const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
-              const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
-              const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
-              const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
-              const uint32_t tb8 = x + n - 8;  // >= 8
-              const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
-              const uint32_t v0 = B.stage[ta], v1 = B.stage[ta + 1], v2 = B.stage[ta + 2];
-              const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
-              const uint64_t tl = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
-              ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
+              ntk = stage_run(B, 16 + kChunk + p, n, L, S.pref, at0, at1);
             } else {
               ntk = 1;
               kind = c == ',' ? K_COMMA : (c == '.' || c == '!') ? K_END : c == '?' ? K_Q : K_OTH;
@@ -1162,9 +1175,8 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
           }
         }
         __syncwarp();
-        for (uint32_t t = 0; t < nt; t += 32)
-          rules_batch(B, cy, tokbase + (int32_t)t, tokbase + (int32_t)nt, lane);
         tokbase += (int32_t)nt;
+        for (; tokbase - tokdone >= 32; tokdone += 32) rules_batch(B, cy, tokdone, tokdone + 32, lane);
         __syncwarp();
       }
       // dropped bytes (rare): count per request
@@ -1181,6 +1193,8 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
       __syncwarp();
     }
+    for (; tokdone < tokbase; tokdone += 32) rules_batch(B, cy, tokdone, min(tokdone + 32, tokbase), lane);
+    __syncwarp();
     // ---- epilogue: lane = request
     if (rv) {
       const uint32_t* ac = B.acc[lane];
