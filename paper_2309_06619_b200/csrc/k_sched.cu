@@ -517,7 +517,9 @@ cudaError_t launch_cpu_big(const SchedLaunch& a, uint32_t lo, uint32_t n, const 
   uint8_t* csel = reinterpret_cast<uint8_t*>(w);
   const uint32_t nch = (n + kPredBlock - 1) / kPredBlock;
   k_cpu_pred<<<nch, 256, 0, s>>>(a, lo, ncpu, pred, chunk_max);
-  const int smem = 2 * kCpuChunk * (sizeof(uint64_t) + 1);
+  // the serial chain is latency-bound: ask for (nearly) a whole SM's shared memory so
+  // that no other kernel's CTA is co-scheduled on its SM
+  const int smem = 200 * 1024;
   if (a.cores <= 4) {
     cudaFuncSetAttribute(k_cpu_chain<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_cpu_chain<4><<<1, 128, smem, s>>>(a.cores, ncpu, pred, chunk_max, csel);

@@ -745,6 +745,7 @@ struct __align__(16) WarpBuf {
   uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
   uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
   uint16_t ev[kChunk + 1];
+  uint8_t evq[kChunk + 1];             // request of each event
   uint32_t rs[32];                     // request starts (absolute byte offsets)
   uint32_t t_attr[kRing];
   uint8_t t_meta[kRing];               // kind | req << 3
@@ -1100,13 +1101,16 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       }
       const uint32_t ph = pend_here ? 1u : 0u;
       const uint32_t nev = __shfl_sync(0xFFFFFFFFu, incl, 31) + ph;
-      {
+      if (E16) {
         uint32_t k = incl - cnt + ph;
         uint32_t e = E16;
+        uint32_t rq = req_of(B.rs, rcnt, g);  // request at this lane's first byte, advanced per event
         while (e) {
           const uint32_t bit = __ffs(e) - 1;
           e &= e - 1u;
-          B.ev[k++] = (uint16_t)(lane * 16u + bit);
+          while (rq + 1 < rcnt && B.rs[rq + 1] <= g + bit) ++rq;
+          B.ev[k] = (uint16_t)(lane * 16u + bit);
+          B.evq[k++] = (uint8_t)rq;
         }
       }
       if (lane == 0 && ph) B.ev[0] = 0xFFFFu;
@@ -1140,7 +1144,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
             rq = req_of(B.rs, rcnt, ps);
           } else {
             const uint32_t c = st8[16 + kChunk + p];
-            rq = req_of(B.rs, rcnt, cb + p);
+            rq = B.evq[k];
             if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
               // run length: up to the first non-word byte or request start
               uint32_t n = 1, qq = p + 1;
