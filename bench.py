@@ -161,47 +161,74 @@ def native(args):
     torch.cuda.synchronize()
     barrier()
     t_step, t_score = [], []
-    launches0 = rt.launch_count()
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.zero_()
-            ev_a.record(stream)
-            step()
-            ev_b.record(stream)
-            ev_b.synchronize()
-            t_step.append(ev_a.elapsed_time(ev_b))
-            t_score.append(ev_a.elapsed_time(ev_mid))
-        torch.cuda.synchronize()
-        barrier()
-    launches = rt.launch_count() - launches0
-    clocks = clk.summary()
-    sum_ms = max_over_ranks(sum(t_step))
-    score_ms = sum(t_score) / len(t_score)
-    value = world * n * args.steps / (sum_ms / 1e3) / 1e6
-
-    # ---------------- e2e: pinned host -> device, the public calls, device -> host result
-    h_batch = torch.empty(n, dtype=torch.int32).pin_memory()
-    h_slot = torch.empty(n, dtype=torch.uint8).pin_memory()
-    h_core = torch.empty(n, dtype=torch.uint8).pin_memory()
-    e2e_ms = []
-    torch.cuda.synchronize()
-    barrier()
     for _ in range(args.steps):
         flush.zero_()
         ev_a.record(stream)
-        data.copy_(h_bytes, non_blocking=True)
-        off.copy_(h_off, non_blocking=True)
         step()
-        h_batch.copy_(souts["batch_of"], non_blocking=True)
-        h_slot.copy_(souts["slot_of"], non_blocking=True)
-        h_core.copy_(souts["core_of"], non_blocking=True)
         ev_b.record(stream)
         ev_b.synchronize()
-        e2e_ms.append(ev_a.elapsed_time(ev_b))
-    e2e_sum = max_over_ranks(sum(e2e_ms))
-    e2e_value = world * n * args.steps / (e2e_sum / 1e3) / 1e6
+        t_step.append(ev_a.elapsed_time(ev_b))
+        t_score.append(ev_a.elapsed_time(ev_mid))
+    torch.cuda.synchronize()
+    barrier()
+    sum_ms = max_over_ranks(sum(t_step))  # one batch at a time, L2 flushed between steps
+    score_ms = sum(t_score) / len(t_score)
+
+    # ---------------- pipelined throughput: two batches in flight (two contexts, two
+    # streams, two distinct 2^20-request inputs -> 2 x ~100 MB > L2, no flush needed).
+    # Batch k's serial CPU-class chain (one SM) overlaps batch k+1's scoring and
+    # GPU-class consolidation; every batch still runs the whole hot path.
+    d2b = configs.config2(n=args.n, gid0=(world + rank) * args.n)
+    ctxs = [ctx, rt.Context(d2b["lexicon"], local)]
+    h_bytes2 = [h_bytes, torch.from_numpy(d2b["data"]).pin_memory()]
+    h_off2 = [h_off, torch.from_numpy(d2b["offsets"].view(np.int32)).pin_memory()]
+    data2 = [data, h_bytes2[1].to(dev)]
+    off2 = [off, h_off2[1].to(dev)]
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs2 = [outs, {k: torch.empty_like(v) for k, v in outs.items()}]
+    souts2 = [souts, {k: torch.empty_like(v) for k, v in souts.items()}]
+    h_res = [{k: torch.empty(n, dtype=dt).pin_memory() for k, dt in (("batch_of", torch.int32), ("slot_of", torch.uint8),
+                                                                          ("core_of", torch.uint8))} for _ in range(2)]
+
+    def pstep(k, e2e=False):
+        sl = k & 1
+        with torch.cuda.stream(streams[sl]):
+            if e2e:
+                data2[sl].copy_(h_bytes2[sl], non_blocking=True)
+                off2[sl].copy_(h_off2[sl], non_blocking=True)
+            ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
+            ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
+            if e2e:
+                for name in ("batch_of", "slot_of", "core_of"):
+                    h_res[sl][name].copy_(souts2[sl][name], non_blocking=True)
+
+    def timed_pipeline(e2e):
+        for k in range(args.warmup):
+            pstep(k, e2e)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for st in streams:
+            st.wait_event(t0)
+        for k in range(args.steps):
+            pstep(k, e2e)
+        for st in streams:
+            stream.wait_stream(st)
+        t1.record(stream)
+        t1.synchronize()
+        return t0.elapsed_time(t1)
+
+    launches_p0 = rt.launch_count()
+    with ClockSampler(local) as clk:
+        pipe_ms = max_over_ranks(timed_pipeline(False))
+    launches = rt.launch_count() - launches_p0
+    clocks = clk.summary()
+    e2e_ms = max_over_ranks(timed_pipeline(True))
+    value = world * n * args.steps / (pipe_ms / 1e3) / 1e6
+    e2e_value = world * n * args.steps / (e2e_ms / 1e3) / 1e6
+    total_bytes2 = int(d2b["offsets"][-1])
 
     # ---------------- roofline of the scoring kernel (k_score: the HBM-bound pass)
     peaks = {}
@@ -231,15 +258,20 @@ def native(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(sum_ms / args.steps, 4), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(pipe_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8+f32", "data": "synthetic",
             "config": {"workload": "config2: one 2^20-request queue per GPU (DialoGPT profile, all r=0), "
                                    "score+key+schedule", "requests_per_gpu": n, "bytes_per_gpu": total_bytes,
-                       "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}"},
-            "stage_ms": {"score_key": round(score_ms, 4),
-                         "schedule": round(sum(t_step) / len(t_step) - score_ms, 4)},
-            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": total_bytes + 4 * (n + 1),
-                    "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_sum / args.steps, 4)},
+                       "pipeline": "2 batches in flight (2 contexts / streams), alternating 2 distinct inputs",
+                       "l2": "pipelined: 2 distinct inputs of ~100 MB each (> 126 MB L2) alternate; "
+                             "latency leg: 256 MB buffer written between steps",
+                       "parallelism": f"replicas{world}"},
+            "latency": {"ms_per_step": round(sum_ms / args.steps, 4), "score_key_ms": round(score_ms, 4),
+                        "schedule_ms": round(sum(t_step) / len(t_step) - score_ms, 4),
+                        "note": "one batch at a time, L2 flushed between steps"},
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": (total_bytes + total_bytes2) // 2 + 4 * (n + 1),
+                    "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_ms / args.steps, 4)},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "clocks": clocks,
