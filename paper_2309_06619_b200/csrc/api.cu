@@ -488,6 +488,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   a.core_of = d_core_of;
   a.seg_count = static_cast<uint32_t*>(c->ws);
   a.seg_batch_off = d_seg_batch_off;
+  a.num_sms = c->num_sms;
   char* big = static_cast<char*>(c->ws) + cnt_bytes;
   cudaError_t e = rtlm::launch_sched_small(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_sched_small");

@@ -112,6 +112,7 @@ struct SchedLaunch {
   uint8_t* core_of;
   uint32_t* seg_count;       // device, nq (local batch counts)
   uint32_t* seg_batch_off;   // device, nq + 1
+  int num_sms;
 };
 // small queues (all segments with n <= kSmallSeg; others skipped)
 cudaError_t launch_sched_small(const SchedLaunch& a, cudaStream_t s);

@@ -19,6 +19,8 @@
 // The last partial windows (stream exhausted) are finished by one warp (tail).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace rtlm {
@@ -205,6 +207,93 @@ __global__ void __launch_bounds__(1024) k_ff_scan(FF f, uint64_t* loc) {
       merge_topk(gp, tmp, nx, K);
       for (uint32_t i = lane; i < KS; i += 32) f.heapH[(size_t)c * KS + i] = nx[i];
       __syncwarp();
+    }
+  }
+}
+
+// ---- K <= 32: top-K lists held in a warp's registers (lane i = i-th largest,
+// zero padding below every real key).
+__device__ __forceinline__ uint64_t sort32_desc(uint64_t v) {  // bitonic sort across the warp
+  const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+      const bool keep_max = ((lane & k) == 0) == ((lane & j) == 0);
+      v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
+    }
+  return v;
+}
+
+// top 32 of the union of two descending lists, descending
+__device__ __forceinline__ uint64_t merge32_desc(uint64_t a, uint64_t b) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t br = __shfl_sync(0xFFFFFFFFu, b, 31 - lane);
+  uint64_t v = a > br ? a : br;  // bitonic (decreasing, then increasing)
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+    v = (lane & j) == 0 ? (v > o ? v : o) : (v < o ? v : o);
+  }
+  return v;
+}
+
+// 2a (K <= 32): top-K of every chunk, one warp per chunk; a batch of 32 keys is
+// merged only if one of them beats the current K-th largest
+__global__ void __launch_bounds__(256) k_ff_topk32(FF f) {
+  const uint32_t G = f.scal[1], K = f.K;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+  const uint32_t p0 = c * B1;
+  if (p0 >= G) return;
+  const uint32_t p1 = min(G, p0 + B1);
+  uint64_t top = 0, thr = 0;
+  for (uint32_t pb = p0; pb < p1; pb += 32) {
+    const uint64_t x = pb + lane < p1 ? f.kk[pb + lane] : 0ull;
+    if (!__any_sync(0xFFFFFFFFu, x > thr)) continue;
+    top = merge32_desc(top, sort32_desc(x));
+    thr = __shfl_sync(0xFFFFFFFFu, top, K - 1);
+  }
+  f.summ[(size_t)c * KS + lane] = lane < K ? top : 0ull;
+}
+
+// 2b (K <= 32): exclusive prefix top-K over chunks, one CTA of 32 warps:
+// running merges inside 32 groups, a scan of the group totals, then
+// H[c] = merge(group prefix, inclusive[c - 1]).
+__global__ void __launch_bounds__(1024) k_ff_scan32(FF f, uint64_t* loc) {
+  __shared__ uint64_t s_tot[32][32], s_pre[32][32];
+  const uint32_t G = f.scal[1], K = f.K;
+  const uint32_t nc = (G + B1 - 1) / B1;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t gs = (nc + 31) / 32;
+  const uint32_t c0 = min(nc, w * gs), c1 = min(nc, c0 + gs);
+  uint64_t acc = 0;
+  uint64_t nxt = c0 < c1 ? f.summ[(size_t)c0 * KS + lane] : 0ull;
+  for (uint32_t c = c0; c < c1; ++c) {
+    const uint64_t t = nxt;
+    if (c + 1 < c1) nxt = f.summ[(size_t)(c + 1) * KS + lane];
+    acc = merge32_desc(acc, t);
+    loc[(size_t)c * KS + lane] = lane < K ? acc : 0ull;
+  }
+  s_tot[w][lane] = lane < K ? acc : 0ull;
+  __syncthreads();
+  if (w == 0) {
+    uint64_t run = 0;
+    for (uint32_t g = 0; g < 32; ++g) {
+      s_pre[g][lane] = run;
+      const uint32_t gc0 = min(nc, g * gs);
+      if (gc0 < min(nc, gc0 + gs)) run = merge32_desc(run, s_tot[g][lane]);
+    }
+    f.hfinal[lane] = lane < K ? run : 0ull;
+    for (uint32_t i = 32 + lane; i < KS; i += 32) f.hfinal[i] = 0ull;
+  }
+  __syncthreads();
+  if (c0 < c1) {
+    const uint64_t gp = lane < K ? s_pre[w][lane] : 0ull;
+    f.heapH[(size_t)c0 * KS + lane] = gp;
+    for (uint32_t c = c0 + 1; c < c1; ++c) {
+      const uint64_t h = merge32_desc(gp, loc[(size_t)(c - 1) * KS + lane]);  // whole warp
+      f.heapH[(size_t)c * KS + lane] = lane < K ? h : 0ull;
     }
   }
 }
@@ -522,17 +611,19 @@ template <class T>
 __global__ void __launch_bounds__(128) k_ff_excursion(FF f) {
   __shared__ uint64_t sm[4][3 * kMaxWindow + kRing];
   const uint32_t wl = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nfail = f.scal[3], NR = f.scal[2];
-  if (gw >= nfail) return;
-  uint32_t j = f.failpos[gw], r = 0;
-  T tr;
-  tr_setup(tr, sm[wl]);
-  tr.init(f, j, NR);
-  const bool back = excursion(f, tr, j, r, NR, [](uint64_t, uint32_t) {}, [](uint32_t, uint32_t, uint32_t) {});
-  if ((threadIdx.x & 31u) == 0) {
-    f.exE[gw] = back ? j : kEnd;
-    f.exR[gw] = r;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < nfail; gw += nw) {
+    uint32_t j = f.failpos[gw], r = 0;
+    T tr;
+    tr_setup(tr, sm[wl]);
+    tr.init(f, j, NR);
+    const bool back = excursion(f, tr, j, r, NR, [](uint64_t, uint32_t) {}, [](uint32_t, uint32_t, uint32_t) {});
+    if ((threadIdx.x & 31u) == 0) {
+      f.exE[gw] = back ? j : kEnd;
+      f.exR[gw] = r;
+    }
+    __syncwarp();
   }
 }
 
@@ -552,34 +643,42 @@ __device__ void run_from(const FF& f, uint32_t z, uint32_t& fail_idx, uint32_t& 
 
 // successor of every node: node i < nfail = failing position; node nfail = start (∅ at 0)
 __global__ void __launch_bounds__(128) k_ff_link(FF f) {
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nfail = f.scal[3];
-  if (gw > nfail) return;
-  uint32_t z, r0;
-  if (gw == nfail) { z = 0; r0 = 0; }
-  else { z = f.exE[gw]; r0 = f.exR[gw]; }
-  uint32_t fi = kEnd, nch = 0;
-  if (z != kEnd) run_from(f, z, fi, nch);
-  if ((threadIdx.x & 31u) == 0) {
-    f.nxt[gw] = fi;
-    f.wr[gw] = r0 + nch;
-    f.runz[gw] = z;
-    f.runn[gw] = nch;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw <= nfail; gw += nw) {
+    uint32_t z, r0;
+    if (gw == nfail) { z = 0; r0 = 0; }
+    else { z = f.exE[gw]; r0 = f.exR[gw]; }
+    uint32_t fi = kEnd, nch = 0;
+    if (z != kEnd) run_from(f, z, fi, nch);
+    if ((threadIdx.x & 31u) == 0) {
+      f.nxt[gw] = fi;
+      f.wr[gw] = r0 + nch;
+      f.runz[gw] = z;
+      f.runn[gw] = nch;
+    }
   }
 }
 
-// pointer doubling level k from k-1
-__global__ void k_ff_double(FF f, uint32_t k) {
+// all doubling levels in one cooperative launch; stops once 2^(k-1) >= nodes
+// (every path is shorter), the number of levels built goes to scal[5]
+__global__ void __launch_bounds__(256) k_ff_double_all(FF f) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const uint32_t nn = f.scal[3] + 1;
-  const uint32_t* n0 = f.nxt + (size_t)(k - 1) * nn;
-  const uint32_t* w0 = f.wr + (size_t)(k - 1) * nn;
-  uint32_t* n1 = f.nxt + (size_t)k * nn;
-  uint32_t* w1 = f.wr + (size_t)k * nn;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
-    const uint32_t a = n0[i];
-    if (a == kEnd) { n1[i] = kEnd; w1[i] = w0[i]; }
-    else { n1[i] = n0[a]; w1[i] = w0[i] + w0[a]; }
+  uint32_t k = 1;
+  for (; k < f.levels && (1ull << (k - 1)) < nn; ++k) {
+    const uint32_t* n0 = f.nxt + (size_t)(k - 1) * nn;
+    const uint32_t* w0 = f.wr + (size_t)(k - 1) * nn;
+    uint32_t* n1 = f.nxt + (size_t)k * nn;
+    uint32_t* w1 = f.wr + (size_t)k * nn;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+      const uint32_t a = n0[i];
+      if (a == kEnd) { n1[i] = kEnd; w1[i] = w0[i]; }
+      else { n1[i] = n0[a]; w1[i] = w0[i] + w0[a]; }
+    }
+    grid.sync();
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) f.scal[5] = k;
 }
 
 // expand the path from the start node (levels high -> low), one CTA; also
@@ -593,7 +692,7 @@ __global__ void __launch_bounds__(1024) k_ff_expand(FF f) {
     f.path_off[0] = 0;
   }
   __syncthreads();
-  for (int k = (int)f.levels - 1; k >= 0; --k) {
+  for (int k = (int)min(f.levels, f.scal[5]) - 1; k >= 0; --k) {
     const uint32_t cur = cnt;
     __syncthreads();
     const uint32_t* nk = f.nxt + (size_t)k * nn;
@@ -628,24 +727,26 @@ template <class T>
 __global__ void __launch_bounds__(128) k_ff_emit_exc(FF f) {
   __shared__ uint64_t sm[4][3 * kMaxWindow + kRing];
   const uint32_t wl = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t np = f.scal[6], nfail = f.scal[3], NR = f.scal[2];
-  if (gw >= np) return;
-  const uint32_t x = f.path_node[gw];
-  if (x == nfail) return;  // start node: no excursion
-  uint32_t j = f.failpos[x], r = 0;
-  const uint32_t b0 = f.path_off[gw];
-  T tr;
-  tr_setup(tr, sm[wl]);
-  tr.init(f, j, NR);
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
-  excursion(f, tr, j, r, NR, [&](uint64_t e, uint32_t slot) { put(f, e, b0 + r, slot); },
-            [&](uint32_t j0, uint32_t c, uint32_t k) {
-              if (lane == 0) {
-                const uint32_t d = atomicAdd(&f.scal[7], 1u);
-                f.ds_j[d] = j0; f.ds_c[d] = c; f.ds_r[d] = k; f.ds_b[d] = b0 + r;
-              }
-            });
+  for (uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < np; gw += nw) {
+    const uint32_t x = f.path_node[gw];
+    if (x == nfail) continue;  // start node: no excursion
+    uint32_t j = f.failpos[x], r = 0;
+    const uint32_t b0 = f.path_off[gw];
+    T tr;
+    tr_setup(tr, sm[wl]);
+    tr.init(f, j, NR);
+    excursion(f, tr, j, r, NR, [&](uint64_t e, uint32_t slot) { put(f, e, b0 + r, slot); },
+              [&](uint32_t j0, uint32_t c, uint32_t k) {
+                if (lane == 0) {
+                  const uint32_t d = atomicAdd(&f.scal[7], 1u);
+                  f.ds_j[d] = j0; f.ds_c[d] = c; f.ds_r[d] = k; f.ds_b[d] = b0 + r;
+                }
+              });
+    __syncwarp();
+  }
 }
 
 // tail: rebuild the path end state, finish with partial windows
@@ -864,10 +965,15 @@ static cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
     note_launch();
   } else {
     const uint32_t nc = (n + B1 - 1) / B1;
-    k_ff_topk<<<nc, 256, 0, s>>>(f);
-    const int scan_smem = 32 * 3 * KS * 8;
-    cudaFuncSetAttribute(k_ff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, scan_smem);
-    k_ff_scan<<<1, 1024, scan_smem, s>>>(f, loc);
+    if (f.K <= 32) {
+      k_ff_topk32<<<(nc * 32 + 255) / 256, 256, 0, s>>>(f);
+      k_ff_scan32<<<1, 1024, 0, s>>>(f, loc);
+    } else {
+      k_ff_topk<<<nc, 256, 0, s>>>(f);
+      const int scan_smem = 32 * 3 * KS * 8;
+      cudaFuncSetAttribute(k_ff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, scan_smem);
+      k_ff_scan<<<1, 1024, scan_smem, s>>>(f, loc);
+    }
     const uint32_t rg = (nc * 32 + 127) / 128;
     if (f.K <= 32) k_ff_replay<1><<<rg, 128, 0, s>>>(f);
     else if (f.K <= 64) k_ff_replay<2><<<rg, 128, 0, s>>>(f);
@@ -880,13 +986,19 @@ static cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
   k_ff_failcount<<<fb, 256, 0, s>>>(f, blocksum);
   k_ff_blockscan<<<1, 1024, 0, s>>>(blocksum, fb, f.scal + 3);
   k_ff_failwrite<<<fb, 256, 0, s>>>(f, blocksum);
-  const uint32_t gw = ((n + 1) * 32 + 127) / 128;
+  // persistent warps (the work counts live on the device; typically a few thousand)
+  const uint32_t gw = std::min<uint32_t>(((n + 1) * 32 + 127) / 128, (uint32_t)a.num_sms * 8u);
   if (f.C <= 32) k_ff_excursion<RegTraj><<<gw, 128, 0, s>>>(f);
   else k_ff_excursion<SmemTraj><<<gw, 128, 0, s>>>(f);
   k_ff_link<<<gw, 128, 0, s>>>(f);
   note_launch(6);
-  for (uint32_t k = 1; k < levels; ++k) {
-    k_ff_double<<<(n + 256) / 256, 256, 0, s>>>(f, k);
+  {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_double_all, 256, 0);
+    const uint32_t gd = std::min<uint32_t>((n + 256) / 256, (uint32_t)(a.num_sms * std::max(1, std::min(per_sm, 4))));
+    void* args[] = {&f};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_ff_double_all, dim3(gd), dim3(256), args, 0, s);
+    if (e != cudaSuccess) return e;
     note_launch();
   }
   k_ff_expand<<<1, 1024, 0, s>>>(f);
