@@ -2,22 +2,22 @@
 // scorers) fused with K2 (weighted-rule regression, deadline, priority key,
 // offload class).  §8(a) rows a1-a4.
 //
-// Design (DESIGN.md §7 K1): persistent CTAs of 256 threads; each tile is 256
-// consecutive requests whose packed bytes are staged HBM -> shared memory with
-// coalesced 128-bit non-allocating loads; then one lane runs one request's
-// finite-state machine over shared memory; the epilogue computes u and the
-// key in registers and writes 4 B + 8 B (+ optional 16 B feature row).
-// The lexicon (<= 1024 lemmas) lives in shared memory as an open-addressing
-// table.  All arithmetic that decides an integer is binary32 with explicit
-// round-to-nearest intrinsics (R-FP).
+// Design (DESIGN.md §7 K1): persistent CTAs of 24 warps; every warp streams
+// the bytes of 32 consecutive requests (a task from a global work counter) in
+// 512-byte chunks: byte classes and word-run starts as bit masks, one lane per
+// token event (run -> clitic split, lemma, lexicon probe), and the six rules
+// as per-token predicates evaluated one token per lane with ballots (see the
+// K1 v4 block).  The epilogue computes u and the key in registers and writes
+// 4 B + 8 B (+ optional 16 B feature row) per request.  The lexicon (<= 1024
+// lemmas) lives in shared memory as an open-addressing table.  All arithmetic
+// that decides an integer is binary32 with explicit round-to-nearest
+// intrinsics (R-FP).  Warps whose offsets decrease use the per-lane byte FSM
+// (Rules::byte), which implements the same rules sequentially.
 #include "internal.cuh"
 
 namespace rtlm {
 
 namespace {
-
-constexpr int kThreads = 256;
-constexpr uint32_t kStage = 32768;  // staged text bytes per tile
 
 // ------------------------------------------------------------ epilogue math
 __device__ __forceinline__ float regress(const uint32_t f[7], const rt_regressor& r) {
@@ -317,117 +317,7 @@ __device__ __forceinline__ uint4 ld_nc_v4(const uint8_t* p) {
   return r;
 }
 
-__global__ void __launch_bounds__(kThreads) k_score(ScoreLaunch a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  // ---- lexicon -> shared memory
-  LexEntry* s_ent = reinterpret_cast<LexEntry*>(smem);
-  const uint32_t ent_bytes = a.lex.n_entries * (uint32_t)sizeof(LexEntry);
-  uint16_t* s_slots = reinterpret_cast<uint16_t*>(smem + ((ent_bytes + 15u) & ~15u));
-  const uint32_t nslots = 1u << a.lex.bits;
-  uint8_t* stage = reinterpret_cast<uint8_t*>(s_slots) + ((nslots * 2u + 15u) & ~15u);
-  {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.lex.entries);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_ent);
-    for (uint32_t i = threadIdx.x; i < ent_bytes / 4; i += kThreads) dst[i] = src[i];
-    for (uint32_t i = threadIdx.x; i < nslots; i += kThreads) s_slots[i] = a.lex.slots[i];
-  }
-  const Lex L{s_ent, s_slots, a.lex.bits};
-  const uint32_t total = a.n ? a.offsets[a.n] : 0u;
-  const uint32_t ntiles = (a.n + kThreads - 1) / kThreads;
-
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t r0 = tile * kThreads;
-    const uint32_t r1 = min(r0 + kThreads, a.n);
-    const uint32_t b0 = a.offsets[r0];
-    uint32_t b1 = a.offsets[r1];
-    if (b1 < b0) b1 = b0;
-    const uint32_t base = b0 & ~15u;
-    const uint32_t span = min(b1 - base, kStage);
-    __syncthreads();  // previous tile done with `stage` (and lexicon copied)
-    for (uint32_t off = threadIdx.x * 16u; off < span; off += kThreads * 16u) {
-      const uint32_t g = base + off;
-      if (g + 16u <= total) {
-        *reinterpret_cast<uint4*>(stage + off) = ld_nc_v4(a.bytes + g);
-      } else {
-#pragma unroll 1
-        for (uint32_t j = 0; j < 16u && g + j < total; ++j) stage[off + j] = a.bytes[g + j];
-      }
-    }
-    __syncthreads();
-
-    const uint32_t r = r0 + threadIdx.x;
-    if (r < r1) {
-      uint32_t s = a.offsets[r], e = a.offsets[r + 1];
-      if (e < s) {
-        atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
-        e = s;
-      }
-      Rules R;
-      R.init();
-      if (s >= base && e <= base + span) {
-        const uint8_t* q = stage + (s - base);
-        const uint32_t len = e - s;
-#pragma unroll 4
-        for (uint32_t i = 0; i < len; ++i) R.byte(q[i], L);
-      } else {
-        for (uint32_t i = s; i < e; ++i) R.byte(__ldg(a.bytes + i), L);
-      }
-      uint32_t f[8];
-      bool sat;
-      R.finish(L, f, sat);
-      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
-      if (!a.fused || a.feat) {
-        uint4 pk = make_uint4(f[0] | (f[1] << 16), f[2] | (f[3] << 16), f[4] | (f[5] << 16), f[6] | (f[7] << 16));
-        *reinterpret_cast<uint4*>(a.feat + (size_t)r * 8) = pk;
-      }
-      if (a.fused) {
-        const float u = regress(f, a.reg);
-        const uint32_t D = a.D_in ? a.D_in[r] : deadline_us(f[6], a.prof);
-        const int64_t arr = a.arrival ? a.arrival[r] : 0;
-        a.u[r] = u;
-        a.key[r] = priority_key(u, D, arr, a.prof);
-        if (a.D_out) a.D_out[r] = D;
-      }
-    }
-  }
-}
-
-
-// ============================================================ K1 v2 (two-phase)
-// Phase 1 (byte-parallel): each thread classifies 128 staged bytes with a
-// bank-replicated class table (W / punctuation / dropped -> one bit each),
-// run starts are derived from the word masks (a run never crosses a request
-// start), a block scan gives every thread its record range, and every token
-// becomes a 16-bit record (kind + lexicon entry) -- words through the lemma,
-// a 2-byte prefilter and at most one hash probe.  Phase 2: one lane per
-// request walks its records with the rule FSM (R-RULES) and runs the fused
-// epilogue.  Tiles whose text or token count does not fit fall back to the
-// per-lane byte FSM over global memory (same rules, same results).
-constexpr uint32_t kT2 = 256;                 // threads = requests per tile
-constexpr uint32_t kStage2 = 32768;           // staged bytes per tile
-constexpr uint32_t kPer = kStage2 / kT2;      // bytes per thread in phase 1 (128)
-constexpr uint32_t kMaxRec = 8192;            // token records per tile
-constexpr uint32_t kW2 = kStage2 / 32;        // mask words per tile
-
-constexpr uint32_t kQ = 1024;                 // run queue entries per warp (reuses the class table)
-
-struct Smem2 {
-  uint32_t lut[256 * 32];        // class table replicated per lane: W 0x1, P 0x100, X 0x10000;
-                                 // reused as per-warp run queues in phase 1c
-  uint8_t pad0[16];              // zeros in front of stage (tail reads may start before 0)
-  uint8_t stage[kStage2 + 64];
-  uint32_t wmask[kW2 + 1];       // word bytes
-  uint32_t emask[kW2 + 1];       // punctuation / dropped bytes
-  uint32_t rmask[kW2 + 1];       // run starts
-  uint32_t marks[kW2 + 1];       // request starts
-  uint16_t rec[kMaxRec];
-  uint32_t rstart[kT2 + 1];      // first record of each request of the tile (+ total)
-  uint32_t tbase[kT2 + 1];
-  uint32_t wsum[kT2 / 32];
-  uint32_t pref[128];
-  uint32_t flag;
-};
-
+// ============================================================ helpers of the scorer
 __device__ __forceinline__ uint32_t class_bits(uint32_t b) {
   const uint32_t lc = b | 0x20u;
   const bool w = (lc - 'a' < 26u) || (b - '0' < 10u) || b == '\'';
@@ -448,271 +338,6 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
     a.u[r] = u;
     a.key[r] = priority_key(u, D, arr, a.prof);
     if (a.D_out) a.D_out[r] = D;
-  }
-}
-
-// number of records produced by events at positions < p (p <= span)
-__device__ __forceinline__ uint32_t rec_index(const Smem2& S, uint32_t p, uint32_t total, uint32_t span) {
-  if (p >= span) return total;
-  const uint32_t t = p / kPer;
-  uint32_t idx = S.tbase[t];
-  const uint32_t w0 = t * (kPer / 32), wp = p >> 5;
-  for (uint32_t w = w0; w < wp; ++w) idx += __popc(S.emask[w]) + 2u * __popc(S.rmask[w]);
-  const uint32_t below = (p & 31u) ? ((1u << (p & 31u)) - 1u) : 0u;
-  idx += __popc(S.emask[wp] & below) + 2u * __popc(S.rmask[wp] & below);
-  return idx;
-}
-
-__global__ void __launch_bounds__(kT2, 2) k_score2(ScoreLaunch a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  Smem2& S = *reinterpret_cast<Smem2*>(smem_raw);
-  uint8_t* tail_mem = smem_raw + ((sizeof(Smem2) + 15) & ~size_t(15));
-  LexEntry* s_ent = reinterpret_cast<LexEntry*>(tail_mem);
-  const uint32_t ent_bytes = a.lex.n_entries * (uint32_t)sizeof(LexEntry);
-  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + ((ent_bytes + 15u) & ~15u));
-  const uint32_t nslots = 1u << a.lex.bits;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
-  // ---- per-CTA tables
-  {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.lex.entries);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_ent);
-    for (uint32_t i = tid; i < ent_bytes / 4; i += kT2) dst[i] = src[i];
-    for (uint32_t i = tid; i < nslots; i += kT2) s_slots[i] = a.lex.slots[i];
-    for (uint32_t i = tid; i < 128; i += kT2) S.pref[i] = 0;
-    for (uint32_t i = tid; i < 16; i += kT2) S.pad0[i] = 0;
-  }
-  __syncthreads();
-  for (uint32_t i = tid; i < a.lex.n_entries; i += kT2) {
-    const LexEntry e = a.lex.entries[i];
-    const uint32_t pi = pref_idx((uint32_t)(e.k0 & 0xFFu), e.len >= 2 ? (uint32_t)((e.k0 >> 8) & 0xFFu) : 0u);
-    atomicOr(&S.pref[pi >> 5], 1u << (pi & 31u));
-  }
-  const Lex L{s_ent, s_slots, a.lex.bits};
-  const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
-  const uint32_t ntiles = (a.n + kT2 - 1) / kT2;
-
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t r0 = tile * kT2;
-    const uint32_t r1 = min(r0 + kT2, a.n);
-    const uint32_t b0 = a.offsets[r0];
-    uint32_t b1 = a.offsets[r1];
-    if (b1 < b0) b1 = b0;
-    const uint32_t base = b0 & ~15u;
-    const uint32_t span = b1 - base;
-    const uint32_t r = r0 + tid;
-    uint32_t s_r = 0, e_r = 0;
-    if (r < r1) {
-      s_r = a.offsets[r];
-      e_r = a.offsets[r + 1];
-      if (e_r < s_r) { atomicOr(a.flags, RT_FLAG_BAD_OFFSETS); e_r = s_r; }
-    }
-    __syncthreads();  // previous tile done with shared buffers (and tables ready)
-    bool fast = span <= kStage2;
-    bool in_order = true;
-    for (uint32_t i = tid; i < 256 * 32; i += kT2) S.lut[i] = class_bits(i >> 5);
-    if (fast) {
-      // ---- stage [base, base + span) and clear the masks
-      for (uint32_t off = tid * 16u; off < span; off += kT2 * 16u) {
-        const uint32_t g = base + off;
-        if (g + 16u <= total_bytes) *reinterpret_cast<uint4*>(S.stage + off) = ld_nc_v4(a.bytes + g);
-        else
-          for (uint32_t j = 0; j < 16u; ++j) S.stage[off + j] = g + j < total_bytes ? a.bytes[g + j] : 0;
-      }
-      for (uint32_t w = tid; w <= kW2; w += kT2) S.marks[w] = 0;
-      if (tid == 0) S.flag = 0;
-      __syncthreads();
-      if (r < r1 && s_r - base < span) atomicOr(&S.marks[(s_r - base) >> 5], 1u << ((s_r - base) & 31u));
-      // requests must be in byte order inside the tile for the record ranges
-      if (r < r1 && r > r0 && s_r < a.offsets[r - 1]) atomicOr(&S.flag, 2u);
-      // ---- phase 1a: classify kPer bytes per thread
-      const uint32_t p0 = tid * kPer;
-#pragma unroll 1
-      for (uint32_t w = 0; w < kPer / 32; ++w) {
-        const uint32_t pos = p0 + w * 32;
-        uint32_t W = 0, E = 0;
-        if (pos < span) {
-          const uint4 q0 = *reinterpret_cast<const uint4*>(S.stage + pos);
-          const uint4 q1 = *reinterpret_cast<const uint4*>(S.stage + pos + 16);
-          const uint32_t words[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc += S.lut[((words[g] >> (8 * i)) & 0xFFu) * 32u + lane] << i;
-            W |= (acc & 0xFu) << (4 * g);
-            E |= (((acc >> 8) | (acc >> 16)) & 0xFu) << (4 * g);
-          }
-          const uint32_t valid = span - pos >= 32 ? 0xFFFFFFFFu : ((1u << (span - pos)) - 1u);
-          W &= valid;
-          E &= valid;
-        }
-        S.wmask[(p0 >> 5) + w] = W;
-        S.emask[(p0 >> 5) + w] = E;
-      }
-      __syncthreads();
-      // ---- phase 1b: run starts and record counts
-      uint32_t cnt = 0;
-#pragma unroll 1
-      for (uint32_t w = 0; w < kPer / 32; ++w) {
-        const uint32_t wi = (p0 >> 5) + w;
-        const uint32_t W = S.wmask[wi];
-        const uint32_t prev = wi ? (S.wmask[wi - 1] >> 31) : 0u;
-        const uint32_t R = (W & ~((W << 1) | prev)) | (W & S.marks[wi]);
-        S.rmask[wi] = R;
-        cnt += __popc(S.emask[wi]) + 2u * __popc(R);
-      }
-      // block exclusive scan of cnt
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= (uint32_t)o) incl += v;
-      }
-      if (lane == 31) S.wsum[wid] = incl;
-      __syncthreads();
-      uint32_t wbase = 0;
-      for (uint32_t k = 0; k < wid; ++k) wbase += S.wsum[k];
-      S.tbase[tid] = wbase + incl - cnt;
-      uint32_t total = 0;
-      for (uint32_t k = 0; k < kT2 / 32; ++k) total += S.wsum[k];
-      if (tid == 0) S.tbase[kT2] = total;
-      in_order = !(S.flag & 2u);
-      fast = total <= kMaxRec && in_order;
-      if (fast) {
-        // ---- phase 1c (i): lanes walk their events; punctuation / dropped bytes
-        // become records, runs go to the warp's queue as (position, record index)
-        __syncthreads();  // class table no longer needed: reuse as run queues
-        uint32_t* q = S.lut + wid * kQ;
-        uint32_t k = wbase + incl - cnt;
-        uint32_t nq_local = 0;
-#pragma unroll 1
-        for (uint32_t w = 0; w < kPer / 32; ++w) {
-          const uint32_t wi = (p0 >> 5) + w;
-          const uint32_t R = S.rmask[wi];
-          uint32_t ev = R | S.emask[wi];
-          nq_local += __popc(R);
-          while (ev) {
-            const uint32_t bit = __ffs(ev) - 1;
-            ev &= ev - 1u;
-            if ((R >> bit) & 1u) { k += 2; continue; }
-            const uint32_t c = S.stage[wi * 32 + bit];
-            uint32_t kind = 7u;  // dropped byte
-            if (c - 0x21u < 0x5Eu) kind = c == ',' ? 2u : c == '.' ? 3u : c == '?' ? 4u : c == '!' ? 5u : 6u;
-            S.rec[k++] = (uint16_t)kind;
-          }
-        }
-        // queue slots: exclusive scan of run counts inside the warp
-        uint32_t qincl = nq_local;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, qincl, o);
-          if (lane >= (uint32_t)o) qincl += v;
-        }
-        const uint32_t qtot = __shfl_sync(0xFFFFFFFFu, qincl, 31);
-        if (qtot > kQ) {
-          if (lane == 0) atomicOr(&S.flag, 4u);  // queue overflow: whole tile falls back
-        } else {
-          uint32_t slot = qincl - nq_local;
-          k = wbase + incl - cnt;
-#pragma unroll 1
-          for (uint32_t w = 0; w < kPer / 32; ++w) {
-            const uint32_t wi = (p0 >> 5) + w;
-            const uint32_t R = S.rmask[wi];
-            uint32_t ev = R | S.emask[wi];
-            while (ev) {
-              const uint32_t bit = __ffs(ev) - 1;
-              ev &= ev - 1u;
-              if ((R >> bit) & 1u) {
-                q[slot++] = (wi * 32 + bit) | (k << 15);
-                k += 2;
-              } else {
-                ++k;
-              }
-            }
-          }
-        }
-        __syncwarp();
-        // ---- phase 1c (ii): the warp processes its runs 32 at a time
-        const uint32_t* st32 = reinterpret_cast<const uint32_t*>(S.stage);
-        for (uint32_t e = lane; e < (qtot > kQ ? 0u : qtot); e += 32) {
-          const uint32_t ent = q[e];
-          const uint32_t x = ent & 0x7FFFu, kk = ent >> 15;
-          // run length: up to the first non-word byte or the next request start
-          uint32_t n = 1;
-          {
-            uint32_t qq = x + 1;
-            for (;;) {
-              if (qq >= span) break;
-              const uint32_t qw = qq >> 5, qb = qq & 31u;
-              const uint32_t stop = (~S.wmask[qw] | S.marks[qw]) >> qb;
-              if (stop) { n += __ffs(stop) - 1; break; }
-              n += 32 - qb;
-              qq += 32 - qb;
-            }
-          }
-          // first 16 bytes (lowercased; bytes past the run are masked by length)
-          const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
-          const uint32_t w0 = st32[a0], w1 = st32[a0 + 1], w2 = st32[a0 + 2], w3 = st32[a0 + 3], w4 = st32[a0 + 4];
-          const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
-          const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
-          const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
-          const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
-          // last (up to) 6 bytes, newest in the low byte: byte-reverse of the 8 bytes ending at x + n
-          const int32_t tb = (int32_t)(x + n) - 8;  // may be negative: stage has a zero pad in front
-          const uint32_t ta = (uint32_t)(tb + 16) >> 2, tsh = ((uint32_t)(tb + 16) & 3u) * 8u;
-          const uint32_t* pz = reinterpret_cast<const uint32_t*>(S.pad0);
-          const uint32_t v0 = pz[ta], v1 = pz[ta + 1], v2 = pz[ta + 2];
-          const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
-          uint64_t tail = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
-          tail = (tail | 0x2020202020202020ull) & mask_bytes(n < 6 ? n : 6);
-          const uint32_t t3 = (uint32_t)(tail & 0xFFFFFFu), t2 = (uint32_t)(tail & 0xFFFFu);
-          uint32_t cut = 0;
-          if (n > 3 && t3 == (('n' << 16) | ('\'' << 8) | 't')) cut = 3;
-          else if (n > 2 && (t2 == (('\'' << 8) | 's') || t2 == (('\'' << 8) | 'm') || t2 == (('\'' << 8) | 'd')))
-            cut = 2;
-          else if (n > 3 && (t3 == (('\'' << 16) | ('r' << 8) | 'e') || t3 == (('\'' << 16) | ('v' << 8) | 'e') ||
-                             t3 == (('\'' << 16) | ('l' << 8) | 'l')))
-            cut = 3;
-          if (!cut) {
-            S.rec[kk] = (uint16_t)(1u | (word_idx(L, S.pref, n, k0, k1, t3) << 3));
-            S.rec[kk + 1] = 0;
-          } else {
-            const uint32_t ns = n - cut;
-            S.rec[kk] = (uint16_t)(1u | (word_idx(L, S.pref, ns, k0, k1, (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu)) << 3));
-            const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
-            S.rec[kk + 1] = (uint16_t)(1u | (word_idx(L, S.pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu)) << 3));
-          }
-        }
-      }
-      __syncthreads();
-      fast = fast && !(S.flag & 4u);
-      __syncthreads();
-      if (fast && r < r1) {
-        // ---- phase 2: rule FSM over this request's records
-        const uint32_t total2 = S.tbase[kT2];
-        const uint32_t i0 = rec_index(S, s_r - base, total2, span);
-        const uint32_t i1 = rec_index(S, e_r - base, total2, span);
-        Rules R;
-        R.init();
-        for (uint32_t i = i0; i < i1; ++i) R.on_record(S.rec[i], L);
-        uint32_t f[8];
-        bool sat;
-        R.finish(L, f, sat);
-        if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
-        epilogue(a, r, f);
-      }
-    }
-    if (!fast && r < r1) {
-      // ---- fallback: per-lane byte FSM over global memory
-      Rules R;
-      R.init();
-      for (uint32_t i = s_r; i < e_r; ++i) R.byte(__ldg(a.bytes + i), L);
-      uint32_t f[8];
-      bool sat;
-      R.finish(L, f, sat);
-      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
-      epilogue(a, r, f);
-    }
   }
 }
 
@@ -817,6 +442,18 @@ __device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint
   const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
   const uint64_t tl = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
   return run_tokens(L, pref, n, k0, k1, tl, at0, at1);
+}
+
+// one request by the per-lane byte FSM (fallback path; kept out of line)
+__device__ __noinline__ void fsm_request(const ScoreLaunch& a, const Lex& L, uint32_t r, uint32_t s, uint32_t e) {
+  Rules R;
+  R.init();
+  for (uint32_t i = s; i < e; ++i) R.byte(__ldg(a.bytes + i), L);
+  uint32_t f[8];
+  bool sat;
+  R.finish(L, f, sat);
+  if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+  epilogue(a, r, f);
 }
 
 struct Carry {
@@ -1002,16 +639,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     if (__any_sync(0xFFFFFFFFu, bad)) {
       // offsets not non-decreasing: per-lane byte FSM (requests with e < s are empty)
       if (bad) atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
-      if (rv) {
-        Rules R;
-        R.init();
-        for (uint32_t i = s_r; i < (bad ? s_r : e_r); ++i) R.byte(__ldg(a.bytes + i), L);
-        uint32_t f[8];
-        bool sat;
-        R.finish(L, f, sat);
-        if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
-        epilogue(a, r, f);
-      }
+      if (rv) fsm_request(a, L, r, s_r, bad ? s_r : e_r);
       continue;
     }
     const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
@@ -1116,11 +744,14 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       if (lane == 0 && ph) B.ev[0] = 0xFFFFu;
       __syncwarp();
       // ---- (3) tokens, 32 events at a time, then (4) rules
-      for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
+      // (at least one pass, so that the last chunk always flushes the rules)
+      for (uint32_t e0 = 0; e0 < max(nev, 1u); e0 += 32) {
         const uint32_t k = e0 + lane;
         uint32_t ntk = 0, at0 = 0, at1 = 0, kind = K_W, rq = 0;
         if (k < nev) {
           const uint32_t p = B.ev[k];
+          uint32_t x = 0, n = 0;
+          bool isrun = false;
           if (p == 0xFFFFu) {
             // carried run: [pend_start, stop) with stop the first non-word byte or request start here
             const uint32_t ps = (uint32_t)pend_start;
@@ -1129,25 +760,27 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               const uint32_t sm = ~B.wm[w] | B.mk[w];
               if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
             }
-            const uint32_t n = cb + stop - ps;
-            if (ps + kChunk >= cb) {
-              ntk = stage_run(B, 16 + kChunk + ps - cb, n, L, S.pref, at0, at1);
-            } else {  // run longer than a chunk: bytes from global memory
-              uint64_t k0 = 0, k1 = 0, tl = 0;
-              for (uint32_t j = 0; j < 16u && j < n; ++j) {
-                const uint64_t c = (uint64_t)(__ldg(a.bytes + ps + j) | 0x20u);
-                if (j < 8) k0 |= c << (8 * j); else k1 |= c << (8 * (j - 8));
-              }
-              for (uint32_t j = 0; j < 6u && j < n; ++j) tl |= (uint64_t)__ldg(a.bytes + ps + n - 1 - j) << (8 * j);
-              ntk = run_tokens(L, S.pref, n, k0, k1, tl, at0, at1);
-            }
+            n = cb + stop - ps;
             rq = req_of(B.rs, rcnt, ps);
+            isrun = true;
+            if (ps + kChunk >= cb) {
+              x = 16 + kChunk + ps - cb;
+            } else {
+              // longer than a chunk (> 512 bytes): its tokens depend only on its last
+              // 6 bytes (any stem is > 16 bytes, no lemma) -> stage them as a 24-byte run
+              const uint32_t pad = 16 + 2 * kChunk + 8;  // in the stage's tail padding
+              uint8_t* st = reinterpret_cast<uint8_t*>(B.stage);
+              for (uint32_t j = 0; j < 8u; ++j) st[pad + j] = __ldg(a.bytes + ps + n - 8 + j);
+              x = pad + 8 - 24;
+              n = 24;
+            }
           } else {
             const uint32_t c = st8[16 + kChunk + p];
             rq = B.evq[k];
             if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
               // run length: up to the first non-word byte or request start
-              uint32_t n = 1, qq = p + 1;
+              uint32_t qq = p + 1;
+              n = 1;
               for (;;) {
                 const uint32_t qw = qq >> 5, qb = qq & 31u;
                 const uint32_t stop = (~B.wm[qw] | B.mk[qw]) >> qb;
@@ -1155,12 +788,14 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
                 n += 32 - qb;
                 qq += 32 - qb;
               }
-              ntk = stage_run(B, 16 + kChunk + p, n, L, S.pref, at0, at1);
+              x = 16 + kChunk + p;
+              isrun = true;
             } else {
               ntk = 1;
               kind = c == ',' ? K_COMMA : (c == '.' || c == '!') ? K_END : c == '?' ? K_Q : K_OTH;
             }
           }
+          if (isrun) ntk = stage_run(B, x, n, L, S.pref, at0, at1);
         }
         uint32_t ti = ntk;
 #pragma unroll
@@ -1180,7 +815,9 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         }
         __syncwarp();
         tokbase += (int32_t)nt;
-        for (; tokbase - tokdone >= 32; tokdone += 32) rules_batch(B, cy, tokdone, tokdone + 32, lane);
+        // full 32-token batches; everything after the last event of the task
+        const int32_t lim = (last_chunk && e0 + 32 >= nev) ? tokbase : tokbase - 31;
+        for (; tokdone < lim; tokdone += 32) rules_batch(B, cy, tokdone, min(tokdone + 32, tokbase), lane);
         __syncwarp();
       }
       // dropped bytes (rare): count per request
@@ -1197,8 +834,6 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
       __syncwarp();
     }
-    for (; tokdone < tokbase; tokdone += 32) rules_batch(B, cy, tokdone, min(tokdone + 32, tokbase), lane);
-    __syncwarp();
     // ---- epilogue: lane = request
     if (rv) {
       const uint32_t* ac = B.acc[lane];
@@ -1235,10 +870,6 @@ __global__ void k_key(const float* __restrict__ u, const uint16_t* __restrict__ 
 
 }  // namespace
 
-size_t score_smem_bytes(const DevLexicon& lex) {
-  return ((lex.n_entries * sizeof(LexEntry) + 15) & ~size_t(15)) + (((size_t(1) << lex.bits) * 2 + 15) & ~size_t(15)) +
-         kStage;
-}
 
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;

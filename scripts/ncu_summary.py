@@ -7,6 +7,7 @@
 import collections
 import csv
 import io
+import json
 import subprocess
 import sys
 
@@ -49,10 +50,18 @@ def full(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     if len(rr) > 2:
-        hdr = rr[0]
+        hdr, units = rr[0], dict(zip(rr[0], rr[1]))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         for row in rr[2:]:
             d = dict(zip(hdr, row))
-            print("   raw:", {k: d.get(k) for k in RAW if k in d})
+            print("   raw:", {k: (d.get(k), units.get(k)) for k in RAW if k in d})
+            try:
+                rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale[units["dram__bytes_read.sum"]]
+                wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale[units["dram__bytes_write.sum"]]
+                print("   traffic_json:", json.dumps({"kernel": d.get("Kernel Name", "")[:60], "dram_read_bytes": rd,
+                                                    "dram_write_bytes": wr, "traffic_bytes": rd + wr}))
+            except (KeyError, ValueError):
+                pass
 
 
 if __name__ == "__main__":
