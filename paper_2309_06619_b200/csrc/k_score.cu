@@ -2,7 +2,7 @@
 // scorers) fused with K2 (weighted-rule regression, deadline, priority key,
 // offload class).  §8(a) rows a1-a4.
 //
-// Design (DESIGN.md §7 K1): persistent CTAs of 24 warps; every warp streams
+// Design (DESIGN.md §7 K1): persistent CTAs of 32 warps; every warp streams
 // the bytes of 32 consecutive requests (a task from a global work counter) in
 // 512-byte chunks: byte classes and word-run starts as bit masks, one lane per
 // token event (run -> clitic split, lemma, lexicon probe), and the six rules
@@ -359,7 +359,7 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
 //      noun, punctuation) obtained with ballots, so the counters become
 //      per-token contributions summed per request (segmented warp scan).
 // Warps whose offsets are not non-decreasing use the per-lane byte FSM.
-constexpr uint32_t kT4 = 768;                 // threads per CTA (24 warps)
+constexpr uint32_t kT4 = 1024;                // threads per CTA (32 warps)
 constexpr uint32_t kW4 = kT4 / 32;
 constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
 constexpr uint32_t kRing = 128;               // token ring per warp
