@@ -469,15 +469,19 @@ __device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, i
   uint32_t meta = 0, attr = 0;
   if (valid) { meta = B.t_meta[T & (kRing - 1)]; attr = B.t_attr[T & (kRing - 1)]; }
   const uint32_t kind = meta & 7u, req = meta >> 3;
-  // three predecessors (same request only)
+  // three predecessors (same request only): from the batch by shuffles, from the ring for lanes < k
   uint32_t pk[4], pa[4];
 #pragma unroll
   for (int k = 1; k <= 3; ++k) {
-    pk[k] = 0; pa[k] = 0;
-    if (valid && T - k >= 0) {
-      const uint32_t m = B.t_meta[(T - k) & (kRing - 1)];
-      if ((m >> 3) == req) { pk[k] = m & 7u; pa[k] = B.t_attr[(T - k) & (kRing - 1)]; }
+    uint32_t m = __shfl_up_sync(0xFFFFFFFFu, meta, k), at = __shfl_up_sync(0xFFFFFFFFu, attr, k);
+    bool have = true;
+    if (lane < (uint32_t)k) {
+      have = T - k >= 0;
+      if (have) { m = B.t_meta[(T - k) & (kRing - 1)]; at = B.t_attr[(T - k) & (kRing - 1)]; }
     }
+    const bool same = valid && have && (m >> 3) == req;
+    pk[k] = same ? (m & 7u) : 0u;
+    pa[k] = same ? at : 0u;
   }
   const bool isW = valid && kind == K_W, isComma = valid && kind == K_COMMA;
   const bool isQ = valid && kind == K_Q, isEnd = valid && (kind == K_END || kind == K_Q);
@@ -642,6 +646,11 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       if (rv) fsm_request(a, L, r, s_r, bad ? s_r : e_r);
       continue;
     }
+    // request of a byte = (# request starts at or before it) - 1; a popcount of the
+    // start marks when no two requests start at the same byte (no empty request
+    // in the middle), else a search of the starts
+    const uint32_t s_prev = __shfl_up_sync(0xFFFFFFFFu, s_r, 1);
+    const bool uniq_starts = !__any_sync(0xFFFFFFFFu, rv && lane > 0 && s_r == s_prev);
     const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
     const uint32_t B1 = __shfl_sync(0xFFFFFFFFu, e_r, rcnt - 1);
     B.rs[lane] = s_r;
@@ -721,24 +730,37 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       }
       const uint32_t E16 = R16 | P16;
       const uint32_t cnt = __popc(E16);
-      uint32_t incl = cnt;
+      // one scan for the event count (low half) and the request-start count (high half)
+      const uint32_t cm = cnt | ((uint32_t)__popc(mk16) << 16);
+      uint32_t incl = cm;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= (uint32_t)o) incl += t;
       }
       const uint32_t ph = pend_here ? 1u : 0u;
-      const uint32_t nev = __shfl_sync(0xFFFFFFFFu, incl, 31) + ph;
+      const uint32_t nev = (__shfl_sync(0xFFFFFFFFu, incl, 31) & 0xFFFFu) + ph;
+      const uint32_t base_rq = __popc(__ballot_sync(0xFFFFFFFFu, rv && s_r < cb));  // requests started earlier
       if (E16) {
-        uint32_t k = incl - cnt + ph;
+        uint32_t k = ((incl - cm) & 0xFFFFu) + ph;
         uint32_t e = E16;
-        uint32_t rq = req_of(B.rs, rcnt, g);  // request at this lane's first byte, advanced per event
-        while (e) {
-          const uint32_t bit = __ffs(e) - 1;
-          e &= e - 1u;
-          while (rq + 1 < rcnt && B.rs[rq + 1] <= g + bit) ++rq;
-          B.ev[k] = (uint16_t)(lane * 16u + bit);
-          B.evq[k++] = (uint8_t)rq;
+        if (uniq_starts) {
+          const uint32_t rq0 = base_rq + ((incl - cm) >> 16) - 1u;  // + starts in this lane up to the byte
+          while (e) {
+            const uint32_t bit = __ffs(e) - 1;
+            e &= e - 1u;
+            B.ev[k] = (uint16_t)(lane * 16u + bit);
+            B.evq[k++] = (uint8_t)(rq0 + __popc(mk16 & ((2u << bit) - 1u)));
+          }
+        } else {
+          uint32_t rq = req_of(B.rs, rcnt, g);  // request at this lane's first byte, advanced per event
+          while (e) {
+            const uint32_t bit = __ffs(e) - 1;
+            e &= e - 1u;
+            while (rq + 1 < rcnt && B.rs[rq + 1] <= g + bit) ++rq;
+            B.ev[k] = (uint16_t)(lane * 16u + bit);
+            B.evq[k++] = (uint8_t)rq;
+          }
         }
       }
       if (lane == 0 && ph) B.ev[0] = 0xFFFFu;
