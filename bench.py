@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--per-trace", type=int, default=1000)
     ap.add_argument("--no-traces", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
     return ap.parse_args()
 
 
@@ -174,24 +175,26 @@ def native(args):
     sum_ms = max_over_ranks(sum(t_step))  # one batch at a time, L2 flushed between steps
     score_ms = sum(t_score) / len(t_score)
 
-    # ---------------- pipelined throughput: two batches in flight (two contexts, two
-    # streams, two distinct 2^20-request inputs -> 2 x ~100 MB > L2, no flush needed).
-    # Batch k's serial CPU-class chain (one SM) overlaps batch k+1's scoring and
-    # GPU-class consolidation; every batch still runs the whole hot path.
-    d2b = configs.config2(n=args.n, gid0=(world + rank) * args.n)
-    ctxs = [ctx, rt.Context(d2b["lexicon"], local)]
-    h_bytes2 = [h_bytes, torch.from_numpy(d2b["data"]).pin_memory()]
-    h_off2 = [h_off, torch.from_numpy(d2b["offsets"].view(np.int32)).pin_memory()]
-    data2 = [data, h_bytes2[1].to(dev)]
-    off2 = [off, h_off2[1].to(dev)]
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    outs2 = [outs, {k: torch.empty_like(v) for k, v in outs.items()}]
-    souts2 = [souts, {k: torch.empty_like(v) for k, v in souts.items()}]
+    # ---------------- pipelined throughput: `depth` batches in flight (one context,
+    # stream and distinct 2^20-request input each -> depth x ~100 MB > L2, no flush
+    # needed).  Batch k's serial CPU-class chain (one SM) overlaps the following
+    # batches' scoring and GPU-class consolidation; every batch still runs the
+    # whole hot path.
+    depth = max(1, args.depth)
+    extra = [configs.config2(n=args.n, gid0=(world * (i + 1) + rank) * args.n) for i in range(depth - 1)]
+    ctxs = [ctx] + [rt.Context(d["lexicon"], local) for d in extra]
+    h_bytes2 = [h_bytes] + [torch.from_numpy(d["data"]).pin_memory() for d in extra]
+    h_off2 = [h_off] + [torch.from_numpy(d["offsets"].view(np.int32)).pin_memory() for d in extra]
+    data2 = [data] + [h.to(dev) for h in h_bytes2[1:]]
+    off2 = [off] + [h.to(dev) for h in h_off2[1:]]
+    streams = [torch.cuda.Stream(dev) for _ in range(depth)]
+    outs2 = [outs] + [{k: torch.empty_like(v) for k, v in outs.items()} for _ in extra]
+    souts2 = [souts] + [{k: torch.empty_like(v) for k, v in souts.items()} for _ in extra]
     h_res = [{k: torch.empty(n, dtype=dt).pin_memory() for k, dt in (("batch_of", torch.int32), ("slot_of", torch.uint8),
-                                                                          ("core_of", torch.uint8))} for _ in range(2)]
+                                                                          ("core_of", torch.uint8))} for _ in range(depth)]
 
     def pstep(k, e2e=False):
-        sl = k & 1
+        sl = k % depth
         with torch.cuda.stream(streams[sl]):
             if e2e:
                 data2[sl].copy_(h_bytes2[sl], non_blocking=True)
@@ -228,7 +231,7 @@ def native(args):
     e2e_ms = max_over_ranks(timed_pipeline(True))
     value = world * n * args.steps / (pipe_ms / 1e3) / 1e6
     e2e_value = world * n * args.steps / (e2e_ms / 1e3) / 1e6
-    total_bytes2 = int(d2b["offsets"][-1])
+    mean_bytes = (total_bytes + sum(int(d["offsets"][-1]) for d in extra)) // depth
 
     # ---------------- roofline of the scoring kernel (k_score: the HBM-bound pass)
     peaks = {}
@@ -268,15 +271,15 @@ def native(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8+f32", "data": "synthetic",
             "config": {"workload": "config2: one 2^20-request queue per GPU (DialoGPT profile, all r=0), "
                                    "score+key+schedule", "requests_per_gpu": n, "bytes_per_gpu": total_bytes,
-                       "pipeline": "2 batches in flight (2 contexts / streams), alternating 2 distinct inputs",
-                       "l2": "pipelined: 2 distinct inputs of ~100 MB each (> 126 MB L2) alternate; "
+                       "pipeline": f"{depth} batches in flight ({depth} contexts / streams), cycling {depth} distinct inputs",
+                       "l2": f"pipelined: {depth} distinct inputs of ~100 MB each (> 126 MB L2) in turn; "
                              "latency leg: 256 MB buffer written between steps",
                        "parallelism": f"replicas{world}"},
             "latency": {"ms_per_step": round(sum_ms / args.steps, 4), "score_key_ms": round(score_ms, 4),
                         "schedule_ms": round(sum(t_step) / len(t_step) - score_ms, 4),
                         "note": "one batch at a time, L2 flushed between steps"},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
-                    "h2d_bytes_per_step": (total_bytes + total_bytes2) // 2 + 4 * (n + 1),
+                    "h2d_bytes_per_step": mean_bytes + 4 * (n + 1),
                     "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_ms / args.steps, 4)},
             "gpu_launches": int(launches),
             "roofline": roofline,
