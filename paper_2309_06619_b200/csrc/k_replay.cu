@@ -23,14 +23,11 @@ struct ReplaySmem {
   };
   uint16_t sidx[kMaxTrace];  // rank -> arrival index
   uint16_t rank[kMaxTrace];  // arrival index -> rank
-  uint16_t len[kMaxTrace];
-  float u[kMaxTrace];
-  uint32_t D[kMaxTrace];
   uint32_t ready_gpu[32], ready_cpu[32], wait_arr[32];
   int64_t core_free[kMaxCores];
   uint32_t W[kMaxWindow], S[kMaxWindow];
-  float Wu[kMaxWindow], Su[kMaxWindow];
-};
+  float Su[kMaxWindow];
+};  // ~14.6 KB: u, D and lengths are read from global memory (L2) when needed
 
 __device__ __forceinline__ int64_t warp_min64(int64_t v) {
 #pragma unroll
@@ -90,12 +87,10 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   }
   const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);  // CPU class = ranks [0, ncpu)
   __syncwarp();
-  for (uint32_t i = lane; i < n; i += 32) {
-    sm.r[i] = a.arrival[lo + i];
-    sm.len[i] = a.len[lo + i];
-    sm.u[i] = a.u[lo + i];
-    sm.D[i] = a.D[lo + i];
-  }
+  for (uint32_t i = lane; i < n; i += 32) sm.r[i] = a.arrival[lo + i];
+  const uint16_t* g_len = a.len + lo;
+  const float* g_u = a.u + lo;
+  const uint32_t* g_D = a.D + lo;
   sm.ready_gpu[lane] = 0; sm.ready_cpu[lane] = 0; sm.wait_arr[lane] = 0;
   sm.core_free[lane] = 0;
   __syncwarp();
@@ -139,12 +134,12 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       const uint32_t word = __shfl_sync(0xFFFFFFFFu, wcpu, wl);
       const uint32_t rk = wl * 32 + (__ffs(word) - 1);
       const uint32_t i = sm.sidx[rk];
-      const int64_t end = now + (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)sm.len[i]);
+      const int64_t end = now + (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)g_len[i]);
       if (lane == 0) {
         sm.core_free[c] = end;
         sm.ready_cpu[wl] = word & (word - 1u);
         resp += end - sm.r[i];
-        misses += end > sm.r[i] + (int64_t)sm.D[i];
+        misses += end > sm.r[i] + (int64_t)g_D[i];
         if (a.end_us) a.end_us[lo + i] = end;
       }
       ++done;
@@ -190,18 +185,26 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           uint32_t cnt;
           const uint32_t* B;
           if (p.consolidate) {
-            for (uint32_t e = lane; e < take; e += 32) sm.Wu[e] = sm.u[sm.sidx[sm.W[e]]];
-            __syncwarp();
-            for (uint32_t e = lane; e < take; e += 32) {  // sort window by (u, rank)
-              const float ue = sm.Wu[e];
-              const uint32_t re = sm.W[e];
+            // sort the window by (u, rank): ranks by shuffles, 32 elements per lane pass
+            for (uint32_t e0 = 0; e0 < take; e0 += 32) {
+              const uint32_t e = e0 + lane;
+              const uint32_t re = e < take ? sm.W[e] : 0xFFFFFFFFu;
+              const float ue = e < take ? g_u[sm.sidx[re]] : 0.0f;
               uint32_t pos = 0;
-              for (uint32_t x = 0; x < take; ++x) {
-                const float ux = sm.Wu[x];
-                pos += (ux < ue) || (ux == ue && sm.W[x] < re);
+              for (uint32_t x0 = 0; x0 < take; x0 += 32) {
+                const uint32_t rx_l = x0 + lane < take ? sm.W[x0 + lane] : 0xFFFFFFFFu;
+                const float ux_l = x0 + lane < take ? g_u[sm.sidx[rx_l]] : 0.0f;
+                const uint32_t lim = min(32u, take - x0);
+                for (uint32_t x = 0; x < lim; ++x) {
+                  const float ux = __shfl_sync(0xFFFFFFFFu, ux_l, x);
+                  const uint32_t rx = __shfl_sync(0xFFFFFFFFu, rx_l, x);
+                  pos += (ux < ue) || (ux == ue && rx < re);
+                }
               }
-              sm.S[pos] = re;
-              sm.Su[pos] = ue;
+              if (e < take) {
+                sm.S[pos] = re;
+                sm.Su[pos] = ue;
+              }
             }
             __syncwarp();
             const uint32_t lim = min(C, take);
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
             B = sm.W;
           }
           uint32_t ml = 0;
-          for (uint32_t e = lane; e < cnt; e += 32) ml = max(ml, (uint32_t)sm.len[sm.sidx[B[e]]]);
+          for (uint32_t e = lane; e < cnt; e += 32) ml = max(ml, (uint32_t)g_len[sm.sidx[B[e]]]);
           ml = __reduce_max_sync(0xFFFFFFFFu, ml);
           const int64_t end = now + gpu_fixed + p.eta_us * (int64_t)ml;
           for (uint32_t e = lane; e < cnt; e += 32) {
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
             atomicAnd(&sm.ready_gpu[rk >> 5], ~(1u << (rk & 31)));
             atomicAnd(&sm.wait_arr[i >> 5], ~(1u << (i & 31)));
             resp += end - sm.r[i];
-            misses += end > sm.r[i] + (int64_t)sm.D[i];
+            misses += end > sm.r[i] + (int64_t)g_D[i];
             if (a.end_us) a.end_us[lo + i] = end;
           }
           done += cnt;
