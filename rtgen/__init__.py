@@ -124,3 +124,20 @@ def shuffle(seed: int, sid: int, n: int) -> np.ndarray:
     out = np.zeros(n, dtype=np.uint32)
     lib.rtgen_shuffle(seed, sid, n, _p(out))
     return out
+
+
+# ---------------------------------------------------------------- MLP weights (NEXT-1)
+MLP_DIMS = (6, 100, 200, 200, 100, 1)
+
+
+def mlp_weights(seed: int):
+    """Random-init weights of the lightweight MLP (no trained weights exist here):
+    He-uniform per layer, small uniform biases, float32, row-major [out][in].
+    Random numbers only; no arithmetic of the method."""
+    rng = np.random.default_rng(seed)
+    ws, bs = [], []
+    for fan_in, fan_out in zip(MLP_DIMS[:-1], MLP_DIMS[1:]):
+        lim = np.sqrt(6.0 / fan_in)
+        ws.append(rng.uniform(-lim, lim, (fan_out, fan_in)).astype(np.float32))
+        bs.append(rng.uniform(-0.1, 0.1, fan_out).astype(np.float32))
+    return ws, bs
