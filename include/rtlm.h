@@ -130,6 +130,28 @@ rt_status rt_score(rt_ctx* ctx, const uint8_t* d_bytes, const uint32_t* d_offset
 rt_status rt_predict(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, const rt_regressor* reg, float* d_u,
                      rt_stream stream);
 
+/* ---------------------------------------------------------------- (2b) MLP (NEXT-1) */
+
+/* The lightweight MLP m_theta of Eq. 1 (hidden sizes P:620 / P:1547;
+ * SPEC S:160-165): layers 6-100-200-200-100-1, ReLU on hidden
+ * layers, identity output, u = max(0, output).  Inputs are the six rule scores
+ * feat[i][0..5] = {S, Y, M, V, O, P}.  Weights are HOST fp32, row-major
+ * [out][in]: w[0] 100x6, w[1] 200x100, w[2] 200x200, w[3] 100x200, w[4] 1x100;
+ * b[l] has `out` entries.  Layers 1 and 5 run in fp32 on the CUDA cores,
+ * layers 2-4 on the tensor cores (tcgen05, BF16 operands, FP32 accumulation);
+ * tolerance vs the fp64 oracle: DESIGN.md §7 K7. */
+typedef struct {
+  const float* w[5];
+  const float* b[5];
+} rt_mlp;
+
+/* Packs and uploads the weights into the context (synchronous; copies the
+ * host arrays).  Replaces any previous model. */
+rt_status rt_set_mlp(rt_ctx* ctx, const rt_mlp* mlp);
+/* u[i] = m_theta(feat[i]) for i < n (d_feat as produced by rt_score).
+ * RT_EINVAL if no model was set. n == 0 is a no-op. */
+rt_status rt_predict_mlp(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, float* d_u, rt_stream stream);
+
 /* ---------------------------------------------------------------- (3) key */
 
 /* Deadline + priority key + class (R-D, R-NUM, R-OVERDUE, R-KEY; Eq. 2/3):

@@ -24,7 +24,8 @@ INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5}
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
-           "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count"]
+           "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
+           "rt_set_mlp", "rt_predict_mlp"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -62,6 +63,14 @@ def make_profile(d: dict) -> Profile:
     p.policy = POLICY[pol] if isinstance(pol, str) else int(pol)
     p.reserved = 0
     return p
+
+
+class Mlp(ctypes.Structure):
+    """rt_mlp: host fp32 weights [out][in] and biases of the 6-100-200-200-100-1 MLP."""
+    _fields_ = [("w", ctypes.c_void_p * 5), ("b", ctypes.c_void_p * 5)]
+
+
+MLP_DIMS = (6, 100, 200, 200, 100, 1)
 
 
 def make_regressor(coefs) -> Regressor:
@@ -111,6 +120,10 @@ def load_library(path: str = LIB_PATH):
     L.rt_simulate.argtypes = [V, P, P, P, P, P, P, U32, P, U32, P, P, P, V]
     L.rt_reduce_stats.restype = I32
     L.rt_reduce_stats.argtypes = [V, P, U32, P, U32, P, V]
+    L.rt_set_mlp.restype = I32
+    L.rt_set_mlp.argtypes = [V, ctypes.POINTER(Mlp)]
+    L.rt_predict_mlp.restype = I32
+    L.rt_predict_mlp.argtypes = [V, P, U32, P, V]
     _lib = L
     return L
 
@@ -208,6 +221,29 @@ class Context:
         r = make_regressor(reg)
         self._check(self._L.rt_predict(self._h, _ptr(feat, torch.int16, "feat"), n, ctypes.byref(r),
                                        _ptr(u, torch.float32, "u"), self._stream()))
+        return u
+
+    def set_mlp(self, weights, biases):
+        """rt_set_mlp: weights[l] fp32 [out][in], biases[l] fp32 [out] (copied at call time)."""
+        ws = [np.ascontiguousarray(w, dtype=np.float32) for w in weights]
+        bs = [np.ascontiguousarray(b, dtype=np.float32) for b in biases]
+        for l, (w, b) in enumerate(zip(ws, bs)):
+            if w.shape != (MLP_DIMS[l + 1], MLP_DIMS[l]) or b.shape != (MLP_DIMS[l + 1],):
+                raise ValueError(f"layer {l}: expected {(MLP_DIMS[l + 1], MLP_DIMS[l])} / {(MLP_DIMS[l + 1],)}")
+        m = Mlp()
+        for l in range(5):
+            m.w[l] = ws[l].ctypes.data
+            m.b[l] = bs[l].ctypes.data
+        self._check(self._L.rt_set_mlp(self._h, ctypes.byref(m)))
+
+    def predict_mlp(self, feat, u=None):
+        """rt_predict_mlp: feat uint16-as-int16 [n, 8] -> u float32 [n]."""
+        torch = _torch()
+        n = feat.shape[0]
+        if u is None:
+            u = self._empty((n,), torch.float32)
+        self._check(self._L.rt_predict_mlp(self._h, _ptr(feat, torch.int16, "feat"), n, _ptr(u, torch.float32, "u"),
+                                           self._stream()))
         return u
 
     def key(self, u, prof: dict, feat=None, arrival=None, D_in=None, key=None, D_out=None):

@@ -24,6 +24,7 @@ struct rt_ctx {
   size_t prof_cap = 0;
   cudaStream_t aux = nullptr;  // internal fork stream (CPU-class list scheduling)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp)
   std::string err;
 };
 
@@ -345,6 +346,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->ws);
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
+    cudaFree(c->d_mlp);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -427,6 +429,34 @@ rt_status rt_predict(rt_ctx* c, const uint16_t* d_feat, uint32_t n, const rt_reg
   DeviceGuard g(c->device);
   cudaError_t e = rtlm::launch_predict(d_feat, n, *reg, d_u, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_predict");
+  return RT_OK;
+}
+
+rt_status rt_set_mlp(rt_ctx* c, const rt_mlp* mlp) {
+  if (!c) return RT_EINVAL;
+  if (!mlp) return fail(c, RT_EINVAL, "mlp is NULL");
+  for (int l = 0; l < 5; ++l)
+    if (!mlp->w[l] || !mlp->b[l]) return fail(c, RT_EINVAL, "null MLP weight or bias");
+  DeviceGuard g(c->device);
+  std::vector<uint8_t> blob(rtlm::mlp_blob_bytes());
+  rtlm::mlp_pack(mlp->w, mlp->b, blob.data());
+  if (!c->d_mlp) {
+    cudaError_t e = cudaMalloc(&c->d_mlp, blob.size());
+    if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("mlp weights: ") + cudaGetErrorString(e));
+  }
+  RT_CUDA(c, cudaMemcpy(c->d_mlp, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  return RT_OK;
+}
+
+rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d_u, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!c->d_mlp) return fail(c, RT_EINVAL, "no MLP model (rt_set_mlp)");
+  if (!n) return RT_OK;
+  if (!d_feat || !d_u) return fail(c, RT_EINVAL, "null argument");
+  if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
+  DeviceGuard g(c->device);
+  cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, c->num_sms, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_mlp");
   return RT_OK;
 }
 

@@ -144,6 +144,10 @@ struct ReplayLaunch {
   int64_t* end_us;
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+// K7 (NEXT-1): lightweight MLP on tcgen05 (k_mlp.cu)
+size_t mlp_blob_bytes();
+void mlp_pack(const float* const w[5], const float* const b[5], uint8_t* blob);
+cudaError_t launch_mlp(const uint16_t* feat, uint32_t n, const uint8_t* blob, float* u, int num_sms, cudaStream_t s);
 cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* group_of, uint32_t ngroups,
                                 int64_t* sums, cudaStream_t s);
 
