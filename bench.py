@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--traces", type=int, default=4096, help="traces per GPU (config 3)")
     ap.add_argument("--per-trace", type=int, default=1000)
     ap.add_argument("--no-traces", action="store_true")
+    ap.add_argument("--no-mlp", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
     return ap.parse_args()
@@ -199,8 +200,10 @@ def native(args):
             if e2e:
                 data2[sl].copy_(h_bytes2[sl], non_blocking=True)
                 off2[sl].copy_(h_off2[sl], non_blocking=True)
-            ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
-            ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
+            if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "score"):
+                ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
+            if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "schedule"):
+                ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
             if e2e:
                 for name in ("batch_of", "slot_of", "core_of"):
                     h_res[sl][name].copy_(souts2[sl][name], non_blocking=True)
@@ -254,6 +257,11 @@ def native(args):
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(score_ms, 5),
                 "step_share": round(score_ms / (sum(t_step) / len(t_step)), 4)}
 
+    # ---------------- MLP leg (NEXT-1): rt_predict_mlp on config 2's features
+    mlp = None
+    if not args.no_mlp:
+        mlp = mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_ranks, flush, peaks)
+
     # ---------------- traces leg (config 3 per GPU)
     traces = None
     if not args.no_traces:
@@ -287,11 +295,51 @@ def native(args):
         }
         if traces is not None:
             line["traces"] = traces
+        if mlp is not None:
+            line["mlp"] = mlp
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_ranks, flush, peaks):
+    """NEXT-1: u = m_theta(feat) for the config-2 queue (features from rt_score),
+    random-init weights (no trained model exists here; the cost does not depend
+    on the values).  Roofline: tensor, algorithmic 2 * 80 700 FLOP per request."""
+    import torch
+    import rtgen
+    feat = ctx.score(data, off)
+    ws, bs = rtgen.mlp_weights(12345)
+    ctx.set_mlp(ws, bs)
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        ctx.predict_mlp(feat, u)
+    torch.cuda.synchronize()
+    barrier()
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev_a.record(stream)
+        ctx.predict_mlp(feat, u)
+        ev_b.record(stream)
+        ev_b.synchronize()
+        ts.append(ev_a.elapsed_time(ev_b))
+    tsum = max_over_ranks(sum(ts))
+    ms = tsum / args.steps
+    flops = 2 * (6 * 100 + 100 * 200 + 200 * 200 + 200 * 100 + 100) * n
+    peak = float(peaks.get("bf16_tflops", 2250.0))
+    achieved = flops / (ms / 1e3) / 1e12
+    return {"metric": "M requests/s (u = m_theta(feat), MLP 6-100-200-200-100-1)", "unit": "Mreq/s",
+            "value": round(world * n / (ms / 1e3) / 1e6, 2), "ms_per_step": round(ms, 4),
+            "dtype": "bf16 tensor cores (tcgen05), fp32 accumulate; layers 1/5 fp32",
+            "roofline": {"bound": "tensor", "kernel": "k_mlp", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "nominal",
+                         "alg_flops_per_launch": flops}}
 
 
 def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):
