@@ -2,8 +2,8 @@
 // 5th-generation tensor cores.  Layers 6-100-200-200-100-1,
 // ReLU on hidden layers, identity output clamped at 0.
 //
-// Persistent CTAs of 128 threads; a tile is 128 requests (one TMEM lane and
-// one thread per request).  Layer 1 (6 -> 100, 600 FMA/request) and layer 5
+// Persistent CTAs of 256 threads; a tile is 128 requests (one TMEM lane and
+// two threads per request, taking alternate 16-column groups).  Layer 1 (6 -> 100, 600 FMA/request) and layer 5
 // (100 -> 1) run on the CUDA cores in fp32.  Layers 2-4 are tcgen05.mma
 // (kind::f16, BF16 operands, FP32 accumulators in TMEM, M = 128):
 //   A = the tile's activations in shared memory, B = the layer's weights,
@@ -24,7 +24,8 @@
 namespace rtlm {
 namespace {
 
-constexpr uint32_t kT = 128;                       // threads = requests per tile
+constexpr uint32_t kT = 128;                       // requests per tile (TMEM lanes)
+constexpr uint32_t kThr = 256;                     // threads: two per request (column halves)
 constexpr uint32_t N1 = 112, N2 = 208, N3 = 208, N4 = 112;
 constexpr uint32_t K2C = 13, K3C = 25, K4C = 25;   // stored 8-wide K chunks of W2, W3, W4
 constexpr uint32_t SZ_W2 = K2C * N2 * 16, SZ_W3 = K3C * N3 * 16, SZ_W4 = K4C * N4 * 16;
@@ -84,10 +85,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// hidden-layer epilogue: TMEM row -> + bias -> ReLU -> bf16 -> the next A operand
+// hidden-layer epilogue: TMEM row -> + bias -> ReLU -> bf16 -> the next A operand;
+// the two threads of a row take alternate 16-column groups
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_row, const float* bias, uint32_t n, uint8_t* sA,
-                                                uint32_t row) {
-  for (uint32_t c0 = 0; c0 < n; c0 += 16) {
+                                                uint32_t row, uint32_t half) {
+  for (uint32_t c0 = half * 16; c0 < n; c0 += 32) {
     float v[16];
     tmem_ld16(tmem_row + c0, v);
     uint32_t p[8];
@@ -106,21 +108,23 @@ __device__ __forceinline__ void sync_for_mma() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat, uint32_t n,
+__global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ feat, uint32_t n,
                                                 const uint8_t* __restrict__ wblob, float* __restrict__ u_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
+  __shared__ float s_part[kT];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t row = tid & (kT - 1), half = tid >> 7;  // warps w and w + 4 share TMEM lanes 32(w & 3)..
   // resident weights: bf16 blob (W2 | W3 | W4) then the fp32 parameters
   {
     const uint4* src = reinterpret_cast<const uint4*>(wblob);
     uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (uint32_t i = tid; i < OFF_A / 16; i += kT) dst[i] = src[i];
+    for (uint32_t i = tid; i < OFF_A / 16; i += kThr) dst[i] = src[i];
     const uint32_t* ps = reinterpret_cast<const uint32_t*>(wblob + OFF_A);
     uint32_t* pd = reinterpret_cast<uint32_t*>(smem + OFF_P);
-    for (uint32_t i = tid; i < P_N; i += kT) pd[i] = ps[i];
-    for (uint32_t i = tid; i < SZ_A / 16; i += kT) reinterpret_cast<uint4*>(smem + OFF_A)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < P_N; i += kThr) pd[i] = ps[i];
+    for (uint32_t i = tid; i < SZ_A / 16; i += kThr) reinterpret_cast<uint4*>(smem + OFF_A)[i] = make_uint4(0, 0, 0, 0);
   }
   const float* P = reinterpret_cast<const float*>(smem + OFF_P);
   const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
@@ -132,13 +136,13 @@ __global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat
   }
   sync_for_mma();
   const uint32_t tmem = tbase;
-  const uint32_t tmem_row = tmem + ((warp * 32u) << 16);  // this warp's TMEM lane quarter
+  const uint32_t tmem_row = tmem + (((warp & 3u) * 32u) << 16);  // this warp's TMEM lane quarter
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
   uint8_t* sA = smem + OFF_A;
   uint32_t phase = 0;
   const uint32_t ntiles = (n + kT - 1) / kT;
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint32_t req = t * kT + tid;
+    const uint32_t req = t * kT + row;
     const bool valid = req < n;
     // ---- layer 1 on the CUDA cores (fp32): x = the six rule scores
     float x[6] = {0, 0, 0, 0, 0, 0};
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat
       x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
     }
 #pragma unroll 1
-    for (uint32_t c = 0; c < N1 / 8; ++c) {
+    for (uint32_t c = half; c < N1 / 8; c += 2) {
       uint32_t p[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat
         }
         p[q] = pack_bf16(h[0], h[1]);
       }
-      *reinterpret_cast<uint4*>(sA + (c * kT + tid) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
+      *reinterpret_cast<uint4*>(sA + (c * kT + row) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
     }
     // ---- layer 2: [128 x 112] . [112 x 208]
     sync_for_mma();
@@ -176,14 +180,14 @@ __global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat
     mbar_wait(mb, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue_hidden(tmem_row, P + P_B2, N2, sA, tid);
+    epilogue_hidden(tmem_row, P + P_B2, N2, sA, row, half);
     // ---- layer 3: [128 x 208] . [208 x 208]
     sync_for_mma();
     if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W3, N3, 13, mb);
     mbar_wait(mb, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue_hidden(tmem_row, P + P_B3, N3, sA, tid);
+    epilogue_hidden(tmem_row, P + P_B3, N3, sA, row, half);
     // ---- layer 4: [128 x 208] . [208 x 112]
     sync_for_mma();
     if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W4, N4, 13, mb);
@@ -191,14 +195,17 @@ __global__ void __launch_bounds__(kT, 1) k_mlp(const uint16_t* __restrict__ feat
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // ---- layer 4 epilogue + layer 5 (100 -> 1) on the CUDA cores, clamp at 0
-    float y = P[P_B5];
-    for (uint32_t c0 = 0; c0 < N4; c0 += 16) {
+    float y = 0.0f;
+    for (uint32_t c0 = half * 16; c0 < N4; c0 += 32) {
       float v[16];
       tmem_ld16(tmem_row + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) y = fmaf(P[P_W5 + c0 + j], fmaxf(v[j] + P[P_B4 + c0 + j], 0.0f), y);
     }
-    if (valid) u_out[req] = fmaxf(y, 0.0f);
+    if (half) s_part[row] = y;
+    __syncthreads();
+    // fixed summation order: bias + half 0's groups + half 1's groups
+    if (!half && valid) u_out[req] = fmaxf((P[P_B5] + y) + s_part[row], 0.0f);
     // the next tile's layer 1 rewrites sA and its MMAs overwrite TMEM
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -241,7 +248,7 @@ cudaError_t launch_mlp(const uint16_t* feat, uint32_t n, const uint8_t* blob, fl
   if (e != cudaSuccess) return e;
   const uint32_t ntiles = (n + kT - 1) / kT;
   const uint32_t grid = ntiles < (uint32_t)num_sms ? ntiles : (uint32_t)num_sms;
-  k_mlp<<<grid, kT, kSmem, s>>>(feat, n, blob, u);
+  k_mlp<<<grid, kThr, kSmem, s>>>(feat, n, blob, u);
   note_launch();
   return cudaGetLastError();
 }
