@@ -69,13 +69,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
                  : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// 16 consecutive accumulator columns of this thread's row (no wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  tmem_ld16_nowait(taddr, r);
+  tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
@@ -87,17 +92,33 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // hidden-layer epilogue: TMEM row -> + bias -> ReLU -> bf16 -> the next A operand;
 // the two threads of a row take alternate 16-column groups
+__device__ __forceinline__ void store_group(const uint32_t (&r)[16], const float* bias, uint32_t c0, uint8_t* sA,
+                                            uint32_t row) {
+  uint32_t p[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    p[j] = pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + bias[c0 + 2 * j], 0.0f),
+                     fmaxf(__uint_as_float(r[2 * j + 1]) + bias[c0 + 2 * j + 1], 0.0f));
+  *reinterpret_cast<uint4*>(sA + ((c0 / 8) * kT + row) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
+  *reinterpret_cast<uint4*>(sA + ((c0 / 8 + 1) * kT + row) * 16) = make_uint4(p[4], p[5], p[6], p[7]);
+}
+
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_row, const float* bias, uint32_t n, uint8_t* sA,
                                                 uint32_t row, uint32_t half) {
-  for (uint32_t c0 = half * 16; c0 < n; c0 += 32) {
-    float v[16];
-    tmem_ld16(tmem_row + c0, v);
-    uint32_t p[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      p[j] = pack_bf16(fmaxf(v[2 * j] + bias[c0 + 2 * j], 0.0f), fmaxf(v[2 * j + 1] + bias[c0 + 2 * j + 1], 0.0f));
-    *reinterpret_cast<uint4*>(sA + ((c0 / 8) * kT + row) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
-    *reinterpret_cast<uint4*>(sA + ((c0 / 8 + 1) * kT + row) * 16) = make_uint4(p[4], p[5], p[6], p[7]);
+  uint32_t c0 = half * 16;
+  for (; c0 + 32 < n; c0 += 64) {  // two groups per wait
+    uint32_t r0[16], r1[16];
+    tmem_ld16_nowait(tmem_row + c0, r0);
+    tmem_ld16_nowait(tmem_row + c0 + 32, r1);
+    tmem_wait_ld();
+    store_group(r0, bias, c0, sA, row);
+    store_group(r1, bias, c0 + 32, sA, row);
+  }
+  if (c0 < n) {
+    uint32_t r0[16];
+    tmem_ld16_nowait(tmem_row + c0, r0);
+    tmem_wait_ld();
+    store_group(r0, bias, c0, sA, row);
   }
 }
 
@@ -141,17 +162,21 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
   uint8_t* sA = smem + OFF_A;
   uint32_t phase = 0;
   const uint32_t ntiles = (n + kT - 1) / kT;
+  auto load_feat = [&](uint32_t t) {
+    const uint32_t rq = t * kT + row;
+    return (t < ntiles && rq < n) ? __ldg(reinterpret_cast<const uint4*>(feat + (size_t)rq * 8)) : make_uint4(0, 0, 0, 0);
+  };
+  uint4 fnext = load_feat(blockIdx.x);
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint32_t req = t * kT + row;
     const bool valid = req < n;
     // ---- layer 1 on the CUDA cores (fp32): x = the six rule scores
-    float x[6] = {0, 0, 0, 0, 0, 0};
-    if (valid) {
-      const uint4 f = *reinterpret_cast<const uint4*>(feat + (size_t)req * 8);
-      x[0] = (float)(f.x & 0xFFFFu); x[1] = (float)(f.x >> 16);
-      x[2] = (float)(f.y & 0xFFFFu); x[3] = (float)(f.y >> 16);
-      x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
-    }
+    const uint4 f = fnext;
+    fnext = load_feat(t + gridDim.x);  // in flight during this tile's layers 2-4
+    float x[6];
+    x[0] = (float)(f.x & 0xFFFFu); x[1] = (float)(f.x >> 16);
+    x[2] = (float)(f.y & 0xFFFFu); x[3] = (float)(f.y >> 16);
+    x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
 #pragma unroll 1
     for (uint32_t c = half; c < N1 / 8; c += 2) {
       uint32_t p[4];
