@@ -317,3 +317,48 @@ def test_config5_sweep_points(ctx_v1, lex_v1, point, mult):
     d = configs.traces(5, range(int(mult * 100), int(mult * 100) + 8), 1000, lambda t: t % 4,
                        beta0=10 * mult, step=1 * mult, beta_max=150 * mult)
     _replay_case(ctx_v1, lex_v1, d, point)
+
+
+def test_score_stream_boundaries(ctx_v1, lex_v1):
+    """K1 streams 512-byte chunks: words and clitics across chunk boundaries, runs
+    longer than one and two chunks, requests splitting a word, and requests with
+    thousands of tokens (many 32-token rule batches, carries across chunks)."""
+    t = []
+    for pad in range(500, 516):  # a word (with clitic) straddling the first chunk boundary
+        t.append("a" * pad + " don't stop.")
+    t += ["x" * 600 + "n't", "y" * 1100 + "'s and stuff", "history" * 100, "Why" + "z" * 530 + "?",
+          "q" * 511 + " " + "r" * 513 + "'ll"]
+    t += ["ab", "cd", "n't", "s", "'s", "", "", "ing", "edges"]  # adjacent requests split words
+    t += ["a, b, c. " * 700, "What causes art? " * 400, "John saw a boy in the park with a telescope. " * 150]
+    rng = np.random.default_rng(5)
+    words = ["the", "art", "of", "and", "stuff", "bats", "what", "why", "flies", "like", "sand", ",", ".", "?",
+             "don't", "it's", "we've", "history", "\xe9"]
+    for _ in range(200):
+        t.append(" ".join(rng.choice(words, size=int(rng.integers(1, 400)))))
+    data, off = rtgen.pack_texts(t)
+    feat = ctx_v1.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex_v1, data, off)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), got[i].tolist(), want[i].tolist()) for i in bad[:5]]
+
+
+def test_score_decreasing_offsets(ctx_v1, lex_v1):
+    """Offsets that decrease: those requests score as empty and set the flag; the
+    other requests of the same warp task (per-lane FSM path) still match."""
+    d = configs.config2(n=100, gid0=4242)
+    data, off = d["data"], d["offsets"].copy()
+    off[37] = off[39]  # request 36 = [off36, off39) overlaps 37; request 37 = [off39, off38) has e < s
+    ctx_v1.flags()  # clear
+    feat = ctx_v1.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got = host(feat, np.uint16)
+    assert ctx_v1.flags() & 2
+    for i in range(100):
+        s, e = int(off[i]), int(off[i + 1])
+        if e < s:
+            assert (got[i] == 0).all()
+            continue
+        seg = np.ascontiguousarray(data[s:e])
+        want = oracle.rule_gen(lex_v1, seg, np.asarray([0, e - s], np.uint32))
+        assert (got[i] == want[0]).all(), i
