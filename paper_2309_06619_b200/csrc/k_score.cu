@@ -413,15 +413,13 @@ __device__ __forceinline__ uint32_t run_tokens(const Lex& L, const uint32_t* pre
   else if (n > 3 && (t3 == (('\'' << 16) | ('r' << 8) | 'e') || t3 == (('\'' << 16) | ('v' << 8) | 'e') ||
                      t3 == (('\'' << 16) | ('l' << 8) | 'l')))
     cut = 3;
-  if (!cut) {
-    const uint32_t e = word_idx(L, pref, n, k0, k1, t3);
-    attr0 = e ? L.e[e - 1].attr : 0u;
-    return 1;
-  }
-  const uint32_t e0 = word_idx(L, pref, n - cut, k0, k1, (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu));
+  // the stem (or the whole run) on every lane, the clitic only where there is one:
+  // a warp runs at most two lexicon lookups per run, whatever its lanes' mix
+  const uint32_t e0 = word_idx(L, pref, n - cut, k0, k1, cut ? (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu) : t3);
+  attr0 = e0 ? L.e[e0 - 1].attr : 0u;
+  if (!cut) return 1;
   const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
   const uint32_t e1 = word_idx(L, pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu));
-  attr0 = e0 ? L.e[e0 - 1].attr : 0u;
   attr1 = e1 ? L.e[e1 - 1].attr : 0u;
   return 2;
 }
