@@ -462,7 +462,9 @@ def reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8+f32", "data": "synthetic",
-        "config": {"workload": "config2 (oracle sample)", "requests_per_step": m},
+        "config": {"workload": "config2: one 2^20-request queue per GPU (DialoGPT profile, all r=0), "
+                               "score+key+schedule", "requests_per_gpu": 1 << 20, "parallelism": "replicas1",
+                   "sample": f"each step: the first {m} requests of the queue (oracle, one host thread)"},
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
