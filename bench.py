@@ -244,10 +244,11 @@ def native(args):
         pass
     peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
     alg_bytes = total_bytes + 4 * (n + 1) + 12 * n  # text + offsets + u (4 B) + key (8 B)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, ncu_note = None, None, None
     try:  # DRAM bytes of one k_score launch from the committed `ncu --set full` capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "k_score_traffic.json")))
         traffic, traffic_src = tj["traffic_bytes"], tj.get("source")
+        ncu_note = {k: tj[k] for k in ("issue_slots_busy_pct", "warp_instructions", "note") if k in tj}
     except Exception:
         pass
     achieved = alg_bytes / (score_ms / 1e3) / 1e9
@@ -255,7 +256,7 @@ def native(args):
                 "peak": peak_gbs, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(score_ms, 5),
-                "step_share": round(score_ms / (sum(t_step) / len(t_step)), 4)}
+                "step_share": round(score_ms / (sum(t_step) / len(t_step)), 4), "ncu": ncu_note}
 
     # ---------------- MLP leg (NEXT-1): rt_predict_mlp on config 2's features
     mlp = None
