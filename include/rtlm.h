@@ -19,7 +19,10 @@
  *  - Data conditions that are NOT errors: non-ASCII bytes are dropped and
  *    counted in feat[7]; counts saturate at 65535 (sticky flag
  *    RT_FLAG_SATURATED, read with rt_get_flags).
- *  - One context per device, used by one host thread at a time.  Kernels are
+ *  - One context per device, used by one host thread at a time.  A context's
+ *    workspace, work counter and fork stream are reused by every call, so calls
+ *    on one context must be ordered (one stream, or events between streams);
+ *    overlap independent batches with one context per stream.  Kernels are
  *    pure functions of their inputs: same inputs -> same bits.
  *
  * Citations: P:a-b = PAPER.md lines (v1 P:1-912, v2 P:913-1887); S:a-b =
