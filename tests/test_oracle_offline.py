@@ -1,0 +1,72 @@
+"""Pins of the NEXT-2 offline-profiling oracle (oracle/offline.py) from SPEC
+S:185-187 and S:214-216 and the mathematics of least squares."""
+import numpy as np
+import pytest
+
+from oracle.offline import DegenerateDesign, fit_weighted_rule, quantile_threshold, u_max
+
+
+def _feat(n, seed):
+    rng = np.random.default_rng(seed)
+    f = np.zeros((n, 8), np.uint16)
+    f[:, :6] = rng.integers(0, 30, (n, 6))
+    return f
+
+
+def test_exact_linear_targets_are_recovered():
+    # S:185 "targets exactly 2*vague + 5 with other features zero -> (0,0,0,2,0,0), intercept 5, within 1e-6"
+    f = _feat(500, 1)
+    y = 2.0 * f[:, 3] + 5.0
+    b = fit_weighted_rule(f, y)
+    assert np.allclose(b, [5, 0, 0, 0, 2, 0, 0], atol=1e-6)
+    # any exact linear map is recovered
+    w = np.array([6.0, 2.0, 1.5, 4.0, 3.0, 5.0, 5.0])
+    y = f[:, :6] @ w[1:] + w[0]
+    assert np.allclose(fit_weighted_rule(f, y), w, atol=1e-6)
+
+
+def test_constant_target_gives_the_intercept():
+    # S:186 "constant target c with nonconstant features -> intercept c, coefficients 0 within 1e-6"
+    f = _feat(400, 2)
+    b = fit_weighted_rule(f, np.full(400, 7.25))
+    assert abs(b[0] - 7.25) < 1e-6 and np.abs(b[1:]).max() < 1e-6
+
+
+def test_residual_is_optimal():
+    # S:187 residual <= that of the zero-coefficient model; and the normal-equation residual
+    # is orthogonal to the design columns (first-order optimality), up to the ridge term
+    f = _feat(1000, 3)
+    rng = np.random.default_rng(4)
+    y = rng.normal(20, 5, 1000)
+    b = fit_weighted_rule(f, y)
+    x = np.hstack([np.ones((1000, 1)), f[:, :6].astype(np.float64)])
+    r = y - x @ b
+    assert r @ r <= y @ y
+    assert np.abs(x.T @ r - 1e-8 * b).max() < 1e-6 * np.abs(x.T @ y).max()
+    for j in range(7):  # any single perturbation of a coefficient increases the residual
+        for d in (-1e-3, 1e-3):
+            bb = b.copy()
+            bb[j] += d
+            rr = y - x @ bb
+            assert rr @ rr >= r @ r
+
+
+def test_degenerate_design():
+    with pytest.raises(DegenerateDesign):
+        fit_weighted_rule(np.zeros((100, 8), np.uint16), np.arange(100.0))
+    with pytest.raises(DegenerateDesign):
+        fit_weighted_rule(_feat(5, 1), np.arange(5.0))
+
+
+def test_nearest_rank_quantile():
+    # S:214-215
+    assert quantile_threshold(np.arange(1, 11), 0.9) == 9
+    assert quantile_threshold([5.0], 0.3) == 5.0
+    s = np.random.default_rng(5).random(1000)
+    for k in (0.001, 0.1, 0.5, 0.9, 0.999, 1.0):
+        assert quantile_threshold(s, k) == np.sort(s)[int(np.ceil(k * 1000)) - 1]
+    assert quantile_threshold(s, 1.0) == u_max(s)
+    # monotone in k
+    ks = np.linspace(0.01, 1, 50)
+    q = [quantile_threshold(s, k) for k in ks]
+    assert all(a <= b for a, b in zip(q, q[1:]))
