@@ -263,6 +263,11 @@ def native(args):
     if not args.no_mlp:
         mlp = mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_ranks, flush, peaks)
 
+    # ---------------- offline-profiling leg (NEXT-2): fit + quantile over config 2
+    offline = None
+    if not args.no_mlp:
+        offline = offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks)
+
     # ---------------- traces leg (config 3 per GPU)
     traces = None
     if not args.no_traces:
@@ -298,6 +303,8 @@ def native(args):
             line["traces"] = traces
         if mlp is not None:
             line["mlp"] = mlp
+        if offline is not None:
+            line["offline"] = offline
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -341,6 +348,37 @@ def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_r
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "nominal",
                          "alg_flops_per_launch": flops}}
+
+
+def offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks):
+    """NEXT-2: weighted-rule fit (normal equations, fp64) over the 2^20 config-2
+    records (features from rt_score, targets = true lengths) and the nearest-rank
+    0.9-quantile + max of u (tau, u_max).  Algorithmic bytes: 20 B/record (fit),
+    the sort's 5 passes x 24 B/record for the quantile."""
+    import torch
+    feat = ctx.score(data, off)
+    y = torch.from_numpy(d2["true_len"].astype(np.float32)).to(dev)
+    u = torch.rand(n, device=dev) * 100
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev_a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        ev_b.record(stream)
+        ev_b.synchronize()
+        return max_over_ranks(ev_a.elapsed_time(ev_b)) / args.steps
+
+    fit_ms = timed(lambda: ctx.fit_rule(feat, y))
+    q_ms = timed(lambda: ctx.quantile(u, 0.9))
+    return {"fit_ms": round(fit_ms, 4), "fit_Mrec_per_s": round(world * n / (fit_ms / 1e3) / 1e6, 1),
+            "fit_GBps": round(20 * n / (fit_ms / 1e3) / 1e9, 1),
+            "quantile_ms": round(q_ms, 4), "quantile_Mrec_per_s": round(world * n / (q_ms / 1e3) / 1e6, 1),
+            "records_per_gpu": n}
 
 
 def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):

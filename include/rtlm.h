@@ -155,6 +155,23 @@ rt_status rt_set_mlp(rt_ctx* ctx, const rt_mlp* mlp);
  * RT_EINVAL if no model was set. n == 0 is a no-op. */
 rt_status rt_predict_mlp(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, float* d_u, rt_stream stream);
 
+/* ---------------------------------------------------------------- (2c) offline profiling (NEXT-2) */
+
+/* Weighted-rule fit ("learning a linear regression"):
+ * target ~ c + sum_k w_k f_k over the six rule scores f = d_feat[i][0..5]
+ * (u16 [n][8], 16-byte aligned) and fp32 targets d_target[n], by the normal
+ * equations with ridge 1e-8 on the diagonal, fp64, solved by Cholesky.
+ * d_out[8] (device fp64): (c, w_S, w_Y, w_M, w_V, w_O, w_P, cond) where cond =
+ * (min/max Cholesky pivot)^2 (S:185 calls the fit degenerate below ~1e-12);
+ * all NaN if the damped matrix is not positive definite.  Reproducible: fixed
+ * reduction order.  RT_EINVAL if n < 7. */
+rt_status rt_fit_rule(rt_ctx* ctx, const uint16_t* d_feat, const float* d_target, uint32_t n, double* d_out,
+                      rt_stream stream);
+/* Nearest-rank quantile (Eq. 4 tau = quantile_k) and
+ * maximum (u_max) of d_u[n]: d_out[0] = sorted(u)[ceil(k n) - 1],
+ * d_out[1] = max(u) (device fp32).  0 < k <= 1; RT_EINVAL if n == 0. */
+rt_status rt_quantile(rt_ctx* ctx, const float* d_u, uint32_t n, double k, float* d_out, rt_stream stream);
+
 /* ---------------------------------------------------------------- (3) key */
 
 /* Deadline + priority key + class (R-D, R-NUM, R-OVERDUE, R-KEY; Eq. 2/3):

@@ -25,7 +25,7 @@ POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
-           "rt_set_mlp", "rt_predict_mlp"]
+           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -124,6 +124,10 @@ def load_library(path: str = LIB_PATH):
     L.rt_set_mlp.argtypes = [V, ctypes.POINTER(Mlp)]
     L.rt_predict_mlp.restype = I32
     L.rt_predict_mlp.argtypes = [V, P, U32, P, V]
+    L.rt_fit_rule.restype = I32
+    L.rt_fit_rule.argtypes = [V, P, P, U32, P, V]
+    L.rt_quantile.restype = I32
+    L.rt_quantile.argtypes = [V, P, U32, ctypes.c_double, P, V]
     _lib = L
     return L
 
@@ -245,6 +249,25 @@ class Context:
         self._check(self._L.rt_predict_mlp(self._h, _ptr(feat, torch.int16, "feat"), n, _ptr(u, torch.float32, "u"),
                                            self._stream()))
         return u
+
+    def fit_rule(self, feat, target, out=None):
+        """rt_fit_rule: feat uint16-as-int16 [n, 8], target float32 [n] -> float64 [8]
+        = (c, w_S, w_Y, w_M, w_V, w_O, w_P, cond)."""
+        torch = _torch()
+        if out is None:
+            out = self._empty((8,), torch.float64)
+        self._check(self._L.rt_fit_rule(self._h, _ptr(feat, torch.int16, "feat"), _ptr(target, torch.float32, "target"),
+                                        feat.shape[0], _ptr(out, torch.float64, "out"), self._stream()))
+        return out
+
+    def quantile(self, u, k: float, out=None):
+        """rt_quantile: -> float32 [2] = (nearest-rank k-quantile, max)."""
+        torch = _torch()
+        if out is None:
+            out = self._empty((2,), torch.float32)
+        self._check(self._L.rt_quantile(self._h, _ptr(u, torch.float32, "u"), u.numel(), float(k),
+                                        _ptr(out, torch.float32, "out"), self._stream()))
+        return out
 
     def key(self, u, prof: dict, feat=None, arrival=None, D_in=None, key=None, D_out=None):
         torch = _torch()

@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/rtlm.h: context, lexicon upload, argument
 // validation, workspace, launches.  No compute happens on the host.
 #include <atomic>
+#include <cmath>
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -457,6 +458,37 @@ rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d
   DeviceGuard g(c->device);
   cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, c->num_sms, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_mlp");
+  return RT_OK;
+}
+
+rt_status rt_fit_rule(rt_ctx* c, const uint16_t* d_feat, const float* d_target, uint32_t n, double* d_out,
+                      rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (n < 7) return fail(c, RT_EINVAL, "fit needs >= 7 records (S:183)");
+  if (!d_feat || !d_target || !d_out) return fail(c, RT_EINVAL, "null argument");
+  if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
+  DeviceGuard g(c->device);
+  rt_status st = ensure_ws(c, rtlm::fit_workspace());
+  if (st != RT_OK) return st;
+  cudaError_t e = rtlm::launch_fit(d_feat, d_target, n, static_cast<double*>(c->ws), d_out, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_fit");
+  return RT_OK;
+}
+
+rt_status rt_quantile(rt_ctx* c, const float* d_u, uint32_t n, double k, float* d_out, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!n) return fail(c, RT_EINVAL, "EmptyScores (S:212)");
+  if (!(k > 0.0 && k <= 1.0)) return fail(c, RT_EINVAL, "k must be in (0, 1]");
+  if (!d_u || !d_out) return fail(c, RT_EINVAL, "null argument");
+  // nearest rank ceil(k n) - 1, with k n computed in fp64 as the oracle does
+  double kn = std::ceil(k * (double)n);
+  uint32_t r = kn < 1.0 ? 0u : (uint32_t)kn - 1u;
+  if (r >= n) r = n - 1;
+  DeviceGuard g(c->device);
+  rt_status st = ensure_ws(c, rtlm::quantile_workspace(n));
+  if (st != RT_OK) return st;
+  cudaError_t e = rtlm::launch_quantile(d_u, n, r, c->ws, d_out, cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_quantile");
   return RT_OK;
 }
 

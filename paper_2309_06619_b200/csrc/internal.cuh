@@ -144,6 +144,11 @@ struct ReplayLaunch {
   int64_t* end_us;
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+// K8 (NEXT-2): offline profiling (k_offline.cu)
+size_t fit_workspace();
+cudaError_t launch_fit(const uint16_t* feat, const float* y, uint32_t n, double* ws, double* out, cudaStream_t s);
+size_t quantile_workspace(uint32_t n);
+cudaError_t launch_quantile(const float* u, uint32_t n, uint32_t r, void* ws, float* out, cudaStream_t s);
 // K7 (NEXT-1): lightweight MLP on tcgen05 (k_mlp.cu)
 size_t mlp_blob_bytes();
 void mlp_pack(const float* const w[5], const float* const b[5], uint8_t* blob);

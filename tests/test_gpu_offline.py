@@ -1,0 +1,80 @@
+"""NEXT-2 parity: rt_fit_rule and rt_quantile against the fp64 oracle
+(oracle/offline.py).  The quantile is an order statistic: exact.  The fit's
+X^T X is an exact integer sum in fp64 on both sides; X^T y and the solve differ
+only in rounding order (Cholesky vs LU), so coefficients agree to ~cond * 1e-16;
+the test allows 1e-9 relative to the largest coefficient."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.offline import fit_weighted_rule, quantile_threshold
+from rtgen import configs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2309_06619_b200 as rt  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return rt.Context(configs.read_lexicon(), 0)
+
+
+def _dev_feat(f):
+    return torch.from_numpy(np.ascontiguousarray(f).view(np.int16)).to(DEV)
+
+
+@pytest.mark.parametrize("n", [7, 1000, 100003])
+def test_fit_on_rule_features(ctx, n):
+    d = configs.config2(n=n, gid0=31337)
+    f = oracle.rule_gen(oracle.Lexicon(configs.read_lexicon()), d["data"], d["offsets"])
+    y = d["true_len"].astype(np.float32)
+    if n == 7:  # make the tiny design non-singular
+        f[:7, :6] = np.eye(7, 6, dtype=np.uint16) * 3 + 1
+    got = ctx.fit_rule(_dev_feat(f), torch.from_numpy(y).to(DEV)).cpu().numpy()
+    want = fit_weighted_rule(f, y)
+    assert np.abs(got[:7] - want).max() <= 1e-9 * max(1.0, np.abs(want).max())
+    assert 0.0 < got[7] <= 1.0
+
+
+def test_fit_exact_linear(ctx):
+    # exactly 2*vague + 5 -> (5, 0, 0, 0, 2, 0, 0)
+    rng = np.random.default_rng(8)
+    f = np.zeros((5000, 8), np.uint16)
+    f[:, :6] = rng.integers(0, 30, (5000, 6))
+    y = (2.0 * f[:, 3] + 5.0).astype(np.float32)
+    got = ctx.fit_rule(_dev_feat(f), torch.from_numpy(y).to(DEV)).cpu().numpy()
+    assert np.allclose(got[:7], [5, 0, 0, 0, 2, 0, 0], atol=1e-6)
+
+
+@pytest.mark.parametrize("n", [1, 10, 1000, 1 << 20])
+def test_quantile_exact(ctx, n):
+    rng = np.random.default_rng(n)
+    u = rng.gamma(2.0, 10.0, n).astype(np.float32)
+    if n >= 1000:
+        u[::7] = u[3]  # ties
+    du = torch.from_numpy(u).to(DEV)
+    for k in (0.001, 0.5, 0.9, 1.0):
+        got = ctx.quantile(du, k).cpu().numpy()
+        assert got[0] == np.float32(quantile_threshold(u, k)), (n, k)
+        assert got[1] == u.max()
+    if n == 10:  # 1..10, k = 0.9 -> 9
+        got = ctx.quantile(torch.arange(1, 11, dtype=torch.float32, device=DEV), 0.9).cpu().numpy()
+        assert got[0] == 9.0 and got[1] == 10.0
+
+
+def test_offline_errors(ctx):
+    with pytest.raises(rt.RtlmError):
+        ctx.quantile(torch.zeros(0, dtype=torch.float32, device=DEV), 0.9)
+    with pytest.raises(rt.RtlmError):
+        ctx.quantile(torch.ones(5, dtype=torch.float32, device=DEV), 0.0)
+    with pytest.raises(rt.RtlmError):
+        ctx.fit_rule(_dev_feat(np.zeros((6, 8), np.uint16)), torch.zeros(6, dtype=torch.float32, device=DEV))
