@@ -56,3 +56,29 @@ def quantile_threshold(scores: np.ndarray, k: float) -> float:
 
 def u_max(scores: np.ndarray) -> float:
     return float(np.max(np.asarray(scores, np.float64)))
+
+
+# ---------------------------------------------------------------- NEXT-4: richer replay statistics
+def trace_report(arrival_us: np.ndarray, end_us: np.ndarray, trace_off: np.ndarray) -> dict:
+    """Per trace (paper tables P:1557-1578 / P:1633-1653):
+    max and nearest-rank p95 of the response end - r (µs), makespan = last end -
+    first arrival (µs), completions (every task completes: O7 has no horizon),
+    and throughput = completions per minute of makespan."""
+    nt = len(trace_off) - 1
+    out = {"max_resp_us": np.zeros(nt, np.int64), "p95_resp_us": np.zeros(nt, np.int64),
+           "makespan_us": np.zeros(nt, np.int64), "n": np.zeros(nt, np.int64)}
+    for t in range(nt):
+        lo, hi = int(trace_off[t]), int(trace_off[t + 1])
+        if hi == lo:
+            continue
+        resp = np.sort(np.asarray(end_us[lo:hi], np.int64) - np.asarray(arrival_us[lo:hi], np.int64))
+        out["max_resp_us"][t] = resp[-1]
+        out["p95_resp_us"][t] = resp[max(0, math.ceil(0.95 * len(resp)) - 1)]
+        out["makespan_us"][t] = int(np.max(end_us[lo:hi])) - int(np.min(arrival_us[lo:hi]))
+        out["n"][t] = hi - lo
+    return out
+
+
+def throughput_per_min(n: int, makespan_us: int) -> float:
+    """completions / (makespan in minutes) (S:539-541)."""
+    return 0.0 if makespan_us <= 0 else n / (makespan_us / 60e6)

@@ -70,3 +70,19 @@ def test_nearest_rank_quantile():
     ks = np.linspace(0.01, 1, 50)
     q = [quantile_threshold(s, k) for k in ks]
     assert all(a <= b for a, b in zip(q, q[1:]))
+
+
+def test_trace_report_pins():
+    from oracle.offline import throughput_per_min, trace_report
+    # responses {1,2,3} -> max 3; single task -> max = p95; p95 vs sort oracle
+    r = np.array([0, 0, 0, 5], np.int64)
+    e = np.array([1, 2, 3, 9], np.int64)
+    rep = trace_report(r, e, np.array([0, 3, 4]))
+    assert rep["max_resp_us"].tolist() == [3, 4] and rep["p95_resp_us"].tolist() == [3, 4]
+    assert rep["makespan_us"].tolist() == [3, 4] and rep["n"].tolist() == [3, 1]
+    rng = np.random.default_rng(1)
+    resp = rng.integers(0, 10**9, 10**4)
+    rep = trace_report(np.zeros(10**4, np.int64), resp, np.array([0, 10**4]))
+    assert rep["p95_resp_us"][0] == np.sort(resp)[9499]
+    # 60 tasks in 2 minutes -> 30/min; zero completions -> 0
+    assert throughput_per_min(60, 120_000_000) == 30.0 and throughput_per_min(0, 0) == 0.0
