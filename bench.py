@@ -440,6 +440,16 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
         ev_b.synchronize()
         ts.append(ev_a.elapsed_time(ev_b))
     tsum = max_over_ranks(sum(ts))
+    # NEXT-4: per-trace max / p95 response and makespan from the end times (one extra replay with end times)
+    _, end = ctx.simulate(arr, tl, u, key, D, d["trace_off"], d["profiles"], tp, want_end=True)
+    ev_a.record(stream)
+    rep = ctx.trace_report(arr, end, d["trace_off"])
+    ev_b.record(stream)
+    ev_b.synchronize()
+    report_ms = ev_a.elapsed_time(ev_b)
+    rep = rep.cpu().numpy()
+    tprof = d["trace_prof"]
+    p95 = [float(np.median(rep[tprof == f, 1])) / 1e6 if (tprof == f).any() else None for f in range(4)]
     s = sums.cpu().numpy()
     mean_resp = [float(s[f, 0]) / max(1, s[f, 1]) / 1e6 for f in range(4)]
     miss = [float(s[f, 2]) / max(1, s[f, 1]) for f in range(4)]
@@ -447,7 +457,9 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
             "requests_per_s": round(world * n * args.steps / (tsum / 1e3), 1),
             "ms_per_step": round(tsum / args.steps, 4),
             "workload": f"config3: {nt} Poisson-ramp traces x {args.per_trace} requests per GPU, 4 LMs, tight, UP+C+O",
-            "mean_response_s_per_lm": [round(x, 4) for x in mean_resp], "miss_ratio_per_lm": [round(x, 4) for x in miss]}
+            "mean_response_s_per_lm": [round(x, 4) for x in mean_resp], "miss_ratio_per_lm": [round(x, 4) for x in miss],
+            "median_p95_response_s_per_lm": [None if x is None else round(x, 4) for x in p95],
+            "trace_report_ms": round(report_ms, 4)}
 
 
 def oracle_requests_timing(d2, n_sample: int, reps: int = 1):

@@ -93,6 +93,14 @@ typedef struct {
 } rt_profile;
 
 typedef struct {
+  int64_t max_resp_us; /* max over tasks of end - arrival */
+  int64_t p95_resp_us; /* nearest-rank 95th percentile of end - arrival */
+  int64_t makespan_us; /* last end - first arrival */
+  uint32_t n;          /* completed tasks (all of the trace: no horizon) */
+  uint32_t reserved;
+} rt_trace_summary;
+
+typedef struct {
   int64_t sum_resp_us; /* sum over tasks of end - arrival */
   uint32_t n;          /* tasks in the trace */
   uint32_t misses;     /* tasks with end > arrival + D */
@@ -220,6 +228,14 @@ rt_status rt_simulate(rt_ctx* ctx, const int64_t* d_arrival_us, const uint16_t* 
                       const uint64_t* d_key, const uint32_t* d_D_us, const uint32_t* h_trace_off, uint32_t nt,
                       const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
                       rt_trace_stats* d_stats, int64_t* d_end_us, rt_stream stream);
+
+/* Richer replay statistics (NEXT-4; tables; SPEC
+ * S:523-546) from per-task end times (rt_simulate's d_end_us): per trace t in
+ * [0, nt) (tasks h_trace_off[t] .. h_trace_off[t+1], HOST offsets, <= 1024 per
+ * trace), d_report[t] = {max response, nearest-rank p95 response, makespan,
+ * n} (rt_trace_summary).  Throughput = n / makespan (completions per unit time). */
+rt_status rt_trace_report(rt_ctx* ctx, const int64_t* d_arrival_us, const int64_t* d_end_us,
+                          const uint32_t* h_trace_off, uint32_t nt, rt_trace_summary* d_report, rt_stream stream);
 
 /* ---------------------------------------------------------------- (6) aggregate */
 

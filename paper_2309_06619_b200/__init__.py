@@ -25,7 +25,7 @@ POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
-           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile"]
+           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -128,6 +128,8 @@ def load_library(path: str = LIB_PATH):
     L.rt_fit_rule.argtypes = [V, P, P, U32, P, V]
     L.rt_quantile.restype = I32
     L.rt_quantile.argtypes = [V, P, U32, ctypes.c_double, P, V]
+    L.rt_trace_report.restype = I32
+    L.rt_trace_report.argtypes = [V, P, P, P, U32, P, V]
     _lib = L
     return L
 
@@ -267,6 +269,19 @@ class Context:
             out = self._empty((2,), torch.float32)
         self._check(self._L.rt_quantile(self._h, _ptr(u, torch.float32, "u"), u.numel(), float(k),
                                         _ptr(out, torch.float32, "out"), self._stream()))
+        return out
+
+    def trace_report(self, arrival, end_us, trace_off, out=None):
+        """rt_trace_report: -> int64 [nt, 4] = (max_resp_us, p95_resp_us, makespan_us, n | reserved << 32)."""
+        torch = _torch()
+        toff = np.ascontiguousarray(trace_off, dtype=np.uint32)
+        nt = len(toff) - 1
+        if out is None:
+            out = self._empty((nt, 4), torch.int64)
+        self._check(self._L.rt_trace_report(self._h, _ptr(arrival, torch.int64, "arrival"),
+                                            _ptr(end_us, torch.int64, "end_us"),
+                                            toff.ctypes.data_as(ctypes.c_void_p), nt, _ptr(out, torch.int64, "out"),
+                                            self._stream()))
         return out
 
     def key(self, u, prof: dict, feat=None, arrival=None, D_in=None, key=None, D_out=None):

@@ -624,4 +624,23 @@ rt_status rt_reduce_stats(rt_ctx* c, const rt_trace_stats* d_stats, uint32_t nt,
   return RT_OK;
 }
 
+rt_status rt_trace_report(rt_ctx* c, const int64_t* d_arrival_us, const int64_t* d_end_us,
+                          const uint32_t* h_trace_off, uint32_t nt, rt_trace_summary* d_report, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!nt) return RT_OK;
+  if (!d_arrival_us || !d_end_us || !h_trace_off || !d_report) return fail(c, RT_EINVAL, "null argument");
+  if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
+  for (uint32_t t = 0; t < nt; ++t) {
+    if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
+    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
+  }
+  DeviceGuard g(c->device);
+  cudaStream_t s = cs(stream);
+  rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
+  if (st != RT_OK) return st;
+  cudaError_t e = rtlm::launch_trace_report(d_arrival_us, d_end_us, c->d_off, nt, d_report, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_trace_report");
+  return RT_OK;
+}
+
 }  // extern "C"

@@ -144,6 +144,8 @@ struct ReplayLaunch {
   int64_t* end_us;
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, const uint32_t* d_trace_off,
+                                uint32_t nt, rt_trace_summary* out, cudaStream_t s);
 // K8 (NEXT-2): offline profiling (k_offline.cu)
 size_t fit_workspace();
 cudaError_t launch_fit(const uint16_t* feat, const float* y, uint32_t n, double* ws, double* out, cudaStream_t s);

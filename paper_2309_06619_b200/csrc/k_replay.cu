@@ -274,7 +274,65 @@ __global__ void k_reduce_stats(const rt_trace_stats* __restrict__ st, uint32_t n
   }
 }
 
+// NEXT-4: per-trace response statistics from the replay's end times (one warp
+// per trace, n <= 1024): max and nearest-rank p95 of end - r,
+// makespan = last end - first arrival, completions.
+__global__ void __launch_bounds__(32) k_trace_report(const int64_t* __restrict__ arrival,
+                                                     const int64_t* __restrict__ end_us,
+                                                     const uint32_t* __restrict__ trace_off,
+                                                     rt_trace_summary* __restrict__ out) {
+  __shared__ int64_t resp[kMaxTrace];
+  const uint32_t t = blockIdx.x, lane = threadIdx.x;
+  const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
+  if (n == 0) {
+    if (lane == 0) out[t] = rt_trace_summary{0, 0, 0, 0u, 0u};
+    return;
+  }
+  uint32_t npow = 32;
+  while (npow < n) npow <<= 1;
+  int64_t mx_end = INT64_MIN, mn_r = INT64_MAX;
+  for (uint32_t i = lane; i < npow; i += 32) {
+    if (i < n) {
+      const int64_t r = arrival[lo + i], e = end_us[lo + i];
+      resp[i] = e - r;
+      mx_end = max(mx_end, e);
+      mn_r = min(mn_r, r);
+    } else {
+      resp[i] = INT64_MAX;  // sorts last
+    }
+  }
+  __syncwarp();
+  for (uint32_t k = 2; k <= npow; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < npow; i += 32) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const int64_t a = resp[i], b = resp[l];
+          if (((i & k) == 0) == (a > b)) { resp[i] = b; resp[l] = a; }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx_end = max(mx_end, __shfl_xor_sync(0xFFFFFFFFu, mx_end, o));
+    mn_r = min(mn_r, __shfl_xor_sync(0xFFFFFFFFu, mn_r, o));
+  }
+  if (lane == 0) {
+    const uint32_t p = (95u * n + 99u) / 100u;  // ceil(0.95 n), nearest rank
+    out[t] = rt_trace_summary{resp[n - 1], resp[p - 1], mx_end - mn_r, n, 0u};
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, const uint32_t* d_trace_off,
+                                uint32_t nt, rt_trace_summary* out, cudaStream_t s) {
+  if (!nt) return cudaSuccess;
+  k_trace_report<<<nt, 32, 0, s>>>(arrival, end_us, d_trace_off, out);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
   if (!a.nt) return cudaSuccess;

@@ -78,3 +78,34 @@ def test_offline_errors(ctx):
         ctx.quantile(torch.ones(5, dtype=torch.float32, device=DEV), 0.0)
     with pytest.raises(rt.RtlmError):
         ctx.fit_rule(_dev_feat(np.zeros((6, 8), np.uint16)), torch.zeros(6, dtype=torch.float32, device=DEV))
+
+
+def test_trace_report_parity(ctx):
+    """NEXT-4: per-trace max / p95 / makespan from the replay's end times, exact."""
+    from oracle.offline import trace_report
+    lex = oracle.Lexicon(configs.read_lexicon())
+    d = configs.traces(3, range(100, 112), 1000, lambda t: t % 4)
+    n = len(d["arrival_us"])
+    f = oracle.rule_gen(lex, d["data"], d["offsets"])
+    u = np.zeros(n, np.float32)
+    k = np.zeros(n, np.uint64)
+    D = np.zeros(n, np.uint32)
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        p = d["profiles"][int(d["trace_prof"][t])]
+        u[lo:hi] = oracle.predict(f[lo:hi], d["regressors"][int(d["trace_prof"][t])])
+        k[lo:hi], D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], p, r_us=d["arrival_us"][lo:hi])
+    _, end = oracle.simulate(d["arrival_us"], d["true_len"], u, k, D, d["trace_off"], d["profiles"], d["trace_prof"],
+                             want_end=True)
+    # ragged traces: sizes 1000, 1, 0, 1024 (rebuild offsets over the same tasks)
+    t9 = int(d["trace_off"][9])
+    toff = np.concatenate([d["trace_off"][:10], [t9 + 1, t9 + 1, t9 + 1 + 1024]])
+    toff = toff.astype(np.uint32)
+    arr = torch.from_numpy(d["arrival_us"]).to(DEV)
+    e = torch.from_numpy(end).to(DEV)
+    rep = ctx.trace_report(arr, e, toff).cpu().numpy()
+    want = trace_report(d["arrival_us"], end, toff)
+    assert (rep[:, 0] == want["max_resp_us"]).all()
+    assert (rep[:, 1] == want["p95_resp_us"]).all()
+    assert (rep[:, 2] == want["makespan_us"]).all()
+    assert ((rep[:, 3] & 0xFFFFFFFF) == want["n"]).all()
