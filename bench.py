@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--per-trace", type=int, default=1000)
     ap.add_argument("--no-traces", action="store_true")
     ap.add_argument("--no-mlp", action="store_true")
+    ap.add_argument("--sweeps", action="store_true", help="also run the NEXT-3 malicious-ratio sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
     return ap.parse_args()
@@ -268,6 +269,11 @@ def native(args):
     if not args.no_mlp:
         offline = offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks)
 
+    # ---------------- malicious sweep (NEXT-3)
+    malicious = None
+    if args.sweeps:
+        malicious = malicious_leg(args, ctx, configs, dev, rank, max_over_ranks)
+
     # ---------------- traces leg (config 3 per GPU)
     traces = None
     if not args.no_traces:
@@ -305,6 +311,8 @@ def native(args):
             line["mlp"] = mlp
         if offline is not None:
             line["offline"] = offline
+        if malicious is not None:
+            line["malicious"] = malicious
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -379,6 +387,66 @@ def offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks)
             "fit_GBps": round(20 * n / (fit_ms / 1e3) / 1e9, 1),
             "quantile_ms": round(q_ms, 4), "quantile_Mrec_per_s": round(world * n / (q_ms / 1e3) / 1e6, 1),
             "records_per_gpu": n}
+
+
+def run_traces_once(ctx, d, dev, profile_overrides=None):
+    """Score (per LM group) + replay one traces() workload on the device; returns
+    (total µs of response, tasks, misses, device ms).  Groups must be contiguous."""
+    import torch
+    n = len(d["arrival_us"])
+    off_np = d["offsets"]
+    arr = torch.from_numpy(d["arrival_us"]).to(dev)
+    tl = torch.from_numpy(d["true_len"].view(np.int16)).to(dev)
+    tp = torch.from_numpy(d["trace_prof"].view(np.int16)).to(dev)
+    profs = [dict(p, **(profile_overrides or {})) for p in d["profiles"]]
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    key = torch.empty(n, dtype=torch.int64, device=dev)
+    D = torch.empty(n, dtype=torch.int32, device=dev)
+    groups = []
+    for f in range(4):
+        sel = np.nonzero(d["trace_prof"] == f)[0]
+        if len(sel) == 0:
+            continue
+        r0, r1 = int(d["trace_off"][sel[0]]), int(d["trace_off"][sel[-1] + 1])
+        b0, b1 = int(off_np[r0]), int(off_np[r1])
+        so = torch.from_numpy((off_np[r0:r1 + 1] - off_np[r0]).astype(np.uint32).view(np.int32)).to(dev)
+        groups.append((f, r0, r1, torch.from_numpy(np.ascontiguousarray(d["data"][b0:b1])).to(dev), so))
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record()
+    for f, r0, r1, gd, so in groups:
+        ctx.score_key(gd, so, d["regressors"][f], profs[f], arrival=arr[r0:r1],
+                      out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
+    stats, _ = ctx.simulate(arr, tl, u, key, D, d["trace_off"], profs, tp)
+    ev_b.record()
+    ev_b.synchronize()
+    import paper_2309_06619_b200 as rt
+    st = rt.decode_stats(stats)
+    return int(st["sum_resp_us"].sum()), int(st["n"].sum()), int(st["misses"].sum()), ev_a.elapsed_time(ev_b)
+
+
+def malicious_leg(args, ctx, configs, dev, rank, max_over_ranks):
+    """NEXT-3: malicious-task ratio sweep 0..100 % in steps of 10 %:
+    crafted suffix + x3 true length on a seeded fraction of the requests; UP+C+O
+    (the profiles as calibrated) against FIFO without consolidation / offloading.
+    128 traces x 1000 requests per point (statistics, not gated)."""
+    nt = 128
+    base = configs.traces(3, range(10000 + rank * nt, 10000 + (rank + 1) * nt), 1000, lambda t: (t % nt) * 4 // nt)
+    ratios = [round(0.1 * i, 1) for i in range(11)]
+    out = {"ratios": ratios, "mean_response_s": {"UP+C+O": [], "FIFO": []}, "miss_ratio": {"UP+C+O": [], "FIFO": []}}
+    dev_ms = 0.0
+    for r in ratios:
+        d = configs.with_malicious(base, r)
+        for name, ov in (("UP+C+O", None), ("FIFO", {"policy": "FIFO", "consolidate": 0, "offload": 0})):
+            resp, cnt, miss, ms = run_traces_once(ctx, d, dev, ov)
+            dev_ms += ms
+            out["mean_response_s"][name].append(round(resp / max(cnt, 1) / 1e6, 4))
+            out["miss_ratio"][name].append(round(miss / max(cnt, 1), 4))
+    out["traces_per_point"] = nt
+    out["device_ms_total"] = round(max_over_ranks(dev_ms), 3)
+    out["traces_per_s"] = round(nt * len(ratios) * 2 / (out["device_ms_total"] / 1e3), 1)
+    out["note"] = ("statistics of the synthetic workload, not gated: config 3's tight deadlines overload the "
+                   "executors (miss ratio > 0.9), and offloaded malicious tasks queue on 4 CPU cores at gamma = 5")
+    return out
 
 
 def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):

@@ -119,3 +119,30 @@ def config4_shard(rank: int, world: int, n_traces: int = 65536, per_trace: int =
     lo = rank * n_traces // world
     hi = (rank + 1) * n_traces // world
     return traces(4, range(lo, hi), per_trace, lambda t: t % 4)
+
+
+# ---------------------------------------------------------------- NEXT-3: malicious tasks
+#: appended to a malicious request: crafted words that raise its rule scores (an
+#: opener, vague and broad words, coordinators, a comma list, a question), like
+#: the paper's crafted inputs that "induce LMs to generate substantially lengthier
+#: outputs" (Table "dialogue_adversary" P:763-776)
+MALICIOUS_SUFFIX = b" Tell me about the history of art, stuff, countries and the world?"
+MALICIOUS_INFLATION = 3  # true output length x3
+
+
+def with_malicious(d: dict, ratio: float, seed: int = ROOT_SEED + 77) -> dict:
+    """A copy of a traces() workload where a seeded `ratio` of the requests
+    (0 % to 100 % in steps of 10 %) are malicious: crafted suffix
+    appended to the text and the true output length inflated x3 (capped at
+    65535).  Arrivals, traces and profiles are unchanged."""
+    n = len(d["true_len"])
+    rng = np.random.default_rng(seed)
+    mal = rng.random(n) < ratio
+    data, off = d["data"], d["offsets"].astype(np.int64)
+    texts = [bytes(data[off[i]:off[i + 1]]) + (MALICIOUS_SUFFIX if mal[i] else b"") for i in range(n)]
+    nd, noff = pack_texts(texts)
+    tl = d["true_len"].astype(np.int64)
+    tl[mal] = np.minimum(tl[mal] * MALICIOUS_INFLATION, 65535)
+    out = dict(d)
+    out.update(data=nd, offsets=noff, true_len=tl.astype(np.uint16), malicious=mal)
+    return out

@@ -362,3 +362,16 @@ def test_score_decreasing_offsets(ctx_v1, lex_v1):
         seg = np.ascontiguousarray(data[s:e])
         want = oracle.rule_gen(lex_v1, seg, np.asarray([0, e - s], np.uint32))
         assert (got[i] == want[0]).all(), i
+
+
+@pytest.mark.parametrize("ratio", [0.0, 0.3, 1.0])
+def test_malicious_workload(ctx_v1, lex_v1, ratio):
+    """NEXT-3: the malicious-task sweep reuses K1-K6 unchanged:
+    scoring of the crafted texts and the replay match the oracle."""
+    d = configs.with_malicious(configs.traces(3, range(200, 216), 1000, lambda t: t % 4), ratio)
+    feat = ctx_v1.score(dev(d["data"]), dev(d["offsets"]))
+    torch.cuda.synchronize()
+    f = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+    assert (host(feat, np.uint16) == f).all()
+    for ov in ({}, {"policy": "FIFO", "consolidate": 0, "offload": 0}):
+        _replay_case(ctx_v1, lex_v1, d, ov)
