@@ -158,7 +158,7 @@ def test_schedule_big_queue(ctx_v1, lex_v1, n):
     for pol in ["UP", "FIFO"]:
         prof = dict(d["profile"], policy=pol)
         out, f, u, k, D = _score_all(ctx_v1, lex_v1, d, prof, d["regressor"], arrival=np.zeros(n, np.int64))
-        seg = np.asarray([0, 1000, 1000 + n, 1000 + n], U32) if False else np.asarray([0, n], U32)
+        seg = np.asarray([0, n], U32)
         g = ctx_v1.schedule(out["key"], out["u"], seg, prof)
         torch.cuda.synchronize()
         s = oracle.schedule(k, u, seg, prof)
