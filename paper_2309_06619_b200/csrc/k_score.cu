@@ -467,17 +467,20 @@ __device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, i
   uint32_t meta = 0, attr = 0;
   if (valid) { meta = B.t_meta[T & (kRing - 1)]; attr = B.t_attr[T & (kRing - 1)]; }
   const uint32_t kind = meta & 7u, req = meta >> 3;
-  // three predecessors (same request only): from the batch by shuffles, from the ring for lanes < k
+  // three predecessors (same request only): shuffles within the batch, and a
+  // halo of the three tokens before it (lanes 0-2 load it once; 0xFF = none)
+  const int32_t hT = tb - 3 + (int32_t)lane;
+  uint32_t hm = 0xFFu, ha = 0;
+  if (lane < 3 && hT >= 0) { hm = B.t_meta[hT & (kRing - 1)]; ha = B.t_attr[hT & (kRing - 1)]; }
   uint32_t pk[4], pa[4];
 #pragma unroll
   for (int k = 1; k <= 3; ++k) {
-    uint32_t m = __shfl_up_sync(0xFFFFFFFFu, meta, k), at = __shfl_up_sync(0xFFFFFFFFu, attr, k);
-    bool have = true;
-    if (lane < (uint32_t)k) {
-      have = T - k >= 0;
-      if (have) { m = B.t_meta[(T - k) & (kRing - 1)]; at = B.t_attr[(T - k) & (kRing - 1)]; }
-    }
-    const bool same = valid && have && (m >> 3) == req;
+    const uint32_t mu = __shfl_up_sync(0xFFFFFFFFu, meta, k), au = __shfl_up_sync(0xFFFFFFFFu, attr, k);
+    const uint32_t src = (lane + 3u - (uint32_t)k) & 31u;  // halo lane for lanes < k
+    const uint32_t mh = __shfl_sync(0xFFFFFFFFu, hm, src), ah = __shfl_sync(0xFFFFFFFFu, ha, src);
+    const bool in_batch = lane >= (uint32_t)k;
+    const uint32_t m = in_batch ? mu : mh, at = in_batch ? au : ah;
+    const bool same = valid && (m >> 3) == req && m != 0xFFu;
     pk[k] = same ? (m & 7u) : 0u;
     pa[k] = same ? at : 0u;
   }
@@ -538,40 +541,34 @@ __device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, i
   const uint32_t lp_link_l = __shfl_sync(0xFFFFFFFFu, link ? 1u : 0u, lpl);
   const uint32_t lp_link = lp >= tb ? lp_link_l : cy.punct_link;
   if (link && !lp_link) cP += 1u;
-  // per-token contributions, packed: ntok 0-6, V 7-13, Y 14-20, S 21-27, O 28-34, P 35-41, nq 42-48, M 49-63
-  uint64_t v = 0;
-  if (valid) {
-    v = 1ull;
-    if (isW) {
-      v |= (uint64_t)(attr & A_VAGUE) << 7;
-      v |= (uint64_t)((attr >> 8) & 1u) << 14;
-      v |= (uint64_t)((attr >> A_SEM_SHIFT) & A_SEM_MASK) << 49;
-    }
-    v |= (uint64_t)cS << 21;
-    v |= (uint64_t)cO << 28;
-    v |= (uint64_t)cP << 35;
-    v |= (uint64_t)(isQ ? 1u : 0u) << 42;
-  }
-  // segmented sum by request (requests are contiguous and increasing)
+  // per-request sums (requests are contiguous, increasing runs of lanes): the
+  // 0/1 counters by popcounts of ballots over the run, the senses count M by a
+  // segmented scan; the run's last lane adds them to the request's accumulators
+  const uint32_t b_V = __ballot_sync(0xFFFFFFFFu, isW && (attr & A_VAGUE));
+  const uint32_t b_Y = __ballot_sync(0xFFFFFFFFu, isW && ((attr >> 8) & 1u));
+  const uint32_t b_S = __ballot_sync(0xFFFFFFFFu, cS != 0u), b_O = __ballot_sync(0xFFFFFFFFu, cO != 0u);
+  const uint32_t b_P = __ballot_sync(0xFFFFFFFFu, cP != 0u), b_Q = __ballot_sync(0xFFFFFFFFu, isQ);
   const uint32_t b_head = __ballot_sync(0xFFFFFFFFu, valid && (lane == 0 || req != prev_req_lane));
   const int32_t head = 31 - (int32_t)__clz(b_head & le);
+  uint32_t msum = isW ? (attr >> A_SEM_SHIFT) & A_SEM_MASK : 0u;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, v, o);
-    if ((int32_t)lane - o >= head) v += up;
+    const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, msum, o);
+    if ((int32_t)lane - o >= head) msum += up;
   }
   const uint32_t next_req = __shfl_down_sync(0xFFFFFFFFu, req, 1);
   const bool next_valid = __shfl_down_sync(0xFFFFFFFFu, valid ? 1u : 0u, 1) != 0u;
   if (valid && (lane == 31 || !next_valid || next_req != req)) {
+    const uint32_t seg = le & ~((1u << head) - 1u);  // lanes head..lane
     uint32_t* a = B.acc[req];
-    a[6] += (uint32_t)(v & 0x7F);
-    a[3] += (uint32_t)((v >> 7) & 0x7F);
-    a[1] += (uint32_t)((v >> 14) & 0x7F);
-    a[0] += (uint32_t)((v >> 21) & 0x7F);
-    a[4] += (uint32_t)((v >> 28) & 0x7F);
-    a[5] += (uint32_t)((v >> 35) & 0x7F);
-    a[8] += (uint32_t)((v >> 42) & 0x7F);
-    a[2] = min(a[2] + (uint32_t)(v >> 49), 0xFFFFFFu);
+    a[6] += __popc(seg);
+    a[3] += __popc(b_V & seg);
+    a[1] += __popc(b_Y & seg);
+    a[0] += __popc(b_S & seg);
+    a[4] += __popc(b_O & seg);
+    a[5] += __popc(b_P & seg);
+    a[8] += __popc(b_Q & seg);
+    a[2] = min(a[2] + msum, 0xFFFFFFu);
   }
   // carries for the next batch
   const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
