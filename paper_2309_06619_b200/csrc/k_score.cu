@@ -366,6 +366,12 @@ constexpr uint32_t kRing = 128;               // token ring per warp
 
 enum : uint32_t { K_W = 1, K_COMMA = 2, K_END = 3, K_Q = 4, K_OTH = 5 };
 
+struct Carry {
+  int32_t rs, end, word, fw, noun, fn, d, punct;
+  uint32_t fn_id, word_broad, punct_comma, punct_link;
+  uint32_t prev_req;  // request of the last token (0xFFFFFFFF: none)
+};
+
 struct __align__(16) WarpBuf {
   uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
   uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
@@ -375,6 +381,7 @@ struct __align__(16) WarpBuf {
   uint32_t t_attr[kRing];
   uint8_t t_meta[kRing];               // kind | req << 3
   uint32_t acc[32][9];                 // S Y M V O P ntok nd nq
+  Carry cy;                            // rule-scan carries between token batches (kept out of registers)
 };
 
 struct Smem4 {
@@ -454,14 +461,10 @@ __device__ __noinline__ void fsm_request(const ScoreLaunch& a, const Lex& L, uin
   epilogue(a, r, f);
 }
 
-struct Carry {
-  int32_t rs, end, word, fw, noun, fn, d, punct;
-  uint32_t fn_id, word_broad, punct_comma, punct_link;
-  uint32_t prev_req;  // request of the last token (0xFFFFFFFF: none)
-};
 
 // rules over tokens [tb, tend) of the ring (tend - tb <= 32)
-__device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, int32_t tend, uint32_t lane) {
+__device__ __forceinline__ void rules_batch(WarpBuf& B, int32_t tb, int32_t tend, uint32_t lane) {
+  Carry cy = B.cy;
   const int32_t T = tb + (int32_t)lane;
   const bool valid = T < tend;
   uint32_t meta = 0, attr = 0;
@@ -530,7 +533,8 @@ __device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, i
   if (isQ && lword >= sst && lw_broad) cO += 1u;
   // content spans: coordinator between words (counted at the word after it)
   uint32_t cP = 0;
-  if (isW && pk[1] == K_W && (pa[1] & A_COORD) && (pk[2] == K_W || (pk[2] == K_COMMA && pk[3] == K_W))) cP = 1u;
+  // (non-short-circuit: no branches)
+  cP = (uint32_t)(isW & (pk[1] == K_W) & ((pa[1] & A_COORD) != 0u) & ((pk[2] == K_W) | ((pk[2] == K_COMMA) & (pk[3] == K_W))));
   // comma chains: link = previous punctuation is a comma with >= 1 word between
   const uint32_t b_p = __ballot_sync(0xFFFFFFFFu, isP);
   const int32_t lp = last_pos(b_p & lt, tb, cy.punct);
@@ -591,6 +595,8 @@ __device__ __forceinline__ void rules_batch(WarpBuf& B, Carry& cy, int32_t tb, i
     }
     cy.punct = last_pos(b_p, tb, cy.punct);
   }
+  if (lane == 0) B.cy = cy;
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work) {
@@ -651,7 +657,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     B.rs[lane] = s_r;
 #pragma unroll
     for (int k = 0; k < 9; ++k) B.acc[lane][k] = 0;
-    Carry cy{-1, -1, -1, -1, -1, -1, -1, -1, 0u, 0u, 0u, 0u, 0xFFFFFFFFu};
+    if (lane == 0) B.cy = Carry{-1, -1, -1, -1, -1, -1, -1, -1, 0u, 0u, 0u, 0u, 0xFFFFFFFFu};
     int32_t tokbase = 0;
     uint32_t prevW = 0;                 // W bit of the byte before the chunk
     int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
@@ -834,7 +840,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         tokbase += (int32_t)nt;
         // full 32-token batches; everything after the last event of the task
         const int32_t lim = (last_chunk && e0 + 32 >= nev) ? tokbase : tokbase - 31;
-        for (; tokdone < lim; tokdone += 32) rules_batch(B, cy, tokdone, min(tokdone + 32, tokbase), lane);
+        for (; tokdone < lim; tokdone += 32) rules_batch(B, tokdone, min(tokdone + 32, tokbase), lane);
         __syncwarp();
       }
       // dropped bytes (rare): count per request
