@@ -513,11 +513,22 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
     ev_a.record(stream)
     rep = ctx.trace_report(arr, end, d["trace_off"])
     ev_b.record(stream)
-    ev_b.synchronize()
+    util = ctx.trace_utilization(tl, key, end, d["trace_off"], d["profiles"], tp)
+    ev_c = torch.cuda.Event(enable_timing=True)
+    ev_c.record(stream)
+    ev_c.synchronize()
     report_ms = ev_a.elapsed_time(ev_b)
+    util_ms = ev_b.elapsed_time(ev_c)
     rep = rep.cpu().numpy()
+    util = util.cpu().numpy()
     tprof = d["trace_prof"]
     p95 = [float(np.median(rep[tprof == f, 1])) / 1e6 if (tprof == f).any() else None for f in range(4)]
+    cores = np.array([d["profiles"][int(f)]["cores"] for f in tprof], np.float64)
+    mk = np.maximum(rep[:, 2], 1).astype(np.float64)
+    gfrac = util[:, 0] / mk
+    cfrac = util[:, 1] / (mk * np.maximum(cores, 1))
+    gutil = [round(float(np.mean(gfrac[tprof == f])), 4) if (tprof == f).any() else None for f in range(4)]
+    cutil = [round(float(np.mean(cfrac[tprof == f])), 4) if (tprof == f).any() else None for f in range(4)]
     s = sums.cpu().numpy()
     mean_resp = [float(s[f, 0]) / max(1, s[f, 1]) / 1e6 for f in range(4)]
     miss = [float(s[f, 2]) / max(1, s[f, 1]) for f in range(4)]
@@ -527,7 +538,8 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
             "workload": f"config3: {nt} Poisson-ramp traces x {args.per_trace} requests per GPU, 4 LMs, tight, UP+C+O",
             "mean_response_s_per_lm": [round(x, 4) for x in mean_resp], "miss_ratio_per_lm": [round(x, 4) for x in miss],
             "median_p95_response_s_per_lm": [None if x is None else round(x, 4) for x in p95],
-            "trace_report_ms": round(report_ms, 4)}
+            "mean_gpu_util_per_lm": gutil, "mean_cpu_util_per_lm": cutil,
+            "trace_report_ms": round(report_ms, 4), "trace_util_ms": round(util_ms, 4)}
 
 
 def oracle_requests_timing(d2, n_sample: int, reps: int = 1):

@@ -101,6 +101,13 @@ typedef struct {
 } rt_trace_summary;
 
 typedef struct {
+  int64_t gpu_busy_us;  /* sum over GPU batches of setup + base + eta*max len */
+  int64_t cpu_busy_us;  /* sum over CPU tasks of gamma*(base + eta*len), all cores */
+  uint32_t gpu_batches; /* GPU batches dispatched */
+  uint32_t cpu_tasks;   /* tasks run on the CPU cores */
+} rt_trace_util;
+
+typedef struct {
   int64_t sum_resp_us; /* sum over tasks of end - arrival */
   uint32_t n;          /* tasks in the trace */
   uint32_t misses;     /* tasks with end > arrival + D */
@@ -236,6 +243,20 @@ rt_status rt_simulate(rt_ctx* ctx, const int64_t* d_arrival_us, const uint16_t* 
  * n} (rt_trace_summary).  Throughput = n / makespan (completions per unit time). */
 rt_status rt_trace_report(rt_ctx* ctx, const int64_t* d_arrival_us, const int64_t* d_end_us,
                           const uint32_t* h_trace_off, uint32_t nt, rt_trace_summary* d_report, rt_stream stream);
+
+/* Executor utilization (NEXT-4, the simulated analogue
+ * of the paper's "CPU / GPU util." table) from rt_simulate's per-task end
+ * times: d_util[t] = {GPU busy µs, CPU busy µs (summed over cores), GPU
+ * batches, CPU tasks} for trace t (same h_trace_off / h_profiles[np] /
+ * d_trace_prof conventions as rt_simulate; the class is d_key >> 63).  GPU
+ * batches are recovered as the GPU-class tasks sharing one end time, exact for
+ * rt_simulate's serial GPU.  Fractions: gpu_busy / makespan and cpu_busy /
+ * (cores * makespan), makespan from rt_trace_report.  RT_EINVAL on null
+ * arguments, bad offsets or traces longer than 1024. */
+rt_status rt_trace_utilization(rt_ctx* ctx, const uint16_t* d_true_len, const uint64_t* d_key,
+                               const int64_t* d_end_us, const uint32_t* h_trace_off, uint32_t nt,
+                               const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
+                               rt_trace_util* d_util, rt_stream stream);
 
 /* ---------------------------------------------------------------- (6) aggregate */
 

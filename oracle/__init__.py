@@ -89,6 +89,7 @@ def _load():
         L.orc_schedule.argtypes = [P, P, P, ctypes.c_uint32, ctypes.POINTER(Profile), ctypes.c_uint32,
                                    P, P, P, P, P]
         L.orc_simulate.argtypes = [P, P, P, P, P, P, ctypes.c_uint32, P, P, P, P]
+        L.orc_simulate_util.argtypes = [P, P, P, P, P, P, ctypes.c_uint32, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -212,8 +213,13 @@ def schedule(key_, u, seg_off, prof: dict, cores: int | None = None):
             "seg_batch_off": sbo, "nbatches": int(nb)}
 
 
-def simulate(r_us, true_len, u, key_, D_us, trace_off, profiles, trace_prof=None, want_end=False):
-    """O7: returns (stats structured array [sum_resp_us, n, misses], end_us or None)."""
+UTIL_DTYPE = [("gpu_busy_us", "<i8"), ("cpu_busy_us", "<i8"), ("gpu_batches", "<u4"), ("cpu_tasks", "<u4")]
+
+
+def simulate(r_us, true_len, u, key_, D_us, trace_off, profiles, trace_prof=None, want_end=False, want_util=False):
+    """O7: returns (stats structured array [sum_resp_us, n, misses], end_us or None),
+    plus, iff want_util, the per-trace executor busy times accumulated by the
+    event loop (UTIL_DTYPE; NEXT-4)."""
     r = np.ascontiguousarray(r_us, dtype=np.int64)
     ln = np.ascontiguousarray(true_len, dtype=np.uint16)
     u = np.ascontiguousarray(u, dtype=np.float32)
@@ -227,6 +233,7 @@ def simulate(r_us, true_len, u, key_, D_us, trace_off, profiles, trace_prof=None
     tp = None if trace_prof is None else np.ascontiguousarray(trace_prof, dtype=np.uint16)
     st = np.zeros(nt, dtype=[("sum_resp_us", "<i8"), ("n", "<u4"), ("misses", "<u4")])
     end = np.zeros(len(r), dtype=np.int64) if want_end else None
-    _load().orc_simulate(_p(r), _p(ln), _p(u), _p(k), _p(D), _p(to), nt, ctypes.cast(parr, ctypes.c_void_p),
-                         _p(tp), _p(st), _p(end))
-    return st, end
+    ut = np.zeros(nt, dtype=UTIL_DTYPE) if want_util else None
+    _load().orc_simulate_util(_p(r), _p(ln), _p(u), _p(k), _p(D), _p(to), nt, ctypes.cast(parr, ctypes.c_void_p),
+                              _p(tp), _p(st), _p(end), _p(ut))
+    return (st, end, ut) if want_util else (st, end)

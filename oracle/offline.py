@@ -82,3 +82,17 @@ def trace_report(arrival_us: np.ndarray, end_us: np.ndarray, trace_off: np.ndarr
 def throughput_per_min(n: int, makespan_us: int) -> float:
     """completions / (makespan in minutes) (S:539-541)."""
     return 0.0 if makespan_us <= 0 else n / (makespan_us / 60e6)
+
+
+def utilization(util, makespan_us, cores) -> tuple[np.ndarray, np.ndarray]:
+    """Executor utilization (the simulated analogue of the paper's
+    "CPU / GPU util." overhead table): busy time / makespan per executor, from
+    the replay's busy accumulators (`simulate(..., want_util=True)`).  The CPU
+    fraction divides by cores x makespan (every core is an executor); a trace
+    with no makespan or no cores reports 0."""
+    ms = np.asarray(makespan_us, np.float64)
+    c = np.broadcast_to(np.asarray(cores, np.float64), ms.shape)
+    g = np.where(ms > 0, util["gpu_busy_us"] / np.where(ms > 0, ms, 1.0), 0.0)
+    den = ms * c
+    cp = np.where(den > 0, util["cpu_busy_us"] / np.where(den > 0, den, 1.0), 0.0)
+    return g, cp

@@ -575,9 +575,18 @@ uint32_t orc_schedule(const uint64_t* key, const float* u, const uint32_t* seg_o
 // O7 replay (§V-A workload P:1580-1589; response P:634-635 / P:1596; miss
 // P:673-676; DESIGN R-REPLAY).  Tasks of trace t are [trace_off[t],
 // trace_off[t+1]) in arrival order.  end_us may be NULL.
-void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const uint64_t* key, const uint32_t* D,
-                  const uint32_t* trace_off, uint32_t nt, const orc_profile* profs, const uint16_t* trace_prof,
-                  orc_stats* stats, int64_t* end_us) {
+// util (nullable, NEXT-4 / SPEC S:374): per trace, the executors' busy
+// time accumulated as the loop dispatches -- each GPU batch adds its duration
+// setup + base + eta*max len, each CPU task gamma*(base + eta*len)
+// -- and the counts of GPU batches and CPU tasks.
+struct orc_util {
+  int64_t gpu_busy_us, cpu_busy_us;
+  uint32_t gpu_batches, cpu_tasks;
+};
+
+void orc_simulate_util(const int64_t* r, const uint16_t* len, const float* u, const uint64_t* key, const uint32_t* D,
+                       const uint32_t* trace_off, uint32_t nt, const orc_profile* profs, const uint16_t* trace_prof,
+                       orc_stats* stats, int64_t* end_us, orc_util* util) {
   for (uint32_t t = 0; t < nt; ++t) {
     const orc_profile& p = profs[trace_prof ? trace_prof[t] : 0];
     const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
@@ -592,6 +601,7 @@ void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const u
     std::set<std::pair<uint32_t, uint32_t>> ready_gpu, ready_cpu;  // (rank, i)
     std::set<uint32_t> gpu_by_arrival;                              // arrival index
     int64_t gpu_free = 0;
+    orc_util ut{0, 0, 0u, 0u};
     uint32_t next = 0, done = 0;
     int64_t now = n ? r[lo] : 0;
     while (done < n) {
@@ -612,6 +622,8 @@ void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const u
         int64_t e = now + int64_t(p.gamma) * (p.base_us + p.eta_us * int64_t(len[lo + i]));
         end[i] = e;
         core_free[c] = e;
+        ut.cpu_busy_us += e - now;
+        ++ut.cpu_tasks;
         ++done;
       }
       // GPU dispatch
@@ -652,6 +664,8 @@ void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const u
             ++done;
           }
           gpu_free = e;
+          ut.gpu_busy_us += e - now;
+          ++ut.gpu_batches;
         }
       }
       if (done == n) break;
@@ -672,7 +686,14 @@ void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const u
       if (end_us) end_us[lo + i] = end[i];
     }
     stats[t] = st;
+    if (util) util[t] = ut;
   }
+}
+
+void orc_simulate(const int64_t* r, const uint16_t* len, const float* u, const uint64_t* key, const uint32_t* D,
+                  const uint32_t* trace_off, uint32_t nt, const orc_profile* profs, const uint16_t* trace_prof,
+                  orc_stats* stats, int64_t* end_us) {
+  orc_simulate_util(r, len, u, key, D, trace_off, nt, profs, trace_prof, stats, end_us, nullptr);
 }
 
 }  // extern "C"

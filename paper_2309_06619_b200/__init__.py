@@ -25,7 +25,8 @@ POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
-           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report"]
+           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report",
+           "rt_trace_utilization"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -130,6 +131,8 @@ def load_library(path: str = LIB_PATH):
     L.rt_quantile.argtypes = [V, P, U32, ctypes.c_double, P, V]
     L.rt_trace_report.restype = I32
     L.rt_trace_report.argtypes = [V, P, P, P, U32, P, V]
+    L.rt_trace_utilization.restype = I32
+    L.rt_trace_utilization.argtypes = [V, P, P, P, P, U32, P, U32, P, P, V]
     _lib = L
     return L
 
@@ -282,6 +285,24 @@ class Context:
                                             _ptr(end_us, torch.int64, "end_us"),
                                             toff.ctypes.data_as(ctypes.c_void_p), nt, _ptr(out, torch.int64, "out"),
                                             self._stream()))
+        return out
+
+    def trace_utilization(self, true_len, key, end_us, trace_off, profiles, trace_prof=None, out=None):
+        """rt_trace_utilization: -> int64 [nt, 3] = (gpu_busy_us, cpu_busy_us, gpu_batches | cpu_tasks << 32)."""
+        torch = _torch()
+        toff = np.ascontiguousarray(trace_off, dtype=np.uint32)
+        nt = len(toff) - 1
+        if isinstance(profiles, dict):
+            profiles = [profiles]
+        parr = (Profile * len(profiles))(*[make_profile(d) for d in profiles])
+        if out is None:
+            out = self._empty((nt, 3), torch.int64)
+        self._check(self._L.rt_trace_utilization(self._h, _ptr(true_len, torch.int16, "true_len"),
+                                                 _ptr(key, torch.int64, "key"), _ptr(end_us, torch.int64, "end_us"),
+                                                 toff.ctypes.data_as(ctypes.c_void_p), nt,
+                                                 ctypes.cast(parr, ctypes.c_void_p), len(profiles),
+                                                 _ptr(trace_prof, torch.int16, "trace_prof"),
+                                                 _ptr(out, torch.int64, "out"), self._stream()))
         return out
 
     def key(self, u, prof: dict, feat=None, arrival=None, D_in=None, key=None, D_out=None):

@@ -566,6 +566,27 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   return RT_OK;
 }
 
+static rt_status upload_profiles(rt_ctx* c, const rt_profile* h_profiles, uint32_t np, cudaStream_t s) {
+  if (np > c->prof_cap) {
+    if (c->d_prof) cudaFree(c->d_prof);
+    c->d_prof = nullptr;
+    c->prof_cap = 0;
+    if (cudaMalloc(&c->d_prof, np * sizeof(rt_profile)) != cudaSuccess) return fail(c, RT_ENOMEM, "profiles");
+    c->prof_cap = np;
+  }
+  RT_CUDA(c, cudaMemcpyAsync(c->d_prof, h_profiles, np * sizeof(rt_profile), cudaMemcpyHostToDevice, s));
+  return RT_OK;
+}
+
+static rt_status check_trace_off(rt_ctx* c, const uint32_t* h_trace_off, uint32_t nt) {
+  if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
+  for (uint32_t t = 0; t < nt; ++t) {
+    if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
+    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
+  }
+  return RT_OK;
+}
+
 rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, const float* d_u,
                       const uint64_t* d_key, const uint32_t* d_D, const uint32_t* h_trace_off, uint32_t nt,
                       const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
@@ -588,14 +609,8 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   cudaStream_t s = cs(stream);
   rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
   if (st != RT_OK) return st;
-  if (np > c->prof_cap) {
-    if (c->d_prof) cudaFree(c->d_prof);
-    c->d_prof = nullptr;
-    c->prof_cap = 0;
-    if (cudaMalloc(&c->d_prof, np * sizeof(rt_profile)) != cudaSuccess) return fail(c, RT_ENOMEM, "profiles");
-    c->prof_cap = np;
-  }
-  RT_CUDA(c, cudaMemcpyAsync(c->d_prof, h_profiles, np * sizeof(rt_profile), cudaMemcpyHostToDevice, s));
+  st = upload_profiles(c, h_profiles, np, s);
+  if (st != RT_OK) return st;
   rtlm::ReplayLaunch a{};
   a.arrival = d_arr;
   a.len = d_len;
@@ -640,6 +655,30 @@ rt_status rt_trace_report(rt_ctx* c, const int64_t* d_arrival_us, const int64_t*
   if (st != RT_OK) return st;
   cudaError_t e = rtlm::launch_trace_report(d_arrival_us, d_end_us, c->d_off, nt, d_report, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_trace_report");
+  return RT_OK;
+}
+
+rt_status rt_trace_utilization(rt_ctx* c, const uint16_t* d_len, const uint64_t* d_key, const int64_t* d_end_us,
+                               const uint32_t* h_trace_off, uint32_t nt, const rt_profile* h_profiles, uint32_t np,
+                               const uint16_t* d_trace_prof, rt_trace_util* d_util, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!nt) return RT_OK;
+  if (!h_trace_off || !h_profiles || !np || !d_util) return fail(c, RT_EINVAL, "null argument");
+  for (uint32_t k = 0; k < np; ++k) {
+    rt_status st = check_profile(c, &h_profiles[k], true);
+    if (st != RT_OK) return st;
+  }
+  rt_status st = check_trace_off(c, h_trace_off, nt);
+  if (st != RT_OK) return st;
+  if (h_trace_off[nt] && (!d_len || !d_key || !d_end_us)) return fail(c, RT_EINVAL, "null task array");
+  DeviceGuard g(c->device);
+  cudaStream_t s = cs(stream);
+  st = upload_offsets(c, h_trace_off, nt + 1, s);
+  if (st != RT_OK) return st;
+  st = upload_profiles(c, h_profiles, np, s);
+  if (st != RT_OK) return st;
+  cudaError_t e = rtlm::launch_trace_util(d_len, d_key, d_end_us, c->d_off, nt, c->d_prof, d_trace_prof, d_util, s);
+  if (e != cudaSuccess) return cuda_fail(c, e, "k_trace_util");
   return RT_OK;
 }
 

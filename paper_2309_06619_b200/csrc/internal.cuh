@@ -144,6 +144,9 @@ struct ReplayLaunch {
   int64_t* end_us;
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,
+                              const uint32_t* d_trace_off, uint32_t nt, const rt_profile* d_prof,
+                              const uint16_t* d_trace_prof, rt_trace_util* out, cudaStream_t s);
 cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, const uint32_t* d_trace_off,
                                 uint32_t nt, rt_trace_summary* out, cudaStream_t s);
 // K8 (NEXT-2): offline profiling (k_offline.cu)

@@ -324,7 +324,90 @@ __global__ void __launch_bounds__(32) k_trace_report(const int64_t* __restrict__
   }
 }
 
+// NEXT-4 executor utilization from the replay's end
+// times, one warp per trace: a CPU task ran gamma*(base + eta*len);
+// the GPU-class tasks that share one end time form one batch (the GPU runs one
+// batch at a time and every batch of positive duration ends strictly after the
+// previous one), whose duration is setup + base + eta*max len.  The
+// GPU tasks are sorted by (end, len) so each batch's last element carries its
+// max len.
+__global__ void __launch_bounds__(32) k_trace_util(const uint16_t* __restrict__ len,
+                                                   const uint64_t* __restrict__ key,
+                                                   const int64_t* __restrict__ end_us,
+                                                   const uint32_t* __restrict__ trace_off,
+                                                   const rt_profile* __restrict__ profiles,
+                                                   const uint16_t* __restrict__ trace_prof,
+                                                   rt_trace_util* __restrict__ out) {
+  __shared__ int64_t se[kMaxTrace];
+  __shared__ uint16_t sl[kMaxTrace];
+  const uint32_t t = blockIdx.x, lane = threadIdx.x;
+  const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
+  const rt_profile& p = profiles[trace_prof ? trace_prof[t] : 0];
+  uint32_t npow = 32;
+  while (npow < n) npow <<= 1;
+  int64_t cbusy = 0;
+  uint32_t ccnt = 0;
+  for (uint32_t i = lane; i < npow; i += 32) {
+    int64_t e = INT64_MAX;  // CPU tasks and padding sort last
+    uint16_t l = 0;
+    if (i < n) {
+      const uint16_t li = len[lo + i];
+      if (key[lo + i] >> 63) {
+        cbusy += (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)li);
+        ++ccnt;
+      } else {
+        e = end_us[lo + i];
+        l = li;
+      }
+    }
+    se[i] = e;
+    sl[i] = l;
+  }
+  __syncwarp();
+  for (uint32_t k = 2; k <= npow; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < npow; i += 32) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const int64_t ea = se[i], eb = se[l];
+          const uint16_t la = sl[i], lb = sl[l];
+          const bool gt = ea > eb || (ea == eb && la > lb);
+          if (((i & k) == 0) == gt) { se[i] = eb; se[l] = ea; sl[i] = lb; sl[l] = la; }
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cbusy += __shfl_xor_sync(0xFFFFFFFFu, cbusy, o);
+    ccnt += __shfl_xor_sync(0xFFFFFFFFu, ccnt, o);
+  }
+  const uint32_t ngpu = n - ccnt;
+  int64_t gbusy = 0;
+  uint32_t gcnt = 0;
+  for (uint32_t i = lane; i < ngpu; i += 32)
+    if (i + 1 == ngpu || se[i + 1] != se[i]) {
+      gbusy += p.setup_us + p.base_us + p.eta_us * (int64_t)sl[i];
+      ++gcnt;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gbusy += __shfl_xor_sync(0xFFFFFFFFu, gbusy, o);
+    gcnt += __shfl_xor_sync(0xFFFFFFFFu, gcnt, o);
+  }
+  if (lane == 0) out[t] = rt_trace_util{gbusy, cbusy, gcnt, ccnt};
+}
+
 }  // namespace
+
+cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,
+                              const uint32_t* d_trace_off, uint32_t nt, const rt_profile* d_prof,
+                              const uint16_t* d_trace_prof, rt_trace_util* out, cudaStream_t s) {
+  if (!nt) return cudaSuccess;
+  k_trace_util<<<nt, 32, 0, s>>>(len, key, end_us, d_trace_off, d_prof, d_trace_prof, out);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, const uint32_t* d_trace_off,
                                 uint32_t nt, rt_trace_summary* out, cudaStream_t s) {

@@ -109,3 +109,44 @@ def test_trace_report_parity(ctx):
     assert (rep[:, 1] == want["p95_resp_us"]).all()
     assert (rep[:, 2] == want["makespan_us"]).all()
     assert ((rep[:, 3] & 0xFFFFFFFF) == want["n"]).all()
+
+
+@pytest.mark.gpu
+def test_trace_utilization_parity(ctx):
+    """NEXT-4: executor busy times from the replay's end times, exact against the
+    event loop's own accumulators (oracle.simulate(want_util=True)); offload on
+    and off, static and consolidated batching."""
+    lex = oracle.Lexicon(configs.read_lexicon())
+    for offload, consolidate in ((1, 1), (0, 1), (1, 0)):
+        d = configs.traces(3, range(200, 210), 1000, lambda t: t % 4)
+        for p in d["profiles"]:
+            p["offload"], p["consolidate"] = offload, consolidate
+        n = len(d["arrival_us"])
+        f = oracle.rule_gen(lex, d["data"], d["offsets"])
+        u = np.zeros(n, np.float32)
+        k = np.zeros(n, np.uint64)
+        D = np.zeros(n, np.uint32)
+        for t in range(len(d["trace_off"]) - 1):
+            lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+            p = d["profiles"][int(d["trace_prof"][t])]
+            u[lo:hi] = oracle.predict(f[lo:hi], d["regressors"][int(d["trace_prof"][t])])
+            k[lo:hi], D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], p, r_us=d["arrival_us"][lo:hi])
+        _, end, ut = oracle.simulate(d["arrival_us"], d["true_len"], u, k, D, d["trace_off"], d["profiles"],
+                                     d["trace_prof"], want_end=True, want_util=True)
+        got = ctx.trace_utilization(torch.from_numpy(d["true_len"].view(np.int16)).to(DEV),
+                                    torch.from_numpy(k.view(np.int64)).to(DEV), torch.from_numpy(end).to(DEV),
+                                    d["trace_off"], d["profiles"],
+                                    torch.from_numpy(d["trace_prof"].astype(np.uint16).view(np.int16)).to(DEV))
+        got = got.cpu().numpy()
+        assert (got[:, 0] == ut["gpu_busy_us"]).all()
+        assert (got[:, 1] == ut["cpu_busy_us"]).all()
+        assert ((got[:, 2] & 0xFFFFFFFF) == ut["gpu_batches"]).all()
+        assert ((got[:, 2] >> 32) == ut["cpu_tasks"]).all()
+        if offload:
+            assert (ut["cpu_tasks"] > 0).any()
+    # an empty trace reports zeros; a null array is an error
+    z = torch.zeros(1, dtype=torch.int64, device=DEV)
+    out = ctx.trace_utilization(z.view(torch.int16)[:1], z, z, np.array([0, 0]), d["profiles"][0])
+    assert (out.cpu().numpy() == 0).all()
+    with pytest.raises(rt.RtlmError):
+        ctx.trace_utilization(None, z, z, np.array([0, 1]), d["profiles"][0])

@@ -86,3 +86,87 @@ def test_trace_report_pins():
     assert rep["p95_resp_us"][0] == np.sort(resp)[9499]
     # 60 tasks in 2 minutes -> 30/min; zero completions -> 0
     assert throughput_per_min(60, 120_000_000) == 30.0 and throughput_per_min(0, 0) == 0.0
+
+
+def _small_traces(offload=True, consolidate=True):
+    """Config-3-shaped traces (4 LMs, Poisson ramp) scored by the oracle."""
+    import oracle
+    from rtgen import configs
+    lex = oracle.Lexicon(configs.read_lexicon())
+    d = configs.traces(3, range(7), 300, lambda t: t % 4)
+    for p in d["profiles"]:
+        p["offload"] = int(offload)
+        p["consolidate"] = int(consolidate)
+    n = len(d["arrival_us"])
+    f = oracle.rule_gen(lex, d["data"], d["offsets"])
+    u = np.zeros(n, np.float32)
+    k = np.zeros(n, np.uint64)
+    D = np.zeros(n, np.uint32)
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        p = d["profiles"][int(d["trace_prof"][t])]
+        u[lo:hi] = oracle.predict(f[lo:hi], d["regressors"][int(d["trace_prof"][t])])
+        k[lo:hi], D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], p, r_us=d["arrival_us"][lo:hi])
+    st, end, ut = oracle.simulate(d["arrival_us"], d["true_len"], u, k, D, d["trace_off"], d["profiles"],
+                                  d["trace_prof"], want_end=True, want_util=True)
+    return d, k, end, ut
+
+
+def test_utilization_pins_special_cases():
+    # S:405 "single serial batch occupying the whole makespan -> GPU fraction 1.0";
+    # S:406 "no CPU offloads -> CPU fraction 0.0"
+    import oracle
+    from oracle.offline import trace_report, utilization
+    from rtgen import configs
+    p = dict(configs.paper_lms()[0], offload=0, consolidate=1, policy=oracle.POLICY["UP"])
+    r = np.zeros(1, np.int64)
+    ln = np.array([40], np.uint16)
+    st, end, ut = oracle.simulate(r, ln, np.ones(1, np.float32), np.zeros(1, np.uint64), np.full(1, 10**9, np.uint32),
+                                  np.array([0, 1]), p, want_end=True, want_util=True)
+    dur = p["setup_us"] + p["base_us"] + p["eta_us"] * 40      # S:386-391 batch latency
+    assert end[0] == dur and ut["gpu_busy_us"][0] == dur and ut["gpu_batches"][0] == 1
+    rep = trace_report(r, end, np.array([0, 1]))
+    g, c = utilization(ut, rep["makespan_us"], p["cores"])
+    assert g[0] == 1.0 and c[0] == 0.0
+    d, k, end, ut = _small_traces(offload=False)
+    assert (ut["cpu_busy_us"] == 0).all() and (ut["cpu_tasks"] == 0).all()
+
+
+def test_utilization_matches_interval_union():
+    # S:407 "random workload -> fractions match an independent interval-union oracle":
+    # rebuild every executor interval from the per-task end times alone (a GPU
+    # batch = the GPU-class tasks sharing one end time, duration setup + base +
+    # eta * max len; a CPU task runs gamma * (base + eta * len) before its end),
+    # merge them, and compare with the event loop's accumulators.
+    from oracle.offline import trace_report, utilization
+    d, k, end, ut = _small_traces()
+    rep = trace_report(d["arrival_us"], end, d["trace_off"])
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        p = d["profiles"][int(d["trace_prof"][t])]
+        cls = (k[lo:hi] >> np.uint64(63)).astype(bool)
+        ln = d["true_len"][lo:hi].astype(np.int64)
+        e = end[lo:hi]
+        gpu = {}
+        for i in np.nonzero(~cls)[0]:
+            gpu.setdefault(int(e[i]), []).append(i)
+        iv = sorted((ee - (p["setup_us"] + p["base_us"] + p["eta_us"] * int(ln[b].max())), ee) for ee, b in gpu.items())
+        for (s0, e0), (s1, e1) in zip(iv, iv[1:]):
+            assert e0 <= s1                       # one GPU: batches never overlap
+        assert all(len(b) <= p["C"] for b in gpu.values())
+        union = sum(e1 - s0 for s0, e1 in iv)
+        assert ut["gpu_busy_us"][t] == union and ut["gpu_batches"][t] == len(gpu)
+        cpu = np.nonzero(cls)[0]
+        assert ut["cpu_tasks"][t] == len(cpu)
+        cdur = p["gamma"] * (p["base_us"] + p["eta_us"] * ln[cpu])
+        assert ut["cpu_busy_us"][t] == int(cdur.sum())
+        # per-core intervals do not overlap: at most `cores` CPU tasks at once
+        ev = sorted([(int(e[i] - c), 1) for i, c in zip(cpu, cdur)] + [(int(e[i]), -1) for i in cpu],
+                    key=lambda x: (x[0], x[1]))
+        live = 0
+        for _, dl in ev:
+            live += dl
+            assert live <= p["cores"]
+    g, c = utilization(ut, rep["makespan_us"], [d["profiles"][int(x)]["cores"] for x in d["trace_prof"]])
+    assert ((0 <= g) & (g <= 1)).all() and ((0 <= c) & (c <= 1)).all()
+    assert (ut["cpu_tasks"] > 0).any() and (ut["gpu_batches"] > 0).all()
