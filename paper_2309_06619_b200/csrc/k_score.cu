@@ -224,28 +224,6 @@ struct Rules {
     prev = T_OTHER;
   }
 
-  // add this thread's partial counters of one request into the tile accumulators
-  __device__ __forceinline__ void flush(uint32_t* acc9) {
-    const uint32_t v[9] = {S, Y, M, V, O, P, ntok, nd, nq};
-#pragma unroll
-    for (int i = 0; i < 9; ++i)
-      if (v[i]) atomicAdd(&acc9[i], v[i]);
-  }
-
-  // token record of the two-phase path: kind in bits 0..2, entry+1 in bits 3..15
-  __device__ __forceinline__ void on_record(uint32_t rec, const Lex& L) {
-    const uint32_t kind = rec & 7u;
-    if (kind == 1u) {
-      const uint32_t e = rec >> 3;
-      on_word(e ? L.e[e - 1].attr : 0u);
-    } else if (kind == 7u) {
-      ++nd;
-    } else if (kind != 0u) {
-      const uint32_t c = kind == 2u ? ',' : kind == 3u ? '.' : kind == 4u ? '?' : kind == 5u ? '!' : '#';
-      on_punct(c);
-    }
-  }
-
   // end of a W run: one clitic split (R-CLITIC), then word tokens
   __device__ __forceinline__ void end_run(const Lex& L) {
     const uint32_t n = wlen;
@@ -362,41 +340,43 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
 constexpr uint32_t kT4 = 1024;                // threads per CTA (32 warps)
 constexpr uint32_t kW4 = kT4 / 32;
 constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
-constexpr uint32_t kRing = 128;               // token ring per warp
+constexpr uint32_t kRing = 1024;              // token ring per warp
+constexpr int32_t kRound = 896;               // tokens buffered before a rule round (+ <= 64 per event batch)
 
 enum : uint32_t { K_W = 1, K_COMMA = 2, K_END = 3, K_Q = 4, K_OTH = 5 };
 
-struct Carry {
-  int32_t rs, end, word, fw, noun, fn, d, punct;
-  uint32_t fn_id, word_broad, punct_comma, punct_link;
-  uint32_t prev_req;  // request of the last token (0xFFFFFFFF: none)
+// Token in the ring (u16): bits 0..10 a code -- 0 a word outside the
+// lexicon, 1..1024 a word with lexicon entry code-1, kPunct + PK_* a
+// punctuation token -- and bits 11..15 the request within the warp task.
+// Smem4::attr maps a code to the entry's attributes (0 for punctuation and
+// for entries without flags or senses).
+enum : uint32_t { PK_COMMA = 1, PK_END = 2, PK_Q = 3, PK_OTH = 4 };
+constexpr uint32_t kPunct = 1024;
+constexpr uint32_t kNoReq = 0xFFFFFFFFu;
+
+// FSM context of the open sentence, carried from one rule round to the next
+struct FsmCtx {
+  uint32_t req, nf, so, sp, n2;  // request, first noun id, O-part state, P-part state, NOUN2
 };
 
 struct __align__(16) WarpBuf {
   uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
   uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
-  uint16_t ev[kChunk + 1];
-  uint8_t evq[kChunk + 1];             // request of each event
+  uint16_t ev[kChunk + 1];             // event: byte in chunk | request << 9 (0xFFFF: carried run)
   uint32_t rs[32];                     // request starts (absolute byte offsets)
-  uint32_t t_attr[kRing];
-  uint8_t t_meta[kRing];               // kind | req << 3
+  uint16_t ring[kRing];                // tokens (code | request << 11)
+  uint32_t ss[kRing / 32];             // sentence starts of a rule round (bit i: token tdone + i)
   uint32_t acc[32][9];                 // S Y M V O P ntok nd nq
-  Carry cy;                            // rule-scan carries between token batches (kept out of registers)
+  FsmCtx cx;
 };
 
 struct Smem4 {
-  uint32_t lut[256 * 32];              // class bits per byte, replicated per lane: W 0x1, P 0x100, X 0x10000
+  uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000
   uint32_t pref[128];
+  uint32_t fa[kPunct + 8];             // token code -> machine attributes (fsm_attr)
+  uint8_t tO[16 * 32], tP[128 * 4];    // O-part and P-part transition tables
   WarpBuf w[kW4];
 };
-
-__device__ __forceinline__ uint32_t lanemask_lt() { uint32_t m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
-__device__ __forceinline__ uint32_t lanemask_le() { uint32_t m; asm("mov.u32 %0, %%lanemask_le;" : "=r"(m)); return m; }
-
-// last position (global token index) among lanes whose bit is set in m, else carry
-__device__ __forceinline__ int32_t last_pos(uint32_t m, int32_t tb, int32_t carry) {
-  return m ? tb + 31 - (int32_t)__clz(m) : carry;
-}
 
 // request index of absolute byte position pos: last i < cnt with rs[i] <= pos
 __device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uint32_t pos) {
@@ -423,11 +403,11 @@ __device__ __forceinline__ uint32_t run_tokens(const Lex& L, const uint32_t* pre
   // the stem (or the whole run) on every lane, the clitic only where there is one:
   // a warp runs at most two lexicon lookups per run, whatever its lanes' mix
   const uint32_t e0 = word_idx(L, pref, n - cut, k0, k1, cut ? (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu) : t3);
-  attr0 = e0 ? L.e[e0 - 1].attr : 0u;
+  attr0 = e0;
   if (!cut) return 1;
   const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
   const uint32_t e1 = word_idx(L, pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu));
-  attr1 = e1 ? L.e[e1 - 1].attr : 0u;
+  attr1 = e1;
   return 2;
 }
 
@@ -462,140 +442,185 @@ __device__ __noinline__ void fsm_request(const ScoreLaunch& a, const Lex& L, uin
 }
 
 
-// rules over tokens [tb, tend) of the ring (tend - tb <= 32)
-__device__ __forceinline__ void rules_batch(WarpBuf& B, int32_t tb, int32_t tend, uint32_t lane) {
-  Carry cy = B.cy;
-  const int32_t T = tb + (int32_t)lane;
-  const bool valid = T < tend;
-  uint32_t meta = 0, attr = 0;
-  if (valid) { meta = B.t_meta[T & (kRing - 1)]; attr = B.t_attr[T & (kRing - 1)]; }
-  const uint32_t kind = meta & 7u, req = meta >> 3;
-  // three predecessors (same request only): shuffles within the batch, and a
-  // halo of the three tokens before it (lanes 0-2 load it once; 0xFF = none)
-  const int32_t hT = tb - 3 + (int32_t)lane;
-  uint32_t hm = 0xFFu, ha = 0;
-  if (lane < 3 && hT >= 0) { hm = B.t_meta[hT & (kRing - 1)]; ha = B.t_attr[hT & (kRing - 1)]; }
-  uint32_t pk[4], pa[4];
-#pragma unroll
-  for (int k = 1; k <= 3; ++k) {
-    const uint32_t mu = __shfl_up_sync(0xFFFFFFFFu, meta, k), au = __shfl_up_sync(0xFFFFFFFFu, attr, k);
-    const uint32_t src = (lane + 3u - (uint32_t)k) & 31u;  // halo lane for lanes < k
-    const uint32_t mh = __shfl_sync(0xFFFFFFFFu, hm, src), ah = __shfl_sync(0xFFFFFFFFu, ha, src);
-    const bool in_batch = lane >= (uint32_t)k;
-    const uint32_t m = in_batch ? mu : mh, at = in_batch ? au : ah;
-    const bool same = valid && (m >> 3) == req && m != 0xFFu;
-    pk[k] = same ? (m & 7u) : 0u;
-    pa[k] = same ? at : 0u;
+// ---- R-RULES as a per-lane finite-state machine over the ring's tokens (O2
+// in the sequential form of Rules::on_word / on_punct).  The machine's
+// context is the same as at a request start at every sentence start (the
+// token after . ! ?, or a request's first token), so a rule round cuts its
+// tokens [tdone, tavail) into 32 runs of whole sentences of about equal length
+// (boundaries at the sentence starts nearest to lane*avail/32); lane 0
+// continues the open sentence of the previous round (carried context B.cx),
+// and the lane that reaches tavail carries its context on.  Counters go to
+// the per-request accumulators at request changes and at the end of a run.
+//
+// The machine is three independent parts (each rule reads only its own
+// part's context):
+//  * O-part (open-endedness): context SWORD (a word seen in the sentence),
+//    BROAD (last word BROAD), wcd (what-countdown 0..3) -> 16 states; token
+//    class: word with flags {OPENER, WHAT, CAUSE, BROAD} (0..15), '?' (16),
+//    '.' '!' (17), other punctuation (18).  Table Smem4::tO[state*32+class] =
+//    next state | O increment << 4.
+//  * P-part (multi-part): context PW, PC, P2W (previous two token kinds),
+//    CPEND (coordinator after a word), WSC (word since the last comma), chain
+//    (0..2) -> 7 bits; token class: word (0), COORD word (1), comma (2), other
+//    punctuation (3).  Table Smem4::tP[state*4+class] = next | P inc << 7.
+//  * S-part (structural): first noun id of the sentence and NOUN2 (a second
+//    distinct noun seen), in registers.
+// Token attributes for the machine (Smem4::fa, by token code):
+//   bit 0 VAGUE, bits 1..10 entry id, bit 11 MULTIPOS, bit 22 '?'   (V, Y, q: packed-count fields)
+//   bits 12..16 O-class, bits 17..18 P-class, bit 19 PREP, bit 20 NOUN, bit 21 END (. ! ?)
+//   bits 24..31 senses - 1
+enum : uint32_t { FA_VAGUE = 1u << 0, FA_MULTI = 1u << 11, FA_Q = 1u << 22, FA_PREP = 1u << 19,
+                  FA_NOUN = 1u << 20, FA_END = 1u << 21 };
+enum : uint32_t { OC_Q = 16, OC_END = 17, OC_PUNCT = 18 };
+enum : uint32_t { PC_WORD = 0, PC_COORD = 1, PC_COMMA = 2, PC_PUNCT = 3 };
+constexpr uint32_t kNoNoun10 = 0xFFFFu;
+
+__host__ __device__ __forceinline__ uint32_t fsm_attr(uint32_t code, uint32_t at) {
+  if (code > kPunct) {
+    const uint32_t pk = code - kPunct;
+    if (pk == PK_COMMA) return (OC_PUNCT << 12) | (PC_COMMA << 17);
+    if (pk == PK_END) return (OC_END << 12) | (PC_PUNCT << 17) | FA_END;
+    if (pk == PK_Q) return (OC_Q << 12) | (PC_PUNCT << 17) | FA_END | FA_Q;
+    return (OC_PUNCT << 12) | (PC_PUNCT << 17);
   }
-  const bool isW = valid && kind == K_W, isComma = valid && kind == K_COMMA;
-  const bool isQ = valid && kind == K_Q, isEnd = valid && (kind == K_END || kind == K_Q);
-  const bool isP = valid && kind >= K_COMMA;
-  const uint32_t prev_req_lane = __shfl_up_sync(0xFFFFFFFFu, req, 1);
-  const bool isRS = valid && (lane == 0 ? req != cy.prev_req : req != prev_req_lane);
-  const uint32_t lt = lanemask_lt(), le = lanemask_le();
-  const int32_t rstart = last_pos(__ballot_sync(0xFFFFFFFFu, isRS) & le, tb, cy.rs);
-  const uint32_t b_end = __ballot_sync(0xFFFFFFFFu, isEnd);
-  const int32_t lend = last_pos(b_end & lt, tb, cy.end);
-  const int32_t sst = max(lend + 1, rstart);  // sentence start
-  const uint32_t b_w = __ballot_sync(0xFFFFFFFFu, isW);
-  const int32_t lword = last_pos(b_w & lt, tb, cy.word);
-  const bool firstW = isW && lword < sst;
-  const uint32_t b_fw = __ballot_sync(0xFFFFFFFFu, firstW);
-  const int32_t f = last_pos(b_fw & le, tb, cy.fw);
-  const bool isN = isW && (attr & A_NOUN);
-  const uint32_t nid = attr >> A_ID_SHIFT;
-  const uint32_t b_n = __ballot_sync(0xFFFFFFFFu, isN);
-  const int32_t lnoun = last_pos(b_n & lt, tb, cy.noun);
-  const bool firstN = isN && lnoun < sst;
-  const uint32_t b_fn = __ballot_sync(0xFFFFFFFFu, firstN);
-  const int32_t fn = last_pos(b_fn & le, tb, cy.fn);
-  const uint32_t fn_id_l = __shfl_sync(0xFFFFFFFFu, nid, (uint32_t)max(fn - tb, 0) & 31u);
-  const uint32_t fn_id = fn >= tb ? fn_id_l : cy.fn_id;
-  const bool isD = isN && fn >= sst && nid != fn_id;
-  const uint32_t b_d = __ballot_sync(0xFFFFFFFFu, isD);
-  const int32_t ld = last_pos(b_d & lt, tb, cy.d);
-  // structural: PREP after a second distinct noun of the sentence
-  const uint32_t cS = (isW && (attr & A_PREP) && ld >= sst) ? 1u : 0u;
-  // open-endedness
-  uint32_t cO = (firstW && (attr & A_OPENER)) ? 1u : 0u;
-  if (isW && !firstW && f >= sst && (attr & A_CAUSE)) {
-    const int32_t dd = T - f;
-    if (dd >= 1 && dd <= 3) {
-      const uint32_t af = pa[dd == 1 ? 1 : dd == 2 ? 2 : 3];
-      bool earlier = false;  // a CAUSE word between f and T
-      if (dd >= 2 && pk[1] == K_W && (pa[1] & A_CAUSE)) earlier = true;
-      if (dd >= 3 && pk[2] == K_W && (pa[2] & A_CAUSE)) earlier = true;
-      if ((af & A_WHAT) && !earlier) cO = 1u;
+  if (code == 0u) return (0u << 12) | (PC_WORD << 17);
+  uint32_t f = 0;
+  f |= (at & A_VAGUE) ? FA_VAGUE : 0u;
+  f |= (at & A_MULTIPOS) ? FA_MULTI : 0u;
+  f |= (at & A_PREP) ? FA_PREP : 0u;
+  f |= (at & A_NOUN) ? FA_NOUN : 0u;
+  const uint32_t oc = ((at & A_OPENER) ? 1u : 0u) | ((at & A_WHAT) ? 2u : 0u) | ((at & A_CAUSE) ? 4u : 0u) |
+                      ((at & A_BROAD) ? 8u : 0u);
+  f |= oc << 12;
+  f |= ((at & A_COORD) ? PC_COORD : PC_WORD) << 17;
+  f |= ((at >> A_ID_SHIFT) & 0x3FFu) << 1;
+  f |= ((at >> A_SEM_SHIFT) & A_SEM_MASK) << 24;
+  return f;
+}
+
+// O-part transition (Rules::on_word / on_punct restricted to SENT_WORD, LAST_BROAD, what_cd)
+__host__ __device__ __forceinline__ uint32_t o_step(uint32_t st, uint32_t cls) {
+  const uint32_t sword = st & 1u, broad = (st >> 1) & 1u, wcd = st >> 2;
+  if (cls < 16u) {  // word
+    const bool first = !sword, cause = sword && wcd && (cls & 4u);
+    const uint32_t inc = ((first && (cls & 1u)) || cause) ? 1u : 0u;
+    const uint32_t w2 = first ? ((cls & 2u) ? 3u : 0u) : ((cause || !wcd) ? 0u : wcd - 1u);
+    return 1u | (((cls >> 3) & 1u) << 1) | (w2 << 2) | (inc << 4);
+  }
+  if (cls == OC_Q) return ((sword && broad) ? 1u : 0u) << 4;  // broad-scope interrogative; sentence ends
+  if (cls == OC_END) return 0u;
+  return sword | (broad << 1) | ((wcd ? wcd - 1u : 0u) << 2);
+}
+
+// P-part transition: bits 0 PW, 1 PC, 2 P2W, 3 CPEND, 4 WSC, 5..6 chain
+__host__ __device__ __forceinline__ uint32_t p_step(uint32_t st, uint32_t cls) {
+  const uint32_t pw = st & 1u, pc = (st >> 1) & 1u, p2w = (st >> 2) & 1u, cp = (st >> 3) & 1u, wsc = (st >> 4) & 1u,
+                 ch = (st >> 5) & 3u;
+  if (cls == PC_WORD || cls == PC_COORD) {
+    const uint32_t cp2 = (cls == PC_COORD && (pw || (pc && p2w))) ? 1u : 0u;
+    return 1u | (pw << 2) | (cp2 << 3) | (1u << 4) | (ch << 5) | (cp << 7);
+  }
+  if (cls == PC_COMMA) {
+    const uint32_t inc = (ch == 1u && wsc) ? 1u : 0u;
+    const uint32_t ch2 = (ch && wsc) ? 2u : 1u;
+    return (1u << 1) | (pw << 2) | (ch2 << 5) | (inc << 7);
+  }
+  return (pw << 2) | (wsc << 4);
+}
+
+__device__ __forceinline__ bool tok_is_end(uint32_t t) {  // . ! or ?
+  return ((t & 0x7FFu) - (kPunct + PK_END)) < 2u;
+}
+
+// packed counts of one request within one run (<= 959 tokens): c1 = V | Y << 11 | q << 22,
+// c2 = S | O << 11 | P << 22, M, and ntok = tokens since the run / request start
+__device__ __forceinline__ void flush_counts(uint32_t* a, uint32_t c1, uint32_t c2, uint32_t M, uint32_t n) {
+  atomicAdd(&a[0], c2 & 0x7FFu);
+  atomicAdd(&a[1], (c1 >> 11) & 0x7FFu);
+  const uint32_t old = atomicAdd(&a[2], M);     // M < 2^18 per run
+  if (old + M >= 0x40000000u) atomicMin(&a[2], 0x40000000u);  // stays < 2^31; saturates to 65535 later
+  atomicAdd(&a[3], c1 & 0x7FFu);
+  atomicAdd(&a[4], (c2 >> 11) & 0x7FFu);
+  atomicAdd(&a[5], c2 >> 22);
+  atomicAdd(&a[6], n);
+  atomicAdd(&a[8], c1 >> 22);
+}
+
+__device__ __forceinline__ void rules_round(WarpBuf& B, const uint32_t* fa_of, const uint8_t* tO, const uint8_t* tP,
+                                            int32_t tdone, int32_t tavail, uint32_t lane) {
+  const int32_t avail = tavail - tdone;
+  if (avail <= 0) return;
+  // sentence starts of the round as a bit mask
+  const int32_t nw = (avail + 31) >> 5;
+  for (int32_t j = 0; j < nw; ++j) {
+    const int32_t T = tdone + j * 32 + (int32_t)lane;
+    bool st = false;
+    if (T < tavail) {
+      if (T == 0) {
+        st = true;
+      } else {
+        const uint32_t t = B.ring[T & (kRing - 1)], pv = B.ring[(T - 1) & (kRing - 1)];
+        st = ((t ^ pv) >> 11) != 0u || tok_is_end(pv);
+      }
     }
+    const uint32_t b = __ballot_sync(0xFFFFFFFFu, st);
+    if (lane == 0) B.ss[j] = b;
   }
-  const uint32_t broad_l = __shfl_sync(0xFFFFFFFFu, (attr & A_BROAD) ? 1u : 0u, (uint32_t)max(lword - tb, 0) & 31u);
-  const uint32_t lw_broad = lword >= tb ? broad_l : cy.word_broad;
-  if (isQ && lword >= sst && lw_broad) cO += 1u;
-  // content spans: coordinator between words (counted at the word after it)
-  uint32_t cP = 0;
-  // (non-short-circuit: no branches)
-  cP = (uint32_t)(isW & (pk[1] == K_W) & ((pa[1] & A_COORD) != 0u) & ((pk[2] == K_W) | ((pk[2] == K_COMMA) & (pk[3] == K_W))));
-  // comma chains: link = previous punctuation is a comma with >= 1 word between
-  const uint32_t b_p = __ballot_sync(0xFFFFFFFFu, isP);
-  const int32_t lp = last_pos(b_p & lt, tb, cy.punct);
-  const uint32_t lpl = (uint32_t)max(lp - tb, 0) & 31u;
-  const uint32_t lp_comma_l = __shfl_sync(0xFFFFFFFFu, isComma ? 1u : 0u, lpl);
-  const uint32_t lp_comma = lp >= tb ? lp_comma_l : cy.punct_comma;
-  const bool link = isComma && lp >= rstart && lp_comma && lp <= T - 2;
-  const uint32_t lp_link_l = __shfl_sync(0xFFFFFFFFu, link ? 1u : 0u, lpl);
-  const uint32_t lp_link = lp >= tb ? lp_link_l : cy.punct_link;
-  if (link && !lp_link) cP += 1u;
-  // per-request sums (requests are contiguous, increasing runs of lanes): the
-  // 0/1 counters by popcounts of ballots over the run, the senses count M by a
-  // segmented scan; the run's last lane adds them to the request's accumulators
-  const uint32_t b_V = __ballot_sync(0xFFFFFFFFu, isW && (attr & A_VAGUE));
-  const uint32_t b_Y = __ballot_sync(0xFFFFFFFFu, isW && ((attr >> 8) & 1u));
-  const uint32_t b_S = __ballot_sync(0xFFFFFFFFu, cS != 0u), b_O = __ballot_sync(0xFFFFFFFFu, cO != 0u);
-  const uint32_t b_P = __ballot_sync(0xFFFFFFFFu, cP != 0u), b_Q = __ballot_sync(0xFFFFFFFFu, isQ);
-  const uint32_t b_head = __ballot_sync(0xFFFFFFFFu, valid && (lane == 0 || req != prev_req_lane));
-  const int32_t head = 31 - (int32_t)__clz(b_head & le);
-  uint32_t msum = isW ? (attr >> A_SEM_SHIFT) & A_SEM_MASK : 0u;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, msum, o);
-    if ((int32_t)lane - o >= head) msum += up;
+  __syncwarp();
+  // this lane's run [s, e): from the sentence start nearest to lane*avail/32
+  int32_t s = 0;
+  if (lane) {
+    const int32_t nom = (int32_t)(((uint32_t)avail * lane) >> 5);
+    int32_t w = nom >> 5;
+    uint32_t m = B.ss[w] & (0xFFFFFFFFu << (nom & 31));
+    while (!m && ++w < nw) m = B.ss[w];
+    const int32_t up = m ? w * 32 + (int32_t)__ffs(m) - 1 : avail;      // first start >= nom
+    w = nom >> 5;
+    m = B.ss[w] & (0xFFFFFFFFu >> (31 - (nom & 31)));
+    while (!m && --w >= 0) m = B.ss[w];
+    const int32_t dn = m ? w * 32 + 31 - (int32_t)__clz(m) : -1;      // last start <= nom
+    s = (dn >= 0 && nom - dn < up - nom) ? dn : up;
   }
-  const uint32_t next_req = __shfl_down_sync(0xFFFFFFFFu, req, 1);
-  const bool next_valid = __shfl_down_sync(0xFFFFFFFFu, valid ? 1u : 0u, 1) != 0u;
-  if (valid && (lane == 31 || !next_valid || next_req != req)) {
-    const uint32_t seg = le & ~((1u << head) - 1u);  // lanes head..lane
-    uint32_t* a = B.acc[req];
-    a[6] += __popc(seg);
-    a[3] += __popc(b_V & seg);
-    a[1] += __popc(b_Y & seg);
-    a[0] += __popc(b_S & seg);
-    a[4] += __popc(b_O & seg);
-    a[5] += __popc(b_P & seg);
-    a[8] += __popc(b_Q & seg);
-    a[2] = min(a[2] + msum, 0xFFFFFFu);
-  }
-  // carries for the next batch
-  const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
-  if (vm) {
-    const int32_t lastT = tb + 31 - (int32_t)__clz(vm);
-    cy.prev_req = __shfl_sync(0xFFFFFFFFu, req, (uint32_t)(lastT - tb));
-    cy.rs = last_pos(__ballot_sync(0xFFFFFFFFu, isRS), tb, cy.rs);
-    cy.end = last_pos(b_end, tb, cy.end);
-    if (b_w) cy.word_broad = __shfl_sync(0xFFFFFFFFu, (attr & A_BROAD) ? 1u : 0u, 31 - __clz(b_w));
-    cy.word = last_pos(b_w, tb, cy.word);
-    cy.fw = last_pos(b_fw, tb, cy.fw);
-    cy.noun = last_pos(b_n, tb, cy.noun);
-    if (b_fn) cy.fn_id = __shfl_sync(0xFFFFFFFFu, nid, 31 - __clz(b_fn));
-    cy.fn = last_pos(b_fn, tb, cy.fn);
-    cy.d = last_pos(b_d, tb, cy.d);
-    if (b_p) {
-      const uint32_t L = 31 - __clz(b_p);
-      cy.punct_comma = __shfl_sync(0xFFFFFFFFu, isComma ? 1u : 0u, L);
-      cy.punct_link = __shfl_sync(0xFFFFFFFFu, link ? 1u : 0u, L);
+  int32_t e = __shfl_down_sync(0xFFFFFFFFu, s, 1);
+  if (lane == 31) e = avail;
+  FsmCtx c;
+  if (lane == 0) c = B.cx;
+  else c = FsmCtx{kNoReq, kNoNoun10, 0u, 0u, 0u};
+  uint32_t c1 = 0, c2 = 0, M = 0;
+  int32_t i0 = s;  // first token of the current request in this run
+  for (int32_t i = s; i < e; ++i) {
+    const uint32_t t = B.ring[(tdone + i) & (kRing - 1)];
+    const uint32_t r = t >> 11;
+    if (r != c.req) {  // request start: flush, fresh context
+      if (c.req != kNoReq) flush_counts(B.acc[c.req], c1, c2, M, (uint32_t)(i - i0));
+      c1 = c2 = M = 0;
+      i0 = i;
+      c = FsmCtx{r, kNoNoun10, 0u, 0u, 0u};
     }
-    cy.punct = last_pos(b_p, tb, cy.punct);
+    const uint32_t a = fa_of[t & 0x7FFu];
+    c1 += a & (FA_VAGUE | FA_MULTI | FA_Q);
+    M += a >> 24;
+    const uint32_t vo = tO[(c.so << 5) | ((a >> 12) & 31u)];
+    const uint32_t vp = tP[(c.sp << 2) | ((a >> 17) & 3u)];
+    c.so = vo & 15u;
+    c.sp = vp & 127u;
+    // S-part: PREP after a second distinct noun of the sentence (PREP tested first)
+    const uint32_t sinc = (a >> 19) & c.n2;
+    if (a & FA_NOUN) {
+      const uint32_t id = (a >> 1) & 0x3FFu;
+      if (c.nf == kNoNoun10) c.nf = id;
+      else c.n2 |= (id != c.nf) ? 1u : 0u;
+    }
+    if (a & FA_END) {
+      c.nf = kNoNoun10;
+      c.n2 = 0u;
+    }
+    c2 += sinc | ((vo >> 4) << 11) | ((vp >> 7) << 22);
   }
-  if (lane == 0) B.cy = cy;
+  if (s < e) {
+    flush_counts(B.acc[c.req], c1, c2, M, (uint32_t)(e - i0));
+    if (e == avail) B.cx = c;
+  }
   __syncwarp();
 }
 
@@ -614,11 +639,16 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     for (uint32_t i = tid; i < ent_bytes / 4; i += kT4) dst[i] = src[i];
     for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
     for (uint32_t i = tid; i < 128; i += kT4) S.pref[i] = 0;
-    for (uint32_t i = tid; i < 256 * 32; i += kT4) S.lut[i] = class_bits(i >> 5);
+    for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i);
+    for (uint32_t i = tid; i < kPunct + 8; i += kT4)
+      S.fa[i] = fsm_attr(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
+    for (uint32_t i = tid; i < 16 * 32; i += kT4) S.tO[i] = (uint8_t)o_step(i >> 5, i & 31u);
+    for (uint32_t i = tid; i < 128 * 4; i += kT4) S.tP[i] = (uint8_t)p_step(i >> 2, i & 3u);
   }
   __syncthreads();
   for (uint32_t i = tid; i < a.lex.n_entries; i += kT4) {
     const LexEntry e = a.lex.entries[i];
+
     const uint32_t pi = pref_idx((uint32_t)(e.k0 & 0xFFu), e.len >= 2 ? (uint32_t)((e.k0 >> 8) & 0xFFu) : 0u);
     atomicOr(&S.pref[pi >> 5], 1u << (pi & 31u));
   }
@@ -657,7 +687,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     B.rs[lane] = s_r;
 #pragma unroll
     for (int k = 0; k < 9; ++k) B.acc[lane][k] = 0;
-    if (lane == 0) B.cy = Carry{-1, -1, -1, -1, -1, -1, -1, -1, 0u, 0u, 0u, 0u, 0xFFFFFFFFu};
+    if (lane == 0) B.cx = FsmCtx{kNoReq, kNoNoun10, 0u, 0u, 0u};
     int32_t tokbase = 0;
     uint32_t prevW = 0;                 // W bit of the byte before the chunk
     int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
@@ -691,7 +721,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t byte = (wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu;
-            const uint32_t c = S.lut[byte * 32u + lane] << i;
+            const uint32_t c = S.lut[byte] << i;
             if (j == 0) accA += c; else accB += c;
           }
       }
@@ -750,8 +780,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
           while (e) {
             const uint32_t bit = __ffs(e) - 1;
             e &= e - 1u;
-            B.ev[k] = (uint16_t)(lane * 16u + bit);
-            B.evq[k++] = (uint8_t)(rq0 + __popc(mk16 & ((2u << bit) - 1u)));
+            B.ev[k++] = (uint16_t)((lane * 16u + bit) | ((rq0 + __popc(mk16 & ((2u << bit) - 1u))) << 9));
           }
         } else {
           uint32_t rq = req_of(B.rs, rcnt, g);  // request at this lane's first byte, advanced per event
@@ -759,8 +788,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
             const uint32_t bit = __ffs(e) - 1;
             e &= e - 1u;
             while (rq + 1 < rcnt && B.rs[rq + 1] <= g + bit) ++rq;
-            B.ev[k] = (uint16_t)(lane * 16u + bit);
-            B.evq[k++] = (uint8_t)rq;
+            B.ev[k++] = (uint16_t)((lane * 16u + bit) | (rq << 9));
           }
         }
       }
@@ -772,10 +800,10 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         const uint32_t k = e0 + lane;
         uint32_t ntk = 0, at0 = 0, at1 = 0, kind = K_W, rq = 0;
         if (k < nev) {
-          const uint32_t p = B.ev[k];
+          const uint32_t pe = B.ev[k];
           uint32_t x = 0, n = 0;
           bool isrun = false;
-          if (p == 0xFFFFu) {
+          if (pe == 0xFFFFu) {
             // carried run: [pend_start, stop) with stop the first non-word byte or request start here
             const uint32_t ps = (uint32_t)pend_start;
             uint32_t stop = 0;
@@ -798,8 +826,9 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               n = 24;
             }
           } else {
+            const uint32_t p = pe & 511u;
             const uint32_t c = st8[16 + kChunk + p];
-            rq = B.evq[k];
+            rq = pe >> 9;
             if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
               // run length: up to the first non-word byte or request start
               uint32_t qq = p + 1;
@@ -829,19 +858,16 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         const uint32_t nt = __shfl_sync(0xFFFFFFFFu, ti, 31);
         if (ntk) {
           const uint32_t t0 = (uint32_t)tokbase + ti - ntk;
-          B.t_meta[t0 & (kRing - 1)] = (uint8_t)(kind | (rq << 3));
-          B.t_attr[t0 & (kRing - 1)] = at0;
-          if (ntk == 2) {
-            B.t_meta[(t0 + 1) & (kRing - 1)] = (uint8_t)(K_W | (rq << 3));
-            B.t_attr[(t0 + 1) & (kRing - 1)] = at1;
-          }
+          B.ring[t0 & (kRing - 1)] = (uint16_t)((kind == K_W ? at0 : kPunct + kind - 1u) | (rq << 11));
+          if (ntk == 2) B.ring[(t0 + 1) & (kRing - 1)] = (uint16_t)(at1 | (rq << 11));
         }
         __syncwarp();
         tokbase += (int32_t)nt;
-        // full 32-token batches; everything after the last event of the task
-        const int32_t lim = (last_chunk && e0 + 32 >= nev) ? tokbase : tokbase - 31;
-        for (; tokdone < lim; tokdone += 32) rules_batch(B, tokdone, min(tokdone + 32, tokbase), lane);
-        __syncwarp();
+        // a rule round every kRound tokens, and after the last event of the task
+        if ((last_chunk && e0 + 32 >= nev) || tokbase - tokdone >= kRound) {
+          rules_round(B, S.fa, S.tO, S.tP, tokdone, tokbase, lane);
+          tokdone = tokbase;
+        }
       }
       // dropped bytes (rare): count per request
       if (__any_sync(0xFFFFFFFFu, X16 != 0u)) {
