@@ -14,8 +14,9 @@ struct rt_ctx {
   int device = 0;
   int num_sms = 148;
   rtlm::LexEntry* d_entries = nullptr;
+  uint4* d_keys = nullptr;
   uint16_t* d_slots = nullptr;
-  uint32_t n_entries = 0, bits = 0;
+  uint32_t n_entries = 0, bits = 0, seed = 0;
   uint32_t* d_flags = nullptr;
   void* ws = nullptr;
   size_t ws_size = 0;
@@ -234,13 +235,15 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
   uint32_t bits = 6;
   while ((1u << bits) < 4 * n) ++bits;  // load factor <= 1/4
   std::vector<LexEntry> ent(n);
-  std::vector<uint16_t> slots(1u << bits, 0);
+  std::vector<uint4> keys(n + 1, uint4{0, 0, 0, 0});
   for (uint32_t k = 0; k < n; ++k) {
     LexEntry e{};
+    uint32_t w[4] = {0, 0, 0, 0};
     for (size_t b = 0; b < lemmas[k].size(); ++b) {
       uint64_t byte = (unsigned char)lemmas[k][b];
       if (b < 8) e.k0 |= byte << (8 * b);
       else e.k1 |= byte << (8 * (b - 8));
+      w[b >> 2] |= (uint32_t)byte << (8 * (b & 3));
     }
     e.len = (uint32_t)lemmas[k].size();
     const HostLemma& h = attrs[k];
@@ -251,20 +254,50 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
     a |= h.id << rtlm::A_ID_SHIFT;
     e.attr = a;
     ent[k] = e;
-    uint32_t hs = rtlm::lex_hash(e.k0, e.k1, e.len, bits);
-    while (slots[hs]) hs = (hs + 1) & ((1u << bits) - 1);
-    slots[hs] = (uint16_t)(k + 1);
+    keys[k + 1] = uint4{w[0], w[1], w[2], w[3]};
+  }
+  // cuckoo placement (two slots per key); a new seed if an insertion cycles
+  std::vector<uint16_t> slots;
+  uint32_t seed = 0;
+  for (;; ++seed) {
+    slots.assign(1u << bits, 0);
+    bool ok = true;
+    for (uint32_t k = 0; k < n && ok; ++k) {
+      uint32_t cur = k + 1;
+      bool placed = false;
+      for (int kick = 0; kick < 512 && !placed; ++kick) {
+        const uint4& q = keys[cur];
+        const uint32_t x = rtlm::lex_mix(q.x, q.y, q.z, q.w, seed);
+        const uint32_t s1 = rtlm::lex_slot1(x, bits), s2 = rtlm::lex_slot2(x, bits);
+        if (!slots[s1]) { slots[s1] = (uint16_t)cur; placed = true; }
+        else if (!slots[s2]) { slots[s2] = (uint16_t)cur; placed = true; }
+        else {  // evict the occupant of the slot that is not where we came from
+          const uint32_t s = (kick & 1) ? s2 : s1;
+          const uint32_t ev = slots[s];
+          slots[s] = (uint16_t)cur;
+          cur = ev;
+        }
+      }
+      ok = placed;
+    }
+    if (ok) break;
+    if (seed > 1000) return fail(c, RT_ELEXICON, "lexicon hash table could not be built");
   }
   c->n_entries = n;
   c->bits = bits;
+  c->seed = seed;
   RT_CUDA(c, cudaMalloc(&c->d_entries, std::max<size_t>(1, n) * sizeof(LexEntry)));
+  RT_CUDA(c, cudaMalloc(&c->d_keys, keys.size() * sizeof(uint4)));
   RT_CUDA(c, cudaMalloc(&c->d_slots, slots.size() * sizeof(uint16_t)));
   if (n) RT_CUDA(c, cudaMemcpy(c->d_entries, ent.data(), n * sizeof(LexEntry), cudaMemcpyHostToDevice));
+  RT_CUDA(c, cudaMemcpy(c->d_keys, keys.data(), keys.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   RT_CUDA(c, cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
   return RT_OK;
 }
 
-rtlm::DevLexicon dev_lex(const rt_ctx* c) { return rtlm::DevLexicon{c->d_entries, c->d_slots, c->n_entries, c->bits}; }
+rtlm::DevLexicon dev_lex(const rt_ctx* c) {
+  return rtlm::DevLexicon{c->d_entries, c->d_keys, c->d_slots, c->n_entries, c->bits, c->seed};
+}
 
 rt_status ensure_ws(rt_ctx* c, size_t bytes) {
   if (bytes <= c->ws_size) return RT_OK;
@@ -342,6 +375,7 @@ rt_status rt_destroy(rt_ctx* c) {
   {
     DeviceGuard g(c->device);
     cudaFree(c->d_entries);
+    cudaFree(c->d_keys);
     cudaFree(c->d_slots);
     cudaFree(c->d_flags);
     cudaFree(c->ws);

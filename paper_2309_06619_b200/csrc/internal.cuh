@@ -34,21 +34,23 @@ struct LexEntry {
 };
 
 struct DevLexicon {
-  const LexEntry* entries;  // n_entries
-  const uint16_t* slots;    // 1 << bits; 0 = empty, else entry index + 1
+  const LexEntry* entries;  // n_entries (global; attributes)
+  const uint4* keys;        // n_entries + 1: keys[0] = 0, keys[i] = zero-padded lemma of entry i - 1
+  const uint16_t* slots;    // 1 << bits; 0 = empty, else entry index + 1 (a key sits at one of its two slots)
   uint32_t n_entries;
   uint32_t bits;
+  uint32_t seed;
 };
 
-__host__ __device__ __forceinline__ uint32_t lex_hash(uint64_t k0, uint64_t k1, uint32_t len, uint32_t bits) {
-  // 32-bit multiply-xor hash of the (<= 16-byte) key (bits >= 6)
-  uint32_t h = (uint32_t)k0 * 0x9E3779B1u;
-  h ^= ((uint32_t)(k0 >> 32) + len) * 0x85EBCA77u;
-  h ^= ((uint32_t)k1 ^ (uint32_t)(k1 >> 32)) * 0xC2B2AE3Du;
-  h ^= h >> 15;
-  h *= 0x2C1B3C6Du;
-  return h >> (32 - bits);
+// Two-choice (cuckoo) hashing of a zero-padded <= 16-byte lemma (four
+// little-endian words): a lemma sits at slot lex_slot1 or lex_slot2 (bits >= 6).
+__host__ __device__ __forceinline__ uint32_t lex_mix(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                                     uint32_t seed) {
+  uint32_t x = (w0 * 0x9E3779B1u) ^ (w1 * 0x85EBCA77u) ^ (w2 * 0xC2B2AE3Du) ^ (w3 * 0x27D4EB2Fu) ^ seed;
+  return x ^ (x >> 15);
 }
+__host__ __device__ __forceinline__ uint32_t lex_slot1(uint32_t x, uint32_t bits) { return (x * 0x2C1B3C6Du) >> (32 - bits); }
+__host__ __device__ __forceinline__ uint32_t lex_slot2(uint32_t x, uint32_t bits) { return (x * 0x297A2D39u) >> (32 - bits); }
 
 // ---------------------------------------------------------------- keys
 __host__ __device__ __forceinline__ uint32_t ord32_bits(uint32_t b) {

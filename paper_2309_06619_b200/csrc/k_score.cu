@@ -68,39 +68,31 @@ __device__ __forceinline__ uint64_t priority_key(float u, uint32_t D_us, int64_t
 }
 
 // ------------------------------------------------------------ lexicon probe
+// Two-choice hashing (DevLexicon): a lemma is at one of its two slots; keys
+// are zero-padded 16-byte words (lemma bytes are never 0, so the padding
+// encodes the length), keys[0] = 0 so an empty slot never matches a lemma.
 struct Lex {
-  const LexEntry* e;
-  const uint16_t* slots;
-  uint32_t bits;
+  const uint4* keys;        // shared memory
+  const uint16_t* slots;    // shared memory
+  const LexEntry* e;        // global (attributes, byte-FSM path only)
+  uint32_t bits, seed;
 };
 
+// token code (entry index + 1, 0 = not in the lexicon) of a zero-padded lemma
+__device__ __forceinline__ uint32_t lookup(const Lex& L, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+  const uint32_t x = lex_mix(w0, w1, w2, w3, L.seed);
+  const uint32_t s1 = L.slots[lex_slot1(x, L.bits)], s2 = L.slots[lex_slot2(x, L.bits)];
+  const uint4 k1 = L.keys[s1], k2 = L.keys[s2];
+  const bool m1 = ((k1.x ^ w0) | (k1.y ^ w1) | (k1.z ^ w2) | (k1.w ^ w3)) == 0u;
+  const bool m2 = ((k2.x ^ w0) | (k2.y ^ w1) | (k2.z ^ w2) | (k2.w ^ w3)) == 0u;
+  return m1 ? s1 : (m2 ? s2 : 0u);
+}
+
 __device__ __forceinline__ uint32_t probe(const Lex& L, uint64_t k0, uint64_t k1, uint32_t len) {
-  const uint32_t mask = (1u << L.bits) - 1u;
-  uint32_t h = lex_hash(k0, k1, len, L.bits);
-  for (;;) {
-    uint32_t s = L.slots[h];
-    if (!s) return 0;
-    const LexEntry& e = L.e[s - 1];
-    if (e.k0 == k0 && e.k1 == k1 && e.len == len) return e.attr;
-    h = (h + 1u) & mask;
-  }
+  (void)len;  // zero padding encodes the length
+  const uint32_t c = lookup(L, (uint32_t)k0, (uint32_t)(k0 >> 32), (uint32_t)k1, (uint32_t)(k1 >> 32));
+  return c ? L.e[c - 1].attr : 0u;
 }
-
-// entry index + 1 of a lemma (0 = not in the lexicon)
-__device__ __forceinline__ uint32_t probe_idx(const Lex& L, uint64_t k0, uint64_t k1, uint32_t len) {
-  const uint32_t mask = (1u << L.bits) - 1u;
-  uint32_t h = lex_hash(k0, k1, len, L.bits);
-  for (;;) {
-    const uint32_t s = L.slots[h];
-    if (!s) return 0;
-    const LexEntry& e = L.e[s - 1];
-    if (e.k0 == k0 && e.k1 == k1 && e.len == len) return s;
-    h = (h + 1u) & mask;
-  }
-}
-
-// 12-bit prefilter index of a lemma from its first two bytes (b1 = 0 if the lemma has one byte)
-__host__ __device__ __forceinline__ uint32_t pref_idx(uint32_t b0, uint32_t b1) { return ((b0 << 5) ^ b1) & 0xFFFu; }
 
 __device__ __forceinline__ uint64_t mask_bytes(uint32_t nbytes) {  // nbytes in 0..8
   return nbytes >= 8 ? ~0ull : ((1ull << (8 * nbytes)) - 1ull);
@@ -108,7 +100,7 @@ __device__ __forceinline__ uint64_t mask_bytes(uint32_t nbytes) {  // nbytes in 
 
 // Lemma attributes of a word token of length L whose first bytes (lowercased,
 // little-endian) are k0/k1 (valid up to min(L,16)) and whose last three bytes
-// are s3 = b[L-3]<<16 | b[L-2]<<8 | b[L-1].  R-LEMMA.
+// are s3 = b[L-3]<<16 | b[L-2]<<8 | b[L-1].  R-LEMMA.  (byte-FSM path)
 __device__ __forceinline__ uint32_t word_attr(const Lex& L, uint32_t len, uint64_t k0, uint64_t k1, uint32_t s3) {
   const uint32_t b1 = s3 & 0xFFu, b2 = (s3 >> 8) & 0xFFu, b3 = (s3 >> 16) & 0xFFu;
   if (len == 3 && s3 == (('n' << 16) | ('\'' << 8) | 't'))  // n't -> not
@@ -125,27 +117,25 @@ __device__ __forceinline__ uint32_t word_attr(const Lex& L, uint32_t len, uint64
   return probe(L, m0, m1, ll);
 }
 
-// Entry index + 1 of a word token (R-LEMMA), with the 2-byte prefilter.
-__device__ __forceinline__ uint32_t word_idx(const Lex& L, const uint32_t* pref, uint32_t len, uint64_t k0,
-                                             uint64_t k1, uint32_t s3) {
-  const uint32_t b1 = s3 & 0xFFu, b2 = (s3 >> 8) & 0xFFu, b3 = (s3 >> 16) & 0xFFu;
-  if (len == 3 && s3 == (('n' << 16) | ('\'' << 8) | 't')) {  // n't -> not
-    const uint32_t pi = pref_idx('n', 'o');
-    if (!((pref[pi >> 5] >> (pi & 31u)) & 1u)) return 0;
-    return probe_idx(L, (uint64_t)'n' | ((uint64_t)'o' << 8) | ((uint64_t)'t' << 16), 0ull, 3);
-  }
+// Token code of a word token (R-LEMMA): len bytes, first 16 (lowercased) in
+// o0..o3, last three s3 = b[len-3]<<16 | b[len-2]<<8 | b[len-1]; branch-free.
+__device__ __forceinline__ uint32_t word_code(const Lex& L, uint32_t len, uint32_t o0, uint32_t o1, uint32_t o2,
+                                              uint32_t o3, uint32_t s3) {
+  constexpr uint32_t NT = ('n' << 16) | ('\'' << 8) | 't';
+  const uint32_t b1 = s3 & 0xFFu, b2 = (s3 >> 8) & 0xFFu, b3 = s3 >> 16;
   uint32_t strip = 0;
+  if (len >= 3 && b1 == 's' && b2 != 's') strip = 1;
+  if (len >= 4 && b2 == 'e' && (b1 == 'd' || b1 == 's')) strip = 2;
   if (len >= 5 && b3 == 'i' && b2 == 'n' && b1 == 'g') strip = 3;
-  else if (len >= 4 && b2 == 'e' && b1 == 'd') strip = 2;
-  else if (len >= 4 && b2 == 'e' && b1 == 's') strip = 2;
-  else if (len >= 3 && b1 == 's' && b2 != 's') strip = 1;
-  const uint32_t ll = len - strip;
-  if (ll == 0 || ll > 16) return 0;
-  const uint32_t pi = pref_idx((uint32_t)(k0 & 0xFFu), ll >= 2 ? (uint32_t)((k0 >> 8) & 0xFFu) : 0u);
-  if (!((pref[pi >> 5] >> (pi & 31u)) & 1u)) return 0;
-  const uint64_t m0 = k0 & mask_bytes(ll < 8 ? ll : 8);
-  const uint64_t m1 = ll > 8 ? (k1 & mask_bytes(ll - 8)) : 0ull;
-  return probe_idx(L, m0, m1, ll);
+  const bool nt = len == 3 && s3 == NT;  // n't -> not
+  const uint32_t ll = nt ? 3u : len - strip;
+  if (nt) o0 = 'n' | ('o' << 8) | ('t' << 16);
+  const int32_t sh = ll > 16u ? 0 : 8 * (int32_t)ll;  // lemma bytes kept (0: no lemma -> code 0)
+  o0 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh, 0));
+  o1 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 32, 0));
+  o2 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 64, 0));
+  o3 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 96, 0));
+  return lookup(L, o0, o1, o2, o3);
 }
 
 // ------------------------------------------------------------ rule FSM
@@ -372,7 +362,6 @@ struct __align__(16) WarpBuf {
 
 struct Smem4 {
   uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000
-  uint32_t pref[128];
   uint32_t fa[kPunct + 8];             // token code -> machine attributes (fsm_attr)
   uint8_t tO[16 * 32], tP[128 * 4];    // O-part and P-part transition tables
   WarpBuf w[kW4];
@@ -387,46 +376,39 @@ __device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uin
   return lo;
 }
 
-// Word token(s) of a run of n bytes whose first 16 bytes (lowercased) are k0/k1
-// and whose last bytes (newest low) are `tail`; returns the token count.
-__device__ __forceinline__ uint32_t run_tokens(const Lex& L, const uint32_t* pref, uint32_t n, uint64_t k0,
-                                               uint64_t k1, uint64_t tail, uint32_t& attr0, uint32_t& attr1) {
-  tail = (tail | 0x2020202020202020ull) & mask_bytes(n < 6 ? n : 6);
-  const uint32_t t3 = (uint32_t)(tail & 0xFFFFFFu), t2 = (uint32_t)(tail & 0xFFFFu);
-  uint32_t cut = 0;
-  if (n > 3 && t3 == (('n' << 16) | ('\'' << 8) | 't')) cut = 3;
-  else if (n > 2 && (t2 == (('\'' << 8) | 's') || t2 == (('\'' << 8) | 'm') || t2 == (('\'' << 8) | 'd')))
-    cut = 2;
-  else if (n > 3 && (t3 == (('\'' << 16) | ('r' << 8) | 'e') || t3 == (('\'' << 16) | ('v' << 8) | 'e') ||
-                     t3 == (('\'' << 16) | ('l' << 8) | 'l')))
-    cut = 3;
-  // the stem (or the whole run) on every lane, the clitic only where there is one:
-  // a warp runs at most two lexicon lookups per run, whatever its lanes' mix
-  const uint32_t e0 = word_idx(L, pref, n - cut, k0, k1, cut ? (uint32_t)((tail >> (8 * cut)) & 0xFFFFFFu) : t3);
-  attr0 = e0;
-  if (!cut) return 1;
-  const uint32_t ck = cut == 3 ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t2, 0, 0x4401);
-  const uint32_t e1 = word_idx(L, pref, cut, (uint64_t)ck, 0ull, t3 & (cut == 3 ? 0xFFFFFFu : 0xFFFFu));
-  attr1 = e1;
-  return 2;
-}
-
-// word token(s) of the run of n bytes at stage byte x
-__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L,
-                                              const uint32_t* pref, uint32_t& at0, uint32_t& at1) {
+// Word token(s) of the run of n bytes at stage byte x: one clitic split
+// (R-CLITIC), then the lemma (R-LEMMA) and code of the stem and of the
+// clitic; returns the token count.  The stem lookup runs on every lane, the
+// clitic lookup only if some lane of the warp has one.
+__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L, uint32_t& c0,
+                                              uint32_t& c1) {
   const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
   const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
                  w4 = B.stage[a0 + 4];
   const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
   const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
-  const uint64_t k0 = (uint64_t)o0 | ((uint64_t)o1 << 32);
-  const uint64_t k1 = (uint64_t)o2 | ((uint64_t)o3 << 32);
   const uint32_t tb8 = x + n - 8;  // >= 8
   const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
   const uint32_t v0 = B.stage[ta], v1 = B.stage[ta + 1], v2 = B.stage[ta + 2];
-  const uint32_t lo8 = __funnelshift_r(v0, v1, tsh), hi8 = __funnelshift_r(v1, v2, tsh);
-  const uint64_t tl = ((uint64_t)__byte_perm(hi8, 0, 0x0123) | ((uint64_t)__byte_perm(lo8, 0, 0x0123) << 32));
-  return run_tokens(L, pref, n, k0, k1, tl, at0, at1);
+  // last 8 bytes, newest first: R = b[n-1] b[n-2] b[n-3] b[n-4] (low to high), R2 = b[n-5] .. b[n-8]
+  // (bytes before the run are garbage; every test below is guarded by the length)
+  const uint32_t R = __byte_perm(__funnelshift_r(v1, v2, tsh), 0, 0x0123) | 0x20202020u;
+  const uint32_t R2 = __byte_perm(__funnelshift_r(v0, v1, tsh), 0, 0x0123) | 0x20202020u;
+  const uint32_t t3 = R & 0xFFFFFFu;
+  const uint32_t l1 = t3 & 0xFFu, l2 = (t3 >> 8) & 0xFFu, l3 = t3 >> 16, lo16 = t3 & 0xFFFFu;
+  const bool c2 = n > 2u && l2 == '\'' && (l1 == 's' || l1 == 'm' || l1 == 'd');
+  const bool c3 = n > 3u && ((l3 == 'n' && l2 == '\'' && l1 == 't') ||
+                             (l3 == '\'' && (lo16 == (('r' << 8) | 'e') || lo16 == (('v' << 8) | 'e') ||
+                                             lo16 == (('l' << 8) | 'l'))));
+  const uint32_t cut = c3 ? 3u : (c2 ? 2u : 0u);
+  const uint32_t s3 = __funnelshift_r(R, R2, 8u * cut) & 0xFFFFFFu;  // last three stem bytes
+  c0 = word_code(L, n - cut, o0, o1, o2, o3, s3);
+  if (!__any_sync(__activemask(), cut != 0u)) return 1;
+  // clitic bytes b[n-cut..n-1] -> little-endian key
+  const uint32_t ck = cut == 3u ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t3, 0, 0x4401);
+  const uint32_t e1 = word_code(L, cut, ck, 0u, 0u, 0u, cut == 3u ? t3 : (t3 & 0xFFFFu));
+  c1 = e1;
+  return cut ? 2u : 1u;
 }
 
 // one request by the per-lane byte FSM (fallback path; kept out of line)
@@ -628,17 +610,14 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem4& S = *reinterpret_cast<Smem4*>(smem_raw);
   uint8_t* tail_mem = smem_raw + ((sizeof(Smem4) + 15) & ~size_t(15));
-  LexEntry* s_ent = reinterpret_cast<LexEntry*>(tail_mem);
-  const uint32_t ent_bytes = a.lex.n_entries * (uint32_t)sizeof(LexEntry);
-  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + ((ent_bytes + 15u) & ~15u));
+  uint4* s_keys = reinterpret_cast<uint4*>(tail_mem);
+  const uint32_t key_bytes = (a.lex.n_entries + 1u) * 16u;
+  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + key_bytes);
   const uint32_t nslots = 1u << a.lex.bits;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
   {
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.lex.entries);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_ent);
-    for (uint32_t i = tid; i < ent_bytes / 4; i += kT4) dst[i] = src[i];
+    for (uint32_t i = tid; i <= a.lex.n_entries; i += kT4) s_keys[i] = a.lex.keys[i];
     for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
-    for (uint32_t i = tid; i < 128; i += kT4) S.pref[i] = 0;
     for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i);
     for (uint32_t i = tid; i < kPunct + 8; i += kT4)
       S.fa[i] = fsm_attr(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
@@ -646,14 +625,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     for (uint32_t i = tid; i < 128 * 4; i += kT4) S.tP[i] = (uint8_t)p_step(i >> 2, i & 3u);
   }
   __syncthreads();
-  for (uint32_t i = tid; i < a.lex.n_entries; i += kT4) {
-    const LexEntry e = a.lex.entries[i];
-
-    const uint32_t pi = pref_idx((uint32_t)(e.k0 & 0xFFu), e.len >= 2 ? (uint32_t)((e.k0 >> 8) & 0xFFu) : 0u);
-    atomicOr(&S.pref[pi >> 5], 1u << (pi & 31u));
-  }
-  __syncthreads();
-  const Lex L{s_ent, s_slots, a.lex.bits};
+  const Lex L{s_keys, s_slots, a.lex.entries, a.lex.bits, a.lex.seed};
   WarpBuf& B = S.w[wid];
   const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
   const uint32_t ntasks = (a.n + 31) / 32;
@@ -847,7 +819,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               kind = c == ',' ? K_COMMA : (c == '.' || c == '!') ? K_END : c == '?' ? K_Q : K_OTH;
             }
           }
-          if (isrun) ntk = stage_run(B, x, n, L, S.pref, at0, at1);
+          if (isrun) ntk = stage_run(B, x, n, L, at0, at1);
         }
         uint32_t ti = ntk;
 #pragma unroll
@@ -922,8 +894,8 @@ __global__ void k_key(const float* __restrict__ u, const uint16_t* __restrict__ 
 
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + ((a.lex.n_entries * sizeof(LexEntry) + 15) & ~size_t(15)) +
-                      (((size_t(1) << a.lex.bits) * 2 + 15) & ~size_t(15));
+  const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + (size_t(a.lex.n_entries) + 1) * 16 +
+                      (size_t(1) << a.lex.bits) * 2;
   cudaError_t e = cudaFuncSetAttribute(k_score4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.work, 0, sizeof(uint32_t), s);
