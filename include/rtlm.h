@@ -22,7 +22,10 @@
  *  - One context per device, used by one host thread at a time.  A context's
  *    workspace, work counter and fork stream are reused by every call, so calls
  *    on one context must be ordered (one stream, or events between streams);
- *    overlap independent batches with one context per stream.  Kernels are
+ *    overlap independent batches with one context per stream.  Small host
+ *    arguments (offsets, profiles) go through a pinned staging buffer, so a
+ *    call returns without waiting for the stream (it waits only for the
+ *    previous call's staging copy on the same context).  Kernels are
  *    pure functions of their inputs: same inputs -> same bits.
  *
  * Citations: P:a-b = PAPER.md lines (v1 P:1-912, v2 P:913-1887); S:a-b =
@@ -131,6 +134,13 @@ int rt_abi_version(void);
 uint64_t rt_launch_count(void);
 /* Number of distinct lexicon lemmas. */
 uint32_t rt_lexicon_size(const rt_ctx* ctx);
+/* Caps the CTAs of this context's persistent kernels (scoring, MLP) at
+ * max_ctas (0 = one per SM, the default).  Use it when several contexts run
+ * concurrently: rt_schedule forks a one-CTA list-scheduling kernel that holds
+ * an SM for ~1 ms per 2^20-request queue, and a persistent kernel with one CTA
+ * per SM would wait for that SM before it can complete.  No effect on
+ * results.  RT_EINVAL if ctx is NULL. */
+rt_status rt_set_sm_limit(rt_ctx* ctx, uint32_t max_ctas);
 
 /* ---------------------------------------------------------------- (1) score */
 

@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librtlm.so")
+LIB_PATH = os.environ.get("RTLM_LIB", os.path.join(_HERE, "librtlm.so"))  # RTLM_LIB: an alternative build (experiments)
 CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
@@ -26,7 +26,7 @@ RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "R
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
            "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report",
-           "rt_trace_utilization"]
+           "rt_trace_utilization", "rt_set_sm_limit"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -107,6 +107,8 @@ def load_library(path: str = LIB_PATH):
     L.rt_launch_count.restype = ctypes.c_uint64
     L.rt_lexicon_size.restype = U32
     L.rt_lexicon_size.argtypes = [V]
+    L.rt_set_sm_limit.restype = I32
+    L.rt_set_sm_limit.argtypes = [V, U32]
     L.rt_score.restype = I32
     L.rt_score.argtypes = [V, P, P, U32, P, V]
     L.rt_predict.restype = I32
@@ -205,6 +207,10 @@ class Context:
     @property
     def lexicon_size(self) -> int:
         return int(self._L.rt_lexicon_size(self._h))
+
+    def set_sm_limit(self, max_ctas: int) -> None:
+        """Caps the CTAs of this context's persistent kernels (rt_set_sm_limit; 0 = one per SM)."""
+        self._check(self._L.rt_set_sm_limit(self._h, int(max_ctas)))
 
     def flags(self) -> int:
         f = ctypes.c_uint32()

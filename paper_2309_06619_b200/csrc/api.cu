@@ -13,6 +13,7 @@
 struct rt_ctx {
   int device = 0;
   int num_sms = 148;
+  uint32_t sm_limit = 0;  // rt_set_sm_limit (0: one CTA per SM)
   rtlm::LexEntry* d_entries = nullptr;
   uint4* d_keys = nullptr;
   uint16_t* d_slots = nullptr;
@@ -27,6 +28,13 @@ struct rt_ctx {
   cudaStream_t aux = nullptr;  // internal fork stream (CPU-class list scheduling)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp)
+  // pinned staging of small host arguments (segment / trace offsets, profiles): a
+  // copy from pageable memory would synchronise the stream before it starts
+  struct HostStage {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+  } st_off, st_prof;
   std::string err;
 };
 
@@ -310,6 +318,24 @@ rt_status ensure_ws(rt_ctx* c, size_t bytes) {
   return RT_OK;
 }
 
+// host -> device copy through a pinned staging buffer (waits only for the
+// previous copy out of the same buffer)
+rt_status stage_copy(rt_ctx* c, rt_ctx::HostStage& st, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!st.ev) RT_CUDA(c, cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+  else RT_CUDA(c, cudaEventSynchronize(st.ev));
+  if (bytes > st.cap) {
+    if (st.p) cudaFreeHost(st.p);
+    st.p = nullptr;
+    st.cap = 0;
+    RT_CUDA(c, cudaMallocHost(&st.p, bytes));
+    st.cap = bytes;
+  }
+  std::memcpy(st.p, src, bytes);
+  RT_CUDA(c, cudaMemcpyAsync(dst, st.p, bytes, cudaMemcpyHostToDevice, s));
+  RT_CUDA(c, cudaEventRecord(st.ev, s));
+  return RT_OK;
+}
+
 rt_status upload_offsets(rt_ctx* c, const uint32_t* h, uint32_t count, cudaStream_t s) {
   if (count > c->off_cap) {
     if (c->d_off) cudaFree(c->d_off);
@@ -318,8 +344,7 @@ rt_status upload_offsets(rt_ctx* c, const uint32_t* h, uint32_t count, cudaStrea
     if (cudaMalloc(&c->d_off, (size_t)count * 4) != cudaSuccess) return fail(c, RT_ENOMEM, "offsets buffer");
     c->off_cap = count;
   }
-  RT_CUDA(c, cudaMemcpyAsync(c->d_off, h, (size_t)count * 4, cudaMemcpyHostToDevice, s));
-  return RT_OK;
+  return stage_copy(c, c->st_off, c->d_off, h, (size_t)count * 4, s);
 }
 
 rt_status check_profile(rt_ctx* c, const rt_profile* p, bool need_cores) {
@@ -382,6 +407,10 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
+    for (rt_ctx::HostStage* st : {&c->st_off, &c->st_prof}) {
+      if (st->p) cudaFreeHost(st->p);
+      if (st->ev) cudaEventDestroy(st->ev);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -393,6 +422,16 @@ rt_status rt_destroy(rt_ctx* c) {
 const char* rt_last_error(const rt_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 uint32_t rt_lexicon_size(const rt_ctx* c) { return c ? c->n_entries : 0; }
+
+rt_status rt_set_sm_limit(rt_ctx* c, uint32_t max_ctas) {
+  if (!c) return RT_EINVAL;
+  c->sm_limit = max_ctas;
+  return RT_OK;
+}
+
+static int persistent_ctas(const rt_ctx* c) {
+  return (c->sm_limit && (int)c->sm_limit < c->num_sms) ? (int)c->sm_limit : c->num_sms;
+}
 
 rt_status rt_get_flags(rt_ctx* c, uint32_t* flags) {
   if (!c || !flags) return fail(c, RT_EINVAL, "null argument");
@@ -437,7 +476,7 @@ static rt_status score_common(rt_ctx* c, const uint8_t* d_bytes, const uint32_t*
   a.D_out = d_D_out;
   a.flags = c->d_flags;
   a.work = c->d_flags + 2;
-  a.num_sms = c->num_sms;
+  a.num_sms = persistent_ctas(c);
   cudaError_t e = rtlm::launch_score(a, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_score");
   return RT_OK;
@@ -490,7 +529,7 @@ rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d
   if (!d_feat || !d_u) return fail(c, RT_EINVAL, "null argument");
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
-  cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, c->num_sms, cs(stream));
+  cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_mlp");
   return RT_OK;
 }
@@ -608,8 +647,7 @@ static rt_status upload_profiles(rt_ctx* c, const rt_profile* h_profiles, uint32
     if (cudaMalloc(&c->d_prof, np * sizeof(rt_profile)) != cudaSuccess) return fail(c, RT_ENOMEM, "profiles");
     c->prof_cap = np;
   }
-  RT_CUDA(c, cudaMemcpyAsync(c->d_prof, h_profiles, np * sizeof(rt_profile), cudaMemcpyHostToDevice, s));
-  return RT_OK;
+  return stage_copy(c, c->st_prof, c->d_prof, h_profiles, np * sizeof(rt_profile), s);
 }
 
 static rt_status check_trace_off(rt_ctx* c, const uint32_t* h_trace_off, uint32_t nt) {

@@ -327,7 +327,10 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
 //      noun, punctuation) obtained with ballots, so the counters become
 //      per-token contributions summed per request (segmented warp scan).
 // Warps whose offsets are not non-decreasing use the per-lane byte FSM.
-constexpr uint32_t kT4 = 1024;                // threads per CTA (32 warps)
+#ifndef KSCORE_THREADS
+#define KSCORE_THREADS 1024
+#endif
+constexpr uint32_t kT4 = KSCORE_THREADS;      // threads per CTA (32 warps)
 constexpr uint32_t kW4 = kT4 / 32;
 constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
 constexpr uint32_t kRing = 1024;              // token ring per warp
