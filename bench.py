@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-traces", action="store_true")
     ap.add_argument("--no-mlp", action="store_true")
     ap.add_argument("--sweeps", action="store_true", help="also run the NEXT-3 malicious-ratio sweep")
+    ap.add_argument("--config4", action="store_true",
+                    help="also run config 4: 65536 traces x 1024 (2^26 requests) split over the ranks (strong)")
+    ap.add_argument("--no-config5", action="store_true", help="skip config 5 (rate/deadline x ablation sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
     return ap.parse_args()
@@ -289,6 +292,16 @@ def native(args):
     if not args.no_traces:
         traces = traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush)
 
+    # ---------------- config 5 sweep (weak: the whole grid over each rank's own traces)
+    sweep5 = None
+    if not args.no_config5:
+        sweep5 = config5_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks)
+
+    # ---------------- config 4 (strong: 2^26 requests split over the ranks)
+    cfg4 = None
+    if args.config4:
+        cfg4 = config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush)
+
     # ---------------- cpu baseline (oracle, rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -324,6 +337,10 @@ def native(args):
             line["offline"] = offline
         if malicious is not None:
             line["malicious"] = malicious
+        if sweep5 is not None:
+            line["config5"] = sweep5
+        if cfg4 is not None:
+            line["config4"] = cfg4
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -551,6 +568,177 @@ def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_ov
             "median_p95_response_s_per_lm": [None if x is None else round(x, 4) for x in p95],
             "mean_gpu_util_per_lm": gutil, "mean_cpu_util_per_lm": cutil,
             "trace_report_ms": round(report_ms, 4), "trace_util_ms": round(util_ms, 4)}
+
+
+def _lm_groups(d, dev):
+    """Contiguous per-LM request ranges of a traces() workload: (lm, r0, r1,
+    16-byte-aligned copy of the group's text, group-relative offsets)."""
+    import torch
+    off_np = d["offsets"]
+    groups = []
+    for f in range(4):
+        sel = np.nonzero(d["trace_prof"] == f)[0]
+        if len(sel) == 0:
+            continue
+        t0, t1 = int(sel[0]), int(sel[-1]) + 1
+        if t1 - t0 != len(sel):
+            raise ValueError("LM groups must be contiguous trace ranges")
+        r0, r1 = int(d["trace_off"][t0]), int(d["trace_off"][t1])
+        b0, b1 = int(off_np[r0]), int(off_np[r1])
+        so = torch.from_numpy((off_np[r0:r1 + 1] - off_np[r0]).astype(np.uint32).view(np.int32)).to(dev)
+        groups.append((f, r0, r1, torch.from_numpy(np.ascontiguousarray(d["data"][b0:b1])).to(dev), so))
+    return groups
+
+
+def config5_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks):
+    """BASELINE configs[4]: the arrival-rate x deadline x ablation sweep
+    (SURVEY §8(d) config 5): 154 points (8 rate multipliers x tightness 1/2 x
+    FIFO/HPF/LUF/MUF/UP/UP+C/UP+C+O, plus alpha 0-2 and b 1.0-3.0 on UP+C+O),
+    each over 64 traces x 1000 requests per LM (256 traces).  Features and u are
+    scored once (rt_score_key); a step recomputes every point's keys and
+    deadlines (rt_key, one launch per point and LM) and replays the whole grid
+    as ONE rt_simulate over 154 x 256 traces (per-trace profile index = point x 4
+    + LM), then sums per (point, LM) (rt_reduce_stats) and all-reduces them (a8).
+    Weak scaling: every rank runs the grid over its own traces."""
+    import torch
+    from paper_2309_06619_b200 import dist as rdist
+    per_lm = 64
+    base = configs.config5_base(20000 + rank * 4 * per_lm, per_lm)
+    pts = configs.config5_points()
+    npt = len(pts)
+    n = len(base["arrival_us"])
+    nt = len(base["trace_off"]) - 1
+    groups = _lm_groups(base, dev)
+    arr_m = {m: torch.from_numpy(configs.config5_arrivals(base, m)).to(dev) for m in configs.CONFIG5_MULTS}
+    feat = torch.empty((n, 8), dtype=torch.int16, device=dev)
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    tmpk = torch.empty(n, dtype=torch.int64, device=dev)
+    for f, r0, r1, gd, so in groups:  # scoring once (features + u per LM regressor)
+        ctx.score_key(gd, so, base["regressors"][f], base["profiles"][f], want_feat=True, want_D=False,
+                      out={"u": u[r0:r1], "key": tmpk[r0:r1], "feat": feat[r0:r1]})
+    # the grid as one trace set: point i's traces are i*nt .. (i+1)*nt - 1
+    arr = torch.cat([arr_m[pt["mult"]] for pt in pts])
+    tl = torch.from_numpy(base["true_len"].view(np.int16)).to(dev).repeat(npt)
+    u_all = u.repeat(npt)
+    key = torch.empty(npt * n, dtype=torch.int64, device=dev)
+    D = torch.empty(npt * n, dtype=torch.int32, device=dev)
+    tprof = torch.from_numpy(np.concatenate([base["trace_prof"].astype(np.int64) + 4 * i for i in range(npt)])
+                             .astype(np.uint16).view(np.int16)).to(dev)
+    toff = (np.arange(npt * nt + 1, dtype=np.uint64) * int(base["trace_off"][1])).astype(np.uint32)
+    profs = [dict(p, **pt["overrides"]) for pt in pts for p in base["profiles"]]
+    stats = torch.empty((npt * nt, 2), dtype=torch.int64, device=dev)
+    sums = torch.zeros((npt * 4, 3), dtype=torch.int64, device=dev)
+
+    def grid():
+        for i in range(npt):
+            o = i * n
+            for f, r0, r1, gd, so in groups:
+                ctx.key(u[r0:r1], profs[4 * i + f], feat=feat[r0:r1], arrival=arr[o + r0:o + r1],
+                        key=key[o + r0:o + r1], D_out=D[o + r0:o + r1])
+        ctx.simulate(arr, tl, u_all, key, D, toff, profs, tprof, stats=stats)
+        sums.zero_()
+        ctx.reduce_stats(stats, tprof, npt * 4, sums=sums)
+        rdist.allreduce_sums(sums)
+
+    steps = max(1, min(args.steps, 5))
+    for _ in range(max(1, min(args.warmup, 3))):
+        grid()
+    torch.cuda.synchronize()
+    barrier()
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record(stream)
+    for _ in range(steps):
+        grid()
+    ev_b.record(stream)
+    ev_b.synchronize()
+    ms = max_over_ranks(ev_a.elapsed_time(ev_b)) / steps
+    s = sums.cpu().numpy().reshape(npt, 4, 3).sum(axis=1)  # over LMs
+    mean_resp = (s[:, 0] / np.maximum(s[:, 1], 1) / 1e6).round(4)
+    miss = (s[:, 2] / np.maximum(s[:, 1], 1)).round(4)
+    by_policy = {}
+    for tight in (1, 2):
+        for name in configs.CONFIG5_POLICIES:
+            idx = [i for i, p in enumerate(pts) if p["name"] == f"{name}/t{tight}"]
+            by_policy[f"{name}/t{tight}"] = {"mean_response_s": [float(mean_resp[i]) for i in idx],
+                                             "miss_ratio": [float(miss[i]) for i in idx]}
+    ab = lambda pre, arr_: [float(arr_[i]) for i, p in enumerate(pts) if p["name"].startswith(pre)]
+    traces_total = world * npt * nt
+    return {"metric": "traces/s", "value": round(traces_total / (ms / 1e3), 1), "unit": "traces/s",
+            "requests_per_s": round(traces_total * (n // max(nt, 1)) / (ms / 1e3), 1),
+            "ms_per_grid": round(ms, 3), "points": npt, "traces_per_point_per_gpu": nt,
+            "workload": "config5: 154 points (rate x0.25..x32 x tightness 1/2 x 7 policies; alpha 0-2 and b 1.0-3.0 "
+                        f"on UP+C+O at rate x{configs.CONFIG5_AB_MULT:g}, tightness {configs.CONFIG5_AB_TIGHTNESS}) "
+                        "x 64 traces x 1000 requests per LM per GPU; keys recomputed per point, one replay launch",
+            "scaling": "weak", "mults": list(configs.CONFIG5_MULTS), "by_policy": by_policy,
+            "alpha": {"mean_response_s": ab("alpha=", mean_resp), "miss_ratio": ab("alpha=", miss)},
+            "b": {"mean_response_s": ab("b=", mean_resp), "miss_ratio": ab("b=", miss)}}
+
+
+def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):
+    """BASELINE configs[3]: 2^26 requests = 65536 traces x 1024, contiguous trace
+    ranges per rank (strong scaling: the job is fixed, each rank takes 1/N of
+    it), score_key per LM + replay + stats, one NCCL all-reduce of the per-LM
+    int64 sums (a8).  value = 2^26 requests / max-over-ranks step time."""
+    import torch
+    from paper_2309_06619_b200 import dist as rdist
+    t0 = time.time()
+    # blocks of 8192 traces (one N=8 rank's shard; u32 text offsets per block)
+    nblk = 8
+    if nblk % world:
+        raise ValueError("config 4 needs world size dividing 8")
+    blocks = []
+    for blk in range(rank * nblk // world, (rank + 1) * nblk // world):
+        d = configs.config4_shard(blk, nblk, grouped=True)
+        nb, ntb = len(d["arrival_us"]), len(d["trace_off"]) - 1
+        blocks.append({"d": d, "groups": _lm_groups(d, dev),
+                       "arr": torch.from_numpy(d["arrival_us"]).to(dev),
+                       "tl": torch.from_numpy(d["true_len"].view(np.int16)).to(dev),
+                       "tp": torch.from_numpy(d["trace_prof"].view(np.int16)).to(dev),
+                       "u": torch.empty(nb, dtype=torch.float32, device=dev),
+                       "key": torch.empty(nb, dtype=torch.int64, device=dev),
+                       "D": torch.empty(nb, dtype=torch.int32, device=dev),
+                       "stats": torch.empty((ntb, 2), dtype=torch.int64, device=dev)})
+        del d["data"]
+    gen_s = time.time() - t0
+    n = sum(len(b["d"]["arrival_us"]) for b in blocks)
+    nt = sum(len(b["d"]["trace_off"]) - 1 for b in blocks)
+    sums = torch.zeros((4, 3), dtype=torch.int64, device=dev)
+
+    def step():
+        sums.zero_()
+        for b in blocks:
+            d, u, key, D, arr = b["d"], b["u"], b["key"], b["D"], b["arr"]
+            for f, r0, r1, gd, so in b["groups"]:
+                ctx.score_key(gd, so, d["regressors"][f], d["profiles"][f], arrival=arr[r0:r1],
+                              out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
+            ctx.simulate(arr, b["tl"], u, key, D, d["trace_off"], d["profiles"], b["tp"], stats=b["stats"])
+            ctx.reduce_stats(b["stats"], b["tp"], 4, sums=sums)
+        rdist.allreduce_sums(sums)
+
+    steps = max(1, min(args.steps, 5))
+    for _ in range(max(1, min(args.warmup, 3))):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        ev_a.record(stream)
+        step()
+        ev_b.record(stream)
+        ev_b.synchronize()
+        ts.append(ev_a.elapsed_time(ev_b))
+    ms = max_over_ranks(sum(ts)) / steps
+    s = sums.cpu().numpy()
+    total_req = 65536 * 1024
+    return {"metric": "M requests scored+scheduled+replayed/s", "value": round(total_req / (ms / 1e3) / 1e6, 2),
+            "unit": "Mreq/s", "traces_per_s": round(65536 / (ms / 1e3), 1), "ms_per_step": round(ms, 3),
+            "scaling": "strong", "requests_per_gpu": n, "traces_per_gpu": nt, "host_gen_s": round(gen_s, 1),
+            "workload": "config4: 65536 Poisson-ramp traces x 1024 requests (2^26) split over the ranks, 4 LMs, "
+                        "tight, UP+C+O; one NCCL all-reduce of per-LM int64 sums",
+            "mean_response_s_per_lm": [round(float(s[f, 0]) / max(1, s[f, 1]) / 1e6, 4) for f in range(4)],
+            "miss_ratio_per_lm": [round(float(s[f, 2]) / max(1, s[f, 1]), 4) for f in range(4)]}
 
 
 def oracle_requests_timing(d2, n_sample: int, reps: int = 1):

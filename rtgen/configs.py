@@ -75,23 +75,38 @@ def config2(n: int = 1 << 20, gid0: int = 0, lm: int = 0):
 
 
 # ---------------------------------------------------------------- traces
-def traces(cfg: int, trace_ids, per_trace: int, lm_of, beta0=10.0, step=1.0, beta_max=150.0, tightness=1):
+def _trace_part(seed, cfg, t, per_trace, f, lm, beta0, step, beta_max):
+    g0 = GID_BASE[cfg] + int(t) * TRACE_STRIDE
+    d, o, lat = text(seed, g0, per_trace, latent=True)
+    return d, o, arrivals(seed, int(t), per_trace, beta0, step, beta_max), true_len(seed, g0, lat, lm["scale"], f)
+
+
+def traces(cfg: int, trace_ids, per_trace: int, lm_of, beta0=10.0, step=1.0, beta_max=150.0, tightness=1,
+           threads: int | None = None):
     """Independent Poisson-ramp traces.  lm_of(trace_id) -> LM index.
-    Returns arrays concatenated trace by trace (arrival order within a trace)."""
+    Returns arrays concatenated trace by trace (arrival order within a trace).
+    Traces are generated independently (counter-based), on `threads` host
+    threads (default: all cores; the result does not depend on it)."""
+    from concurrent.futures import ThreadPoolExecutor
     seed = ROOT_SEED + cfg
     lms = paper_lms()
-    datas, offs, r_all, tl_all, lm_idx = [], [], [], [], []
+    ids = [int(t) for t in trace_ids]
+    lm_idx = [lm_of(t) for t in ids]
+    args = [(seed, cfg, t, per_trace, f, lms[f], beta0, step, beta_max) for t, f in zip(ids, lm_idx)]
+    nthr = threads or min(32, os.cpu_count() or 1)
+    if nthr > 1 and len(ids) > 64:
+        with ThreadPoolExecutor(nthr) as ex:  # ctypes calls release the GIL
+            parts = list(ex.map(lambda a: _trace_part(*a), args))
+    else:
+        parts = [_trace_part(*a) for a in args]
+    datas, offs, r_all, tl_all = [], [], [], []
     total = 0
-    for t in trace_ids:
-        g0 = GID_BASE[cfg] + int(t) * TRACE_STRIDE
-        d, o, lat = text(seed, g0, per_trace, latent=True)
-        f = lm_of(int(t))
+    for d, o, r, tl in parts:
         datas.append(d)
         offs.append(o[:-1].astype(np.uint64) + total)
         total += int(o[-1])
-        r_all.append(arrivals(seed, int(t), per_trace, beta0, step, beta_max))
-        tl_all.append(true_len(seed, g0, lat, lms[f]["scale"], f))
-        lm_idx.append(f)
+        r_all.append(r)
+        tl_all.append(tl)
     off = np.concatenate(offs + [np.asarray([total], np.uint64)])
     if total >= 2**32:
         raise OverflowError("trace shard text >= 4 GiB")
@@ -102,9 +117,10 @@ def traces(cfg: int, trace_ids, per_trace: int, lm_of, beta0=10.0, step=1.0, bet
         q["tightness"] = tightness
         profiles.append(q)
     return {"data": np.concatenate(datas) if datas else np.zeros(0, np.uint8), "offsets": off.astype(np.uint32),
-            "arrival_us": np.concatenate(r_all), "true_len": np.concatenate(tl_all),
+            "arrival_us": np.concatenate(r_all) if r_all else np.zeros(0, np.int64),
+            "true_len": np.concatenate(tl_all) if tl_all else np.zeros(0, np.uint16),
             "trace_off": (np.arange(nt + 1, dtype=np.uint64) * per_trace).astype(np.uint32),
-            "trace_prof": np.asarray(lm_idx, np.uint16), "profiles": profiles,
+            "trace_prof": np.asarray(lm_idx, np.uint16), "profiles": profiles, "trace_ids": np.asarray(ids, np.int64),
             "regressors": [regressor(p) for p in lms], "lexicon": read_lexicon()}
 
 
@@ -114,11 +130,68 @@ def config3(n_traces: int = 4096, per_trace: int = 1000, first: int = 0):
     return traces(3, range(first, first + n_traces), per_trace, lambda t: (t // per_lm) % 4)
 
 
-def config4_shard(rank: int, world: int, n_traces: int = 65536, per_trace: int = 1024):
-    """2^26 requests = 65536 traces x 1024, contiguous trace ranges per rank."""
+def config4_shard(rank: int, world: int, n_traces: int = 65536, per_trace: int = 1024, grouped: bool = False):
+    """2^26 requests = 65536 traces x 1024, contiguous trace ranges per rank
+    (LM of trace t = t mod 4).  grouped=True lists the same traces ordered by
+    (LM, t), so that each LM's requests are one contiguous range (one scoring
+    launch per LM regressor); traces are independent, so the order does not
+    change any per-trace result."""
     lo = rank * n_traces // world
     hi = (rank + 1) * n_traces // world
-    return traces(4, range(lo, hi), per_trace, lambda t: t % 4)
+    ids = range(lo, hi)
+    if grouped:
+        ids = sorted(ids, key=lambda t: (t % 4, t))
+    return traces(4, ids, per_trace, lambda t: t % 4)
+
+
+#: config 5 (SURVEY §8(d)): arrival-rate multipliers x tightness x policies, plus
+#: alpha and b steps on UP+C+O.  SURVEY fixes no rate or tightness for the alpha
+#: and b steps; they run at multiplier 8 (the knee of the lighter LMs, SURVEY
+#: §8(d) "where overload starts") with loose deadlines, where tasks are not
+#: overdue on arrival and the numerator (alpha) and window (b) can matter
+CONFIG5_AB_MULT = 8.0
+CONFIG5_AB_TIGHTNESS = 2
+CONFIG5_MULTS = (0.25, 0.5, 1.0, 2.0, 4.0, 8.0, 16.0, 32.0)
+CONFIG5_POLICIES = {
+    "FIFO": {"policy": "FIFO", "consolidate": 0, "offload": 0},
+    "HPF": {"policy": "HPF", "consolidate": 0, "offload": 0},
+    "LUF": {"policy": "LUF", "consolidate": 0, "offload": 0},
+    "MUF": {"policy": "MUF", "consolidate": 0, "offload": 0},
+    "UP": {"policy": "UP", "consolidate": 0, "offload": 0},
+    "UP+C": {"policy": "UP", "consolidate": 1, "offload": 0},
+    "UP+C+O": {"policy": "UP", "consolidate": 1, "offload": 1},
+}
+
+
+def config5_points() -> list[dict]:
+    """The 154 sweep points: {"mult", "name", "overrides"} (8 x 2 x 7 + 21 alpha + 21 b)."""
+    pts = []
+    for m in CONFIG5_MULTS:
+        for tight in (1, 2):
+            for name, ov in CONFIG5_POLICIES.items():
+                pts.append({"mult": m, "name": f"{name}/t{tight}", "overrides": dict(ov, tightness=tight)})
+    for i in range(21):
+        pts.append({"mult": CONFIG5_AB_MULT, "name": f"alpha={i / 10:.1f}",
+                    "overrides": dict(CONFIG5_POLICIES["UP+C+O"], alpha=i / 10, tightness=CONFIG5_AB_TIGHTNESS)})
+    for b10 in range(10, 31):
+        pts.append({"mult": CONFIG5_AB_MULT, "name": f"b={b10 / 10:.1f}",
+                    "overrides": dict(CONFIG5_POLICIES["UP+C+O"], b10=b10, tightness=CONFIG5_AB_TIGHTNESS)})
+    return pts
+
+
+def config5_base(first: int, per_lm: int = 64, per_trace: int = 1000):
+    """The sweep's traces: 4 x per_lm traces (LM blocks contiguous) at multiplier 1."""
+    nt = 4 * per_lm
+    return traces(5, range(first, first + nt), per_trace, lambda t: ((t - first) // per_lm) % 4)
+
+
+def config5_arrivals(d: dict, mult: float) -> np.ndarray:
+    """Arrivals of the same traces under the ramp scaled by `mult`
+    (rate min(10 m + m j, 150 m) per minute; P:1586-1587 scaled)."""
+    seed = ROOT_SEED + 5
+    per = int(d["trace_off"][1] - d["trace_off"][0]) if len(d["trace_off"]) > 1 else 0
+    return np.concatenate([arrivals(seed, int(t), per, 10.0 * mult, 1.0 * mult, 150.0 * mult)
+                           for t in d["trace_ids"]])
 
 
 # ---------------------------------------------------------------- NEXT-3: malicious tasks

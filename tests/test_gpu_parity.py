@@ -319,6 +319,35 @@ def test_config5_sweep_points(ctx_v1, lex_v1, point, mult):
     _replay_case(ctx_v1, lex_v1, d, point)
 
 
+def test_config5_grid_as_one_replay(ctx_v1, lex_v1):
+    """bench.py's config-5 leg replays the whole sweep grid in ONE rt_simulate:
+    the same traces repeated per point, with per-trace profile index point*4 + LM
+    and the point's arrivals (rate multiplier).  Stats per (point, LM) through
+    rt_reduce_stats; everything against the oracle, point by point."""
+    base = configs.config5_base(900, per_lm=2)
+    pts = [p for p in configs.config5_points() if p["name"] in ("FIFO/t1", "UP+C+O/t2", "alpha=0.5", "b=2.5")]
+    pts = [dict(p, mult=m) for p, m in zip(pts, (0.25, 32.0, 8.0, 8.0))]
+    npt, n, nt = len(pts), len(base["arrival_us"]), len(base["trace_off"]) - 1
+    d = dict(base)
+    d["data"] = np.concatenate([base["data"]] * npt)
+    tot = int(base["offsets"][-1])
+    d["offsets"] = np.concatenate([base["offsets"][:-1].astype(np.uint64) + i * tot for i in range(npt)]
+                                  + [np.asarray([npt * tot], np.uint64)]).astype(np.uint32)
+    d["arrival_us"] = np.concatenate([configs.config5_arrivals(base, p["mult"]) for p in pts])
+    d["true_len"] = np.tile(base["true_len"], npt)
+    d["trace_off"] = (np.arange(npt * nt + 1, dtype=np.uint64) * int(base["trace_off"][1])).astype(U32)
+    d["trace_prof"] = np.concatenate([base["trace_prof"] + 4 * i for i in range(npt)]).astype(np.uint16)
+    d["profiles"] = [dict(p, **pt["overrides"]) for pt in pts for p in base["profiles"]]
+    d["regressors"] = [r for _ in pts for r in base["regressors"]]
+    st = _replay_case(ctx_v1, lex_v1, d, {})
+    gsums = ctx_v1.reduce_stats(dev(st.view(np.int64).reshape(-1, 2)), dev(d["trace_prof"]), npt * 4)
+    torch.cuda.synchronize()
+    for g in range(npt * 4):
+        sel = d["trace_prof"] == g
+        assert gsums[g, 0].item() == int(st["sum_resp_us"][sel].sum())
+        assert gsums[g, 2].item() == int(st["misses"][sel].sum())
+
+
 def test_score_stream_boundaries(ctx_v1, lex_v1):
     """K1 streams 512-byte chunks: words and clitics across chunk boundaries, runs
     longer than one and two chunks, requests splitting a word, and requests with
