@@ -2,8 +2,8 @@
 // 5th-generation tensor cores.  Layers 6-100-200-200-100-1,
 // ReLU on hidden layers, identity output clamped at 0.
 //
-// Persistent CTAs of 256 threads; a tile is 128 requests (one TMEM lane and
-// two threads per request, taking alternate 16-column groups).  Layer 1 (6 -> 100, 600 FMA/request) and layer 5
+// Persistent CTAs of 1024 threads; a tile is 128 requests (one TMEM lane and
+// kQ = 8 threads per request, taking every eighth 16-column group).  Layer 1 (6 -> 100, 600 FMA/request) and layer 5
 // (100 -> 1) run on the CUDA cores in fp32.  Layers 2-4 are tcgen05.mma
 // (kind::f16, BF16 operands, FP32 accumulators in TMEM, M = 128):
 //   A = the tile's activations in shared memory, B = the layer's weights,
@@ -25,7 +25,11 @@ namespace rtlm {
 namespace {
 
 constexpr uint32_t kT = 128;                       // requests per tile (TMEM lanes)
-constexpr uint32_t kThr = 256;                     // threads: two per request (column halves)
+#ifndef KMLP_THREADS
+#define KMLP_THREADS 1024
+#endif
+constexpr uint32_t kThr = KMLP_THREADS;            // threads: kQ per request (column groups)
+constexpr uint32_t kQ = kThr / kT;
 constexpr uint32_t N1 = 112, N2 = 208, N3 = 208, N4 = 112;
 constexpr uint32_t K2C = 13, K3C = 25, K4C = 25;   // stored 8-wide K chunks of W2, W3, W4
 constexpr uint32_t SZ_W2 = K2C * N2 * 16, SZ_W3 = K3C * N3 * 16, SZ_W4 = K4C * N4 * 16;
@@ -91,7 +95,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 // hidden-layer epilogue: TMEM row -> + bias -> ReLU -> bf16 -> the next A operand;
-// the two threads of a row take alternate 16-column groups
+// the kQ threads of a row take every kQ-th 16-column group
 __device__ __forceinline__ void store_group(const uint32_t (&r)[16], const float* bias, uint32_t c0, uint8_t* sA,
                                             uint32_t row) {
   uint32_t p[8];
@@ -104,15 +108,16 @@ __device__ __forceinline__ void store_group(const uint32_t (&r)[16], const float
 }
 
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_row, const float* bias, uint32_t n, uint8_t* sA,
-                                                uint32_t row, uint32_t half) {
-  uint32_t c0 = half * 16;
-  for (; c0 + 32 < n; c0 += 64) {  // two groups per wait
+                                                uint32_t row, uint32_t q) {
+  constexpr uint32_t S = 16 * kQ;
+  uint32_t c0 = q * 16;
+  for (; c0 + S < n; c0 += 2 * S) {  // two groups per wait
     uint32_t r0[16], r1[16];
     tmem_ld16_nowait(tmem_row + c0, r0);
-    tmem_ld16_nowait(tmem_row + c0 + 32, r1);
+    tmem_ld16_nowait(tmem_row + c0 + S, r1);
     tmem_wait_ld();
     store_group(r0, bias, c0, sA, row);
-    store_group(r1, bias, c0 + 32, sA, row);
+    store_group(r1, bias, c0 + S, sA, row);
   }
   if (c0 < n) {
     uint32_t r0[16];
@@ -134,9 +139,8 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
-  __shared__ float s_part[kT];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t row = tid & (kT - 1), half = tid >> 7;  // warps w and w + 4 share TMEM lanes 32(w & 3)..
+  const uint32_t row = tid & (kT - 1), half = tid >> 7;  // warps w, w + 4, .. share TMEM lanes 32(w & 3)..
   // resident weights: bf16 blob (W2 | W3 | W4) then the fp32 parameters
   {
     const uint4* src = reinterpret_cast<const uint4*>(wblob);
@@ -160,6 +164,9 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
   const uint32_t tmem_row = tmem + (((warp & 3u) * 32u) << 16);  // this warp's TMEM lane quarter
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
   uint8_t* sA = smem + OFF_A;
+  // layer-5 partial sums of threads 1..kQ-1 of a row: in the activation region,
+  // which is free between the layer-4 MMA and the next tile's layer 1
+  float(*s_part)[kT] = reinterpret_cast<float(*)[kT]>(sA);
   uint32_t phase = 0;
   const uint32_t ntiles = (n + kT - 1) / kT;
   auto load_feat = [&](uint32_t t) {
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
     x[2] = (float)(f.y & 0xFFFFu); x[3] = (float)(f.y >> 16);
     x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
 #pragma unroll 1
-    for (uint32_t c = half; c < N1 / 8; c += 2) {
+    for (uint32_t c = half; c < N1 / 8; c += kQ) {
       uint32_t p[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -221,16 +228,21 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // ---- layer 4 epilogue + layer 5 (100 -> 1) on the CUDA cores, clamp at 0
     float y = 0.0f;
-    for (uint32_t c0 = half * 16; c0 < N4; c0 += 32) {
+    for (uint32_t c0 = half * 16; c0 < N4; c0 += 16 * kQ) {
       float v[16];
       tmem_ld16(tmem_row + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) y = fmaf(P[P_W5 + c0 + j], fmaxf(v[j] + P[P_B4 + c0 + j], 0.0f), y);
     }
-    if (half) s_part[row] = y;
+    if (half) s_part[half][row] = y;
     __syncthreads();
-    // fixed summation order: bias + half 0's groups + half 1's groups
-    if (!half && valid) u_out[req] = fmaxf((P[P_B5] + y) + s_part[row], 0.0f);
+    // fixed summation order: bias + thread 0's groups + thread 1's groups + ...
+    if (!half && valid) {
+      float acc = P[P_B5] + y;
+#pragma unroll
+      for (uint32_t k = 1; k < kQ; ++k) acc += s_part[k][row];
+      u_out[req] = fmaxf(acc, 0.0f);
+    }
     // the next tile's layer 1 rewrites sA and its MMAs overwrite TMEM
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

@@ -294,6 +294,14 @@ __device__ __forceinline__ uint32_t class_bits(uint32_t b) {
   return w ? 0x1u : (p ? 0x100u : (sp ? 0u : 0x10000u));
 }
 
+// token kind of a punctuation byte (K_* below; 0 for other bytes).  The class
+// table carries it in bits 24..26: classify's shifted sums of 8 bytes only
+// spill upwards from there, so the W / P / X fields stay exact
+__device__ __forceinline__ uint32_t punct_kind(uint32_t b) {
+  if (!(class_bits(b) & 0x100u)) return 0u;
+  return b == ',' ? 2u : (b == '.' || b == '!') ? 3u : b == '?' ? 4u : 5u;
+}
+
 __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const uint32_t f[8]) {
   if (!a.fused || a.feat) {
     uint4 pk = make_uint4(f[0] | (f[1] << 16), f[2] | (f[3] << 16), f[4] | (f[5] << 16), f[6] | (f[7] << 16));
@@ -355,6 +363,7 @@ struct FsmCtx {
 struct __align__(16) WarpBuf {
   uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
   uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
+  uint32_t sp[kChunk / 32 + 2];        // run stops: ~wm | mk (words 16, 17: all ones)
   uint16_t ev[kChunk + 1];             // event: byte in chunk | request << 9 (0xFFFF: carried run)
   uint32_t rs[32];                     // request starts (absolute byte offsets)
   uint16_t ring[kRing];                // tokens (code | request << 11)
@@ -364,7 +373,7 @@ struct __align__(16) WarpBuf {
 };
 
 struct Smem4 {
-  uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000
+  uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000; punct kind << 24
   uint32_t fa[kPunct + 8];             // token code -> machine attributes (fsm_attr)
   uint8_t tO[16 * 32], tP[128 * 4];    // O-part and P-part transition tables
   WarpBuf w[kW4];
@@ -591,14 +600,14 @@ __device__ __forceinline__ void rules_round(WarpBuf& B, const uint32_t* fa_of, c
     c.sp = vp & 127u;
     // S-part: PREP after a second distinct noun of the sentence (PREP tested first)
     const uint32_t sinc = (a >> 19) & c.n2;
-    if (a & FA_NOUN) {
+    {
       const uint32_t id = (a >> 1) & 0x3FFu;
-      if (c.nf == kNoNoun10) c.nf = id;
-      else c.n2 |= (id != c.nf) ? 1u : 0u;
-    }
-    if (a & FA_END) {
-      c.nf = kNoNoun10;
-      c.n2 = 0u;
+      const bool noun = (a & FA_NOUN) != 0u, first = noun && c.nf == kNoNoun10;
+      c.n2 |= (noun && !first && id != c.nf) ? 1u : 0u;
+      c.nf = first ? id : c.nf;
+      const bool end = (a & FA_END) != 0u;  // sentence end: fresh S-part
+      c.nf = end ? kNoNoun10 : c.nf;
+      c.n2 = end ? 0u : c.n2;
     }
     c2 += sinc | ((vo >> 4) << 11) | ((vp >> 7) << 22);
   }
@@ -621,7 +630,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
   {
     for (uint32_t i = tid; i <= a.lex.n_entries; i += kT4) s_keys[i] = a.lex.keys[i];
     for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
-    for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i);
+    for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i) | (punct_kind(i) << 24);
     for (uint32_t i = tid; i < kPunct + 8; i += kT4)
       S.fa[i] = fsm_attr(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
     for (uint32_t i = tid; i < 16 * 32; i += kT4) S.tO[i] = (uint8_t)o_step(i >> 5, i & 31u);
@@ -666,6 +675,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
     int32_t tokbase = 0;
     uint32_t prevW = 0;                 // W bit of the byte before the chunk
     int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
+    uint32_t pend_rq = 0;               // its request (within the task)
     const uint32_t base = B0 & ~15u;
     uint4 qprev = make_uint4(0, 0, 0, 0);
     int32_t tokdone = 0;                // tokens already through the rules
@@ -712,6 +722,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       if (lane == 0) B.wm[kChunk / 32] = 0;
       __syncwarp();
       // ---- (2) events
+      if (lane < kChunk / 32 + 2) B.sp[lane] = lane < kChunk / 32 ? (~B.wm[lane] | B.mk[lane]) : 0xFFFFFFFFu;
       const uint32_t mk16 = (B.mk[lane >> 1] >> (16u * (lane & 1u))) & 0xFFFFu;
       const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W16, 1);
       const uint32_t pw = lane ? (Wp >> 15) & 1u : prevW;
@@ -722,12 +733,14 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
       const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R16 != 0u);
       bool pend_here = false;  // the carried run ends in this chunk
       int32_t new_pend = -1;
+      uint32_t new_pend_rq = 0;
       if (defer) {
         if (b_r) {
           const uint32_t L2 = 31 - __clz(b_r);
           const uint32_t top = __shfl_sync(0xFFFFFFFFu, R16, L2);
           const uint32_t bit = 31 - __clz(top);
           new_pend = (int32_t)(cb + L2 * 16u + bit);
+          new_pend_rq = __popc(__ballot_sync(0xFFFFFFFFu, rv && s_r <= (uint32_t)new_pend)) - 1u;
           if (lane == L2) R16 &= ~(1u << bit);
           pend_here = pend_start >= 0;
         }  // else: the carried run spans the whole chunk
@@ -783,11 +796,11 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
             const uint32_t ps = (uint32_t)pend_start;
             uint32_t stop = 0;
             for (uint32_t w = 0;; ++w) {
-              const uint32_t sm = ~B.wm[w] | B.mk[w];
+              const uint32_t sm = B.sp[w];
               if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
             }
             n = cb + stop - ps;
-            rq = req_of(B.rs, rcnt, ps);
+            rq = pend_rq;
             isrun = true;
             if (ps + kChunk >= cb) {
               x = 16 + kChunk + ps - cb;
@@ -805,21 +818,25 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
             const uint32_t c = st8[16 + kChunk + p];
             rq = pe >> 9;
             if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
-              // run length: up to the first non-word byte or request start
-              uint32_t qq = p + 1;
-              n = 1;
-              for (;;) {
-                const uint32_t qw = qq >> 5, qb = qq & 31u;
-                const uint32_t stop = (~B.wm[qw] | B.mk[qw]) >> qb;
-                if (stop) { n += __ffs(stop) - 1; break; }
-                n += 32 - qb;
-                qq += 32 - qb;
+              // run length: up to the first non-word byte or request start (two stop
+              // words cover runs of <= 32 bytes; sp[16], sp[17] stop at the chunk end)
+              const uint32_t qq = p + 1, qw = qq >> 5, qb = qq & 31u;
+              const uint64_t st2 = ((uint64_t)B.sp[qw] | ((uint64_t)B.sp[qw + 1] << 32)) >> qb;
+              if (st2) {
+                n = (uint32_t)__ffsll((long long)st2);
+              } else {
+                n = 65u - qb;
+                for (uint32_t w = qw + 2;; ++w) {
+                  const uint32_t stop = B.sp[w];
+                  if (stop) { n += __ffs(stop) - 1; break; }
+                  n += 32u;
+                }
               }
               x = 16 + kChunk + p;
               isrun = true;
             } else {
               ntk = 1;
-              kind = c == ',' ? K_COMMA : (c == '.' || c == '!') ? K_END : c == '?' ? K_Q : K_OTH;
+              kind = S.lut[c] >> 24;
             }
           }
           if (isrun) ntk = stage_run(B, x, n, L, at0, at1);
@@ -854,7 +871,10 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         }
       }
       if (pend_here) pend_start = -1;
-      if (defer && b_r) pend_start = new_pend;
+      if (defer && b_r) {
+        pend_start = new_pend;
+        pend_rq = new_pend_rq;
+      }
       prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
       __syncwarp();
     }
