@@ -3,14 +3,18 @@
 // ReLU on hidden layers, identity output clamped at 0.
 //
 // Persistent CTAs of 1024 threads; a tile is 128 requests (one TMEM lane and
-// kQ = 8 threads per request, taking every eighth 16-column group).  Layer 1 (6 -> 100, 600 FMA/request) and layer 5
-// (100 -> 1) run on the CUDA cores in fp32.  Layers 2-4 are tcgen05.mma
-// (kind::f16, BF16 operands, FP32 accumulators in TMEM, M = 128):
+// kQ = 8 threads per request, taking every eighth 16-column group).  Layer 1
+// (6 -> 100, 600 FMA/request) and layer 5 (100 -> 1) run on the CUDA cores in
+// fp32.  Layers 2-4 are tcgen05.mma (kind::f16, BF16 operands, FP32
+// accumulators in TMEM, M = 128):
 //   A = the tile's activations in shared memory, B = the layer's weights,
 //   resident in shared memory for the whole kernel (bf16, K-major, no swizzle:
 //   8-row x 16-byte core matrices, [k/8][row][8]), issued by one thread and
 //   committed to an mbarrier.  The epilogue of layer l (tcgen05.ld 32x32b ->
 //   bias -> ReLU -> bf16 -> st.shared) writes the A operand of layer l+1.
+// Software pipeline across a CTA's tiles: layer 4 accumulates in its own TMEM
+// region, so as soon as it completes the next tile's layer 1 is written and its
+// layer-2 MMA issued, running under this tile's layer-4 epilogue + layer 5.
 // Padding: widths 100/200 -> 112/208 (N multiple of 16 at M = 128) with zero
 // weight rows and zero biases, so padded activations are exactly 0; the last
 // 8-wide K chunk of every weight matrix (all-zero columns) is not stored: the
@@ -134,13 +138,59 @@ __device__ __forceinline__ void sync_for_mma() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// layer 1 (6 -> 100, fp32 on the CUDA cores, ReLU) of one request: this
+// thread's 8-column chunks c = q, q + kQ, .. (< N1 / 8) packed to bf16 in h
+constexpr uint32_t kL1C = (N1 / 8 + kQ - 1) / kQ;  // chunks per thread
+__device__ __forceinline__ void layer1(const float* P, uint4 f, uint32_t q, uint4 (&h)[kL1C]) {
+  float x[6];
+  x[0] = (float)(f.x & 0xFFFFu); x[1] = (float)(f.x >> 16);
+  x[2] = (float)(f.y & 0xFFFFu); x[3] = (float)(f.y >> 16);
+  x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
+#pragma unroll
+  for (uint32_t k = 0; k < kL1C; ++k) {
+    const uint32_t c = q + k * kQ;
+    uint32_t p[4] = {0u, 0u, 0u, 0u};
+    if (c < N1 / 8) {
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float hh[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t j = c * 8 + qq * 2 + e;
+          float acc = 0.0f;
+          if (j < 100) {
+            acc = P[P_B1 + j];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) acc = fmaf(P[P_W1 + j * 6 + i], x[i], acc);
+            acc = fmaxf(acc, 0.0f);
+          }
+          hh[e] = acc;
+        }
+        p[qq] = pack_bf16(hh[0], hh[1]);
+      }
+    }
+    h[k] = make_uint4(p[0], p[1], p[2], p[3]);
+  }
+}
+__device__ __forceinline__ void store_layer1(uint8_t* sA, uint32_t row, uint32_t q, const uint4 (&h)[kL1C]) {
+#pragma unroll
+  for (uint32_t k = 0; k < kL1C; ++k) {
+    const uint32_t c = q + k * kQ;
+    if (c < N1 / 8) *reinterpret_cast<uint4*>(sA + (c * kT + row) * 16) = h[k];
+  }
+}
+
+// TMEM columns: region A (D2, then D3) 0..207, region B (D4) 256..367, the
+// layer-5 partial sums of a row's kQ threads at 384..384+kQ-1
+constexpr uint32_t TM_D4 = 256, TM_PART = 384;
+
 __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ feat, uint32_t n,
                                                 const uint8_t* __restrict__ wblob, float* __restrict__ u_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t row = tid & (kT - 1), half = tid >> 7;  // warps w, w + 4, .. share TMEM lanes 32(w & 3)..
+  const uint32_t row = tid & (kT - 1), q = tid >> 7;  // warps w, w + 4, .. share TMEM lanes 32(w & 3)..
   // resident weights: bf16 blob (W2 | W3 | W4) then the fp32 parameters
   {
     const uint4* src = reinterpret_cast<const uint4*>(wblob);
@@ -155,7 +205,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
   const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
   if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         (uint32_t)__cvta_generic_to_shared(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -164,91 +214,87 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp(const uint16_t* __restrict__ fe
   const uint32_t tmem_row = tmem + (((warp & 3u) * 32u) << 16);  // this warp's TMEM lane quarter
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
   uint8_t* sA = smem + OFF_A;
-  // layer-5 partial sums of threads 1..kQ-1 of a row: in the activation region,
-  // which is free between the layer-4 MMA and the next tile's layer 1
-  float(*s_part)[kT] = reinterpret_cast<float(*)[kT]>(sA);
   uint32_t phase = 0;
   const uint32_t ntiles = (n + kT - 1) / kT;
   auto load_feat = [&](uint32_t t) {
     const uint32_t rq = t * kT + row;
     return (t < ntiles && rq < n) ? __ldg(reinterpret_cast<const uint4*>(feat + (size_t)rq * 8)) : make_uint4(0, 0, 0, 0);
   };
-  uint4 fnext = load_feat(blockIdx.x);
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint32_t req = t * kT + row;
-    const bool valid = req < n;
-    // ---- layer 1 on the CUDA cores (fp32): x = the six rule scores
-    const uint4 f = fnext;
-    fnext = load_feat(t + gridDim.x);  // in flight during this tile's layers 2-4
-    float x[6];
-    x[0] = (float)(f.x & 0xFFFFu); x[1] = (float)(f.x >> 16);
-    x[2] = (float)(f.y & 0xFFFFu); x[3] = (float)(f.y >> 16);
-    x[4] = (float)(f.z & 0xFFFFu); x[5] = (float)(f.z >> 16);
-#pragma unroll 1
-    for (uint32_t c = half; c < N1 / 8; c += kQ) {
-      uint32_t p[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float h[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint32_t j = c * 8 + q * 2 + e;
-          float acc = 0.0f;
-          if (j < 100) {
-            acc = P[P_B1 + j];
-#pragma unroll
-            for (int i = 0; i < 6; ++i) acc = fmaf(P[P_W1 + j * 6 + i], x[i], acc);
-            acc = fmaxf(acc, 0.0f);
-          }
-          h[e] = acc;
-        }
-        p[q] = pack_bf16(h[0], h[1]);
-      }
-      *reinterpret_cast<uint4*>(sA + (c * kT + row) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
-    }
-    // ---- layer 2: [128 x 112] . [112 x 208]
+  auto wait_mma = [&]() {
+    mbar_wait(mb, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  };
+  // Software pipeline over this CTA's tiles t, t + G, ..: layer 1 of the next
+  // tile runs on the CUDA cores while layer 4's MMA runs, and the next tile's
+  // layer-2 MMA runs while this tile's layer-4 epilogue + layer 5 run.
+  uint32_t t = blockIdx.x;
+  uint4 h1[kL1C];
+  if (t < ntiles) {
+    layer1(P, load_feat(t), q, h1);
+    store_layer1(sA, row, q, h1);
     sync_for_mma();
     if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W2, N2, 7, mb);
-    mbar_wait(mb, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue_hidden(tmem_row, P + P_B2, N2, sA, row, half);
-    // ---- layer 3: [128 x 208] . [208 x 208]
+  }
+  uint4 fnext = load_feat(t + gridDim.x);
+  for (; t < ntiles; t += gridDim.x) {
+    const uint32_t tn = t + gridDim.x;
+    const uint32_t req = t * kT + row;
+    // ---- layer 2 done: epilogue -> A operand of layer 3: [128 x 208] . [208 x 208]
+    wait_mma();
+    epilogue_hidden(tmem_row, P + P_B2, N2, sA, row, q);
     sync_for_mma();
     if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W3, N3, 13, mb);
-    mbar_wait(mb, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    epilogue_hidden(tmem_row, P + P_B3, N3, sA, row, half);
-    // ---- layer 4: [128 x 208] . [208 x 112]
+    wait_mma();
+    epilogue_hidden(tmem_row, P + P_B3, N3, sA, row, q);
+    // ---- layer 4: [128 x 208] . [208 x 112] -> region B; next tile's layer 1 meanwhile
     sync_for_mma();
-    if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W4, N4, 13, mb);
-    mbar_wait(mb, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) mma_layer(tmem + TM_D4, s0 + OFF_A, s0 + OFF_W4, N4, 13, mb);
+    const uint4 f = fnext;
+    fnext = load_feat(tn + gridDim.x);
+    wait_mma();
+    if (tn < ntiles) layer1(P, f, q, h1);
+    // ---- the activation region is free: next tile's layer 1 -> its layer-2 MMA
+    if (tn < ntiles) {
+      store_layer1(sA, row, q, h1);
+      sync_for_mma();
+      if (tid == 0) mma_layer(tmem, s0 + OFF_A, s0 + OFF_W2, N2, 7, mb);
+    }
     // ---- layer 4 epilogue + layer 5 (100 -> 1) on the CUDA cores, clamp at 0
     float y = 0.0f;
-    for (uint32_t c0 = half * 16; c0 < N4; c0 += 16 * kQ) {
+    for (uint32_t c0 = q * 16; c0 < N4; c0 += 16 * kQ) {
       float v[16];
-      tmem_ld16(tmem_row + c0, v);
+      tmem_ld16(tmem_row + TM_D4 + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) y = fmaf(P[P_W5 + c0 + j], fmaxf(v[j] + P[P_B4 + c0 + j], 0.0f), y);
     }
-    if (half) s_part[half][row] = y;
-    __syncthreads();
-    // fixed summation order: bias + thread 0's groups + thread 1's groups + ...
-    if (!half && valid) {
-      float acc = P[P_B5] + y;
-#pragma unroll
-      for (uint32_t k = 1; k < kQ; ++k) acc += s_part[k][row];
-      u_out[req] = fmaxf(acc, 0.0f);
-    }
-    // the next tile's layer 1 rewrites sA and its MMAs overwrite TMEM
+    // partial sums of the row's kQ threads meet in TMEM (same lane, column TM_PART + q)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem_row + TM_PART + q),
+                 "r"(__float_as_uint(y)) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (q == 0) {
+      uint32_t r[kQ];
+      static_assert(kQ == 8, "partial-sum load is x8");
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tmem_row + TM_PART));
+      tmem_wait_ld();
+      // fixed summation order: bias + thread 0's groups + thread 1's groups + ...
+      float acc = P[P_B5] + y;
+#pragma unroll
+      for (uint32_t k = 1; k < kQ; ++k) acc += __uint_as_float(r[k]);
+      if (req < n) u_out[req] = fmaxf(acc, 0.0f);
+    }
+    // region C / region B are rewritten only after later barriers
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace
