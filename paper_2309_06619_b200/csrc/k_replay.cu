@@ -25,7 +25,7 @@ struct ReplaySmem {
   uint16_t rank[kMaxTrace];  // arrival index -> rank
   uint32_t ready_gpu[32], ready_cpu[32], wait_arr[32];
   int64_t core_free[kMaxCores];
-  uint32_t W[kMaxWindow], S[kMaxWindow];
+  uint32_t W[kMaxWindow];
   float Su[kMaxWindow];
 };  // ~14.6 KB: u, D and lengths are read from global memory (L2) when needed
 
@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   const int64_t gpu_fixed = p.setup_us + p.base_us;
   int64_t now = sm.r[0], gpu_free = 0;
   uint32_t next = 0, done = 0;
+  uint32_t cpu_ready = 0, gpu_ready = 0;  // ready-set sizes (warp-uniform)
   int64_t resp = 0;     // per-lane partial sums
   uint32_t misses = 0;
   const uint32_t lt = (1u << lane) - 1u;
@@ -110,8 +111,11 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       const bool arr = i < n && sm.r[i] <= now;
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
       const uint32_t cnt = __popc(bal);  // a prefix of ones
+      const uint32_t rk = arr ? (uint32_t)sm.rank[i] : 0xFFFFFFFFu;
+      const uint32_t nc = __popc(__ballot_sync(0xFFFFFFFFu, rk < ncpu));
+      cpu_ready += nc;
+      gpu_ready += cnt - nc;
       if (arr) {
-        const uint32_t rk = sm.rank[i];
         if (rk < ncpu) {
           atomicOr(&sm.ready_cpu[rk >> 5], 1u << (rk & 31));
         } else {
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     }
     __syncwarp();
     // ---- CPU cores: highest-key ready CPU task -> lowest-index free core
-    for (;;) {
+    while (cpu_ready) {
       const uint32_t wcpu = sm.ready_cpu[lane];
       const uint32_t any = __ballot_sync(0xFFFFFFFFu, wcpu != 0);
       if (!any) break;
@@ -143,15 +147,14 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
         if (a.end_us) a.end_us[lo + i] = end;
       }
       ++done;
+      --cpu_ready;
       __syncwarp();
     }
     // ---- GPU dispatch
     bool waiting = false;
     int64_t oldest_r = 0;
     if (gpu_free <= now) {
-      uint32_t gw = sm.ready_gpu[lane];
-      const uint32_t cl = __popc(gw);
-      const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, cl);
+      const uint32_t total = gpu_ready;
       if (total) {
         const uint32_t aw = sm.wait_arr[lane];
         const uint32_t anyw = __ballot_sync(0xFFFFFFFFu, aw != 0);
@@ -166,6 +169,8 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           waiting = true;
         } else {
           // first `take` set bits in rank order -> W
+          uint32_t gw = sm.ready_gpu[lane];
+          const uint32_t cl = __popc(gw);
           uint32_t excl = cl;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -182,29 +187,62 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
             }
           }
           __syncwarp();
+          // the window's elements stay on the lanes that loaded them (lane e % 32,
+          // slot e / 32): rank, arrival index, u, length, deadline and arrival,
+          // all loads issued together; each element learns its position in the
+          // (u, rank) order, and the batch is the positions below cnt
+          constexpr uint32_t kCh = kMaxWindow / 32;
+          const uint32_t nch = (take + 31u) >> 5;
+          uint32_t re[kCh], pos[kCh], len_e[kCh], D_e[kCh];
+          float ue[kCh];
+          int64_t r_e[kCh];
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k) {
+            const uint32_t e = k * 32u + lane;
+            re[k] = 0xFFFFFFFFu; ue[k] = 0.0f; len_e[k] = 0u; D_e[k] = 0u; r_e[k] = 0; pos[k] = 0xFFFFFFFFu;
+            if (k < nch && e < take) {
+              re[k] = sm.W[e];
+              const uint32_t i = sm.sidx[re[k]];
+              ue[k] = g_u[i];
+              len_e[k] = g_len[i];
+              D_e[k] = g_D[i];
+              r_e[k] = sm.r[i];
+              pos[k] = e;
+              re[k] |= i << 16;  // rank (low 16 bits) | arrival index (high)
+            }
+          }
           uint32_t cnt;
-          const uint32_t* B;
           if (p.consolidate) {
-            // sort the window by (u, rank): ranks by shuffles, 32 elements per lane pass
-            for (uint32_t e0 = 0; e0 < take; e0 += 32) {
-              const uint32_t e = e0 + lane;
-              const uint32_t re = e < take ? sm.W[e] : 0xFFFFFFFFu;
-              const float ue = e < take ? g_u[sm.sidx[re]] : 0.0f;
-              uint32_t pos = 0;
-              for (uint32_t x0 = 0; x0 < take; x0 += 32) {
-                const uint32_t rx_l = x0 + lane < take ? sm.W[x0 + lane] : 0xFFFFFFFFu;
-                const float ux_l = x0 + lane < take ? g_u[sm.sidx[rx_l]] : 0.0f;
-                const uint32_t lim = min(32u, take - x0);
-                for (uint32_t x = 0; x < lim; ++x) {
-                  const float ux = __shfl_sync(0xFFFFFFFFu, ux_l, x);
-                  const uint32_t rx = __shfl_sync(0xFFFFFFFFu, rx_l, x);
-                  pos += (ux < ue) || (ux == ue && rx < re);
+            // position in the (u asc, rank asc) order, by shuffles over all elements
+#pragma unroll
+            for (uint32_t k = 0; k < kCh; ++k) pos[k] = 0u;
+            if (nch == 1) {  // windows of <= 32 (m = 19 at C = 11)
+              const uint32_t r0 = re[0] & 0xFFFFu;
+              for (uint32_t x = 0; x < take; ++x) {
+                const float ux = __shfl_sync(0xFFFFFFFFu, ue[0], x);
+                const uint32_t rx = __shfl_sync(0xFFFFFFFFu, re[0], x) & 0xFFFFu;
+                pos[0] += (ux < ue[0]) || (ux == ue[0] && rx < r0);
+              }
+            } else {
+#pragma unroll
+              for (uint32_t xk = 0; xk < kCh; ++xk) {
+                if (xk < nch) {
+                  const uint32_t lim = min(32u, take - xk * 32u);
+                  for (uint32_t x = 0; x < lim; ++x) {
+                    const float ux = __shfl_sync(0xFFFFFFFFu, ue[xk], x);
+                    const uint32_t rx = __shfl_sync(0xFFFFFFFFu, re[xk], x) & 0xFFFFu;
+#pragma unroll
+                    for (uint32_t k = 0; k < kCh; ++k)
+                      pos[k] += (ux < ue[k]) || (ux == ue[k] && rx < (re[k] & 0xFFFFu));
+                  }
                 }
               }
-              if (e < take) {
-                sm.S[pos] = re;
-                sm.Su[pos] = ue;
-              }
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < kCh; ++k) {
+              const uint32_t e = k * 32u + lane;
+              if (k < nch && e < take) sm.Su[pos[k]] = ue[k];
+              else pos[k] = 0xFFFFFFFFu;
             }
             __syncwarp();
             const uint32_t lim = min(C, take);
@@ -218,25 +256,28 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
                 break;
               }
             }
-            B = sm.S;
           } else {
             cnt = take;
-            B = sm.W;
           }
           uint32_t ml = 0;
-          for (uint32_t e = lane; e < cnt; e += 32) ml = max(ml, (uint32_t)g_len[sm.sidx[B[e]]]);
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k)
+            if (pos[k] < cnt) ml = max(ml, len_e[k]);
           ml = __reduce_max_sync(0xFFFFFFFFu, ml);
           const int64_t end = now + gpu_fixed + p.eta_us * (int64_t)ml;
-          for (uint32_t e = lane; e < cnt; e += 32) {
-            const uint32_t rk = B[e];
-            const uint32_t i = sm.sidx[rk];
-            atomicAnd(&sm.ready_gpu[rk >> 5], ~(1u << (rk & 31)));
-            atomicAnd(&sm.wait_arr[i >> 5], ~(1u << (i & 31)));
-            resp += end - sm.r[i];
-            misses += end > sm.r[i] + (int64_t)g_D[i];
-            if (a.end_us) a.end_us[lo + i] = end;
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k) {
+            if (pos[k] < cnt) {
+              const uint32_t rk = re[k] & 0xFFFFu, i = re[k] >> 16;
+              atomicAnd(&sm.ready_gpu[rk >> 5], ~(1u << (rk & 31)));
+              atomicAnd(&sm.wait_arr[i >> 5], ~(1u << (i & 31)));
+              resp += end - r_e[k];
+              misses += end > r_e[k] + (int64_t)D_e[k];
+              if (a.end_us) a.end_us[lo + i] = end;
+            }
           }
           done += cnt;
+          gpu_ready -= cnt;
           gpu_free = end;
           __syncwarp();
         }
@@ -247,7 +288,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     int64_t nxt = INT64_MAX;
     if (next < n) nxt = sm.r[next];
     if (gpu_free > now) nxt = min(nxt, gpu_free);
-    const bool cpu_waiting = __ballot_sync(0xFFFFFFFFu, sm.ready_cpu[lane] != 0) != 0;
+    const bool cpu_waiting = cpu_ready != 0;
     if (cpu_waiting) {
       int64_t cf = (lane < cores && sm.core_free[lane] > now) ? sm.core_free[lane] : INT64_MAX;
       nxt = min(nxt, warp_min64(cf));
