@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   int64_t now = sm.r[0], gpu_free = 0;
   uint32_t next = 0, done = 0;
   uint32_t cpu_ready = 0, gpu_ready = 0;  // ready-set sizes (warp-uniform)
+  bool have_oldest = false;                // oldest_r = arrival of the oldest waiting GPU-class task
+  int64_t oldest_r = 0;
   int64_t resp = 0;     // per-lane partial sums
   uint32_t misses = 0;
   const uint32_t lt = (1u << lane) - 1u;
@@ -112,7 +114,12 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
       const uint32_t cnt = __popc(bal);  // a prefix of ones
       const uint32_t rk = arr ? (uint32_t)sm.rank[i] : 0xFFFFFFFFu;
-      const uint32_t nc = __popc(__ballot_sync(0xFFFFFFFFu, rk < ncpu));
+      const uint32_t cb = __ballot_sync(0xFFFFFFFFu, rk < ncpu);
+      const uint32_t nc = __popc(cb);
+      if (gpu_ready == 0 && (bal & ~cb)) {  // the first waiting GPU-class task is the oldest
+        oldest_r = sm.r[next + __ffs(bal & ~cb) - 1];
+        have_oldest = true;
+      }
       cpu_ready += nc;
       gpu_ready += cnt - nc;
       if (arr) {
@@ -152,16 +159,17 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     }
     // ---- GPU dispatch
     bool waiting = false;
-    int64_t oldest_r = 0;
     if (gpu_free <= now) {
       const uint32_t total = gpu_ready;
       if (total) {
-        const uint32_t aw = sm.wait_arr[lane];
-        const uint32_t anyw = __ballot_sync(0xFFFFFFFFu, aw != 0);
-        const uint32_t owl = __ffs(anyw) - 1;
-        const uint32_t oword = __shfl_sync(0xFFFFFFFFu, aw, owl);
-        const uint32_t oldest = owl * 32 + (__ffs(oword) - 1);
-        oldest_r = sm.r[oldest];
+        if (!have_oldest) {  // after a dispatch: lowest set bit of the arrival-index bitmap
+          const uint32_t aw = sm.wait_arr[lane];
+          const uint32_t anyw = __ballot_sync(0xFFFFFFFFu, aw != 0);
+          const uint32_t owl = __ffs(anyw) - 1;
+          const uint32_t oword = __shfl_sync(0xFFFFFFFFu, aw, owl);
+          oldest_r = sm.r[owl * 32 + (__ffs(oword) - 1)];
+          have_oldest = true;
+        }
         const bool flush = (oldest_r <= now - p.xi_us) || next == n;
         const uint32_t full = p.consolidate ? m : C;
         const uint32_t take = total >= full ? full : (flush ? total : 0u);
@@ -278,6 +286,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           }
           done += cnt;
           gpu_ready -= cnt;
+          have_oldest = false;
           gpu_free = end;
           __syncwarp();
         }
