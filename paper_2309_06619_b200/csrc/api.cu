@@ -695,6 +695,9 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   a.trace_prof = d_trace_prof;
   a.stats = d_stats;
   a.end_us = d_end_us;
+  st = ensure_ws(c, (size_t)nt * rtlm::kMaxTrace * sizeof(uint16_t));
+  if (st != RT_OK) return st;
+  a.sidx = static_cast<uint16_t*>(c->ws);
   cudaError_t e = rtlm::launch_replay(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
   return RT_OK;

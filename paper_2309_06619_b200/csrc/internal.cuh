@@ -144,6 +144,7 @@ struct ReplayLaunch {
   const uint16_t* trace_prof;
   rt_trace_stats* stats;
   int64_t* end_us;
+  uint16_t* sidx;             // workspace: nt x kMaxTrace (rank -> arrival index)
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
 cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,

@@ -3,7 +3,8 @@
 //
 // One warp (one CTA) per trace of <= 1024 tasks (R-REPLAY; §V-A).
 // Priorities are static per task (Eq. 3 depends on d - r, not on the clock,
-// P:377), so the trace's keys are sorted once in shared memory and every
+// P:377), so the trace's keys are sorted once (k_trace_rank, a CTA per trace)
+// and every
 // "ready" set is a 1024-bit bitmap over key rank, one 32-bit word per lane:
 // the top-m ready tasks are the first m set bits (popc + warp scan), the
 // highest-key CPU task is the first set bit, and a second bitmap over arrival
@@ -16,11 +17,7 @@ namespace rtlm {
 namespace {
 
 struct ReplaySmem {
-  // s_r aliases s_key: keys are only needed until the ranks are known
-  union {
-    uint64_t key[kMaxTrace];
-    int64_t r[kMaxTrace];
-  };
+  int64_t r[kMaxTrace];      // arrival times
   uint16_t sidx[kMaxTrace];  // rank -> arrival index
   uint16_t rank[kMaxTrace];  // arrival index -> rank
   uint32_t ready_gpu[32], ready_cpu[32], wait_arr[32];
@@ -43,6 +40,46 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
   return v;
 }
 
+// Priority order of every trace: stable sort of (key desc, arrival index asc)
+// by a bitonic network in shared memory, one CTA per trace; writes the
+// arrival index of each rank (u16, kMaxTrace per trace) for k_replay.
+constexpr uint32_t kRankThr = 256;
+__global__ void __launch_bounds__(kRankThr) k_trace_rank(const uint64_t* __restrict__ key,
+                                                         const uint32_t* __restrict__ trace_off,
+                                                         uint16_t* __restrict__ sidx_out) {
+  __shared__ uint64_t sk[kMaxTrace];
+  __shared__ uint16_t si[kMaxTrace];
+  const uint32_t t = blockIdx.x, tid = threadIdx.x;
+  const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
+  if (n == 0) return;
+  uint32_t npow = 2;
+  while (npow < n) npow <<= 1;
+  for (uint32_t i = tid; i < npow; i += kRankThr) {
+    sk[i] = i < n ? key[lo + i] : 0ull;
+    si[i] = i < n ? (uint16_t)i : (uint16_t)0xFFFF;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= npow; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < npow; i += kRankThr) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t ki = sk[i], kl = sk[l];
+          const uint32_t ii = si[i], il = si[l];
+          const bool l_first = kl > ki || (kl == ki && il < ii);
+          const bool i_first = ki > kl || (ki == kl && ii < il);
+          if ((i & k) == 0 ? l_first : i_first) {
+            sk[i] = kl; sk[l] = ki;
+            si[i] = (uint16_t)il; si[l] = (uint16_t)ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t j = tid; j < n; j += kRankThr) sidx_out[(size_t)t * kMaxTrace + j] = si[j];
+}
+
 __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   ReplaySmem& sm = *reinterpret_cast<ReplaySmem*>(smem_raw);
@@ -54,39 +91,17 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     if (lane == 0) a.stats[t] = rt_trace_stats{0, 0u, 0u};
     return;
   }
-  // ---- key rank: bitonic sort of (key desc, arrival index asc)
-  uint32_t npow = 32;
-  while (npow < n) npow <<= 1;
-  for (uint32_t i = lane; i < npow; i += 32) {
-    sm.key[i] = i < n ? a.key[lo + i] : 0ull;
-    sm.sidx[i] = i < n ? (uint16_t)i : (uint16_t)0xFFFF;
-  }
-  __syncwarp();
-  for (uint32_t k = 2; k <= npow; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < npow; i += 32) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const uint64_t ki = sm.key[i], kl = sm.key[l];
-          const uint32_t ii = sm.sidx[i], il = sm.sidx[l];
-          const bool l_first = kl > ki || (kl == ki && il < ii);
-          const bool i_first = ki > kl || (ki == kl && ii < il);
-          if ((i & k) == 0 ? l_first : i_first) {
-            sm.key[i] = kl; sm.key[l] = ki;
-            sm.sidx[i] = (uint16_t)il; sm.sidx[l] = (uint16_t)ii;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
+  // ---- key rank (sorted by k_trace_rank): rank -> arrival index and back;
+  // the CPU class is the ranks [0, ncpu) (class bit on top of the key)
   uint32_t ncpu_l = 0;
+  const uint16_t* g_sidx = a.sidx + (size_t)t * kMaxTrace;
   for (uint32_t j = lane; j < n; j += 32) {
-    sm.rank[sm.sidx[j]] = (uint16_t)j;
-    ncpu_l += (uint32_t)(sm.key[j] >> 63);
+    const uint32_t i = g_sidx[j];
+    sm.sidx[j] = (uint16_t)i;
+    sm.rank[i] = (uint16_t)j;
+    ncpu_l += (uint32_t)(a.key[lo + j] >> 63);
   }
-  const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);  // CPU class = ranks [0, ncpu)
-  __syncwarp();
+  const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);
   for (uint32_t i = lane; i < n; i += 32) sm.r[i] = a.arrival[lo + i];
   const uint16_t* g_len = a.len + lo;
   const float* g_u = a.u + lo;
@@ -472,6 +487,8 @@ cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
   const size_t smem = sizeof(ReplaySmem);
   cudaError_t e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  k_trace_rank<<<a.nt, kRankThr, 0, s>>>(a.key, a.trace_off, a.sidx);
+  note_launch();
   k_replay<<<a.nt, 32, smem, s>>>(a);
   note_launch();
   return cudaGetLastError();
