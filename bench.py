@@ -272,6 +272,20 @@ def native(args):
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(score_ms, 5),
                 "step_share": round(score_ms / (sum(t_step) / len(t_step)), 4), "ncu": ncu_note}
 
+    # the kernel's binding resource is instruction issue (ncu: ~80 % of issue slots
+    # busy at < 4 % of HBM): its issue roofline from the committed ncu instruction
+    # count and the live launch time; peak = 148 SMs x 4 schedulers x 1 warp
+    # instruction per cycle at the SM clock sampled under load
+    if ncu_note and ncu_note.get("warp_instructions"):
+        props = torch.cuda.get_device_properties(dev)
+        mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+        peak_gips = props.multi_processor_count * 4 * mhz * 1e6 / 1e9
+        got_gips = ncu_note["warp_instructions"] / (score_ms / 1e3) / 1e9
+        roofline["issue"] = {"bound": "issue", "achieved": round(got_gips, 1), "peak": round(peak_gips, 1),
+                             "unit": "G warp-inst/s", "frac": round(got_gips / peak_gips, 4),
+                             "warp_instructions_per_launch": ncu_note["warp_instructions"],
+                             "peak_source": f"{props.multi_processor_count} SMs x 4 schedulers x {mhz:.0f} MHz"}
+
     # ---------------- MLP leg (NEXT-1): rt_predict_mlp on config 2's features
     mlp = None
     if not args.no_mlp:
