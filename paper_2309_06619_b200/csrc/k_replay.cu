@@ -43,41 +43,52 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 // Priority order of every trace: stable sort of (key desc, arrival index asc)
 // by a bitonic network in shared memory, one CTA per trace; writes the
 // arrival index of each rank (u16, kMaxTrace per trace) for k_replay.
-constexpr uint32_t kRankThr = 256;
+// Thread p holds the element at position p (key, arrival index); partners at
+// distance j < 32 are exchanged by shuffles, larger distances through shared
+// memory (double-buffered, one barrier per step).
+constexpr uint32_t kRankThr = kMaxTrace;
 __global__ void __launch_bounds__(kRankThr) k_trace_rank(const uint64_t* __restrict__ key,
                                                          const uint32_t* __restrict__ trace_off,
                                                          uint16_t* __restrict__ sidx_out) {
-  __shared__ uint64_t sk[kMaxTrace];
-  __shared__ uint16_t si[kMaxTrace];
-  const uint32_t t = blockIdx.x, tid = threadIdx.x;
+  __shared__ uint64_t sk[2][kMaxTrace];
+  __shared__ uint16_t si[2][kMaxTrace];
+  const uint32_t t = blockIdx.x, p = threadIdx.x;
   const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
   if (n == 0) return;
   uint32_t npow = 2;
   while (npow < n) npow <<= 1;
-  for (uint32_t i = tid; i < npow; i += kRankThr) {
-    sk[i] = i < n ? key[lo + i] : 0ull;
-    si[i] = i < n ? (uint16_t)i : (uint16_t)0xFFFF;
-  }
-  __syncthreads();
+  // padding (positions >= n) sorts last: key 0, index 0xFFFF; threads >= npow
+  // only ever pair among themselves
+  uint64_t k0 = p < n ? key[lo + p] : 0ull;
+  uint32_t i0 = p < n ? p : 0xFFFFu;
+  uint32_t buf = 0;
   for (uint32_t k = 2; k <= npow; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < npow; i += kRankThr) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const uint64_t ki = sk[i], kl = sk[l];
-          const uint32_t ii = si[i], il = si[l];
-          const bool l_first = kl > ki || (kl == ki && il < ii);
-          const bool i_first = ki > kl || (ki == kl && ii < il);
-          if ((i & k) == 0 ? l_first : i_first) {
-            sk[i] = kl; sk[l] = ki;
-            si[i] = (uint16_t)il; si[l] = (uint16_t)ii;
-          }
-        }
+      uint64_t k1;
+      uint32_t i1;
+      if (j >= 32u) {
+        sk[buf][p] = k0;
+        si[buf][p] = (uint16_t)i0;
+        __syncthreads();
+        k1 = sk[buf][p ^ j];
+        i1 = si[buf][p ^ j];
+        buf ^= 1u;
+      } else {
+        k1 = __shfl_xor_sync(0xFFFFFFFFu, k0, j);
+        i1 = __shfl_xor_sync(0xFFFFFFFFu, i0, j);
       }
-      __syncthreads();
+      // order: key descending, arrival index ascending; the lower position of
+      // a pair takes the first element when ((lower & k) == 0), else the later
+      const bool mine_first = k0 > k1 || (k0 == k1 && i0 < i1);
+      const bool lower = (p & j) == 0;
+      const bool want_first = lower == ((p & k) == 0);
+      if (mine_first != want_first) {
+        k0 = k1;
+        i0 = i1;
+      }
     }
   }
-  for (uint32_t j = tid; j < n; j += kRankThr) sidx_out[(size_t)t * kMaxTrace + j] = si[j];
+  if (p < n) sidx_out[(size_t)t * kMaxTrace + p] = (uint16_t)i0;
 }
 
 __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
