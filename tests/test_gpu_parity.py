@@ -404,3 +404,30 @@ def test_malicious_workload(ctx_v1, lex_v1, ratio):
     assert (host(feat, np.uint16) == f).all()
     for ov in ({}, {"policy": "FIFO", "consolidate": 0, "offload": 0}):
         _replay_case(ctx_v1, lex_v1, d, ov)
+
+
+@pytest.mark.parametrize("policy_ov", [{}, {"consolidate": 0}, {"offload": 0, "cores": 1}])
+def test_replay_rank_ties_and_ragged_traces(ctx_v1, policy_ov):
+    """k_trace_rank + k_replay on ragged traces (1 .. 1024 tasks, non-powers of
+    two) whose keys and u take only a few distinct values: the priority order
+    is then decided by the arrival-index tie-break (R-TIE) and the window's
+    (u, rank) order by the rank; end times against the oracle."""
+    rng = np.random.default_rng(11)
+    sizes = [1, 2, 3, 31, 32, 33, 63, 500, 1000, 1023, 1024, 7]
+    toff = np.concatenate([[0], np.cumsum(sizes)]).astype(U32)
+    n = int(toff[-1])
+    arr = np.concatenate([np.sort(rng.integers(0, 30_000_000, s)) for s in sizes]).astype(np.int64)
+    arr[toff[3]:toff[4]] = 5_000_000  # a trace whose tasks all arrive together
+    low = rng.choice(np.asarray([3, 3, 7, 1 << 40], np.uint64), n)
+    cls = (rng.random(n) < 0.2).astype(np.uint64) << np.uint64(63)
+    key = (cls | low).astype(np.uint64)
+    u = rng.choice(np.asarray([5.0, 5.0, 12.5, 40.0], np.float32), n)
+    tl = rng.integers(1, 80, n).astype(np.uint16)
+    D = rng.integers(1_000_000, 20_000_000, n).astype(U32)
+    profs = [dict(p, **policy_ov) for p in configs.paper_lms()]
+    tp = (np.arange(len(sizes)) % 4).astype(np.uint16)
+    st, end = oracle.simulate(arr, tl, u, key, D, toff, profs, tp, want_end=True)
+    gs, gend = ctx_v1.simulate(dev(arr), dev(tl), dev(u), dev(key), dev(D), toff, profs, dev(tp), want_end=True)
+    torch.cuda.synchronize()
+    assert (rt.decode_stats(gs) == st).all()
+    assert (gend.cpu().numpy() == end).all()
