@@ -201,16 +201,13 @@ def native(args):
     def pstep(k, e2e=False):
         sl = k % depth
         with torch.cuda.stream(streams[sl]):
-            if e2e:
-                data2[sl].copy_(h_bytes2[sl], non_blocking=True)
-                off2[sl].copy_(h_off2[sl], non_blocking=True)
+            if e2e:  # the C ABI's host-buffer entry: H2D copies, score+key+schedule, D2H of the assignment
+                ctxs[sl].score_schedule_host(h_bytes2[sl], h_off2[sl], reg, prof, h_res[sl])
+                return
             if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "score"):
                 ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
             if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "schedule"):
                 ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
-            if e2e:
-                for name in ("batch_of", "slot_of", "core_of"):
-                    h_res[sl][name].copy_(souts2[sl][name], non_blocking=True)
 
     def timed_pipeline(e2e):
         for k in range(args.warmup):
@@ -338,7 +335,9 @@ def native(args):
                         "note": "one batch at a time, L2 flushed between steps"},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                     "h2d_bytes_per_step": mean_bytes + 4 * (n + 1),
-                    "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_ms / args.steps, 4)},
+                    "d2h_bytes_per_step": 6 * n, "ms_per_step": round(e2e_ms / args.steps, 4),
+                    "path": "rt_score_schedule_host (C ABI): pinned host text + offsets -> H2D, score+key+schedule, "
+                            "D2H of batch/slot/core; one context and stream per in-flight batch"},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "clocks": clocks,

@@ -268,6 +268,24 @@ rt_status rt_trace_utilization(rt_ctx* ctx, const uint16_t* d_true_len, const ui
                                const rt_profile* h_profiles, uint32_t np, const uint16_t* d_trace_prof,
                                rt_trace_util* d_util, rt_stream stream);
 
+/* ---------------------------------------------------------------- (4b) end to end from host */
+
+/* The whole requests path of one queue from HOST buffers (the bench's e2e
+ * leg): copies h_bytes[0 .. h_offsets[n]) and h_offsets[n+1] to device buffers
+ * owned by the context, runs rt_score_key (1)-(3) and rt_schedule (4) on the
+ * queue [0, n), and copies the assignment back: h_batch_of[n] (global GPU
+ * batch id, UINT32_MAX for CPU tasks), h_slot_of[n], h_core_of[n] (as in
+ * rt_schedule).  All copies and kernels are asynchronous on `stream`: the
+ * host inputs must stay unchanged and the outputs are valid only after the
+ * stream has executed the call (page-locked host memory makes the copies
+ * asynchronous; pageable memory makes them synchronous).  h_offsets[n] is read
+ * by the host at call time (the byte count).  Same errors as rt_score_key /
+ * rt_schedule; RT_ENOMEM if the context's buffers cannot grow (growing frees
+ * the previous buffers, an implicit device synchronisation). */
+rt_status rt_score_schedule_host(rt_ctx* ctx, const uint8_t* h_bytes, const uint32_t* h_offsets, uint32_t n,
+                                 const rt_regressor* reg, const rt_profile* prof, uint32_t cores,
+                                 uint32_t* h_batch_of, uint8_t* h_slot_of, uint8_t* h_core_of, rt_stream stream);
+
 /* ---------------------------------------------------------------- (6) aggregate */
 
 /* Integer sums per group (O8): d_sums[g*3 + {0,1,2}] += {sum_resp_us, n,

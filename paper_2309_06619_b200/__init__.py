@@ -26,7 +26,7 @@ RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "R
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
            "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report",
-           "rt_trace_utilization", "rt_set_sm_limit"]
+           "rt_trace_utilization", "rt_set_sm_limit", "rt_score_schedule_host"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -135,6 +135,9 @@ def load_library(path: str = LIB_PATH):
     L.rt_trace_report.argtypes = [V, P, P, P, U32, P, V]
     L.rt_trace_utilization.restype = I32
     L.rt_trace_utilization.argtypes = [V, P, P, P, P, U32, P, U32, P, P, V]
+    L.rt_score_schedule_host.restype = I32
+    L.rt_score_schedule_host.argtypes = [V, P, P, U32, ctypes.POINTER(Regressor), ctypes.POINTER(Profile), U32,
+                                         P, P, P, V]
     _lib = L
     return L
 
@@ -157,6 +160,18 @@ def _ptr(t, dtype=None, name="tensor"):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
     if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must have dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(t, dtype, name="tensor"):
+    """Host pointer of a contiguous CPU tensor (page-locked for asynchronous copies)."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a CPU tensor")
+    if t.dtype != dtype:
         raise TypeError(f"{name} must have dtype {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
@@ -350,6 +365,23 @@ class Context:
         if want_feat:
             res["feat"] = feat
         return res
+
+    def score_schedule_host(self, h_bytes, h_offsets, reg, prof: dict, out, cores: int | None = None):
+        """rt_score_schedule_host: one queue end to end from HOST tensors (pinned
+        for asynchronous copies): h_bytes u8, h_offsets int32 (u32 bits, n+1);
+        `out` = dict of host tensors batch_of (int32), slot_of (uint8), core_of
+        (uint8), valid after the current stream synchronises."""
+        torch = _torch()
+        n = h_offsets.numel() - 1
+        r = make_regressor(reg)
+        p = make_profile(prof)
+        c = int(prof["cores"] if cores is None else cores)
+        self._check(self._L.rt_score_schedule_host(
+            self._h, _hptr(h_bytes, torch.uint8, "h_bytes"), _hptr(h_offsets, torch.int32, "h_offsets"), n,
+            ctypes.byref(r), ctypes.byref(p), c, _hptr(out["batch_of"], torch.int32, "batch_of"),
+            _hptr(out["slot_of"], torch.uint8, "slot_of"), _hptr(out["core_of"], torch.uint8, "core_of"),
+            self._stream()))
+        return out
 
     def schedule(self, key, u, seg_off, prof: dict, cores: int | None = None, out=None):
         """rt_schedule.  seg_off: host array (nq+1).  Returns dict of device tensors."""

@@ -28,6 +28,8 @@ struct rt_ctx {
   cudaStream_t aux = nullptr;  // internal fork stream (CPU-class list scheduling)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp)
+  void* io = nullptr;        // device buffers of rt_score_schedule_host
+  size_t io_size = 0;
   // pinned staging of small host arguments (segment / trace offsets, profiles): a
   // copy from pageable memory would synchronise the stream before it starts
   struct HostStage {
@@ -407,6 +409,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
+    cudaFree(c->io);
     for (rt_ctx::HostStage* st : {&c->st_off, &c->st_prof}) {
       if (st->p) cudaFreeHost(st->p);
       if (st->ev) cudaEventDestroy(st->ev);
@@ -700,6 +703,51 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   a.sidx = static_cast<uint16_t*>(c->ws);
   cudaError_t e = rtlm::launch_replay(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
+  return RT_OK;
+}
+
+rt_status rt_score_schedule_host(rt_ctx* c, const uint8_t* h_bytes, const uint32_t* h_offsets, uint32_t n,
+                                 const rt_regressor* reg, const rt_profile* prof, uint32_t cores,
+                                 uint32_t* h_batch_of, uint8_t* h_slot_of, uint8_t* h_core_of, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!n) return RT_OK;
+  if (!h_bytes || !h_offsets || !reg || !prof || !h_batch_of || !h_slot_of || !h_core_of)
+    return fail(c, RT_EINVAL, "null argument");
+  const size_t nbytes = h_offsets[n];
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t need = up(nbytes) + up(4 * ((size_t)n + 1)) + up(4 * (size_t)n) + up(8 * (size_t)n) +
+                      3 * up(4 * (size_t)n) + 2 * up(n) + up(8);
+  DeviceGuard g(c->device);
+  if (need > c->io_size) {
+    if (c->io) cudaFree(c->io);  // implicit device sync: no in-flight user
+    c->io = nullptr;
+    c->io_size = 0;
+    cudaError_t e = cudaMalloc(&c->io, need);
+    if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("io buffers: ") + cudaGetErrorString(e));
+    c->io_size = need;
+  }
+  char* p = static_cast<char*>(c->io);
+  auto take = [&](size_t b) { char* r = p; p += up(b); return r; };
+  uint8_t* d_bytes = reinterpret_cast<uint8_t*>(take(nbytes));
+  uint32_t* d_off = reinterpret_cast<uint32_t*>(take(4 * ((size_t)n + 1)));
+  float* d_u = reinterpret_cast<float*>(take(4 * (size_t)n));
+  uint64_t* d_key = reinterpret_cast<uint64_t*>(take(8 * (size_t)n));
+  uint32_t* d_perm = reinterpret_cast<uint32_t*>(take(4 * (size_t)n));
+  uint32_t* d_batch = reinterpret_cast<uint32_t*>(take(4 * (size_t)n));
+  uint32_t* d_sbo = reinterpret_cast<uint32_t*>(take(8));
+  uint8_t* d_slot = reinterpret_cast<uint8_t*>(take(n));
+  uint8_t* d_core = reinterpret_cast<uint8_t*>(take(n));
+  cudaStream_t s = cs(stream);
+  RT_CUDA(c, cudaMemcpyAsync(d_bytes, h_bytes, nbytes, cudaMemcpyHostToDevice, s));
+  RT_CUDA(c, cudaMemcpyAsync(d_off, h_offsets, 4 * ((size_t)n + 1), cudaMemcpyHostToDevice, s));
+  rt_status st = rt_score_key(c, d_bytes, d_off, n, reg, prof, nullptr, nullptr, nullptr, d_u, d_key, nullptr, stream);
+  if (st != RT_OK) return st;
+  const uint32_t seg[2] = {0u, n};
+  st = rt_schedule(c, d_key, d_u, seg, 1, prof, cores, d_perm, d_batch, d_slot, d_core, d_sbo, stream);
+  if (st != RT_OK) return st;
+  RT_CUDA(c, cudaMemcpyAsync(h_batch_of, d_batch, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  RT_CUDA(c, cudaMemcpyAsync(h_slot_of, d_slot, n, cudaMemcpyDeviceToHost, s));
+  RT_CUDA(c, cudaMemcpyAsync(h_core_of, d_core, n, cudaMemcpyDeviceToHost, s));
   return RT_OK;
 }
 

@@ -431,3 +431,24 @@ def test_replay_rank_ties_and_ragged_traces(ctx_v1, policy_ov):
     torch.cuda.synchronize()
     assert (rt.decode_stats(gs) == st).all()
     assert (gend.cpu().numpy() == end).all()
+
+
+def test_score_schedule_host_matches_oracle(ctx_v1, lex_v1):
+    """rt_score_schedule_host (the e2e entry: host buffers in, host assignment
+    out) equals the oracle's one-pass schedule on a config-2 prefix queue."""
+    d = configs.config2(n=20000)
+    n = len(d["offsets"]) - 1
+    hb = torch.from_numpy(d["data"]).pin_memory()
+    ho = torch.from_numpy(d["offsets"].view(np.int32)).pin_memory()
+    out = {"batch_of": torch.empty(n, dtype=torch.int32).pin_memory(),
+           "slot_of": torch.empty(n, dtype=torch.uint8).pin_memory(),
+           "core_of": torch.empty(n, dtype=torch.uint8).pin_memory()}
+    ctx_v1.score_schedule_host(hb, ho, d["regressor"], d["profile"], out)
+    torch.cuda.synchronize()
+    f = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+    u = oracle.predict(f, d["regressor"])
+    k, _ = oracle.key(u, f, d["profile"])
+    s = oracle.schedule(k, u, np.asarray([0, n], U32), d["profile"])
+    assert (out["batch_of"].numpy().view(U32) == s["batch_of"]).all()
+    assert (out["slot_of"].numpy() == s["slot_of"]).all()
+    assert (out["core_of"].numpy() == s["core_of"]).all()
