@@ -37,6 +37,13 @@ struct rt_ctx {
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
   } st_off, st_prof;
+  // pinned blocks staged while a stream was being captured into a CUDA graph:
+  // the graph's copy nodes read them at every replay, so they are never reused
+  // (freed with the context)
+  std::vector<void*> captured_stage;
+  // device buffers replaced after a capture: a graph may still address them
+  bool captured = false;
+  std::vector<void*> retired;
   std::string err;
 };
 
@@ -309,9 +316,30 @@ rtlm::DevLexicon dev_lex(const rt_ctx* c) {
   return rtlm::DevLexicon{c->d_entries, c->d_keys, c->d_slots, c->n_entries, c->bits, c->seed};
 }
 
-rt_status ensure_ws(rt_ctx* c, size_t bytes) {
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive;
+}
+
+// a device buffer being replaced: freed, unless a graph captured on this
+// context may still address it (then kept until rt_destroy)
+void retire(rt_ctx* c, void* p) {
+  if (!p) return;
+  if (c->captured) c->retired.push_back(p);
+  else cudaFree(p);
+}
+
+// device buffers only grow outside graph capture (a free would synchronise)
+rt_status no_growth_in_capture(rt_ctx* c, cudaStream_t s) {
+  if (capturing(s))
+    return fail(c, RT_EINVAL, "buffer growth during CUDA graph capture: run the call once before capturing it");
+  return RT_OK;
+}
+
+rt_status ensure_ws(rt_ctx* c, size_t bytes, cudaStream_t s) {
   if (bytes <= c->ws_size) return RT_OK;
-  if (c->ws) cudaFree(c->ws);  // implicit device sync: no in-flight user
+  if (no_growth_in_capture(c, s) != RT_OK) return RT_EINVAL;
+  retire(c, c->ws);  // cudaFree: implicit device sync, no in-flight user
   c->ws = nullptr;
   c->ws_size = 0;
   cudaError_t e = cudaMalloc(&c->ws, bytes);
@@ -323,6 +351,15 @@ rt_status ensure_ws(rt_ctx* c, size_t bytes) {
 // host -> device copy through a pinned staging buffer (waits only for the
 // previous copy out of the same buffer)
 rt_status stage_copy(rt_ctx* c, rt_ctx::HostStage& st, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (capturing(s)) {  // a block of its own for the graph (see rt_ctx::captured_stage)
+    c->captured = true;
+    void* p = nullptr;
+    RT_CUDA(c, cudaMallocHost(&p, bytes));
+    c->captured_stage.push_back(p);
+    std::memcpy(p, src, bytes);
+    RT_CUDA(c, cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+    return RT_OK;
+  }
   if (!st.ev) RT_CUDA(c, cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
   else RT_CUDA(c, cudaEventSynchronize(st.ev));
   if (bytes > st.cap) {
@@ -340,7 +377,8 @@ rt_status stage_copy(rt_ctx* c, rt_ctx::HostStage& st, void* dst, const void* sr
 
 rt_status upload_offsets(rt_ctx* c, const uint32_t* h, uint32_t count, cudaStream_t s) {
   if (count > c->off_cap) {
-    if (c->d_off) cudaFree(c->d_off);
+    if (no_growth_in_capture(c, s) != RT_OK) return RT_EINVAL;
+    retire(c, c->d_off);
     c->d_off = nullptr;
     c->off_cap = 0;
     if (cudaMalloc(&c->d_off, (size_t)count * 4) != cudaSuccess) return fail(c, RT_ENOMEM, "offsets buffer");
@@ -410,6 +448,8 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
     cudaFree(c->io);
+    for (void* p : c->captured_stage) cudaFreeHost(p);
+    for (void* p : c->retired) cudaFree(p);
     for (rt_ctx::HostStage* st : {&c->st_off, &c->st_prof}) {
       if (st->p) cudaFreeHost(st->p);
       if (st->ev) cudaEventDestroy(st->ev);
@@ -463,6 +503,7 @@ static rt_status score_common(rt_ctx* c, const uint8_t* d_bytes, const uint32_t*
     return fail(c, RT_EINVAL, "d_feat is NULL");
   }
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   rtlm::ScoreLaunch a{};
   a.bytes = d_bytes;
   a.offsets = d_offsets;
@@ -504,6 +545,7 @@ rt_status rt_predict(rt_ctx* c, const uint16_t* d_feat, uint32_t n, const rt_reg
   if (!d_feat || !reg || !d_u) return fail(c, RT_EINVAL, "null argument");
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaError_t e = rtlm::launch_predict(d_feat, n, *reg, d_u, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_predict");
   return RT_OK;
@@ -532,6 +574,7 @@ rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d
   if (!d_feat || !d_u) return fail(c, RT_EINVAL, "null argument");
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_mlp");
   return RT_OK;
@@ -544,7 +587,8 @@ rt_status rt_fit_rule(rt_ctx* c, const uint16_t* d_feat, const float* d_target, 
   if (!d_feat || !d_target || !d_out) return fail(c, RT_EINVAL, "null argument");
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
-  rt_status st = ensure_ws(c, rtlm::fit_workspace());
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
+  rt_status st = ensure_ws(c, rtlm::fit_workspace(), cs(stream));
   if (st != RT_OK) return st;
   cudaError_t e = rtlm::launch_fit(d_feat, d_target, n, static_cast<double*>(c->ws), d_out, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_fit");
@@ -561,7 +605,8 @@ rt_status rt_quantile(rt_ctx* c, const float* d_u, uint32_t n, double k, float* 
   uint32_t r = kn < 1.0 ? 0u : (uint32_t)kn - 1u;
   if (r >= n) r = n - 1;
   DeviceGuard g(c->device);
-  rt_status st = ensure_ws(c, rtlm::quantile_workspace(n));
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
+  rt_status st = ensure_ws(c, rtlm::quantile_workspace(n), cs(stream));
   if (st != RT_OK) return st;
   cudaError_t e = rtlm::launch_quantile(d_u, n, r, c->ws, d_out, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_quantile");
@@ -577,6 +622,7 @@ rt_status rt_key(rt_ctx* c, const float* d_u, const uint16_t* d_feat, const int6
   rt_status st = check_profile(c, prof, false);
   if (st != RT_OK) return st;
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaError_t e = rtlm::launch_key(d_u, d_feat, d_arr, d_D_in, n, *prof, d_key, d_D_out, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_key");
   return RT_OK;
@@ -598,6 +644,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
   if (n && (!d_key || !d_u || !d_perm || !d_batch_of || !d_slot_of || !d_core_of))
     return fail(c, RT_EINVAL, "null device buffer");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaStream_t s = cs(stream);
   // workspace: seg counts | big-queue sort + gather
   size_t big_ws = 0;
@@ -609,7 +656,7 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
     }
   }
   const size_t cnt_bytes = (((size_t)nq + 1) * 4 + 255) & ~size_t(255);
-  st = ensure_ws(c, cnt_bytes + big_ws);
+  st = ensure_ws(c, cnt_bytes + big_ws, s);
   if (st != RT_OK) return st;
   st = upload_offsets(c, h_seg_off, nq + 1, s);
   if (st != RT_OK) return st;
@@ -644,7 +691,8 @@ rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const 
 
 static rt_status upload_profiles(rt_ctx* c, const rt_profile* h_profiles, uint32_t np, cudaStream_t s) {
   if (np > c->prof_cap) {
-    if (c->d_prof) cudaFree(c->d_prof);
+    if (no_growth_in_capture(c, s) != RT_OK) return RT_EINVAL;
+    retire(c, c->d_prof);
     c->d_prof = nullptr;
     c->prof_cap = 0;
     if (cudaMalloc(&c->d_prof, np * sizeof(rt_profile)) != cudaSuccess) return fail(c, RT_ENOMEM, "profiles");
@@ -681,6 +729,7 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   }
   if (h_trace_off[nt] && (!d_arr || !d_len || !d_u || !d_key || !d_D)) return fail(c, RT_EINVAL, "null task array");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaStream_t s = cs(stream);
   rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
   if (st != RT_OK) return st;
@@ -698,7 +747,7 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   a.trace_prof = d_trace_prof;
   a.stats = d_stats;
   a.end_us = d_end_us;
-  st = ensure_ws(c, (size_t)nt * rtlm::kMaxTrace * sizeof(uint16_t));
+  st = ensure_ws(c, (size_t)nt * rtlm::kMaxTrace * sizeof(uint16_t), s);
   if (st != RT_OK) return st;
   a.sidx = static_cast<uint16_t*>(c->ws);
   cudaError_t e = rtlm::launch_replay(a, s);
@@ -718,8 +767,10 @@ rt_status rt_score_schedule_host(rt_ctx* c, const uint8_t* h_bytes, const uint32
   const size_t need = up(nbytes) + up(4 * ((size_t)n + 1)) + up(4 * (size_t)n) + up(8 * (size_t)n) +
                       3 * up(4 * (size_t)n) + 2 * up(n) + up(8);
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   if (need > c->io_size) {
-    if (c->io) cudaFree(c->io);  // implicit device sync: no in-flight user
+    if (no_growth_in_capture(c, cs(stream)) != RT_OK) return RT_EINVAL;
+    retire(c, c->io);  // cudaFree: implicit device sync, no in-flight user
     c->io = nullptr;
     c->io_size = 0;
     cudaError_t e = cudaMalloc(&c->io, need);
@@ -757,6 +808,7 @@ rt_status rt_reduce_stats(rt_ctx* c, const rt_trace_stats* d_stats, uint32_t nt,
   if (!nt) return RT_OK;
   if (!d_stats || !d_sums || !ngroups) return fail(c, RT_EINVAL, "null argument");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaError_t e = rtlm::launch_reduce_stats(d_stats, nt, d_group_of, ngroups, d_sums, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_reduce_stats");
   return RT_OK;
@@ -773,6 +825,7 @@ rt_status rt_trace_report(rt_ctx* c, const int64_t* d_arrival_us, const int64_t*
     if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
   }
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaStream_t s = cs(stream);
   rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
   if (st != RT_OK) return st;
@@ -795,6 +848,7 @@ rt_status rt_trace_utilization(rt_ctx* c, const uint16_t* d_len, const uint64_t*
   if (st != RT_OK) return st;
   if (h_trace_off[nt] && (!d_len || !d_key || !d_end_us)) return fail(c, RT_EINVAL, "null task array");
   DeviceGuard g(c->device);
+  if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaStream_t s = cs(stream);
   st = upload_offsets(c, h_trace_off, nt + 1, s);
   if (st != RT_OK) return st;

@@ -452,3 +452,34 @@ def test_score_schedule_host_matches_oracle(ctx_v1, lex_v1):
     assert (out["batch_of"].numpy().view(U32) == s["batch_of"]).all()
     assert (out["slot_of"].numpy() == s["slot_of"]).all()
     assert (out["core_of"].numpy() == s["core_of"]).all()
+
+
+def test_graph_capture_of_the_step(ctx_v1, lex_v1):
+    """rt_score_key + rt_schedule captured in a CUDA graph (the bench's pipelined
+    step) and replayed: bit-identical to the call-by-call path; staged host
+    offsets of the capture stay valid after later normal calls."""
+    d = configs.config2(n=30000)
+    n = len(d["offsets"]) - 1
+    data, off = dev(d["data"]), dev(d["offsets"])
+    seg = np.asarray([0, n], U32)
+    o1 = ctx_v1.score_key(data, off, d["regressor"], d["profile"], want_D=False)
+    s1 = ctx_v1.schedule(o1["key"], o1["u"], seg, d["profile"])
+    ref = {k: v.clone() for k, v in s1.items()}
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream(DEV)
+    outs = {"u": torch.empty(n, dtype=torch.float32, device=DEV), "key": torch.empty(n, dtype=torch.int64, device=DEV)}
+    souts = {k: torch.empty_like(v) for k, v in ref.items()}
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st, capture_error_mode="relaxed"):
+        ctx_v1.score_key(data, off, d["regressor"], d["profile"], want_D=False, out=outs)
+        ctx_v1.schedule(outs["key"], outs["u"], seg, d["profile"], out=souts)
+    for k in souts:
+        souts[k].zero_()
+    # a normal call on another queue size in between (re-stages offsets)
+    o2 = ctx_v1.score_key(data, off, d["regressor"], d["profile"], want_D=False)
+    ctx_v1.schedule(o2["key"], o2["u"], np.asarray([0, 100, n], U32), d["profile"])
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    for k in ref:
+        assert torch.equal(souts[k], ref[k]), k
