@@ -27,6 +27,13 @@
  *    call returns without waiting for the stream (it waits only for the
  *    previous call's staging copy on the same context).  Kernels are
  *    pure functions of their inputs: same inputs -> same bits.
+ *  - CUDA graphs: every call may be captured (relaxed capture mode) once the
+ *    same call has run outside capture (so no context buffer has to grow
+ *    during capture; growth under capture fails with RT_EINVAL).  Host
+ *    arguments staged under capture get a pinned block of their own that the
+ *    graph's copy node reads at every replay; buffers a graph may address are
+ *    kept until rt_destroy even if a later call replaces them.  Replays of a
+ *    context's graphs and its other calls must be ordered like ordinary calls.
  *
  * Citations: P:a-b = PAPER.md lines (v1 P:1-912, v2 P:913-1887); S:a-b =
  * SPEC.md lines; R-* = readings in DESIGN.md §2.
