@@ -240,6 +240,16 @@ rt_status rt_schedule(rt_ctx* ctx, const uint64_t* d_key, const float* d_u, cons
                       const rt_profile* prof, uint32_t cores, uint32_t* d_perm, uint32_t* d_batch_of,
                       uint8_t* d_slot_of, uint8_t* d_core_of, uint32_t* d_seg_batch_off, rt_stream stream);
 
+/* The north-star form rt_schedule(queue, deadlines, cores): the priority keys
+ * are computed in-call from d_u and the caller's relative deadlines d_D_us
+ * (as rt_key with d_D_in = d_D_us; d_arrival_us, nullable, for FIFO/EDF) into
+ * a buffer owned by the context, then the queues are scheduled exactly as by
+ * rt_schedule.  Same outputs and errors as rt_schedule. */
+rt_status rt_schedule_deadlines(rt_ctx* ctx, const float* d_u, const uint32_t* d_D_us, const int64_t* d_arrival_us,
+                                const uint32_t* h_seg_off, uint32_t nq, const rt_profile* prof, uint32_t cores,
+                                uint32_t* d_perm, uint32_t* d_batch_of, uint8_t* d_slot_of, uint8_t* d_core_of,
+                                uint32_t* d_seg_batch_off, rt_stream stream);
+
 /* ---------------------------------------------------------------- (5) simulate */
 
 /* Discrete-event replay of nt traces (§V-A; R-REPLAY, R-LAT,

@@ -26,7 +26,8 @@ RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "R
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
            "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report",
-           "rt_trace_utilization", "rt_set_sm_limit", "rt_score_schedule_host"]
+           "rt_trace_utilization", "rt_set_sm_limit", "rt_score_schedule_host",
+           "rt_schedule_deadlines"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -135,6 +136,8 @@ def load_library(path: str = LIB_PATH):
     L.rt_trace_report.argtypes = [V, P, P, P, U32, P, V]
     L.rt_trace_utilization.restype = I32
     L.rt_trace_utilization.argtypes = [V, P, P, P, P, U32, P, U32, P, P, V]
+    L.rt_schedule_deadlines.restype = I32
+    L.rt_schedule_deadlines.argtypes = [V, P, P, P, P, U32, ctypes.POINTER(Profile), U32, P, P, P, P, P, V]
     L.rt_score_schedule_host.restype = I32
     L.rt_score_schedule_host.argtypes = [V, P, P, U32, ctypes.POINTER(Regressor), ctypes.POINTER(Profile), U32,
                                          P, P, P, V]
@@ -380,6 +383,26 @@ class Context:
             self._h, _hptr(h_bytes, torch.uint8, "h_bytes"), _hptr(h_offsets, torch.int32, "h_offsets"), n,
             ctypes.byref(r), ctypes.byref(p), c, _hptr(out["batch_of"], torch.int32, "batch_of"),
             _hptr(out["slot_of"], torch.uint8, "slot_of"), _hptr(out["core_of"], torch.uint8, "core_of"),
+            self._stream()))
+        return out
+
+    def schedule_deadlines(self, u, D, seg_off, prof: dict, arrival=None, cores: int | None = None):
+        """rt_schedule_deadlines: keys from u and relative deadlines D (int32 view of
+        u32 µs) in-call, then the one-pass schedule.  Returns dict of device tensors."""
+        torch = _torch()
+        so = np.ascontiguousarray(np.asarray(seg_off, dtype=np.uint32))
+        nq = len(so) - 1
+        n = int(so[-1])
+        out = {"perm": self._empty((n,), torch.int32), "batch_of": self._empty((n,), torch.int32),
+               "slot_of": self._empty((n,), torch.uint8), "core_of": self._empty((n,), torch.uint8),
+               "seg_batch_off": self._empty((nq + 1,), torch.int32)}
+        p = make_profile(prof)
+        c = int(prof["cores"] if cores is None else cores)
+        self._check(self._L.rt_schedule_deadlines(
+            self._h, _ptr(u, torch.float32, "u"), _ptr(D, torch.int32, "D"), _ptr(arrival, torch.int64, "arrival"),
+            so.ctypes.data_as(ctypes.c_void_p), nq, ctypes.byref(p), c, _ptr(out["perm"], torch.int32, "perm"),
+            _ptr(out["batch_of"], torch.int32, "batch_of"), _ptr(out["slot_of"], torch.uint8, "slot_of"),
+            _ptr(out["core_of"], torch.uint8, "core_of"), _ptr(out["seg_batch_off"], torch.int32, "seg_batch_off"),
             self._stream()))
         return out
 

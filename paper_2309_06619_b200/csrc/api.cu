@@ -30,6 +30,8 @@ struct rt_ctx {
   uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp)
   void* io = nullptr;        // device buffers of rt_score_schedule_host
   size_t io_size = 0;
+  uint64_t* kbuf = nullptr;  // keys of rt_schedule_deadlines
+  size_t kbuf_n = 0;
   // pinned staging of small host arguments (segment / trace offsets, profiles): a
   // copy from pageable memory would synchronise the stream before it starts
   struct HostStage {
@@ -448,6 +450,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
     cudaFree(c->io);
+    cudaFree(c->kbuf);
     for (void* p : c->captured_stage) cudaFreeHost(p);
     for (void* p : c->retired) cudaFree(p);
     for (rt_ctx::HostStage* st : {&c->st_off, &c->st_prof}) {
@@ -753,6 +756,29 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   cudaError_t e = rtlm::launch_replay(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
   return RT_OK;
+}
+
+rt_status rt_schedule_deadlines(rt_ctx* c, const float* d_u, const uint32_t* d_D_us, const int64_t* d_arrival_us,
+                                const uint32_t* h_seg_off, uint32_t nq, const rt_profile* prof, uint32_t cores,
+                                uint32_t* d_perm, uint32_t* d_batch_of, uint8_t* d_slot_of, uint8_t* d_core_of,
+                                uint32_t* d_seg_batch_off, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (!h_seg_off) return fail(c, RT_EINVAL, "h_seg_off is NULL");
+  const uint32_t n = h_seg_off[nq];
+  if (n && (!d_u || !d_D_us)) return fail(c, RT_EINVAL, "u / deadlines are NULL");
+  if (n > c->kbuf_n) {
+    if (no_growth_in_capture(c, cs(stream)) != RT_OK) return RT_EINVAL;
+    DeviceGuard g(c->device);
+    retire(c, c->kbuf);
+    c->kbuf = nullptr;
+    c->kbuf_n = 0;
+    if (cudaMalloc(&c->kbuf, (size_t)n * sizeof(uint64_t)) != cudaSuccess) return fail(c, RT_ENOMEM, "key buffer");
+    c->kbuf_n = n;
+  }
+  rt_status st = rt_key(c, d_u, nullptr, d_arrival_us, d_D_us, n, prof, c->kbuf, nullptr, stream);
+  if (st != RT_OK) return st;
+  return rt_schedule(c, c->kbuf, d_u, h_seg_off, nq, prof, cores, d_perm, d_batch_of, d_slot_of, d_core_of,
+                     d_seg_batch_off, stream);
 }
 
 rt_status rt_score_schedule_host(rt_ctx* c, const uint8_t* h_bytes, const uint32_t* h_offsets, uint32_t n,

@@ -483,3 +483,24 @@ def test_graph_capture_of_the_step(ctx_v1, lex_v1):
     torch.cuda.synchronize()
     for k in ref:
         assert torch.equal(souts[k], ref[k]), k
+
+
+@pytest.mark.parametrize("policy", ["UP", "EDF", "FIFO"])
+def test_schedule_deadlines_form(ctx_v1, lex_v1, policy):
+    """rt_schedule_deadlines (north-star form: queue, deadlines, cores): keys from
+    u and caller deadlines in-call; equals the oracle's key + schedule on several
+    queues (one big, two small), arrivals given for FIFO/EDF."""
+    d = configs.config2(n=6000)
+    prof = dict(d["profile"], policy=policy)
+    n = len(d["offsets"]) - 1
+    rng = np.random.default_rng(5)
+    f = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+    u = oracle.predict(f, d["regressor"])
+    D = rng.integers(1, 3_000_000, n).astype(U32)
+    arr = np.sort(rng.integers(0, 10_000_000, n)).astype(np.int64)
+    k, _ = oracle.key(u, f, prof, r_us=arr, D_in=D)
+    seg = np.asarray([0, 100, 2148, n], U32)
+    s = oracle.schedule(k, u, seg, prof)
+    g = ctx_v1.schedule_deadlines(dev(u), dev(D), seg, prof, arrival=dev(arr))
+    torch.cuda.synchronize()
+    _check_schedule(g, s, 3)
