@@ -353,6 +353,11 @@ def native(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_requests_timing(d2, n, reps=4)
+        if traces is not None:
+            try:
+                traces["cpu_baseline"] = oracle_traces_timing(args.per_trace)
+            except Exception as e:  # reported, never fatal for the bench line
+                traces["cpu_baseline"] = {"error": repr(e)[:200]}
 
     if rank == 0:
         line = {
@@ -789,6 +794,66 @@ def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_
                         "tight, UP+C+O; one NCCL all-reduce of per-LM int64 sums",
             "mean_response_s_per_lm": [round(float(s[f, 0]) / max(1, s[f, 1]) / 1e6, 4) for f in range(4)],
             "miss_ratio_per_lm": [round(float(s[f, 2]) / max(1, s[f, 1]), 4) for f in range(4)]}
+
+
+def _oracle_traces_worker(args):
+    """One host process of the traces CPU baseline: the oracle (single thread, as
+    it stands) scores, keys and replays its own config-3 traces; returns (traces,
+    seconds of oracle work)."""
+    first, count, per_trace = args
+    import oracle
+    from rtgen import configs
+    per_lm = 1024
+    d = configs.traces(3, range(first, first + count), per_trace, lambda t: (t // per_lm) % 4)
+    lex = oracle.Lexicon(d["lexicon"])
+    t0 = time.time()
+    f = oracle.rule_gen(lex, d["data"], d["offsets"])
+    n = len(f)
+    u = np.zeros(n, np.float32)
+    k = np.zeros(n, np.uint64)
+    D = np.zeros(n, np.uint32)
+    for t in range(count):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        lm = int(d["trace_prof"][t])
+        u[lo:hi] = oracle.predict(f[lo:hi], d["regressors"][lm])
+        k[lo:hi], D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], d["profiles"][lm], r_us=d["arrival_us"][lo:hi])
+    oracle.simulate(d["arrival_us"], d["true_len"], u, k, D, d["trace_off"], d["profiles"], d["trace_prof"])
+    return count, time.time() - t0
+
+
+def oracle_traces_timing(per_trace: int, single: int = 512, per_proc: int = 128):
+    """The oracle on config-3 traces (SURVEY §8(d) Oracle (i) and (ii)): one
+    thread on `single` traces, and one process per host core on `per_proc`
+    traces each (disjoint trace ids); traces/s = traces / the slowest process's
+    oracle seconds."""
+    n1, s1 = _oracle_traces_worker((0, single, per_trace))
+    procs = min(os.cpu_count() or 1, 128)  # one per host core (capped)
+    # one plain subprocess per core (no multiprocessing pool: a worker that
+    # fails to start must not hang the bench), each killed after 180 s
+    code = ("import sys, json; sys.path.insert(0, {root!r}); import bench; "
+            "print(json.dumps(bench._oracle_traces_worker(({first}, {count}, {per}))))")
+    ps = [subprocess.Popen([sys.executable, "-c", code.format(root=ROOT, first=single + i * per_proc, count=per_proc,
+                                                              per=per_trace)],
+                           stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for i in range(procs)]
+    res = []
+    t_end = time.time() + 180
+    for p in ps:
+        try:
+            out, _ = p.communicate(timeout=max(1.0, t_end - time.time()))
+            res.append(tuple(json.loads(out.strip().splitlines()[-1])))
+        except Exception:
+            p.kill()
+    if not res:
+        raise RuntimeError("no oracle worker finished")
+    tot = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"single_thread": {"value": round(n1 / s1, 2), "unit": "traces/s", "cores": 1, "kind": "oracle",
+                              "sample": f"{single} config-3 traces x {per_trace} requests (score+key+replay)",
+                              "seconds": round(s1, 3)},
+            "per_core": {"value": round(tot / wall, 2), "unit": "traces/s", "cores": len(res), "kind": "oracle",
+                         "host_cores": os.cpu_count(),
+                         "sample": f"{len(res)} processes x {per_proc} disjoint config-3 traces x {per_trace} requests",
+                         "seconds": round(wall, 3)}}
 
 
 def oracle_requests_timing(d2, n_sample: int, reps: int = 1):
