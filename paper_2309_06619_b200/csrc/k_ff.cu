@@ -358,35 +358,48 @@ __device__ __forceinline__ bool ratio_bad(uint64_t lo, uint64_t hi, float lam) {
   return !(kk_u(hi) <= __fmul_rn(lam, kk_u(lo)));
 }
 
+// The λ-chain of a chunk depends only on its multiset of u values: equal
+// values are adjacent in the (u, rank) order and never violate u <= λ·u, so
+// the violating adjacent pairs are those between consecutive DISTINCT values.
+// Adding x to a chunk: no change if its u is already present, else the pairs
+// (pred, x), (x, succ) replace (pred, succ), with pred / succ the nearest
+// smaller / larger distinct u.  All comparisons on the u bits (u >= 0, so bit
+// order = value order), stored + 1 so that 0 means "none".
 __global__ void __launch_bounds__(256) k_ff_vtab(FF f) {
-  __shared__ uint64_t t[256 + kMaxWindow];
+  __shared__ uint32_t t[256 + kMaxWindow];
   const uint32_t NR = f.scal[2], C = f.C;
   const uint32_t j0 = blockIdx.x * 256u;
   const uint32_t nwords = (NR + 31) / 32 + 1;
   if (j0 >= nwords * 32) return;  // block-uniform
   const uint32_t j = j0 + threadIdx.x;
-  for (uint32_t i = threadIdx.x; i < 256 + C; i += 256) t[i] = j0 + i < NR ? f.rseq[j0 + i] : 0ull;
+  for (uint32_t i = threadIdx.x; i < 256 + C; i += 256)
+    t[i] = j0 + i < NR ? __float_as_uint(kk_u(f.rseq[j0 + i])) + 1u : 0u;
   __syncthreads();
-  const uint64_t* w = t + threadIdx.x;
+  const uint32_t* w = t + threadIdx.x;
   const float lam = f.lambda;
+  auto bad2 = [&](uint32_t lo1, uint32_t hi1) {  // u values + 1
+    return !(__uint_as_float(hi1 - 1u) <= __fmul_rn(lam, __uint_as_float(lo1 - 1u)));
+  };
   int bad = 0;
-  uint64_t mx = 0;
+  uint32_t mx = 0;
   bool passC = false;
   for (uint32_t c = 1; c <= C; ++c) {
     const bool full = j + c <= NR;
     if (full) {
-      const uint64_t x = w[c - 1];
-      uint64_t pred = 0, succ = kInf;
+      const uint32_t x = w[c - 1];
+      uint32_t pred = 0u, succ = 0xFFFFFFFFu;
+      bool dup = false;
       for (uint32_t b = 0; b + 1 < c; ++b) {
-        const uint64_t y = w[b];
+        const uint32_t y = w[b];
         pred = (y < x && y > pred) ? y : pred;
         succ = (y > x && y < succ) ? y : succ;
+        dup |= y == x;
       }
-      const bool hp = pred != 0, hs = succ != kInf;
-      bad += (hp && ratio_bad(pred, x, lam)) + (hs && ratio_bad(x, succ, lam)) - (hp && hs && ratio_bad(pred, succ, lam));
+      const bool hp = pred != 0u, hs = succ != 0xFFFFFFFFu;
+      if (!dup) bad += (hp && bad2(pred, x)) + (hs && bad2(x, succ)) - (hp && hs && bad2(pred, succ));
       mx = x > mx ? x : mx;
     }
-    if (j < NR) f.vt[(size_t)(c - 1) * f.vstride + j] = (full && bad == 0) ? kk_u(mx) : __int_as_float(0x7f800000);
+    if (j < NR) f.vt[(size_t)(c - 1) * f.vstride + j] = (full && bad == 0) ? __uint_as_float(mx - 1u) : __int_as_float(0x7f800000);
     if (c == C) passC = full && bad == 0;
   }
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, passC);
