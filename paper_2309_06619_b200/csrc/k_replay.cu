@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       const uint32_t rk = wl * 32 + (__ffs(word) - 1);
       const uint32_t i = sm.sidx[rk];
       const int64_t end = now + (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)g_len[i]);
+      __syncwarp();  // every lane's reads of ready_cpu / core_free before lane 0 updates them
       if (lane == 0) {
         sm.core_free[c] = end;
         sm.ready_cpu[wl] = word & (word - 1u);
