@@ -242,9 +242,11 @@ rt_status rt_schedule(rt_ctx* ctx, const uint64_t* d_key, const float* d_u, cons
 
 /* The north-star form rt_schedule(queue, deadlines, cores): the priority keys
  * are computed in-call from d_u and the caller's relative deadlines d_D_us
- * (as rt_key with d_D_in = d_D_us; d_arrival_us, nullable, for FIFO/EDF) into
- * a buffer owned by the context, then the queues are scheduled exactly as by
- * rt_schedule.  Same outputs and errors as rt_schedule. */
+ * (the user deadline t_J of P:1286; as rt_key with d_D_in = d_D_us, Eq. 3
+ * P:376-378 / Eq. 2 P:363-365 / baselines P:637-646; d_arrival_us, nullable,
+ * for FIFO/EDF) into a buffer owned by the context, then the queues are
+ * scheduled exactly as by rt_schedule (Alg. 1).  Same outputs and
+ * errors as rt_schedule. */
 rt_status rt_schedule_deadlines(rt_ctx* ctx, const float* d_u, const uint32_t* d_D_us, const int64_t* d_arrival_us,
                                 const uint32_t* h_seg_off, uint32_t nq, const rt_profile* prof, uint32_t cores,
                                 uint32_t* d_perm, uint32_t* d_batch_of, uint8_t* d_slot_of, uint8_t* d_core_of,
@@ -288,7 +290,8 @@ rt_status rt_trace_utilization(rt_ctx* ctx, const uint16_t* d_true_len, const ui
 /* ---------------------------------------------------------------- (4b) end to end from host */
 
 /* The whole requests path of one queue from HOST buffers (the bench's e2e
- * leg): copies h_bytes[0 .. h_offsets[n]) and h_offsets[n+1] to device buffers
+ * leg; RuleGen + Eq. 1 + Eq. 3 + Alg. 1's online part, P:211-233, P:346-378,
+ * P:467-481): copies h_bytes[0 .. h_offsets[n]) and h_offsets[n+1] to device buffers
  * owned by the context, runs rt_score_key (1)-(3) and rt_schedule (4) on the
  * queue [0, n), and copies the assignment back: h_batch_of[n] (global GPU
  * batch id, UINT32_MAX for CPU tasks), h_slot_of[n], h_core_of[n] (as in
