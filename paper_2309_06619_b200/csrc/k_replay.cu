@@ -131,19 +131,22 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   int64_t resp = 0;     // per-lane partial sums
   uint32_t misses = 0;
   const uint32_t lt = (1u << lane) - 1u;
+  // the next 32 arrival times, one per lane (index next + lane), reloaded only
+  // when `next` advances: events that admit nothing read no arrival times
+  int64_t rw = lane < n ? sm.r[lane] : INT64_MAX;
 
   for (;;) {
     // ---- admit arrivals <= now (arrival order is non-decreasing)
     while (next < n) {
       const uint32_t i = next + lane;
-      const bool arr = i < n && sm.r[i] <= now;
+      const bool arr = rw <= now;  // rw = INT64_MAX past the end
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
       const uint32_t cnt = __popc(bal);  // a prefix of ones
       const uint32_t rk = arr ? (uint32_t)sm.rank[i] : 0xFFFFFFFFu;
       const uint32_t cb = __ballot_sync(0xFFFFFFFFu, rk < ncpu);
       const uint32_t nc = __popc(cb);
       if (gpu_ready == 0 && (bal & ~cb)) {  // the first waiting GPU-class task is the oldest
-        oldest_r = sm.r[next + __ffs(bal & ~cb) - 1];
+        oldest_r = __shfl_sync(0xFFFFFFFFu, rw, __ffs(bal & ~cb) - 1);
         have_oldest = true;
       }
       cpu_ready += nc;
@@ -156,7 +159,10 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           atomicOr(&sm.wait_arr[i >> 5], 1u << (i & 31));
         }
       }
-      next += cnt;
+      if (cnt) {
+        next += cnt;
+        rw = next + lane < n ? sm.r[next + lane] : INT64_MAX;
+      }
       if (cnt < 32) break;
     }
     __syncwarp();
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     if (done >= n) break;
     // ---- next event time
     int64_t nxt = INT64_MAX;
-    if (next < n) nxt = sm.r[next];
+    if (next < n) nxt = __shfl_sync(0xFFFFFFFFu, rw, 0);
     if (gpu_free > now) nxt = min(nxt, gpu_free);
     const bool cpu_waiting = cpu_ready != 0;
     if (cpu_waiting) {
