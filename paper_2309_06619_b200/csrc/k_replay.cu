@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       const uint32_t i = next + lane;
       const bool arr = rw <= now;  // rw = INT64_MAX past the end
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
+      if (!bal) break;  // no arrival due (most events)
       const uint32_t cnt = __popc(bal);  // a prefix of ones
       const uint32_t rk = arr ? (uint32_t)sm.rank[i] : 0xFFFFFFFFu;
       const uint32_t cb = __ballot_sync(0xFFFFFFFFu, rk < ncpu);
@@ -167,12 +168,11 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     }
     __syncwarp();
     // ---- CPU cores: highest-key ready CPU task -> lowest-index free core
-    while (cpu_ready) {
-      const uint32_t wcpu = sm.ready_cpu[lane];
-      const uint32_t any = __ballot_sync(0xFFFFFFFFu, wcpu != 0);
-      if (!any) break;
+    while (cpu_ready) {  // the ready bitmap is non-empty: find a free core first
       const uint32_t fm = __ballot_sync(0xFFFFFFFFu, lane < cores && sm.core_free[lane] <= now);
       if (!fm) break;
+      const uint32_t wcpu = sm.ready_cpu[lane];
+      const uint32_t any = __ballot_sync(0xFFFFFFFFu, wcpu != 0);
       const uint32_t c = __ffs(fm) - 1, wl = __ffs(any) - 1;
       const uint32_t word = __shfl_sync(0xFFFFFFFFu, wcpu, wl);
       const uint32_t rk = wl * 32 + (__ffs(word) - 1);
