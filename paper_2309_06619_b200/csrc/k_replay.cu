@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   uint32_t next = 0, done = 0;
   uint32_t cpu_ready = 0, gpu_ready = 0;  // ready-set sizes (warp-uniform)
   bool have_oldest = false;                // oldest_r = arrival of the oldest waiting GPU-class task
+  int64_t cpu_min_free = INT64_MAX;        // min core clock while CPU tasks wait (see below)
+  bool cpu_min_valid = false;
   int64_t oldest_r = 0;
   int64_t resp = 0;     // per-lane partial sums
   uint32_t misses = 0;
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     }
     __syncwarp();
     // ---- CPU cores: highest-key ready CPU task -> lowest-index free core
+    bool cpu_started = false;
     while (cpu_ready) {  // the ready bitmap is non-empty: find a free core first
       const uint32_t fm = __ballot_sync(0xFFFFFFFFu, lane < cores && sm.core_free[lane] <= now);
       if (!fm) break;
@@ -188,8 +191,10 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       }
       ++done;
       --cpu_ready;
+      cpu_started = true;
       __syncwarp();
     }
+    if (cpu_started) cpu_min_valid = false;  // a core clock changed
     // ---- GPU dispatch
     bool waiting = false;
     if (gpu_free <= now) {
@@ -332,8 +337,13 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     if (gpu_free > now) nxt = min(nxt, gpu_free);
     const bool cpu_waiting = cpu_ready != 0;
     if (cpu_waiting) {
-      int64_t cf = (lane < cores && sm.core_free[lane] > now) ? sm.core_free[lane] : INT64_MAX;
-      nxt = min(nxt, warp_min64(cf));
+      // earliest core clock, recomputed only after a core was given a task: while
+      // CPU tasks stay ready every core is busy, so this is the next CPU event
+      if (!cpu_min_valid) {
+        cpu_min_free = warp_min64(lane < cores ? sm.core_free[lane] : INT64_MAX);
+        cpu_min_valid = true;
+      }
+      nxt = min(nxt, cpu_min_free);
     }
     if (waiting) nxt = min(nxt, oldest_r + p.xi_us);
     if (nxt == INT64_MAX) break;  // unreachable with valid inputs (cores >= 1)
