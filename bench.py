@@ -525,11 +525,53 @@ def malicious_leg(args, ctx, configs, dev, rank, max_over_ranks):
             out["mean_response_s"][name].append(round(resp / max(cnt, 1) / 1e6, 4))
             out["miss_ratio"][name].append(round(miss / max(cnt, 1), 4))
     out["traces_per_point"] = nt
+    # periodic release: each task released at the previous task's
+    # deadline, tight / loose; deadlines from the GPU path (rt_score_key)
+    out["periodic"] = periodic_leg(ctx, configs.traces(3, range(12000 + rank * nt, 12000 + (rank + 1) * nt), 1000,
+                                                       lambda t: ((t - 12000 - rank * nt) * 4) // nt), dev)
     out["device_ms_total"] = round(max_over_ranks(dev_ms), 3)
     out["traces_per_s"] = round(nt * len(ratios) * 2 / (out["device_ms_total"] / 1e3), 1)
     out["note"] = ("statistics of the synthetic workload, not gated: config 3's tight deadlines overload the "
                    "executors (miss ratio > 0.9), and offloaded malicious tasks queue on 4 CPU cores at gamma = 5")
     return out
+
+
+def periodic_leg(ctx, base, dev):
+    """Miss ratio under periodic release for UP+C+O, EDF, LUF, MUF,
+    tight and loose deadlines; arrivals r_{i+1} = r_i + D_i from the device-computed
+    deadlines (statistics, not gated)."""
+    import torch
+    from rtgen import configs
+    import paper_2309_06619_b200 as rt
+    n = len(base["arrival_us"])
+    feat = torch.empty((n, 8), dtype=torch.int16, device=dev)
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    tmpk = torch.empty(n, dtype=torch.int64, device=dev)
+    groups = _lm_groups(base, dev)
+    for f, r0, r1, gd, so in groups:
+        ctx.score_key(gd, so, base["regressors"][f], base["profiles"][f], want_feat=True, want_D=False,
+                      out={"u": u[r0:r1], "key": tmpk[r0:r1], "feat": feat[r0:r1]})
+    tl = torch.from_numpy(base["true_len"].view(np.int16)).to(dev)
+    tp = torch.from_numpy(base["trace_prof"].view(np.int16)).to(dev)
+    pols = {"UP+C+O": {}, "EDF": {"policy": "EDF", "consolidate": 0, "offload": 0},
+            "LUF": {"policy": "LUF", "consolidate": 0, "offload": 0},
+            "MUF": {"policy": "MUF", "consolidate": 0, "offload": 0}}
+    res = {}
+    for tight in (1, 2):
+        for name, ov in pols.items():
+            profs = [dict(p, tightness=tight, **ov) for p in base["profiles"]]
+            D = torch.empty(n, dtype=torch.int32, device=dev)
+            key = torch.empty(n, dtype=torch.int64, device=dev)
+            for f, r0, r1, gd, so in groups:
+                ctx.key(u[r0:r1], profs[f], feat=feat[r0:r1], key=key[r0:r1], D_out=D[r0:r1])
+            arr_np = configs.periodic_arrivals(base["trace_off"], D.cpu().numpy().view(np.uint32))
+            arr = torch.from_numpy(arr_np).to(dev)
+            for f, r0, r1, gd, so in groups:  # EDF keys depend on the release times
+                ctx.key(u[r0:r1], profs[f], feat=feat[r0:r1], arrival=arr[r0:r1], key=key[r0:r1], D_out=D[r0:r1])
+            stats, _ = ctx.simulate(arr, tl, u, key, D, base["trace_off"], profs, tp)
+            st = rt.decode_stats(stats)
+            res[f"{name}/{'tight' if tight == 1 else 'loose'}"] = round(float(st["misses"].sum()) / max(1, int(st["n"].sum())), 4)
+    return {"miss_ratio": res, "traces": len(base["trace_off"]) - 1}
 
 
 def traces_leg(args, rt, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):

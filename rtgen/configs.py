@@ -194,6 +194,23 @@ def config5_arrivals(d: dict, mult: float) -> np.ndarray:
                            for t in d["trace_ids"]])
 
 
+# ---------------------------------------------------------------- NEXT-3: periodic release
+def periodic_arrivals(trace_off, D_us) -> np.ndarray:
+    """Periodic release ("the deadline of one task serves as the
+    release time for the subsequent one"): within each trace r_0 = 0 and
+    r_{i+1} = r_i + D_i, with D the tasks' relative deadlines (µs) as computed
+    by the path (tight: mu*|J|, loose: twice that).  Workload
+    construction only (a running sum of the given deadlines)."""
+    D = np.asarray(D_us, dtype=np.int64)
+    toff = np.asarray(trace_off, dtype=np.int64)
+    r = np.zeros(len(D), np.int64)
+    for t in range(len(toff) - 1):
+        lo, hi = int(toff[t]), int(toff[t + 1])
+        if hi > lo + 1:
+            r[lo + 1:hi] = np.cumsum(D[lo:hi - 1])
+    return r
+
+
 # ---------------------------------------------------------------- NEXT-3: malicious tasks
 #: appended to a malicious request: crafted words that raise its rule scores (an
 #: opener, vague and broad words, coordinators, a comma list, a question), like

@@ -504,3 +504,44 @@ def test_schedule_deadlines_form(ctx_v1, lex_v1, policy):
     g = ctx_v1.schedule_deadlines(dev(u), dev(D), seg, prof, arrival=dev(arr))
     torch.cuda.synchronize()
     _check_schedule(g, s, 3)
+
+
+@pytest.mark.parametrize("tight", [1, 2])
+@pytest.mark.parametrize("ov", [{}, {"policy": "EDF", "consolidate": 0, "offload": 0}, {"policy": "LUF", "consolidate": 0,
+                                                                                        "offload": 0}])
+def test_periodic_release_replay(ctx_v1, lex_v1, tight, ov):
+    """NEXT-3 periodic scenario: each task is released at the
+    previous task's deadline, tight (mu*|J|) or loose (twice).  Deadlines and
+    keys from the GPU path, arrivals from them, replay; all against the oracle
+    (the oracle computes its own deadlines and keys from the same features)."""
+    d = configs.traces(3, range(300, 308), 400, lambda t: t % 4)
+    profs = [dict(p, tightness=tight, **ov) for p in d["profiles"]]
+    n = len(d["true_len"])
+    f = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+    u = np.zeros(n, np.float32)
+    D = np.zeros(n, U32)
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        lm = int(d["trace_prof"][t])
+        u[lo:hi] = oracle.predict(f[lo:hi], d["regressors"][lm])
+        _, D[lo:hi] = oracle.key(u[lo:hi], f[lo:hi], profs[lm])
+    arr = configs.periodic_arrivals(d["trace_off"], D)
+    k = np.zeros(n, np.uint64)
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        k[lo:hi], _ = oracle.key(u[lo:hi], f[lo:hi], profs[int(d["trace_prof"][t])], r_us=arr[lo:hi])
+    st, end = oracle.simulate(arr, d["true_len"], u, k, D, d["trace_off"], profs, d["trace_prof"], want_end=True)
+    # GPU: keys from the device path with the periodic arrivals, then the replay
+    gk = torch.empty(n, dtype=torch.int64, device=DEV)
+    gD = torch.empty(n, dtype=torch.int32, device=DEV)
+    gfeat, gu, garr = dev(f), dev(u), dev(arr)
+    for t in range(len(d["trace_off"]) - 1):
+        lo, hi = int(d["trace_off"][t]), int(d["trace_off"][t + 1])
+        ctx_v1.key(gu[lo:hi], profs[int(d["trace_prof"][t])], feat=gfeat[lo:hi], arrival=garr[lo:hi], key=gk[lo:hi],
+                   D_out=gD[lo:hi])
+    gs, gend = ctx_v1.simulate(garr, dev(d["true_len"]), gu, gk, gD, d["trace_off"], profs, dev(d["trace_prof"]),
+                               want_end=True)
+    torch.cuda.synchronize()
+    assert (gD.cpu().numpy().view(U32) == D).all()
+    assert (rt.decode_stats(gs) == st).all()
+    assert (gend.cpu().numpy() == end).all()

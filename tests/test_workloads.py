@@ -65,3 +65,10 @@ def test_traces_threads_do_not_change_data():
     b = configs.traces(3, range(100, 180), 50, lambda t: t % 4, threads=8)
     for k in ("data", "offsets", "arrival_us", "true_len", "trace_off", "trace_prof"):
         assert (a[k] == b[k]).all(), k
+
+
+def test_periodic_arrivals_definition():
+    # r_{i+1} = r_i + D_i within each trace, r_0 = 0
+    D = np.asarray([5, 7, 11, 2, 3, 4], np.uint32)
+    r = configs.periodic_arrivals(np.asarray([0, 3, 3, 6], np.uint32), D)
+    assert list(r) == [0, 5, 12, 0, 2, 5]
