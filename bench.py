@@ -529,11 +529,57 @@ def malicious_leg(args, ctx, configs, dev, rank, max_over_ranks):
     # deadline, tight / loose; deadlines from the GPU path (rt_score_key)
     out["periodic"] = periodic_leg(ctx, configs.traces(3, range(12000 + rank * nt, 12000 + (rank + 1) * nt), 1000,
                                                        lambda t: ((t - 12000 - rank * nt) * 4) // nt), dev)
+    out["variance"] = variance_leg(ctx, rank, dev)
     out["device_ms_total"] = round(max_over_ranks(dev_ms), 3)
     out["traces_per_s"] = round(nt * len(ratios) * 2 / (out["device_ms_total"] / 1e3), 1)
     out["note"] = ("statistics of the synthetic workload, not gated: config 3's tight deadlines overload the "
                    "executors (miss ratio > 0.9), and offloaded malicious tasks queue on 4 CPU cores at gamma = 5")
     return out
+
+
+def variance_leg(ctx, rank, dev):
+    """NEXT-3 variance subsets: a DialoGPT pool of 64 traces x 1000
+    requests scored on the GPU; 20 000 tasks each with small / medium / large
+    spread of u (configs.variance_subsets), packed into 20 Poisson traces of
+    1000; mean response time for FIFO, LUF, MUF (no consolidation / offload)
+    and UP+C+O.  Statistics, not gated."""
+    import torch
+    import rtgen
+    from rtgen import configs
+    import paper_2309_06619_b200 as rt
+    nt_pool, per, size = 64, 1000, 20000
+    first = 14000 + rank * nt_pool
+    pool = configs.traces(3, range(first, first + nt_pool), per, lambda t: 0)
+    n = len(pool["true_len"])
+    feat = torch.empty((n, 8), dtype=torch.int16, device=dev)
+    u = torch.empty(n, dtype=torch.float32, device=dev)
+    tmpk = torch.empty(n, dtype=torch.int64, device=dev)
+    for f, r0, r1, gd, so in _lm_groups(pool, dev):
+        ctx.score_key(gd, so, pool["regressors"][f], pool["profiles"][f], want_feat=True, want_D=False,
+                      out={"u": u[r0:r1], "key": tmpk[r0:r1], "feat": feat[r0:r1]})
+    subs = configs.variance_subsets(u.cpu().numpy(), size)
+    nt = size // per
+    toff = (np.arange(nt + 1) * per).astype(np.uint32)
+    arr = torch.from_numpy(np.concatenate([rtgen.arrivals(rtgen.ROOT_SEED + 3, 900000 + first + t, per)
+                                           for t in range(nt)])).to(dev)
+    tp = torch.zeros(nt, dtype=torch.int16, device=dev)
+    tl_all = torch.from_numpy(pool["true_len"].view(np.int16)).to(dev)
+    pols = {"FIFO": {"policy": "FIFO", "consolidate": 0, "offload": 0},
+            "LUF": {"policy": "LUF", "consolidate": 0, "offload": 0},
+            "MUF": {"policy": "MUF", "consolidate": 0, "offload": 0}, "UP+C+O": {}}
+    res = {}
+    for which, idx in subs.items():
+        ix = torch.from_numpy(idx.astype(np.int64)).to(dev)
+        fs, us, tl = feat[ix].contiguous(), u[ix].contiguous(), tl_all[ix].contiguous()
+        row = {"u_std": round(float(us.std().item()), 3)}
+        for name, ov in pols.items():
+            prof = dict(pool["profiles"][0], **ov)
+            key, D = ctx.key(us, prof, feat=fs, arrival=arr)
+            stats, _ = ctx.simulate(arr, tl, us, key, D, toff, [prof], tp)
+            st = rt.decode_stats(stats)
+            row[name] = round(float(st["sum_resp_us"].sum()) / max(1, int(st["n"].sum())) / 1e6, 4)
+        res[which] = row
+    return {"mean_response_s": res, "tasks_per_subset": size}
 
 
 def periodic_leg(ctx, base, dev):

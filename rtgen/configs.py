@@ -211,6 +211,25 @@ def periodic_arrivals(trace_off, D_us) -> np.ndarray:
     return r
 
 
+# ---------------------------------------------------------------- NEXT-3: variance subsets
+def variance_subsets(u, size: int, seed: int = ROOT_SEED + 51) -> dict:
+    """Three task subsets with small / medium / large variance of the
+    uncertainty scores u: `size` tasks nearest the median u; `size`
+    tasks drawn from the central two thirds of the u order; `size` tasks drawn
+    from all.  Returns index arrays into the pool, each in a seeded random order
+    (harness selection only: u comes from the caller)."""
+    u = np.asarray(u)
+    order = np.argsort(u, kind="stable")
+    n = len(u)
+    rng = np.random.default_rng(seed)
+    mid = n // 2
+    small = order[max(0, mid - size // 2): max(0, mid - size // 2) + size]
+    central = order[n // 6: n - n // 6]
+    medium = rng.choice(central, size=min(size, len(central)), replace=False)
+    large = rng.choice(n, size=min(size, n), replace=False)
+    return {k: rng.permutation(v) for k, v in (("small", small), ("medium", medium), ("large", large))}
+
+
 # ---------------------------------------------------------------- NEXT-3: malicious tasks
 #: appended to a malicious request: crafted words that raise its rule scores (an
 #: opener, vague and broad words, coordinators, a comma list, a question), like

@@ -545,3 +545,30 @@ def test_periodic_release_replay(ctx_v1, lex_v1, tight, ov):
     assert (gD.cpu().numpy().view(U32) == D).all()
     assert (rt.decode_stats(gs) == st).all()
     assert (gend.cpu().numpy() == end).all()
+
+
+@pytest.mark.parametrize("which", ["small", "medium", "large"])
+def test_variance_subset_traces(ctx_v1, lex_v1, which):
+    """NEXT-3 variance subsets: tasks gathered from a scored pool by the
+    spread of u, packed into Poisson traces; keys and replay on the GPU against
+    the oracle (FIFO / LUF / MUF without consolidation, UP+C+O)."""
+    pool = configs.traces(3, range(500, 504), 1000, lambda t: 0)
+    f = oracle.rule_gen(lex_v1, pool["data"], pool["offsets"])
+    u = oracle.predict(f, pool["regressors"][0])
+    idx = configs.variance_subsets(u, 1200)[which]
+    per, nt = 400, 3
+    toff = (np.arange(nt + 1) * per).astype(U32)
+    arr = np.concatenate([rtgen.arrivals(rtgen.ROOT_SEED + 3, 700 + t, per) for t in range(nt)])
+    fs, us, tl = f[idx], u[idx], pool["true_len"][idx]
+    tp = np.zeros(nt, np.uint16)
+    for ov in ({"policy": "FIFO", "consolidate": 0, "offload": 0}, {"policy": "LUF", "consolidate": 0, "offload": 0},
+               {"policy": "MUF", "consolidate": 0, "offload": 0}, {}):
+        prof = dict(pool["profiles"][0], **ov)
+        k, D = oracle.key(us, fs, prof, r_us=arr)
+        st, end = oracle.simulate(arr, tl, us, k, D, toff, [prof], tp, want_end=True)
+        gk, gD = ctx_v1.key(dev(us), prof, feat=dev(fs), arrival=dev(arr))
+        gs, gend = ctx_v1.simulate(dev(arr), dev(tl), dev(us), gk, gD, toff, [prof], dev(tp), want_end=True)
+        torch.cuda.synchronize()
+        assert (host(gk, np.uint64) == k).all()
+        assert (rt.decode_stats(gs) == st).all()
+        assert (gend.cpu().numpy() == end).all()

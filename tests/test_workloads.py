@@ -72,3 +72,12 @@ def test_periodic_arrivals_definition():
     D = np.asarray([5, 7, 11, 2, 3, 4], np.uint32)
     r = configs.periodic_arrivals(np.asarray([0, 3, 3, 6], np.uint32), D)
     assert list(r) == [0, 5, 12, 0, 2, 5]
+
+
+def test_variance_subsets_order_spread():
+    rng = np.random.default_rng(3)
+    u = rng.gamma(2.0, 10.0, 6000).astype(np.float32)
+    sub = configs.variance_subsets(u, 1000)
+    assert all(len(v) == 1000 and len(set(v.tolist())) == 1000 for v in sub.values())
+    sd = {k: float(np.std(u[v])) for k, v in sub.items()}
+    assert sd["small"] < sd["medium"] < sd["large"]
