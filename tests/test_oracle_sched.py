@@ -412,3 +412,172 @@ def test_fixture_search_runs_fast():
                          capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
     assert out.returncode == 0, out.stderr
     assert time.time() - t < 10
+
+
+# ------------------------------------------------------------------ O6 CPU class (R-CORE)
+def _cpu_fixture_inputs(fx):
+    n = len(fx["perm"])
+    key = np.zeros(n, np.uint64)
+    u = np.zeros(n, np.float32)
+    for j, i in enumerate(fx["perm"]):
+        key[i] = (np.uint64(fx["cpu"][j]) << np.uint64(63)) | np.uint64(100 - j)
+        u[i] = np.float32(fx["u"][j])
+    p = prof(cores=fx["cores"], gamma=fx["gamma"], base_us=fx["base_us"], eta_us=fx["eta_us"], offload=1)
+    return key, u, p
+
+
+def _list_schedule_variant(fx, *, rnd="ceil", ties="low", base=True, fp64=False):
+    """The hand table's rule and its plausible mis-readings (used only to show
+    that the fixture tells them apart; the expected values are the table's)."""
+    clocks = [0] * fx["cores"]
+    out = []
+    for j in range(len(fx["perm"])):
+        if not fx["cpu"][j]:
+            continue
+        x = float(fx["eta_us"]) * float(np.float32(fx["u"][j])) if fp64 else \
+            float(np.float32(fx["eta_us"]) * np.float32(fx["u"][j]))
+        t = {"ceil": math.ceil(x), "trunc": int(x), "round": round(x)}[rnd]
+        pred = fx["gamma"] * ((fx["base_us"] if base else 0) + t)
+        lo = min(clocks)
+        c = clocks.index(lo) if ties == "low" else len(clocks) - 1 - clocks[::-1].index(lo)
+        clocks[c] += pred
+        out.append(c)
+    return out
+
+
+def test_cpu_core_list_schedule_hand_tables(golden):
+    """R-CORE pin: the oracle's core_of equals the hand-derived list schedules
+    (tests/golden/cpu_cores.json) -- lowest-index ties, ceil of the single fp32
+    product eta*u, base_us inside the latency, GPU-class tasks untouched."""
+    for fx in golden("cpu_cores.json")["fixtures"]:
+        key, u, p = _cpu_fixture_inputs(fx)
+        n = len(u)
+        s = oracle.schedule(key, u, np.uint32([0, n]), p)
+        assert s["perm"].tolist() == fx["perm"], fx["name"]
+        want = [st["core"] for st in fx["steps"]]
+        got = [int(s["core_of"][fx["perm"][st["j"]]]) for st in fx["steps"]]
+        assert got == want, fx["name"]
+        for j, i in enumerate(fx["perm"]):
+            if not fx["cpu"][j]:
+                assert s["core_of"][i] == 0xFF and s["batch_of"][i] != 0xFFFFFFFF
+            else:
+                assert s["batch_of"][i] == 0xFFFFFFFF
+        # the table's clocks are consistent with its own predicted latencies
+        clocks = [0] * fx["cores"]
+        for st in fx["steps"]:
+            clocks[st["core"]] += st["pred"]
+            assert clocks == st["clocks_after"], (fx["name"], st["j"])
+    # each table separates the rule from its plausible mis-readings
+    f3, f2 = golden("cpu_cores.json")["fixtures"]
+    want3 = [st["core"] for st in f3["steps"]]
+    want2 = [st["core"] for st in f2["steps"]]
+    assert _list_schedule_variant(f3) == want3 and _list_schedule_variant(f2) == want2
+    assert _list_schedule_variant(f3, ties="high") != want3
+    assert _list_schedule_variant(f3, rnd="trunc") != want3
+    assert _list_schedule_variant(f3, rnd="round") != want3
+    assert _list_schedule_variant(f3, base=False) != want3
+    assert _list_schedule_variant(f2, fp64=True) != want2
+
+
+def test_cpu_core_choice_is_greedy_minimum():
+    """R-CORE checker on large random queues: replay the oracle's core_of in key
+    order, rebuilding each core's predicted clock from the definition
+    gamma*(base + ceil(fp32(eta*u))); every choice must be a core of minimal
+    clock, the lowest-index one among ties.  Includes crafted ties (equal u)."""
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n = int(rng.integers(50, 3000))
+        cores = int(rng.integers(1, 9))
+        u = np.where(rng.random(n) < 0.3, np.float32(rng.integers(1, 4)), rng.uniform(0.1, 200, n)).astype(np.float32)
+        cpu = rng.random(n) < 0.7
+        key = (cpu.astype(np.uint64) << np.uint64(63)) | rng.permutation(n).astype(np.uint64)
+        p = prof(cores=cores, gamma=int(rng.integers(1, 6)), base_us=int(rng.integers(0, 200000)),
+                 eta_us=int(rng.integers(1, 120000)), offload=1)
+        s = oracle.schedule(key, u, np.uint32([0, n]), p)
+        clocks = [0] * cores
+        seen = 0
+        for i in s["perm"]:
+            if not cpu[i]:
+                assert s["core_of"][i] == 0xFF
+                continue
+            c = int(s["core_of"][i])
+            lo = min(clocks)
+            assert clocks[c] == lo and clocks.index(lo) == c, (trial, seen)
+            eu = np.float32(p["eta_us"]) * np.float32(u[i])
+            clocks[c] += p["gamma"] * (p["base_us"] + math.ceil(float(eu)))
+            seen += 1
+        assert seen == int(cpu.sum())
+
+
+def test_cpu_core_choice_invariant_under_gamma():
+    """gamma scales every predicted latency by the same factor, so the argmin
+    choices (ties included) cannot change with gamma."""
+    c2 = configs.config2(n=4000, gid0=77)
+    lex = oracle.Lexicon(c2["lexicon"])
+    f = oracle.rule_gen(lex, c2["data"], c2["offsets"])
+    u = oracle.predict(f, c2["regressor"])
+    p = dict(c2["profile"], tau=float(np.quantile(u, 0.5)))
+    k, _ = oracle.key(u, f, p)
+    ref = oracle.schedule(k, u, np.uint32([0, 4000]), dict(p, gamma=1))["core_of"]
+    for g in (2, 5, 7):
+        assert (oracle.schedule(k, u, np.uint32([0, 4000]), dict(p, gamma=g))["core_of"] == ref).all()
+
+
+def _moore_hodgson(p_us, d_us):
+    """Minimum number of late jobs on one machine, all released at 0
+    (Moore-Hodgson): EDF order; whenever the running completion exceeds the
+    current job's due date, drop the longest job scheduled so far."""
+    import heapq
+    t, heap, late = 0, [], 0
+    for i in sorted(range(len(p_us)), key=lambda i: d_us[i]):
+        t += p_us[i]
+        heapq.heappush(heap, -p_us[i])
+        if t > d_us[i]:
+            t += heapq.heappop(heap)
+            late += 1
+    return late
+
+
+def test_bruteforce_misses_up_vs_moore_hodgson(golden):
+    """Config 1 (C = 1, no offload, exact predictions, all r = 0) and the Fig. 6
+    instance: the minimum number of misses over ALL orders (brute force) equals
+    Moore-Hodgson's optimum; the replay's miss count for the UP order equals the
+    brute-force evaluator's count for that same order; UP never beats the
+    optimum.  Paper intuition (Fig. 6): on the Fig. 6 instance EUDF
+    (= UP) misses one deadline, and that is the optimum.  On config 1 the
+    paper's deadlines d = mu*|J| are shorter than almost every service time, so
+    UP's count is reported next to the optimum (not gated beyond >= optimum)."""
+    c1 = configs.config1()
+    lex = oracle.Lexicon(c1["lexicon"])
+    f = oracle.rule_gen(lex, c1["data"], c1["offsets"])
+    ln = c1["true_len"].astype(np.int64)
+    u = ln.astype(np.float32)
+    report = {}
+    for tight in (1, 2, 4, 8):
+        p = dict(c1["profile"], C=1, consolidate=0, offload=0, tightness=tight)
+        _, D = oracle.key(u, f, p)
+        svc = [int(x) for x in p["setup_us"] + p["base_us"] + p["eta_us"] * ln]
+        Dl = [int(x) for x in D]
+
+        def misses(order):
+            t, m = 0, 0
+            for i in order:
+                t += svc[i]
+                m += t > Dl[i]
+            return m
+        best = min(misses(o) for o in itertools.permutations(range(8)))
+        assert _moore_hodgson(svc, Dl) == best
+        q = dict(p, policy="UP")
+        k, _ = oracle.key(u, f, q, r_us=np.zeros(8, np.int64))
+        st, end = _sim(np.zeros(8), ln, u, k, D, q)
+        order = sorted(range(8), key=lambda i: end[i])
+        assert int(st["misses"]) == misses(order)
+        assert int(st["misses"]) >= best
+        report[tight] = (int(st["misses"]), best)
+    print("config-1 UP misses vs optimum by tightness:", report)
+    g = golden("fig6.json")
+    ln6 = [int(x) * g["unit_us"] for x in g["len"]]
+    d6 = [int(x) * g["unit_us"] for x in g["deadline_units"]]
+    best6 = min(sum(t > d6[i] for t, i in zip(itertools.accumulate(ln6[j] for j in o), o))
+                for o in itertools.permutations(range(5)))
+    assert best6 == _moore_hodgson(ln6, d6) == g["misses"]["UP"] == 1
