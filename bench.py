@@ -52,8 +52,11 @@ def parse():
     ap.add_argument("--no-traces", action="store_true")
     ap.add_argument("--no-mlp", action="store_true")
     ap.add_argument("--sweeps", action="store_true", help="also run the NEXT-3 malicious-ratio sweep")
-    ap.add_argument("--config4", action="store_true",
-                    help="also run config 4: 65536 traces x 1024 (2^26 requests) split over the ranks (strong)")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip config 4: 65536 traces x 1024 (2^26 requests) split over the ranks (strong scaling)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: run the N-rank plumbing (self-spawn, gloo init, config-4 block shards, int64 SUM "
+                         "all-reduce, MAX-over-ranks timing, rank-0 JSON line) without any kernel; for tests")
     ap.add_argument("--no-config5", action="store_true", help="skip config 5 (rate/deadline x ablation sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
@@ -65,6 +68,103 @@ def parse():
 def dist_env():
     from paper_2309_06619_b200 import dist as rdist
     return rdist.env()
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: start N ranks of this script (one process per
+    GPU, RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR / MASTER_PORT set as torchrun
+    would), wait for all of them and return the worst exit code.  Rank 0 prints
+    the JSON line on the inherited stdout."""
+    port = _free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus), LOCAL_WORLD_SIZE=str(args.gpus),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    codes = [p.wait() for p in procs]
+    return max(codes, key=abs)
+
+
+def init_ranks(args, world: int, local: int, backend: str):
+    """One process group over the ranks (NCCL over NVLink for GPUs, gloo for the
+    CPU dry run), with NCCL's communicator lines on stderr; returns (barrier,
+    max_over_ranks).  max_over_ranks all-reduces a float64 with MAX (device
+    tensors under NCCL): every timing in the line is the slowest rank's."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
+    dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    return barrier, max_over_ranks
+
+
+CONFIG4_BLOCKS = 8  # config 4 = 8 blocks of 8192 traces x 1024 requests (one N=8 rank's shard each)
+
+
+def config4_blocks(rank: int, world: int) -> range:
+    """This rank's contiguous blocks of config 4 (strong scaling: the 2^26-request
+    job is fixed, rank r of N takes blocks [8r/N, 8(r+1)/N))."""
+    if CONFIG4_BLOCKS % world:
+        raise ValueError("config 4 needs a world size dividing 8")
+    from paper_2309_06619_b200 import dist as rdist
+    return rdist.shard(rank, world, CONFIG4_BLOCKS)
+
+
+def dry_run(args):
+    """CPU plumbing check (tests): the same rank discovery, process group, config-4
+    block sharding, int64 SUM all-reduce (paper_2309_06619_b200.dist, as the GPU
+    legs use it) and MAX-over-ranks timing as the native arm, on gloo; each rank's
+    "statistics" are synthetic integers derived from its block ids (no kernels,
+    no method arithmetic).  Prints the rank-0 JSON line, marked dry_run."""
+    import torch
+    from paper_2309_06619_b200 import dist as rdist
+    rank, world, local = dist_env()
+    barrier, max_over_ranks = init_ranks(args, world, local, "gloo")
+    t0 = time.perf_counter()
+    mine = list(config4_blocks(rank, world))
+    sums = torch.zeros((4, 3), dtype=torch.int64)
+    for b in mine:  # per-LM rows (sum_resp_us, n, misses) of a stand-in block
+        for f in range(4):
+            sums[f] += torch.tensor([1000 * (b + 1) + f, 8192 * 1024 // 4, b], dtype=torch.int64)
+    rdist.allreduce_sums(sums)
+    covered = torch.zeros(CONFIG4_BLOCKS, dtype=torch.int64)
+    covered[mine] = 1
+    rdist.allreduce_sums(covered)
+    barrier()
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3 + rank)  # + rank: MAX must pick the last rank
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+                          "higher_is_better": True, "scaling": "strong", "backend": "gloo",
+                          "config4_blocks_covered": covered.tolist(), "sums": sums.tolist(),
+                          "max_ms_includes_rank": world - 1}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ clocks
@@ -120,23 +220,12 @@ def native(args):
     from rtgen import configs
 
     rank, world, local = dist_env()
-    if args.gpus > 1 or world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (run without torchrun to self-spawn the ranks)")
+    barrier, max_over_ranks = init_ranks(args, world, local, "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     # ---------------- inputs (config 2 queue, this rank's gid range)
     d2 = configs.config2(n=args.n, gid0=rank * args.n)
@@ -346,7 +435,7 @@ def native(args):
 
     # ---------------- config 4 (strong: 2^26 requests split over the ranks)
     cfg4 = None
-    if args.config4:
+    if not args.no_config4:
         cfg4 = config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush)
 
     # ---------------- cpu baseline (oracle, rank 0, N = 1)
@@ -381,6 +470,10 @@ def native(args):
                     "path": "rt_score_schedule_host (C ABI): pinned host text + offsets -> H2D, score+key+schedule, "
                             "D2H of batch/slot/core; one context and stream per in-flight batch"},
             "gpu_launches": int(launches),
+            "ranks": {"world": world, "backend": "nccl" if world > 1 else None,
+                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 else None,
+                      "launch": "torchrun" if os.environ.get("TORCHELASTIC_RUN_ID") else
+                                ("self-spawned (bench.py --gpus N)" if world > 1 else "single process")},
             "roofline": roofline,
             "clocks": clocks,
         }
@@ -485,15 +578,7 @@ def run_traces_once(ctx, d, dev, profile_overrides=None):
     u = torch.empty(n, dtype=torch.float32, device=dev)
     key = torch.empty(n, dtype=torch.int64, device=dev)
     D = torch.empty(n, dtype=torch.int32, device=dev)
-    groups = []
-    for f in range(4):
-        sel = np.nonzero(d["trace_prof"] == f)[0]
-        if len(sel) == 0:
-            continue
-        r0, r1 = int(d["trace_off"][sel[0]]), int(d["trace_off"][sel[-1] + 1])
-        b0, b1 = int(off_np[r0]), int(off_np[r1])
-        so = torch.from_numpy((off_np[r0:r1 + 1] - off_np[r0]).astype(np.uint32).view(np.int32)).to(dev)
-        groups.append((f, r0, r1, torch.from_numpy(np.ascontiguousarray(d["data"][b0:b1])).to(dev), so))
+    groups = _lm_groups(d, dev)  # raises on non-contiguous LM ranges
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev_a.record()
     for f, r0, r1, gd, so in groups:
@@ -513,7 +598,8 @@ def malicious_leg(args, ctx, configs, dev, rank, max_over_ranks):
     (the profiles as calibrated) against FIFO without consolidation / offloading.
     128 traces x 1000 requests per point (statistics, not gated)."""
     nt = 128
-    base = configs.traces(3, range(10000 + rank * nt, 10000 + (rank + 1) * nt), 1000, lambda t: (t % nt) * 4 // nt)
+    first = 10000 + rank * nt
+    base = configs.traces(3, range(first, first + nt), 1000, lambda t: ((t - first) * 4) // nt)
     ratios = [round(0.1 * i, 1) for i in range(11)]
     out = {"ratios": ratios, "mean_response_s": {"UP+C+O": [], "FIFO": []}, "miss_ratio": {"UP+C+O": [], "FIFO": []}}
     dev_ms = 0.0
@@ -826,12 +912,9 @@ def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_
     from paper_2309_06619_b200 import dist as rdist
     t0 = time.time()
     # blocks of 8192 traces (one N=8 rank's shard; u32 text offsets per block)
-    nblk = 8
-    if nblk % world:
-        raise ValueError("config 4 needs world size dividing 8")
     blocks = []
-    for blk in range(rank * nblk // world, (rank + 1) * nblk // world):
-        d = configs.config4_shard(blk, nblk, grouped=True)
+    for blk in config4_blocks(rank, world):
+        d = configs.config4_shard(blk, CONFIG4_BLOCKS, grouped=True)
         nb, ntb = len(d["arrival_us"]), len(d["trace_off"]) - 1
         blocks.append({"d": d, "groups": _lm_groups(d, dev),
                        "arr": torch.from_numpy(d["arrival_us"]).to(dev),
@@ -1005,8 +1088,13 @@ def reference(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.impl == "reference":  # rank 0 alone (under torchrun the other ranks exit 0 without work)
         reference(args)
+        return
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        dry_run(args)
     else:
         native(args)
 

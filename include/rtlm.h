@@ -90,7 +90,7 @@ typedef struct {
   float alpha;      /* uncertainty weight of Eq. 3 */
   float tau;        /* offload threshold: CPU iff u > tau (Alg. 1; Eq. 4) */
   float u_max;      /* normaliser of alpha*u (R-NUM), > 0 */
-  int32_t C;        /* batch size C_f, 1..255 */
+  int32_t C;        /* batch size C_f, 1..128 */
   int32_t b10;      /* b in tenths (R-B): window m = b10*C/10, 10..; m <= 128 */
   int32_t tightness;/* 1 tight, 2 loose */
   int32_t gamma;    /* CPU slowdown (R-LAT) */
@@ -228,7 +228,9 @@ rt_status rt_score_key(rt_ctx* ctx, const uint8_t* d_bytes, const uint32_t* d_of
  * P:490-492; R-CONS, R-CARRY, R-FLUSH, R-CORE) of nq queues; queue q is
  * elements [h_seg_off[q], h_seg_off[q+1]) (HOST array, nq+1 entries).
  * Inputs: d_key (priority keys, e.g. from rt_score_key) and d_u.
- * `cores` overrides prof->cores for the CPU class.
+ * `cores` overrides prof->cores for the CPU class (0..32; RT_EINVAL if 0 while
+ * prof->offload is set: the CPU class would have no core).  Every argument
+ * check runs before anything is enqueued.
  * Outputs (device, n = h_seg_off[nq]):
  *   d_perm[n]      priority order per queue (global indices), stable descending key;
  *   d_batch_of[n]  global GPU batch id (queues' batches are numbered

@@ -631,17 +631,27 @@ rt_status rt_key(rt_ctx* c, const float* d_u, const uint16_t* d_feat, const int6
   return RT_OK;
 }
 
-rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const uint32_t* h_seg_off, uint32_t nq,
-                      const rt_profile* prof, uint32_t cores, uint32_t* d_perm, uint32_t* d_batch_of,
-                      uint8_t* d_slot_of, uint8_t* d_core_of, uint32_t* d_seg_batch_off, rt_stream stream) {
-  if (!c) return RT_EINVAL;
+// Argument checks of a one-pass schedule (rt_schedule and the calls built on it),
+// run before anything is enqueued (rtlm.h: argument checks launch nothing).
+static rt_status check_schedule_args(rt_ctx* c, const uint32_t* h_seg_off, uint32_t nq, const rt_profile* prof,
+                                     uint32_t cores) {
   if (!h_seg_off) return fail(c, RT_EINVAL, "h_seg_off is NULL");
   rt_status st = check_profile(c, prof, false);
   if (st != RT_OK) return st;
   if (cores > rtlm::kMaxCores) return fail(c, RT_EINVAL, "cores must be <= 32");
+  if (prof->offload && cores == 0) return fail(c, RT_EINVAL, "offload needs cores >= 1 (CPU-class tasks need a core)");
   if (h_seg_off[0] != 0) return fail(c, RT_EINVAL, "h_seg_off[0] must be 0");
   for (uint32_t q = 0; q < nq; ++q)
     if (h_seg_off[q + 1] < h_seg_off[q]) return fail(c, RT_EINVAL, "h_seg_off must be non-decreasing");
+  return RT_OK;
+}
+
+rt_status rt_schedule(rt_ctx* c, const uint64_t* d_key, const float* d_u, const uint32_t* h_seg_off, uint32_t nq,
+                      const rt_profile* prof, uint32_t cores, uint32_t* d_perm, uint32_t* d_batch_of,
+                      uint8_t* d_slot_of, uint8_t* d_core_of, uint32_t* d_seg_batch_off, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  rt_status st = check_schedule_args(c, h_seg_off, nq, prof, cores);
+  if (st != RT_OK) return st;
   const uint32_t n = h_seg_off[nq];
   if (!d_seg_batch_off) return fail(c, RT_EINVAL, "d_seg_batch_off is NULL");
   if (n && (!d_key || !d_u || !d_perm || !d_batch_of || !d_slot_of || !d_core_of))
@@ -763,9 +773,12 @@ rt_status rt_schedule_deadlines(rt_ctx* c, const float* d_u, const uint32_t* d_D
                                 uint32_t* d_perm, uint32_t* d_batch_of, uint8_t* d_slot_of, uint8_t* d_core_of,
                                 uint32_t* d_seg_batch_off, rt_stream stream) {
   if (!c) return RT_EINVAL;
-  if (!h_seg_off) return fail(c, RT_EINVAL, "h_seg_off is NULL");
+  rt_status st0 = check_schedule_args(c, h_seg_off, nq, prof, cores);
+  if (st0 != RT_OK) return st0;
   const uint32_t n = h_seg_off[nq];
   if (n && (!d_u || !d_D_us)) return fail(c, RT_EINVAL, "u / deadlines are NULL");
+  if (n && (!d_perm || !d_batch_of || !d_slot_of || !d_core_of)) return fail(c, RT_EINVAL, "null device buffer");
+  if (!d_seg_batch_off) return fail(c, RT_EINVAL, "d_seg_batch_off is NULL");
   if (n > c->kbuf_n) {
     if (no_growth_in_capture(c, cs(stream)) != RT_OK) return RT_EINVAL;
     DeviceGuard g(c->device);
@@ -788,6 +801,12 @@ rt_status rt_score_schedule_host(rt_ctx* c, const uint8_t* h_bytes, const uint32
   if (!n) return RT_OK;
   if (!h_bytes || !h_offsets || !reg || !prof || !h_batch_of || !h_slot_of || !h_core_of)
     return fail(c, RT_EINVAL, "null argument");
+  {
+    const uint32_t seg0[2] = {0u, n};
+    rt_status st0 = check_schedule_args(c, seg0, 1, prof, cores);
+    if (st0 != RT_OK) return st0;
+  }
+  if ((uint64_t)h_offsets[n] >= (1ull << 32) - 1) return fail(c, RT_EOVERFLOW, "text too large");
   const size_t nbytes = h_offsets[n];
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t need = up(nbytes) + up(4 * ((size_t)n + 1)) + up(4 * (size_t)n) + up(8 * (size_t)n) +

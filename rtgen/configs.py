@@ -227,6 +227,9 @@ def variance_subsets(u, size: int, seed: int = ROOT_SEED + 51) -> dict:
     central = order[n // 6: n - n // 6]
     medium = rng.choice(central, size=min(size, len(central)), replace=False)
     large = rng.choice(n, size=min(size, n), replace=False)
+    for name, v in (("small", small), ("medium", medium), ("large", large)):
+        if len(v) != size:  # the caller builds traces of exactly `size` tasks
+            raise ValueError(f"variance_subsets: pool of {n} cannot give {size} {name}-variance tasks")
     return {k: rng.permutation(v) for k, v in (("small", small), ("medium", medium), ("large", large))}
 
 

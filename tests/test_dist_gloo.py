@@ -85,3 +85,40 @@ def test_allreduce_equals_single_process():
         assert t == float(world)         # MAX over ranks
     means = rdist.means_from_sums(torch.from_numpy(want))
     assert all(m > 0 for m, _ in means)
+
+
+def test_bench_self_spawns_ranks_world2():
+    """`python bench.py --gpus 2` without torchrun: the bench
+    starts its own two ranks, which run the same process-group set-up, config-4
+    block sharding, int64 SUM all-reduce and MAX-over-ranks timing as the GPU
+    arm (here on gloo, --dry-run: no kernels), and rank 0 prints the line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    line = lines[0]
+    assert line["dry_run"] is True and line["n_gpus"] == 2 and line["backend"] == "gloo"
+    assert line["config4_blocks_covered"] == [1] * 8  # every block on exactly one rank
+    want = [[sum(1000 * (b + 1) + f for b in range(8)), 8 * 8192 * 1024 // 4, sum(range(8))] for f in range(4)]
+    assert line["sums"] == want  # exact int64 SUM over the ranks
+    assert line["ms_per_step"] >= 1.0  # the MAX over ranks saw rank 1's (+1 ms) time
+
+
+def test_bench_config4_block_shards():
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for world in (1, 2, 4, 8):
+        got = [b for r in range(world) for b in bench.config4_blocks(r, world)]
+        assert got == list(range(8))
+        assert all(len(bench.config4_blocks(r, world)) == 8 // world for r in range(world))
+    with pytest.raises(ValueError):
+        bench.config4_blocks(0, 3)

@@ -1,0 +1,311 @@
+"""GPU parity of the launch configurations and kernel paths the round-1 tests did
+not reach ("Next round" item 2):
+
+* the bench's timed requests step exactly as bench.py runs it: `depth` = 4
+  batches in flight, one context + stream + distinct 2^20-request input per
+  batch, the persistent scoring kernel capped by rt_set_sm_limit(nsm - 4),
+  issued call by call and replayed from CUDA graphs -- every batch's order,
+  batches, slots and cores against the oracle;
+* crafted-u big queues (> 2048, the parallel consolidation path of k_ff.cu):
+  the exact fp32 lambda boundary (u == fl(lambda * u_prev), and one ulp above),
+  runs of u = 0, all-equal streams, u monotone along the priority order;
+* the CPU-class list-scheduling chain on 4 cores in all three arithmetic
+  forms of k_cpu_chain (u32 offsets from a base, u32 deltas, u64 keys), which
+  only predicted CPU latencies above ~119 s reach (u >~ 475 tokens at
+  DialoGPT's gamma and eta);
+* a 1024-entry lexicon (the cap) of 12-16-byte lemmas, with near misses in
+  bytes 13-16, inflected and clitic forms;
+* argument checks that must launch nothing (rtlm.h: argument checks are
+  synchronous and launch nothing), including offload with zero cores.
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import rtgen
+from rtgen import configs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2309_06619_b200 as rt  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+U32 = np.uint32
+
+
+def dev(a):
+    a = np.ascontiguousarray(a)
+    view = {np.dtype(np.uint32): np.int32, np.dtype(np.uint16): np.int16, np.dtype(np.uint64): np.int64}
+    if a.dtype in view:
+        a = a.view(view[a.dtype])
+    return torch.from_numpy(a).to(DEV)
+
+
+def host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+def check_schedule(g, s, nq):
+    assert (host(g["perm"], U32) == s["perm"]).all(), "perm"
+    assert (host(g["batch_of"], U32) == s["batch_of"]).all(), "batch_of"
+    assert (g["slot_of"].cpu().numpy() == s["slot_of"]).all(), "slot_of"
+    assert (g["core_of"].cpu().numpy() == s["core_of"]).all(), "core_of"
+    assert (host(g["seg_batch_off"], U32)[:nq + 1] == s["seg_batch_off"]).all(), "seg_batch_off"
+
+
+@pytest.fixture(scope="module")
+def ctx_v1():
+    return rt.Context(configs.read_lexicon(), 0)
+
+
+# ------------------------------------------------------------------ the bench's timed step
+@pytest.mark.parametrize("graphs", [False, True])
+def test_bench_pipeline_launch_configuration(lex_v1, graphs):
+    """bench.py's pipelined requests leg (depth 4, per-slot contexts and streams,
+    rt_set_sm_limit(nsm - depth), two waves of steps so that every slot runs
+    while the others' kernels are in flight), with and without CUDA graphs."""
+    n, depth, steps = 1 << 20, 4, 8
+    nsm = torch.cuda.get_device_properties(DEV).multi_processor_count
+    ds = [configs.config2(n=n, gid0=i * n) for i in range(depth)]
+    prof, reg = ds[0]["profile"], ds[0]["regressor"]
+    seg = np.asarray([0, n], U32)
+    ctxs = [rt.Context(d["lexicon"], 0) for d in ds]
+    for c in ctxs:
+        c.set_sm_limit(max(1, nsm - depth))
+    data = [dev(d["data"]) for d in ds]
+    off = [dev(d["offsets"]) for d in ds]
+    streams = [torch.cuda.Stream(DEV) for _ in range(depth)]
+    outs = [{"u": torch.empty(n, dtype=torch.float32, device=DEV), "key": torch.empty(n, dtype=torch.int64, device=DEV)}
+            for _ in range(depth)]
+    souts = [{"perm": torch.empty(n, dtype=torch.int32, device=DEV),
+              "batch_of": torch.empty(n, dtype=torch.int32, device=DEV),
+              "slot_of": torch.empty(n, dtype=torch.uint8, device=DEV),
+              "core_of": torch.empty(n, dtype=torch.uint8, device=DEV),
+              "seg_batch_off": torch.empty(2, dtype=torch.int32, device=DEV)} for _ in range(depth)]
+
+    def pstep(k):
+        sl = k % depth
+        with torch.cuda.stream(streams[sl]):
+            ctxs[sl].score_key(data[sl], off[sl], reg, prof, want_D=False, out=outs[sl])
+            ctxs[sl].schedule(outs[sl]["key"], outs[sl]["u"], seg, prof, out=souts[sl])
+
+    for k in range(depth):  # warm-up: every slot runs before its capture
+        pstep(k)
+    torch.cuda.synchronize()
+    for o in souts:  # poison the outputs: the timed-style waves below must rewrite them
+        for t in o.values():
+            t.fill_(-1 if t.dtype != torch.uint8 else 0x7F)
+    torch.cuda.synchronize()
+    if graphs:
+        gs = []
+        for sl in range(depth):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=streams[sl], capture_error_mode="relaxed"):
+                pstep(sl)
+            gs.append(g)
+        torch.cuda.synchronize()
+        for k in range(steps):
+            with torch.cuda.stream(streams[k % depth]):
+                gs[k % depth].replay()
+    else:
+        for k in range(steps):
+            pstep(k)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.set_sm_limit(0)
+    for sl, d in enumerate(ds):
+        f = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+        u = oracle.predict(f, reg)
+        k, _ = oracle.key(u, f, prof)
+        assert (host(outs[sl]["key"], np.uint64) == k).all(), f"slot {sl}: keys"
+        assert (outs[sl]["u"].cpu().numpy().view(U32) == u.view(U32)).all(), f"slot {sl}: u"
+        check_schedule(souts[sl], oracle.schedule(k, u, seg, prof), 1)
+
+
+# ------------------------------------------------------------------ crafted-u big queues
+def crafted_u(kind: str, n: int, rng) -> np.ndarray:
+    if kind == "lambda_boundary":
+        # u_{j+1} = fl(1.5 * u_j) exactly (8 * 1.5^j is exact in binary32 for j < 20),
+        # the next binary32 above it, and a few random values
+        geo = (8.0 * 1.5 ** np.arange(12)).astype(np.float32)
+        above = np.nextafter(geo, np.float32(np.inf)).astype(np.float32)
+        below = np.nextafter(geo, np.float32(0)).astype(np.float32)
+        pool = np.concatenate([geo, geo, geo, above, below, rng.uniform(1, 600, 8).astype(np.float32)])
+        return rng.choice(pool, n).astype(np.float32)
+    if kind == "zero_runs":
+        u = rng.uniform(0.5, 30, n).astype(np.float32)
+        i = 0
+        while i < n:  # runs of zeros of random length
+            L = int(rng.integers(1, 200))
+            if rng.random() < 0.5:
+                u[i:i + L] = 0.0
+            i += L + int(rng.integers(1, 100))
+        return u
+    if kind == "all_equal":
+        return np.full(n, 7.25, np.float32)
+    if kind in ("monotone_up", "monotone_down"):
+        return rng.uniform(0.0, 600.0, n).astype(np.float32)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("n", [3001, 40000])
+@pytest.mark.parametrize("kind", ["lambda_boundary", "zero_runs", "all_equal", "monotone_up", "monotone_down"])
+@pytest.mark.parametrize("lam,C,b10", [(1.5, 11, 18), (1.5, 33, 30), (1.0, 8, 10)])
+def test_schedule_crafted_u(ctx_v1, kind, n, lam, C, b10):
+    rng = np.random.default_rng(zlib.crc32(f"{kind}/{n}/{lam}/{C}".encode()))
+    u = crafted_u(kind, n, rng)
+    # monotone along the priority order: LUF serves ascending u, MUF descending u
+    policy = {"monotone_up": "LUF", "monotone_down": "MUF"}.get(kind, "UP")
+    prof = dict(configs.paper_lms()[0], policy=policy, offload=0, C=C, b10=b10, **{"lambda": lam})
+    D = rng.integers(1, 3_000_000, n).astype(U32)
+    f = np.zeros((n, 8), np.uint16)
+    k, _ = oracle.key(u, f, prof, D_in=D)
+    seg = np.asarray([0, n], U32)
+    s = oracle.schedule(k, u, seg, prof)
+    g = ctx_v1.schedule_deadlines(dev(u), dev(D), seg, prof)
+    torch.cuda.synchronize()
+    check_schedule(g, s, 1)
+    if kind == "lambda_boundary" and lam == 1.5:
+        # the boundary is really exercised: some batch holds a pair (x, fl(1.5 x)) adjacent in u order
+        bo, uu = s["batch_of"], u
+        hit = False
+        for b in np.unique(bo)[:2000]:
+            m = np.sort(uu[bo == b])
+            if len(m) > 1 and np.any(m[1:] == (np.float32(1.5) * m[:-1]).astype(np.float32)) and np.any(m[1:] != m[:-1]):
+                hit = True
+                break
+        assert hit
+
+
+def test_cpu_chain_arithmetic_forms(ctx_v1):
+    """k_cpu_chain on 4 cores: the CPU class in ascending-u order (LUF) passes from
+    small predicted latencies (u32 offsets from a base), through 119-134 s (u32
+    deltas: u in [475, 536]), to latencies above 2^27 us (u64 keys)."""
+    n = 60000
+    rng = np.random.default_rng(2024)
+    prof = dict(configs.paper_lms()[0], policy="LUF", offload=1, cores=4)
+    gpu = rng.uniform(0.0, 35.0, 24000)
+    bands = [rng.uniform(35.5, 400.0, 12000), rng.uniform(480.0, 530.0, 12000), rng.uniform(600.0, 2.0e5, 12000)]
+    u = np.concatenate([gpu] + bands).astype(np.float32)
+    rng.shuffle(u)
+    D = rng.integers(1, 3_000_000, n).astype(U32)
+    f = np.zeros((n, 8), np.uint16)
+    k, _ = oracle.key(u, f, prof, D_in=D)
+    seg = np.asarray([0, n], U32)
+    eta, gam, base = np.float32(prof["eta_us"]), prof["gamma"], prof["base_us"]
+    pred = gam * (base + np.ceil((eta * u).astype(np.float32)).astype(np.int64))
+    assert pred.max() >= 1 << 27 and ((pred >= 119_000_000) & (pred < 1 << 27)).sum() > 4096
+    s = oracle.schedule(k, u, seg, prof)
+    g = ctx_v1.schedule_deadlines(dev(u), dev(D), seg, prof)
+    torch.cuda.synchronize()
+    check_schedule(g, s, 1)
+
+
+# ------------------------------------------------------------------ 1024-entry lexicon
+def long_lexicon(rng):
+    """1024 distinct lemmas of 12-16 letters that the loader's lemmatizer leaves
+    unchanged (no final s / ed / ing), spread over every section."""
+    alpha = np.frombuffer(b"abcdefghijklmnopqrtuvwxyz", np.uint8)  # no 's'
+    words = set()
+    while len(words) < 1024:
+        L = int(rng.integers(12, 17))
+        w = bytes(rng.choice(alpha, L)).decode()
+        if w.endswith(("ed", "ing", "s")):
+            continue
+        words.add(w)
+    words = sorted(words)
+    rng.shuffle(words)
+    sec = {"vague": words[0:200], "polysemy": words[200:400], "pos": words[400:700], "wh": words[700:820],
+           "coord": words[820:900], "prep": words[900:1024]}
+    lines = ["vague:"] + sec["vague"]
+    lines += ["polysemy:"] + [f"{w}\t{int(rng.integers(2, 9))}" for w in sec["polysemy"]]
+    tags = ["NOUN", "PROPN", "VERB", "ADJ", "NOUN,VERB", "VERB,ADP", "NOUN,ADJ"]
+    lines += ["pos:"] + [f"{w}\t{tags[int(rng.integers(0, len(tags)))]}" for w in sec["pos"]]
+    flags = ["OPENER", "WHAT", "CAUSE", "BROAD", "OPENER|BROAD", "WHAT|CAUSE"]
+    lines += ["wh:"] + [f"{w}\t{flags[int(rng.integers(0, len(flags)))]}" for w in sec["wh"]]
+    lines += ["coord:"] + sec["coord"] + ["prep:"] + sec["prep"]
+    return "\n".join(lines) + "\n", words
+
+
+def near_miss_texts(words, rng):
+    out = []
+    for _ in range(3000):
+        toks = []
+        for _ in range(int(rng.integers(1, 30))):
+            w = words[int(rng.integers(0, len(words)))]
+            r = rng.random()
+            if r < 0.3:
+                pass                                                     # exact hit
+            elif r < 0.5 and len(w) >= 13:                               # near miss in bytes 13..16
+                j = int(rng.integers(12, len(w)))
+                w = w[:j] + ("z" if w[j] != "z" else "y") + w[j + 1:]
+            elif r < 0.6:
+                w = w + "x"                                              # 13..17 bytes: extension
+            elif r < 0.65:
+                w = w[:-1]                                               # truncation
+            elif r < 0.75:
+                w = w + ["s", "ed", "ing", "es"][int(rng.integers(0, 4))]  # inflections -> lemma (R-LEMMA)
+            elif r < 0.85:
+                w = w + ["'s", "n't", "'ll", "'re", "'d"][int(rng.integers(0, 5))]  # clitics (R-CLITIC)
+            elif r < 0.92:
+                w = w.upper()
+            else:
+                w = ["?", ",", ".", "!", "and", "the"][int(rng.integers(0, 6))]
+            toks.append(w)
+        out.append(" ".join(toks))
+    return out
+
+
+def test_lexicon_1024_long_lemmas():
+    rng = np.random.default_rng(1024)
+    text, words = long_lexicon(rng)
+    lex = oracle.Lexicon(text)
+    assert len(lex) == 1024
+    ctx = rt.Context(text, 0)
+    assert ctx.lexicon_size == 1024
+    data, off = rtgen.pack_texts(near_miss_texts(words, rng))
+    feat = ctx.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex, data, off)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), got[i].tolist(), want[i].tolist()) for i in bad[:5]]
+    assert (want[:, 3] > 0).mean() > 0.3 and (want[:, 2] > 0).mean() > 0.3  # V and M really fire
+    # one more distinct lemma than the cap is a lexicon error
+    with pytest.raises(rt.RtlmError, match="more than 1024"):
+        rt.Context(text + "vague:\nqqqqqqqqqqqqqq\n", 0)
+
+
+# ------------------------------------------------------------------ argument checks launch nothing
+def test_schedule_argument_checks_launch_nothing(ctx_v1):
+    n = 5000
+    u = torch.ones(n, dtype=torch.float32, device=DEV)
+    D = torch.full((n,), 1000, dtype=torch.int32, device=DEV)
+    key = torch.zeros(n, dtype=torch.int64, device=DEV)
+    p = dict(configs.paper_lms()[0])
+    torch.cuda.synchronize()
+    l0 = rt.launch_count()
+    with pytest.raises(rt.RtlmError, match="cores"):
+        ctx_v1.schedule(key, u, np.asarray([0, n], U32), dict(p, offload=1), cores=0)
+    with pytest.raises(rt.RtlmError, match="cores"):
+        ctx_v1.schedule_deadlines(u, D, np.asarray([0, n], U32), dict(p, offload=1), cores=0)
+    with pytest.raises(rt.RtlmError, match="non-decreasing"):
+        ctx_v1.schedule_deadlines(u, D, np.asarray([0, 3000, 2000, n], U32), p)
+    with pytest.raises(rt.RtlmError, match="lambda"):
+        ctx_v1.schedule_deadlines(u, D, np.asarray([0, n], U32), dict(p, **{"lambda": 0.5}))
+    h = torch.from_numpy(np.zeros(64, np.uint8))
+    ho = torch.from_numpy(np.asarray([0, 32, 64], np.int32))
+    res = {"batch_of": torch.empty(2, dtype=torch.int32), "slot_of": torch.empty(2, dtype=torch.uint8),
+           "core_of": torch.empty(2, dtype=torch.uint8)}
+    with pytest.raises(rt.RtlmError, match="cores"):
+        ctx_v1.score_schedule_host(h, ho, configs.regressor(p), dict(p, offload=1, cores=0), res)
+    assert rt.launch_count() == l0, "a rejected call launched kernels"
+    # without offload, zero cores is valid (no CPU class)
+    g = ctx_v1.schedule(key, u, np.asarray([0, n], U32), dict(p, offload=0), cores=0)
+    torch.cuda.synchronize()
+    assert (g["core_of"].cpu().numpy() == 0xFF).all()
