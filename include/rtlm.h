@@ -258,8 +258,12 @@ rt_status rt_schedule_deadlines(rt_ctx* ctx, const float* d_u, const uint32_t* d
 
 /* Discrete-event replay of nt traces (§V-A; R-REPLAY, R-LAT,
  * R-XI).  Trace t = tasks [h_trace_off[t], h_trace_off[t+1]) (HOST array),
- * at most 1024 tasks, in arrival order (d_arrival_us non-decreasing within
- * the trace).  Per task: arrival (int64 µs), true output length, u, key, D_us.
+ * at most 65536 tasks (RT_EINVAL beyond), in arrival order (d_arrival_us
+ * non-decreasing within the trace).  Traces of <= 1024 tasks are replayed by
+ * one warp each with register-word ready bitmaps; longer ones (e.g. the
+ * paper's full 141-minute beta = 10..150 ramp, ~11 280 tasks)
+ * are rank-sorted by a radix sort per trace and replayed by one warp each with
+ * multi-word bitmaps (same events, same results).  Per task: arrival (int64 µs), true output length, u, key, D_us.
  * h_profiles[np] (host), d_trace_prof[nt] (u16 profile index; NULL = 0).
  * Output d_stats[nt]; d_end_us[n] (nullable) receives each task's end time. */
 rt_status rt_simulate(rt_ctx* ctx, const int64_t* d_arrival_us, const uint16_t* d_true_len, const float* d_u,

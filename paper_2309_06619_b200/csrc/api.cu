@@ -736,10 +736,12 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
     if (st != RT_OK) return st;
   }
   if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
+  uint32_t longest = 0;
   for (uint32_t t = 0; t < nt; ++t) {
     if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
-    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
+    longest = std::max(longest, h_trace_off[t + 1] - h_trace_off[t]);
   }
+  if (longest > rtlm::kMaxLongTrace) return fail(c, RT_EINVAL, "trace longer than 65536");
   if (h_trace_off[nt] && (!d_arr || !d_len || !d_u || !d_key || !d_D)) return fail(c, RT_EINVAL, "null task array");
   DeviceGuard g(c->device);
   if (capturing(cs(stream))) c->captured = true;  // see retire()
@@ -760,10 +762,31 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
   a.trace_prof = d_trace_prof;
   a.stats = d_stats;
   a.end_us = d_end_us;
-  st = ensure_ws(c, (size_t)nt * rtlm::kMaxTrace * sizeof(uint16_t), s);
+  // workspace: per-trace rank order of short traces (u16) | long traces: rank order
+  // and its inverse over all tasks (u32) and the radix sort's buffers
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t total = h_trace_off[nt];
+  const size_t sidx_bytes = up((size_t)nt * rtlm::kMaxTrace * sizeof(uint16_t));
+  size_t long_bytes = 0;
+  if (longest > rtlm::kMaxTrace) long_bytes = 2 * up(total * 4) + rtlm::radix_sort_workspace(longest);
+  st = ensure_ws(c, sidx_bytes + long_bytes, s);
   if (st != RT_OK) return st;
   a.sidx = static_cast<uint16_t*>(c->ws);
-  cudaError_t e = rtlm::launch_replay(a, s);
+  cudaError_t e = cudaSuccess;
+  if (long_bytes) {
+    char* lp = static_cast<char*>(c->ws) + sidx_bytes;
+    uint32_t* perm = reinterpret_cast<uint32_t*>(lp);
+    a.long_perm = perm;
+    a.long_rank = reinterpret_cast<uint32_t*>(lp + up(total * 4));
+    void* rws = lp + 2 * up(total * 4);
+    for (uint32_t t = 0; t < nt; ++t) {  // stable sort by key desc of each long trace (R-TIE)
+      const uint32_t lo = h_trace_off[t], m = h_trace_off[t + 1] - lo;
+      if (m <= rtlm::kMaxTrace) continue;
+      e = rtlm::radix_sort_desc(d_key + lo, lo, m, perm + lo, 1, rws, s);
+      if (e != cudaSuccess) return cuda_fail(c, e, "long-trace rank sort");
+    }
+  }
+  e = rtlm::launch_replay(a, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
   return RT_OK;
 }

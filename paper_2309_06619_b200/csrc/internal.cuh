@@ -61,7 +61,8 @@ __host__ __device__ __forceinline__ uint32_t ord32_bits(uint32_t b) {
 constexpr uint32_t kNoBatch = 0xFFFFFFFFu;
 constexpr uint32_t kSmallSeg = 2048;     // queues up to this size are scheduled inside one CTA
 constexpr uint32_t kMaxWindow = 128;     // m = b10*C/10 <= 128
-constexpr uint32_t kMaxTrace = 1024;     // tasks per replayed trace
+constexpr uint32_t kMaxTrace = 1024;     // tasks per trace on the short replay path (and in rt_trace_report / _utilization)
+constexpr uint32_t kMaxLongTrace = 65536; // tasks per replayed trace (rt_simulate)
 constexpr uint32_t kMaxCores = 32;
 
 // ---------------------------------------------------------------- launchers
@@ -145,6 +146,8 @@ struct ReplayLaunch {
   rt_trace_stats* stats;
   int64_t* end_us;
   uint16_t* sidx;             // workspace: nt x kMaxTrace (rank -> arrival index)
+  const uint32_t* long_perm;  // traces > kMaxTrace: rank -> global index at [lo, lo + n) (NULL: none)
+  uint32_t* long_rank;        //                      arrival index -> rank (workspace)
 };
 cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
 cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,

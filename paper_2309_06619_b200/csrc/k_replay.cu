@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kRankThr) k_trace_rank(const uint64_t* __restr
   __shared__ uint16_t si[2][kMaxTrace];
   const uint32_t t = blockIdx.x, p = threadIdx.x;
   const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
-  if (n == 0) return;
+  if (n == 0 || n > kMaxTrace) return;  // long traces: radix sort + k_replay_long
   uint32_t npow = 2;
   while (npow < n) npow <<= 1;
   // padding (positions >= n) sorts last: key 0, index 0xFFFF; threads >= npow
@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   const uint32_t lane = threadIdx.x;
   const uint32_t t = blockIdx.x;
   const uint32_t lo = a.trace_off[t], n = a.trace_off[t + 1] - lo;
+  if (n > kMaxTrace) return;  // k_replay_long's
   const rt_profile p = a.profiles[a.trace_prof ? a.trace_prof[t] : 0];
   if (n == 0) {
     if (lane == 0) a.stats[t] = rt_trace_stats{0, 0u, 0u};
@@ -355,6 +356,294 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   if (lane == 0) a.stats[t] = rt_trace_stats{sr, n, ms};
 }
 
+// ---- K5 for long traces (kMaxTrace < n <= kMaxLongTrace tasks, e.g. the paper's
+// full beta = 10..150 ramp, ~11 280 arrivals): the same event loop
+// (R-REPLAY) as k_replay, with the ready sets as multi-word bitmaps in shared
+// memory plus a summary bitmap of their non-zero words (first set bit = two
+// ballots; the top-m ready tasks = a scan over the set summary bits), the rank
+// order from a radix sort of the trace's keys (launched per long trace by the
+// host, stable: key desc, arrival index asc, R-TIE) and the arrival times, ranks
+// and task data read from global memory (L2).  One warp per trace.
+constexpr uint32_t kLW = kMaxLongTrace / 32;  // bitmap words
+constexpr uint32_t kLS = kLW / 32;            // summary words
+enum : uint32_t { BM_GPU = 0, BM_CPU = 1, BM_WAIT = 2 };
+
+struct LongSmem {
+  uint32_t bits[3][kLW];  // ready GPU-class (by rank), ready CPU-class (by rank), waiting GPU-class (by arrival)
+  uint32_t sums[3][kLS];  // bit (w & 31) of sums[b][w >> 5]: bits[b][w] != 0
+  int64_t core_free[kMaxCores];
+  uint32_t W[kMaxWindow];
+  float Su[kMaxWindow];
+};
+
+__device__ __forceinline__ void lbit_set(LongSmem& sm, uint32_t b, uint32_t x) {
+  atomicOr(&sm.bits[b][x >> 5], 1u << (x & 31u));
+  atomicOr(&sm.sums[b][x >> 10], 1u << ((x >> 5) & 31u));
+}
+__device__ __forceinline__ void lbit_clear(LongSmem& sm, uint32_t b, uint32_t x) {
+  const uint32_t m = 1u << (x & 31u);
+  const uint32_t old = atomicAnd(&sm.bits[b][x >> 5], ~m);
+  if ((old & ~m) == 0u) atomicAnd(&sm.sums[b][x >> 10], ~(1u << ((x >> 5) & 31u)));
+}
+// lowest set bit of a non-empty bitmap (warp-uniform)
+__device__ __forceinline__ uint32_t lbit_first(const LongSmem& sm, uint32_t b, uint32_t lane) {
+  static_assert(kLS == 64, "two summary words per lane");
+  const uint32_t s0 = sm.sums[b][lane], s1 = sm.sums[b][lane + 32];
+  const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, s0 != 0u), b1 = __ballot_sync(0xFFFFFFFFu, s1 != 0u);
+  const uint32_t src = b0 ? __ffs(b0) - 1u : __ffs(b1) - 1u;
+  const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, s0, src), w1 = __shfl_sync(0xFFFFFFFFu, s1, src);
+  const uint32_t sw = b0 ? src : 32u + src, sword = b0 ? w0 : w1;
+  const uint32_t w = sw * 32u + __ffs(sword) - 1u;
+  return w * 32u + __ffs(sm.bits[b][w]) - 1u;
+}
+// the first `take` set bits of the GPU-class ready bitmap (rank order) -> sm.W
+__device__ __forceinline__ void lbit_take(LongSmem& sm, uint32_t take, uint32_t lane) {
+  uint32_t got = 0;
+  for (uint32_t sw = 0; sw < kLS && got < take; ++sw) {
+    const uint32_t sbits = sm.sums[BM_GPU][sw];
+    if (!sbits) continue;
+    uint32_t w = 0, word = 0;
+    if (lane < (uint32_t)__popc(sbits)) {
+      w = sw * 32u + __fns(sbits, 0, (int)lane + 1);
+      word = sm.bits[BM_GPU][w];
+    }
+    const uint32_t c = __popc(word);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += v;
+    }
+    const uint32_t excl = incl - c, tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (got + excl < take) {
+      const uint32_t k = min(c, take - got - excl);
+      for (uint32_t e = 0; e < k; ++e) {
+        sm.W[got + excl + e] = w * 32u + (__ffs(word) - 1u);
+        word &= word - 1u;
+      }
+    }
+    got += tot;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) k_replay_long(ReplayLaunch a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  LongSmem& sm = *reinterpret_cast<LongSmem*>(smem_raw);
+  const uint32_t lane = threadIdx.x;
+  const uint32_t t = blockIdx.x;
+  const uint32_t lo = a.trace_off[t], n = a.trace_off[t + 1] - lo;
+  if (n <= kMaxTrace) return;  // k_replay's
+  const rt_profile p = a.profiles[a.trace_prof ? a.trace_prof[t] : 0];
+  const uint32_t* perm = a.long_perm + lo;  // rank -> global index (radix sort)
+  uint32_t* rank = a.long_rank + lo;        // arrival index -> rank
+  uint32_t ncpu_l = 0;
+  for (uint32_t j = lane; j < n; j += 32) {
+    rank[perm[j] - lo] = j;
+    ncpu_l += (uint32_t)(a.key[lo + j] >> 63);
+  }
+  const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);
+  const uint32_t nw = (n + 31) / 32;
+  for (uint32_t w = lane; w < nw; w += 32) {
+    sm.bits[0][w] = 0; sm.bits[1][w] = 0; sm.bits[2][w] = 0;
+  }
+  for (uint32_t w = lane; w < kLS; w += 32) {
+    sm.sums[0][w] = 0; sm.sums[1][w] = 0; sm.sums[2][w] = 0;
+  }
+  sm.core_free[lane] = 0;
+  const int64_t* g_r = a.arrival + lo;
+  const uint16_t* g_len = a.len + lo;
+  const float* g_u = a.u + lo;
+  const uint32_t* g_D = a.D + lo;
+  __syncwarp();
+
+  const uint32_t C = (uint32_t)p.C, m = (uint32_t)p.b10 * C / 10u, cores = (uint32_t)p.cores;
+  const int64_t gpu_fixed = p.setup_us + p.base_us;
+  int64_t now = g_r[0], gpu_free = 0;
+  uint32_t next = 0, done = 0;
+  uint32_t cpu_ready = 0, gpu_ready = 0;
+  bool have_oldest = false;
+  int64_t cpu_min_free = INT64_MAX;
+  bool cpu_min_valid = false;
+  int64_t oldest_r = 0;
+  int64_t resp = 0;
+  uint32_t misses = 0;
+  int64_t rw = lane < n ? g_r[lane] : INT64_MAX;
+
+  for (;;) {
+    // ---- admit arrivals <= now
+    while (next < n) {
+      const uint32_t i = next + lane;
+      const bool arr = rw <= now;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, arr);
+      if (!bal) break;
+      const uint32_t cnt = __popc(bal);
+      const uint32_t rk = arr ? rank[i] : 0xFFFFFFFFu;
+      const uint32_t cb = __ballot_sync(0xFFFFFFFFu, rk < ncpu);
+      const uint32_t nc = __popc(cb);
+      if (gpu_ready == 0 && (bal & ~cb)) {
+        oldest_r = __shfl_sync(0xFFFFFFFFu, rw, __ffs(bal & ~cb) - 1);
+        have_oldest = true;
+      }
+      cpu_ready += nc;
+      gpu_ready += cnt - nc;
+      if (arr) {
+        if (rk < ncpu) {
+          lbit_set(sm, BM_CPU, rk);
+        } else {
+          lbit_set(sm, BM_GPU, rk);
+          lbit_set(sm, BM_WAIT, i);
+        }
+      }
+      next += cnt;
+      rw = next + lane < n ? g_r[next + lane] : INT64_MAX;
+      if (cnt < 32) break;
+    }
+    __syncwarp();
+    // ---- CPU cores: highest-key ready CPU task -> lowest-index free core
+    bool cpu_started = false;
+    while (cpu_ready) {
+      const uint32_t fm = __ballot_sync(0xFFFFFFFFu, lane < cores && sm.core_free[lane] <= now);
+      if (!fm) break;
+      const uint32_t c = __ffs(fm) - 1;
+      const uint32_t rk = lbit_first(sm, BM_CPU, lane);
+      const uint32_t i = perm[rk] - lo;
+      const int64_t end = now + (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)g_len[i]);
+      __syncwarp();
+      if (lane == 0) {
+        sm.core_free[c] = end;
+        lbit_clear(sm, BM_CPU, rk);
+        const int64_t ri = g_r[i];
+        resp += end - ri;
+        misses += end > ri + (int64_t)g_D[i];
+        if (a.end_us) a.end_us[lo + i] = end;
+      }
+      ++done;
+      --cpu_ready;
+      cpu_started = true;
+      __syncwarp();
+    }
+    if (cpu_started) cpu_min_valid = false;
+    // ---- GPU dispatch
+    bool waiting = false;
+    if (gpu_free <= now) {
+      const uint32_t total = gpu_ready;
+      if (total) {
+        if (!have_oldest) {
+          oldest_r = g_r[lbit_first(sm, BM_WAIT, lane)];
+          have_oldest = true;
+        }
+        const bool flush = (oldest_r <= now - p.xi_us) || next == n;
+        const uint32_t full = p.consolidate ? m : C;
+        const uint32_t take = total >= full ? full : (flush ? total : 0u);
+        if (!take) {
+          waiting = true;
+        } else {
+          lbit_take(sm, take, lane);
+          constexpr uint32_t kCh = kMaxWindow / 32;
+          const uint32_t nch = (take + 31u) >> 5;
+          uint32_t re[kCh], ix[kCh], pos[kCh], len_e[kCh], D_e[kCh];
+          float ue[kCh];
+          int64_t r_e[kCh];
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k) {
+            const uint32_t e = k * 32u + lane;
+            re[k] = 0xFFFFFFFFu; ix[k] = 0; ue[k] = 0.0f; len_e[k] = 0u; D_e[k] = 0u; r_e[k] = 0;
+            pos[k] = 0xFFFFFFFFu;
+            if (k < nch && e < take) {
+              re[k] = sm.W[e];
+              const uint32_t i = perm[re[k]] - lo;
+              ix[k] = i;
+              ue[k] = g_u[i];
+              len_e[k] = g_len[i];
+              D_e[k] = g_D[i];
+              r_e[k] = g_r[i];
+              pos[k] = e;
+            }
+          }
+          uint32_t cnt;
+          if (p.consolidate) {
+            // position in the (u asc, rank asc) order (R-TIE), by shuffles
+#pragma unroll
+            for (uint32_t k = 0; k < kCh; ++k) pos[k] = 0u;
+#pragma unroll
+            for (uint32_t xk = 0; xk < kCh; ++xk) {
+              if (xk < nch) {
+                const uint32_t lim = min(32u, take - xk * 32u);
+                for (uint32_t x = 0; x < lim; ++x) {
+                  const float ux = __shfl_sync(0xFFFFFFFFu, ue[xk], x);
+                  const uint32_t rx = __shfl_sync(0xFFFFFFFFu, re[xk], x);
+#pragma unroll
+                  for (uint32_t k = 0; k < kCh; ++k) pos[k] += (ux < ue[k]) || (ux == ue[k] && rx < re[k]);
+                }
+              }
+            }
+#pragma unroll
+            for (uint32_t k = 0; k < kCh; ++k) {
+              const uint32_t e = k * 32u + lane;
+              if (k < nch && e < take) sm.Su[pos[k]] = ue[k];
+              else pos[k] = 0xFFFFFFFFu;
+            }
+            __syncwarp();
+            const uint32_t lim = min(C, take);
+            cnt = lim;
+            for (uint32_t base = 1; base < lim; base += 32) {
+              const uint32_t ii = base + lane;
+              const bool bad = ii < lim && !(sm.Su[ii] <= __fmul_rn(p.lambda, sm.Su[ii - 1]));
+              const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bad);
+              if (bal) {
+                cnt = base + __ffs(bal) - 1;
+                break;
+              }
+            }
+          } else {
+            cnt = take;
+          }
+          uint32_t ml = 0;
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k)
+            if (pos[k] < cnt) ml = max(ml, len_e[k]);
+          ml = __reduce_max_sync(0xFFFFFFFFu, ml);
+          const int64_t end = now + gpu_fixed + p.eta_us * (int64_t)ml;
+#pragma unroll
+          for (uint32_t k = 0; k < kCh; ++k) {
+            if (pos[k] < cnt) {
+              lbit_clear(sm, BM_GPU, re[k]);
+              lbit_clear(sm, BM_WAIT, ix[k]);
+              resp += end - r_e[k];
+              misses += end > r_e[k] + (int64_t)D_e[k];
+              if (a.end_us) a.end_us[lo + ix[k]] = end;
+            }
+          }
+          done += cnt;
+          gpu_ready -= cnt;
+          have_oldest = false;
+          gpu_free = end;
+          __syncwarp();
+        }
+      }
+    }
+    if (done >= n) break;
+    // ---- next event time
+    int64_t nxt = INT64_MAX;
+    if (next < n) nxt = __shfl_sync(0xFFFFFFFFu, rw, 0);
+    if (gpu_free > now) nxt = min(nxt, gpu_free);
+    if (cpu_ready != 0) {
+      if (!cpu_min_valid) {
+        cpu_min_free = warp_min64(lane < cores ? sm.core_free[lane] : INT64_MAX);
+        cpu_min_valid = true;
+      }
+      nxt = min(nxt, cpu_min_free);
+    }
+    if (waiting) nxt = min(nxt, oldest_r + p.xi_us);
+    if (nxt == INT64_MAX) break;
+    now = nxt;
+  }
+  const int64_t sr = warp_sum64(resp);
+  const uint32_t ms = __reduce_add_sync(0xFFFFFFFFu, misses);
+  if (lane == 0) a.stats[t] = rt_trace_stats{sr, n, ms};
+}
+
 __global__ void k_reduce_stats(const rt_trace_stats* __restrict__ st, uint32_t nt, const uint16_t* __restrict__ grp,
                                uint32_t ngroups, int64_t* __restrict__ sums) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
@@ -519,6 +808,12 @@ cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
   note_launch();
   k_replay<<<a.nt, 32, smem, s>>>(a);
   note_launch();
+  if (a.long_perm) {  // some trace is longer than kMaxTrace (its rank order is already in long_perm)
+    e = cudaFuncSetAttribute(k_replay_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LongSmem));
+    if (e != cudaSuccess) return e;
+    k_replay_long<<<a.nt, 32, sizeof(LongSmem), s>>>(a);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -309,3 +309,73 @@ def test_schedule_argument_checks_launch_nothing(ctx_v1):
     g = ctx_v1.schedule(key, u, np.asarray([0, n], U32), dict(p, offload=0), cores=0)
     torch.cuda.synchronize()
     assert (g["core_of"].cpu().numpy() == 0xFF).all()
+
+
+# ------------------------------------------------------------------ long traces (k_replay_long)
+def _replay_vs_oracle(ctx, arr, tl, u, key, D, toff, profs, tp):
+    st, end = oracle.simulate(arr, tl, u, key, D, toff, profs, tp, want_end=True)
+    gs, gend = ctx.simulate(dev(arr), dev(tl), dev(u), dev(key), dev(D), toff, profs, dev(tp), want_end=True)
+    torch.cuda.synchronize()
+    g = rt.decode_stats(gs)
+    assert (g == st).all(), [(i, g[i], st[i]) for i in np.nonzero(g != st)[0][:3]]
+    assert (gend.cpu().numpy() == end).all()
+    return st
+
+
+@pytest.mark.parametrize("ov", [{}, {"consolidate": 0}, {"offload": 0}, {"policy": "EDF"}, {"tightness": 2},
+                                {"policy": "FIFO", "consolidate": 0, "offload": 0}])
+def test_replay_full_paper_ramp(ctx_v1, lex_v1, ov):
+    """Whole traces of the paper's workload: beta = 10, 11, .., 150 arrivals per
+    minute, one minute each = 11 280 Poisson arrivals per trace,
+    beside ordinary 1000-task traces in the same call; end times and stats
+    exact against the oracle."""
+    d = configs.traces(3, range(900, 904), 11280, lambda t: t % 4)
+    assert d["arrival_us"][11279] > 130 * 60_000_000  # the ramp really spans ~141 minutes
+    short = configs.traces(3, range(950, 953), 1000, lambda t: (t + 1) % 4)
+    cat = {k: np.concatenate([d[k], short[k]]) for k in ("arrival_us", "true_len", "trace_prof")}
+    toff = np.concatenate([d["trace_off"], d["trace_off"][-1] + short["trace_off"][1:]]).astype(U32)
+    profs = [dict(p, **ov) for p in d["profiles"]]
+    u, k, D = [], [], []
+    for dd in (d, short):
+        f = oracle.rule_gen(lex_v1, dd["data"], dd["offsets"])
+        for t in range(len(dd["trace_off"]) - 1):
+            lo, hi = int(dd["trace_off"][t]), int(dd["trace_off"][t + 1])
+            lm = int(dd["trace_prof"][t])
+            ut = oracle.predict(f[lo:hi], dd["regressors"][lm])
+            kt, Dt = oracle.key(ut, f[lo:hi], profs[lm], r_us=dd["arrival_us"][lo:hi])
+            u.append(ut), k.append(kt), D.append(Dt)
+    st = _replay_vs_oracle(ctx_v1, cat["arrival_us"], cat["true_len"], np.concatenate(u), np.concatenate(k),
+                           np.concatenate(D), toff, profs, cat["trace_prof"])
+    assert st["n"][0] == 11280 and st["n"][-1] == 1000
+
+
+@pytest.mark.parametrize("policy_ov", [{}, {"consolidate": 0}, {"offload": 0, "cores": 1}, {"b10": 30, "C": 33}])
+def test_replay_long_ties_and_sizes(ctx_v1, policy_ov):
+    """k_replay_long on traces of 1025 .. 65536 tasks with few distinct keys and u
+    values (rank ties broken by arrival index, R-TIE), bursts arriving together,
+    and an overload that keeps thousands of tasks ready."""
+    rng = np.random.default_rng(77)
+    sizes = [1025, 2048, 3001, 1024, 17, 65536]
+    toff = np.concatenate([[0], np.cumsum(sizes)]).astype(U32)
+    n = int(toff[-1])
+    arr = np.concatenate([np.sort(rng.integers(0, 20_000_000 * max(1, s // 1000), s)) for s in sizes]).astype(np.int64)
+    arr[toff[1]:toff[1] + 700] = arr[toff[1]]  # a burst of 700 simultaneous arrivals
+    arr[toff[1]:toff[2]] = np.sort(arr[toff[1]:toff[2]])
+    low = rng.choice(np.asarray([3, 3, 7, 1 << 40], np.uint64), n)
+    cls = (rng.random(n) < 0.2).astype(np.uint64) << np.uint64(63)
+    key = (cls | low).astype(np.uint64)
+    u = rng.choice(np.asarray([5.0, 5.0, 12.5, 40.0], np.float32), n)
+    tl = rng.integers(1, 80, n).astype(np.uint16)
+    D = rng.integers(1_000_000, 20_000_000, n).astype(U32)
+    profs = [dict(p, **policy_ov) for p in configs.paper_lms()]
+    tp = (np.arange(len(sizes)) % 4).astype(np.uint16)
+    _replay_vs_oracle(ctx_v1, arr, tl, u, key, D, toff, profs, tp)
+
+
+def test_replay_rejects_traces_over_65536(ctx_v1):
+    n = 65537
+    z = torch.zeros(n, dtype=torch.int64, device=DEV)
+    with pytest.raises(rt.RtlmError, match="65536"):
+        ctx_v1.simulate(z, torch.zeros(n, dtype=torch.int16, device=DEV), torch.zeros(n, device=DEV), z,
+                        torch.zeros(n, dtype=torch.int32, device=DEV), np.asarray([0, n], U32),
+                        [configs.paper_lms()[0]], None)
