@@ -316,8 +316,14 @@ __global__ void __launch_bounds__(128) k_ff_replay(FF f) {
   for (uint32_t pb = p0; pb < p1; pb += 32) {
     const uint64_t mine = pb + lane < p1 ? f.kk[pb + lane] : 0ull;
     const uint32_t cnt = min(32u, p1 - pb);
-    uint64_t outv = 0;
-    for (uint32_t i = 0; i < cnt; ++i) {
+    // a key below the heap's minimum at the start of the batch is evicted at once
+    // (the minimum only grows), so only the others go through the insertion
+    const uint64_t hmin = __shfl_sync(0xFFFFFFFFu, h[0], 0);
+    uint64_t outv = mine;
+    uint32_t todo = __ballot_sync(0xFFFFFFFFu, lane < cnt && mine > hmin);
+    while (todo) {
+      const uint32_t i = __ffs(todo) - 1;
+      todo &= todo - 1u;
       const uint64_t x = __shfl_sync(0xFFFFFFFFu, mine, i);
       uint32_t c = 0;
 #pragma unroll
@@ -1008,7 +1014,9 @@ static cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
   {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_double_all, 256, 0);
-    const uint32_t gd = std::min<uint32_t>((n + 256) / 256, (uint32_t)(a.num_sms * std::max(1, std::min(per_sm, 4))));
+    // few CTAs: a level is one pass over the nfail + 1 nodes (typically a few
+    // thousand), so a full grid would hold every SM through 13 grid barriers
+    const uint32_t gd = std::min<uint32_t>({(n + 256) / 256, (uint32_t)(a.num_sms * std::max(1, std::min(per_sm, 4))), 16u});
     void* args[] = {&f};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_ff_double_all, dim3(gd), dim3(256), args, 0, s);
     if (e != cudaSuccess) return e;
