@@ -59,7 +59,7 @@ def parse():
                          "all-reduce, MAX-over-ranks timing, rank-0 JSON line) without any kernel; for tests")
     ap.add_argument("--no-config5", action="store_true", help="skip config 5 (rate/deadline x ablation sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--depth", type=int, default=4, help="batches in flight (contexts / streams / distinct inputs)")
+    ap.add_argument("--depth", type=int, default=6, help="batches in flight (contexts / streams / distinct inputs)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay one CUDA graph per batch slot instead of issuing the pipelined step call by call")
     return ap.parse_args()
@@ -169,27 +169,48 @@ def dry_run(args):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock / throttle-reason sampling during the timed region: NVML
+    (nvidia_ml_py) every 2 ms, falling back to nvidia-smi every 200 ms."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            self._stop.wait(0.002)
+        pynvml.nvmlShutdown()
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        bits = [0x8, 0x40, 0x20, 0x4]
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
+                    r = [x.strip() for x in line.split(",")]
+                    m = sum(b for b, v in zip(bits, r[2:]) if v == "Active")
+                    self.rows.append((float(r[0]), float(r[1]), m))
             except Exception:
                 pass
             self._stop.wait(0.2)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -203,11 +224,8 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+        reasons = sorted({k for r in self.rows for k, b in self.REASONS.items() if int(r[2]) & b})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": reasons, "samples": len(self.rows)}
 
 
@@ -289,16 +307,33 @@ def native(args):
     h_res = [{k: torch.empty(n, dtype=dt).pin_memory() for k, dt in (("batch_of", torch.int32), ("slot_of", torch.uint8),
                                                                           ("core_of", torch.uint8))} for _ in range(depth)]
 
+    # scoring of every batch on one stream (in batch order) and each batch's
+    # schedule on its slot's stream: the persistent scoring kernels never run two
+    # at a time, so they never take the SMs the slots' one-SM list-scheduling
+    # chains run on; slot buffers are reused only after the slot's schedule
+    score_stream = torch.cuda.Stream(dev)
+    ev_scored = [torch.cuda.Event() for _ in range(depth)]
+    ev_sched = [torch.cuda.Event() for _ in range(depth)]
+    split_streams = os.environ.get("RTLM_SCORE_STREAM", "1") == "1" and not args.graphs
+
     def pstep(k, e2e=False):
         sl = k % depth
-        with torch.cuda.stream(streams[sl]):
-            if e2e:  # the C ABI's host-buffer entry: H2D copies, score+key+schedule, D2H of the assignment
-                ctxs[sl].score_schedule_host(h_bytes2[sl], h_off2[sl], reg, prof, h_res[sl])
-                return
-            if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "score"):
+        if e2e or not split_streams:
+            with torch.cuda.stream(streams[sl]):
+                if e2e:  # the C ABI's host-buffer entry: H2D copies, score+key+schedule, D2H of the assignment
+                    ctxs[sl].score_schedule_host(h_bytes2[sl], h_off2[sl], reg, prof, h_res[sl])
+                    return
                 ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
-            if os.environ.get("RTLM_BENCH_PART", "all") in ("all", "schedule"):
                 ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
+            return
+        with torch.cuda.stream(score_stream):
+            score_stream.wait_event(ev_sched[sl])  # the slot's previous schedule has read u / key
+            ctxs[sl].score_key(data2[sl], off2[sl], reg, prof, want_D=False, out=outs2[sl])
+            ev_scored[sl].record(score_stream)
+        with torch.cuda.stream(streams[sl]):
+            streams[sl].wait_event(ev_scored[sl])
+            ctxs[sl].schedule(outs2[sl]["key"], outs2[sl]["u"], seg, prof, out=souts2[sl])
+            ev_sched[sl].record(streams[sl])
 
     # --graphs: one CUDA graph per batch slot holding that slot's whole step
     # (rt_score_key + rt_schedule: ~50 kernels, the CPU-class fork/join and the
@@ -337,23 +372,29 @@ def native(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for st in streams:
+        for st in streams + [score_stream]:
             st.wait_event(t0)
         for k in range(args.steps):
             if use_graphs:
                 gstep(k)
             else:
                 pstep(k, e2e)
-        for st in streams:
+        for st in streams + [score_stream]:
             stream.wait_stream(st)
         t1.record(stream)
         t1.synchronize()
         return t0.elapsed_time(t1)
 
-    # each in-flight batch forks a one-CTA list-scheduling chain that holds an SM for
-    # ~1.3 ms; the persistent scoring kernels leave `depth` SMs to them (rt_set_sm_limit)
+    # SM partition: the persistent scoring kernel (one at a time, on the scoring
+    # stream) gets ~2/3 of the SMs; the slots' schedules (GPU-class consolidation
+    # kernels and the one-SM CPU-class list-scheduling chains) run concurrently on
+    # the rest.  Measured (profiles/notes/r02_schedule_pipeline.md): 100 of 148
+    # SMs at depth 6 -> 0.665 ms/batch vs 0.858 with all-SM scoring per slot stream.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    score_ctas = max(1, nsm - depth) if depth > 1 else nsm
+    if split_streams:
+        score_ctas = max(1, (nsm * 27) // 40) if depth > 1 else nsm
+    else:
+        score_ctas = max(1, nsm - depth) if depth > 1 else nsm
     if os.environ.get("RTLM_SCORE_CTAS"):
         score_ctas = int(os.environ["RTLM_SCORE_CTAS"])
     for c in ctxs:
@@ -457,6 +498,8 @@ def native(args):
                                    "score+key+schedule", "requests_per_gpu": n, "bytes_per_gpu": total_bytes,
                        "pipeline": f"{depth} batches in flight ({depth} contexts / streams), cycling {depth} distinct inputs, "
                                    f"scoring on {score_ctas} CTAs"
+                                   + ("; scoring of every batch on one stream, each batch's schedule on its slot's "
+                                      "stream (event-ordered)" if split_streams else "")
                                    + ("; each slot's step replayed from one CUDA graph" if args.graphs else ""),
                        "l2": f"pipelined: {depth} distinct inputs of ~100 MB each (> 126 MB L2) in turn; "
                              "latency leg: 256 MB buffer written between steps",
@@ -499,39 +542,58 @@ def native(args):
 def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_ranks, flush, peaks):
     """NEXT-1: u = m_theta(feat) for the config-2 queue (features from rt_score),
     random-init weights (no trained model exists here; the cost does not depend
-    on the values).  Roofline: tensor, algorithmic 2 * 80 700 FLOP per request."""
+    on the values), in both precisions: fp32 (default; CUDA-core binary32 FMA
+    chains, k_mlp_f32) and bf16 (opt-in; tcgen05 tensor cores, k_mlp).
+    Algorithmic 2 * 80 700 FLOP per request.  Rooflines: fp32 against the
+    CUDA-core FMA peak (148 SMs x 128 FP32 lanes x 2 FLOP x the SM clock,
+    derived: the profiling guide and MEASURED_PEAKS.json give no fp32 number);
+    bf16 against MEASURED_PEAKS.json bf16_tflops."""
     import torch
     import rtgen
     feat = ctx.score(data, off)
     ws, bs = rtgen.mlp_weights(12345)
     ctx.set_mlp(ws, bs)
     u = torch.empty(n, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
-        ctx.predict_mlp(feat, u)
-    torch.cuda.synchronize()
-    barrier()
-    ev_a = torch.cuda.Event(enable_timing=True)
-    ev_b = torch.cuda.Event(enable_timing=True)
-    ts = []
-    for _ in range(args.steps):
-        flush.zero_()
-        ev_a.record(stream)
-        ctx.predict_mlp(feat, u)
-        ev_b.record(stream)
-        ev_b.synchronize()
-        ts.append(ev_a.elapsed_time(ev_b))
-    tsum = max_over_ranks(sum(ts))
-    ms = tsum / args.steps
     flops = 2 * (6 * 100 + 100 * 200 + 200 * 200 + 200 * 100 + 100) * n
-    peak = float(peaks.get("bf16_tflops", 2250.0))
-    achieved = flops / (ms / 1e3) / 1e12
-    return {"metric": "M requests/s (u = m_theta(feat), MLP 6-100-200-200-100-1)", "unit": "Mreq/s",
-            "value": round(world * n / (ms / 1e3) / 1e6, 2), "ms_per_step": round(ms, 4),
-            "dtype": "bf16 tensor cores (tcgen05), fp32 accumulate; layers 1/5 fp32",
-            "roofline": {"bound": "tensor", "kernel": "k_mlp", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "nominal",
-                         "alg_flops_per_launch": flops}}
+    props = torch.cuda.get_device_properties(dev)
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    out = {"metric": "M requests/s (u = m_theta(feat), MLP 6-100-200-200-100-1)", "unit": "Mreq/s",
+           "alg_flops_per_launch": flops}
+    for prec in ("fp32", "bf16"):
+        ctx.set_mlp_precision(prec)
+        for _ in range(args.warmup):
+            ctx.predict_mlp(feat, u)
+        torch.cuda.synchronize()
+        barrier()
+        ev_a = torch.cuda.Event(enable_timing=True)
+        ev_b = torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(max(3, args.steps // 4) if prec == "fp32" else args.steps):
+            flush.zero_()
+            ev_a.record(stream)
+            ctx.predict_mlp(feat, u)
+            ev_b.record(stream)
+            ev_b.synchronize()
+            ts.append(ev_a.elapsed_time(ev_b))
+        ms = max_over_ranks(sum(ts)) / len(ts)
+        achieved = flops / (ms / 1e3) / 1e12
+        if prec == "fp32":
+            peak = props.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+            roof = {"bound": "alu", "kernel": "k_mlp_f32", "achieved": round(achieved, 2), "peak": round(peak, 2),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FP32 FMA/clk x 2 x {mhz:.0f} MHz"}
+            dtype = "fp32 CUDA cores (binary32 FMA chains in index order)"
+        else:
+            peak = float(peaks.get("bf16_tflops", 2250.0))
+            roof = {"bound": "tensor", "kernel": "k_mlp", "achieved": round(achieved, 1), "peak": peak,
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "nominal"}
+            dtype = "bf16 tensor cores (tcgen05), fp32 accumulate; layers 1/5 fp32"
+        out[prec] = {"value": round(world * n / (ms / 1e3) / 1e6, 2), "ms_per_step": round(ms, 4), "dtype": dtype,
+                     "roofline": roof}
+    ctx.set_mlp_precision("fp32")
+    out["value"] = out["fp32"]["value"]  # the default precision
+    return out
 
 
 def offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks):

@@ -25,7 +25,7 @@ POLICY = {"FIFO": 0, "EDF": 1, "HPF": 1, "LUF": 2, "MUF": 3, "SLACK": 4, "UP": 5
 RT_STATUS = {0: "RT_OK", 1: "RT_EINVAL", 2: "RT_ELEXICON", 3: "RT_ENOMEM", 4: "RT_ECUDA", 5: "RT_EOVERFLOW"}
 EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_version", "rt_lexicon_size",
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
-           "rt_set_mlp", "rt_predict_mlp", "rt_fit_rule", "rt_quantile", "rt_trace_report",
+           "rt_set_mlp", "rt_predict_mlp", "rt_set_mlp_precision", "rt_fit_rule", "rt_quantile", "rt_trace_report",
            "rt_trace_utilization", "rt_set_sm_limit", "rt_score_schedule_host",
            "rt_schedule_deadlines"]
 NO_BATCH = 0xFFFFFFFF
@@ -128,6 +128,8 @@ def load_library(path: str = LIB_PATH):
     L.rt_set_mlp.argtypes = [V, ctypes.POINTER(Mlp)]
     L.rt_predict_mlp.restype = I32
     L.rt_predict_mlp.argtypes = [V, P, U32, P, V]
+    L.rt_set_mlp_precision.restype = I32
+    L.rt_set_mlp_precision.argtypes = [V, ctypes.c_int]
     L.rt_fit_rule.restype = I32
     L.rt_fit_rule.argtypes = [V, P, P, U32, P, V]
     L.rt_quantile.restype = I32
@@ -268,6 +270,11 @@ class Context:
             m.w[l] = ws[l].ctypes.data
             m.b[l] = bs[l].ctypes.data
         self._check(self._L.rt_set_mlp(self._h, ctypes.byref(m)))
+
+    def set_mlp_precision(self, precision: str) -> None:
+        """rt_set_mlp_precision: "fp32" (default, CUDA-core binary32) or "bf16"
+        (tcgen05 tensor cores, opt-in fast mode)."""
+        self._check(self._L.rt_set_mlp_precision(self._h, {"fp32": 0, "bf16": 1}[precision]))
 
     def predict_mlp(self, feat, u=None):
         """rt_predict_mlp: feat uint16-as-int16 [n, 8] -> u float32 [n]."""

@@ -27,7 +27,9 @@ struct rt_ctx {
   size_t prof_cap = 0;
   cudaStream_t aux = nullptr;  // internal fork stream (CPU-class list scheduling)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp)
+  uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp): bf16 tensor-core blob
+  float* d_mlp32 = nullptr;  // fp32 blob (k_mlp_f32)
+  int mlp_precision = RT_MLP_FP32;
   void* io = nullptr;        // device buffers of rt_score_schedule_host
   size_t io_size = 0;
   uint64_t* kbuf = nullptr;  // keys of rt_schedule_deadlines
@@ -449,6 +451,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
+    cudaFree(c->d_mlp32);
     cudaFree(c->io);
     cudaFree(c->kbuf);
     for (void* p : c->captured_stage) cudaFreeHost(p);
@@ -567,6 +570,20 @@ rt_status rt_set_mlp(rt_ctx* c, const rt_mlp* mlp) {
     if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("mlp weights: ") + cudaGetErrorString(e));
   }
   RT_CUDA(c, cudaMemcpy(c->d_mlp, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  std::vector<float> blob32(rtlm::mlp_f32_blob_bytes() / 4);
+  rtlm::mlp_f32_pack(mlp->w, mlp->b, blob32.data());
+  if (!c->d_mlp32) {
+    cudaError_t e = cudaMalloc(&c->d_mlp32, rtlm::mlp_f32_blob_bytes());
+    if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("mlp weights: ") + cudaGetErrorString(e));
+  }
+  RT_CUDA(c, cudaMemcpy(c->d_mlp32, blob32.data(), rtlm::mlp_f32_blob_bytes(), cudaMemcpyHostToDevice));
+  return RT_OK;
+}
+
+rt_status rt_set_mlp_precision(rt_ctx* c, int precision) {
+  if (!c) return RT_EINVAL;
+  if (precision != RT_MLP_FP32 && precision != RT_MLP_BF16) return fail(c, RT_EINVAL, "unknown MLP precision");
+  c->mlp_precision = precision;
   return RT_OK;
 }
 
@@ -578,8 +595,10 @@ rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
   if (capturing(cs(stream))) c->captured = true;  // see retire()
-  cudaError_t e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream));
-  if (e != cudaSuccess) return cuda_fail(c, e, "k_mlp");
+  cudaError_t e = c->mlp_precision == RT_MLP_BF16
+                      ? rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream))
+                      : rtlm::launch_mlp_f32(d_feat, n, c->d_mlp32, d_u, persistent_ctas(c), cs(stream));
+  if (e != cudaSuccess) return cuda_fail(c, e, c->mlp_precision == RT_MLP_BF16 ? "k_mlp" : "k_mlp_f32");
   return RT_OK;
 }
 

@@ -164,6 +164,11 @@ cudaError_t launch_quantile(const float* u, uint32_t n, uint32_t r, void* ws, fl
 size_t mlp_blob_bytes();
 void mlp_pack(const float* const w[5], const float* const b[5], uint8_t* blob);
 cudaError_t launch_mlp(const uint16_t* feat, uint32_t n, const uint8_t* blob, float* u, int num_sms, cudaStream_t s);
+// K7 fp32 mode (k_mlp_f32.cu): CUDA-core binary32 FMA chains
+size_t mlp_f32_blob_bytes();
+void mlp_f32_pack(const float* const w[5], const float* const b[5], float* blob);
+cudaError_t launch_mlp_f32(const uint16_t* feat, uint32_t n, const float* blob, float* u, int num_sms,
+                           cudaStream_t s);
 cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* group_of, uint32_t ngroups,
                                 int64_t* sums, cudaStream_t s);
 

@@ -65,22 +65,31 @@ def ctx_v1():
 
 
 # ------------------------------------------------------------------ the bench's timed step
-@pytest.mark.parametrize("graphs", [False, True])
-def test_bench_pipeline_launch_configuration(lex_v1, graphs):
-    """bench.py's pipelined requests leg (depth 4, per-slot contexts and streams,
-    rt_set_sm_limit(nsm - depth), two waves of steps so that every slot runs
-    while the others' kernels are in flight), with and without CUDA graphs."""
-    n, depth, steps = 1 << 20, 4, 8
+@pytest.mark.parametrize("mode", ["split", "slot", "graphs"])
+def test_bench_pipeline_launch_configuration(lex_v1, mode):
+    """bench.py's pipelined requests leg in each of its launch forms: "split"
+    (the default: every batch's scoring on one stream with the persistent
+    kernel capped at ~2/3 of the SMs, each batch's schedule on its slot's stream,
+    ordered by events; depth 6), "slot" (score + schedule on the slot's stream,
+    scoring capped at nsm - depth; depth 4) and "graphs" (slot form, each slot's
+    step replayed from one CUDA graph).  Two waves of steps so that every slot
+    runs while other slots' kernels are in flight; every batch against the oracle."""
+    n = 1 << 20
+    depth = 6 if mode == "split" else 4
+    steps = 2 * depth
     nsm = torch.cuda.get_device_properties(DEV).multi_processor_count
     ds = [configs.config2(n=n, gid0=i * n) for i in range(depth)]
     prof, reg = ds[0]["profile"], ds[0]["regressor"]
     seg = np.asarray([0, n], U32)
     ctxs = [rt.Context(d["lexicon"], 0) for d in ds]
     for c in ctxs:
-        c.set_sm_limit(max(1, nsm - depth))
+        c.set_sm_limit((nsm * 27) // 40 if mode == "split" else max(1, nsm - depth))
     data = [dev(d["data"]) for d in ds]
     off = [dev(d["offsets"]) for d in ds]
     streams = [torch.cuda.Stream(DEV) for _ in range(depth)]
+    score_stream = torch.cuda.Stream(DEV)
+    ev_scored = [torch.cuda.Event() for _ in range(depth)]
+    ev_sched = [torch.cuda.Event() for _ in range(depth)]
     outs = [{"u": torch.empty(n, dtype=torch.float32, device=DEV), "key": torch.empty(n, dtype=torch.int64, device=DEV)}
             for _ in range(depth)]
     souts = [{"perm": torch.empty(n, dtype=torch.int32, device=DEV),
@@ -91,6 +100,16 @@ def test_bench_pipeline_launch_configuration(lex_v1, graphs):
 
     def pstep(k):
         sl = k % depth
+        if mode == "split":
+            with torch.cuda.stream(score_stream):
+                score_stream.wait_event(ev_sched[sl])
+                ctxs[sl].score_key(data[sl], off[sl], reg, prof, want_D=False, out=outs[sl])
+                ev_scored[sl].record(score_stream)
+            with torch.cuda.stream(streams[sl]):
+                streams[sl].wait_event(ev_scored[sl])
+                ctxs[sl].schedule(outs[sl]["key"], outs[sl]["u"], seg, prof, out=souts[sl])
+                ev_sched[sl].record(streams[sl])
+            return
         with torch.cuda.stream(streams[sl]):
             ctxs[sl].score_key(data[sl], off[sl], reg, prof, want_D=False, out=outs[sl])
             ctxs[sl].schedule(outs[sl]["key"], outs[sl]["u"], seg, prof, out=souts[sl])
@@ -98,11 +117,11 @@ def test_bench_pipeline_launch_configuration(lex_v1, graphs):
     for k in range(depth):  # warm-up: every slot runs before its capture
         pstep(k)
     torch.cuda.synchronize()
-    for o in souts:  # poison the outputs: the timed-style waves below must rewrite them
+    for o in souts:  # poison the outputs: the waves below must rewrite them
         for t in o.values():
             t.fill_(-1 if t.dtype != torch.uint8 else 0x7F)
     torch.cuda.synchronize()
-    if graphs:
+    if mode == "graphs":
         gs = []
         for sl in range(depth):
             g = torch.cuda.CUDAGraph()
