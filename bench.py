@@ -658,34 +658,45 @@ def malicious_leg(args, ctx, configs, dev, rank, max_over_ranks):
     """NEXT-3: malicious-task ratio sweep 0..100 % in steps of 10 %:
     crafted suffix + x3 true length on a seeded fraction of the requests; UP+C+O
     (the profiles as calibrated) against FIFO without consolidation / offloading.
-    128 traces x 1000 requests per point (statistics, not gated)."""
+    128 traces x 1000 requests per point, at two operating points: the paper's
+    ramp with tight deadlines (x1/tight: every task is overdue on arrival, so
+    the policies can only differ in response time) and an 8x faster ramp with
+    loose deadlines (x8/loose, config 5's knee: queues form, ready sets hold
+    many tasks, and the policies' orders matter).  Statistics, not gated."""
     nt = 128
     first = 10000 + rank * nt
-    base = configs.traces(3, range(first, first + nt), 1000, lambda t: ((t - first) * 4) // nt)
     ratios = [round(0.1 * i, 1) for i in range(11)]
-    out = {"ratios": ratios, "mean_response_s": {"UP+C+O": [], "FIFO": []}, "miss_ratio": {"UP+C+O": [], "FIFO": []}}
+    out = {"ratios": ratios, "traces_per_point": nt}
     dev_ms = 0.0
-    for r in ratios:
-        d = configs.with_malicious(base, r)
-        for name, ov in (("UP+C+O", None), ("FIFO", {"policy": "FIFO", "consolidate": 0, "offload": 0})):
-            resp, cnt, miss, ms = run_traces_once(ctx, d, dev, ov)
-            dev_ms += ms
-            out["mean_response_s"][name].append(round(resp / max(cnt, 1) / 1e6, 4))
-            out["miss_ratio"][name].append(round(miss / max(cnt, 1), 4))
-    out["traces_per_point"] = nt
+    for op, mult, tight in (("x1/tight", 1.0, 1), ("x8/loose", 8.0, 2)):
+        base = configs.traces(3, range(first, first + nt), 1000, lambda t: ((t - first) * 4) // nt,
+                              beta0=10.0 * mult, step=mult, beta_max=150.0 * mult)
+        res = {"mean_response_s": {"UP+C+O": [], "FIFO": []}, "miss_ratio": {"UP+C+O": [], "FIFO": []}}
+        for r in ratios:
+            d = configs.with_malicious(base, r)
+            for name, ov in (("UP+C+O", {"tightness": tight}),
+                             ("FIFO", {"policy": "FIFO", "consolidate": 0, "offload": 0, "tightness": tight})):
+                resp, cnt, miss, ms = run_traces_once(ctx, d, dev, ov)
+                dev_ms += ms
+                res["mean_response_s"][name].append(round(resp / max(cnt, 1) / 1e6, 4))
+                res["miss_ratio"][name].append(round(miss / max(cnt, 1), 4))
+        out[op] = res
     # periodic release (P:672-676): each task released at the previous task's
     # deadline, tight / loose; deadlines from the GPU path (rt_score_key)
     out["periodic"] = periodic_leg(ctx, configs.traces(3, range(12000 + rank * nt, 12000 + (rank + 1) * nt), 1000,
                                                        lambda t: ((t - 12000 - rank * nt) * 4) // nt), dev)
-    out["variance"] = variance_leg(ctx, rank, dev)
+    # the variance subsets are single-LM DialoGPT traces: queues form only above
+    # ~x32 (a C = 11 batch of ~1.5 s serves ~400 tasks per minute)
+    out["variance"] = {op: variance_leg(ctx, rank, dev, mult, tight) for op, mult, tight in
+                       (("x1/tight", 1.0, 1), ("x32/loose", 32.0, 2))}
     out["device_ms_total"] = round(max_over_ranks(dev_ms), 3)
-    out["traces_per_s"] = round(nt * len(ratios) * 2 / (out["device_ms_total"] / 1e3), 1)
-    out["note"] = ("statistics of the synthetic workload, not gated: config 3's tight deadlines overload the "
-                   "executors (miss ratio > 0.9), and offloaded malicious tasks queue on 4 CPU cores at gamma = 5")
+    out["traces_per_s"] = round(nt * len(ratios) * 4 / (out["device_ms_total"] / 1e3), 1)
+    out["note"] = ("statistics of the synthetic workload, not gated; x1/tight: config 3's tight deadlines make "
+                   "every task overdue on arrival; x8/loose: queues form, so the orders of the policies differ")
     return out
 
 
-def variance_leg(ctx, rank, dev):
+def variance_leg(ctx, rank, dev, mult=1.0, tight=1):
     """NEXT-3 variance subsets: a DialoGPT pool of 64 traces x 1000
     requests scored on the GPU; 20 000 tasks each with small / medium / large
     spread of u (configs.variance_subsets), packed into 20 Poisson traces of
@@ -708,8 +719,8 @@ def variance_leg(ctx, rank, dev):
     subs = configs.variance_subsets(u.cpu().numpy(), size)
     nt = size // per
     toff = (np.arange(nt + 1) * per).astype(np.uint32)
-    arr = torch.from_numpy(np.concatenate([rtgen.arrivals(rtgen.ROOT_SEED + 3, 900000 + first + t, per)
-                                           for t in range(nt)])).to(dev)
+    arr = torch.from_numpy(np.concatenate([rtgen.arrivals(rtgen.ROOT_SEED + 3, 900000 + first + t, per, 10.0 * mult,
+                                                          mult, 150.0 * mult) for t in range(nt)])).to(dev)
     tp = torch.zeros(nt, dtype=torch.int16, device=dev)
     tl_all = torch.from_numpy(pool["true_len"].view(np.int16)).to(dev)
     pols = {"FIFO": {"policy": "FIFO", "consolidate": 0, "offload": 0},
@@ -721,13 +732,13 @@ def variance_leg(ctx, rank, dev):
         fs, us, tl = feat[ix].contiguous(), u[ix].contiguous(), tl_all[ix].contiguous()
         row = {"u_std": round(float(us.std().item()), 3)}
         for name, ov in pols.items():
-            prof = dict(pool["profiles"][0], **ov)
+            prof = dict(pool["profiles"][0], tightness=tight, **ov)
             key, D = ctx.key(us, prof, feat=fs, arrival=arr)
             stats, _ = ctx.simulate(arr, tl, us, key, D, toff, [prof], tp)
             st = rt.decode_stats(stats)
             row[name] = round(float(st["sum_resp_us"].sum()) / max(1, int(st["n"].sum())) / 1e6, 4)
         res[which] = row
-    return {"mean_response_s": res, "tasks_per_subset": size}
+    return {"mean_response_s": res, "tasks_per_subset": size, "rate_multiplier": mult, "tightness": tight}
 
 
 def periodic_leg(ctx, base, dev):
