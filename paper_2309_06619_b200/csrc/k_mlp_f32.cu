@@ -6,13 +6,12 @@
 // the default (rt_set_mlp_precision), the bf16 tensor-core kernel (k_mlp.cu)
 // the opt-in fast mode.
 //
-// Persistent CTAs of 256 threads, a tile is 64 requests.  Activations of the
-// tile stay in shared memory (two 64 x 204 fp32 buffers, row-major, rows
+// Persistent CTAs of 256 threads (two per SM), a tile is 64 requests.  The
+// tile's activations stay in shared memory (one 64 x 204 fp32 buffer that each
+// layer overwrites in place, row-major, rows
 // padded to 204 words), weights stream from L2 in k-chunks of 32 (k-major,
-// [k][208]), double-buffered with cp.async.  Thread (rg, cg) = (tid / 16,
-// tid % 16) owns rows 4rg..4rg+3 and columns cg + 16j, j = 0..12: every 4 k,
-// four 128-bit activation loads (broadcast within half-warps) and 4 x 13
-// conflict-free weight loads feed 208 FMAs.
+// [k][208]), double-buffered with cp.async; a 4-row x 16-column register tile
+// per thread (see layer()).
 #include "internal.cuh"
 
 namespace rtlm {
@@ -23,7 +22,6 @@ constexpr uint32_t kThr = 256;
 constexpr uint32_t kXS = 204;      // activation row stride (words)
 constexpr uint32_t kNW = 208;      // weight chunk row (output columns, padded)
 constexpr uint32_t kKC = 32;       // k per weight chunk
-constexpr uint32_t kCols = 13;     // columns per thread (cg + 16 j)
 // fp32 blob (mlp_f32_pack): W1[100][6] b1[100] | W2t[100][208] b2[208] | W3t[200][208] b3[208] |
 // W4t[200][208] b4[208] | W5[100] b5  -- Wlt = W_l transposed to [in][out], out padded to 208
 constexpr uint32_t F_W1 = 0, F_B1 = 600, F_W2 = 700, F_B2 = F_W2 + 100 * kNW, F_W3 = F_B2 + kNW,
@@ -31,7 +29,7 @@ constexpr uint32_t F_W1 = 0, F_B1 = 600, F_W2 = 700, F_B2 = F_W2 + 100 * kNW, F_
                    F_B5 = F_W5 + 100, F_N = F_B5 + 4;
 
 struct Smem {
-  float X[2][kT][kXS];          // activations (ping-pong)
+  float X[kT][kXS];             // activations (each layer overwrites its input in place)
   float W[2][kKC][kNW];         // weight chunks (double buffer)
   float w1[600], b1[100], w5[100];
 };
@@ -53,14 +51,23 @@ __device__ __forceinline__ void stage_w(float (*dst)[kNW], const float* __restri
   cp_commit();
 }
 
-// one hidden layer: Y[64][N] = relu(X[64][K] . Wt[K][N] + b), fma chain in k order
-__device__ __forceinline__ void layer(Smem& S, const float (*X)[kXS], float (*Y)[kXS], const float* __restrict__ Wt,
-                                      const float* __restrict__ b, uint32_t K, uint32_t N) {
-  const uint32_t rg = threadIdx.x >> 4, cg = threadIdx.x & 15u;
-  float acc[4][kCols];
+// one hidden layer: Y[64][N] = relu(X[64][K] . Wt[K][N] + b), fma chain in k order.
+// Thread t < 208 owns rows 4 rg .. 4 rg + 3 (rg = t / 13) and the 16 columns
+// 4 cg + 52 v + e (cg = t % 13, v, e < 4; consecutive threads read consecutive
+// 16-byte quads: no bank conflicts): every 4 k, four 128-bit activation loads
+// and sixteen 128-bit weight loads feed 256 FMAs.
+__device__ __forceinline__ void layer(Smem& S, const float* __restrict__ Wt, const float* __restrict__ b, uint32_t K,
+                                      uint32_t N) {
+  float (*X)[kXS] = S.X;
+  const uint32_t t = threadIdx.x;
+  const bool act = t < 16u * 13u;
+  const uint32_t rg = act ? t / 13u : 0u, cg = act ? t % 13u : 0u;
+  const uint32_t c0 = 4u * cg;
+  auto colof = [&](int j) { return c0 + 52u * (uint32_t)(j >> 2) + (uint32_t)(j & 3); };
+  float acc[4][16];
 #pragma unroll
-  for (int j = 0; j < (int)kCols; ++j) {
-    const uint32_t col = cg + 16u * j;
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t col = colof(j);
     const float bj = col < N ? __ldg(b + col) : 0.0f;
 #pragma unroll
     for (int r = 0; r < 4; ++r) acc[r][j] = bj;
@@ -74,34 +81,44 @@ __device__ __forceinline__ void layer(Smem& S, const float (*X)[kXS], float (*Y)
     __syncthreads();  // chunk c visible to all; chunk c-1's buffer free
     if (c + 1 < nch) stage_w(S.W[(c + 1) & 1], Wt, k0 + kKC, min(kKC, K - k0 - kKC));
     const float (*Wc)[kNW] = S.W[c & 1];
-    for (uint32_t kk = 0; kk < kc; kk += 4) {  // K is a multiple of 4 (100, 200)
-      float4 a[4];
+    if (act) {
+      for (uint32_t kk = 0; kk < kc; kk += 4) {  // K is a multiple of 4 (100, 200)
+        float4 a[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const float4*>(&X[4 * rg + r][k0 + kk]);
+        for (int r = 0; r < 4; ++r) a[r] = *reinterpret_cast<const float4*>(&X[4 * rg + r][k0 + kk]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float w[kCols];
+        for (int q = 0; q < 4; ++q) {
+          float4 w[4];
 #pragma unroll
-        for (int j = 0; j < (int)kCols; ++j) w[j] = Wc[kk + q][cg + 16u * j];
+          for (int v = 0; v < 4; ++v) w[v] = *reinterpret_cast<const float4*>(&Wc[kk + q][c0 + 52 * v]);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float av = q == 0 ? a[r].x : q == 1 ? a[r].y : q == 2 ? a[r].z : a[r].w;
+          for (int r = 0; r < 4; ++r) {
+            const float av = q == 0 ? a[r].x : q == 1 ? a[r].y : q == 2 ? a[r].z : a[r].w;
 #pragma unroll
-          for (int j = 0; j < (int)kCols; ++j) acc[r][j] = __fmaf_rn(av, w[j], acc[r][j]);
+            for (int v = 0; v < 4; ++v) {
+              acc[r][4 * v + 0] = __fmaf_rn(av, w[v].x, acc[r][4 * v + 0]);
+              acc[r][4 * v + 1] = __fmaf_rn(av, w[v].y, acc[r][4 * v + 1]);
+              acc[r][4 * v + 2] = __fmaf_rn(av, w[v].z, acc[r][4 * v + 2]);
+              acc[r][4 * v + 3] = __fmaf_rn(av, w[v].w, acc[r][4 * v + 3]);
+            }
+          }
         }
       }
     }
   }
+  __syncthreads();  // every thread has read its inputs: overwrite X with the outputs
+  if (act) {
 #pragma unroll
-  for (int j = 0; j < (int)kCols; ++j) {
-    const uint32_t col = cg + 16u * j;
-    if (col < N)
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t col = colof(j);
+      if (col < N)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) Y[4 * rg + r][col] = fmaxf(acc[r][j], 0.0f);
+        for (int r = 0; r < 4; ++r) X[4 * rg + r][col] = fmaxf(acc[r][j], 0.0f);
+    }
   }
 }
 
-__global__ void __launch_bounds__(kThr, 1) k_mlp_f32(const uint16_t* __restrict__ feat, uint32_t n,
+__global__ void __launch_bounds__(kThr, 2) k_mlp_f32(const uint16_t* __restrict__ feat, uint32_t n,
                                                     const float* __restrict__ P, float* __restrict__ u_out) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -129,18 +146,18 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_f32(const uint16_t* __restrict_
         for (int i = 0; i < 6; ++i) acc = __fmaf_rn(S.w1[j * 6 + i], x[i], acc);
         acc = fmaxf(acc, 0.0f);
       }
-      S.X[0][r][j] = acc;
+      S.X[r][j] = acc;
     }
     // ---- layers 2-4
-    layer(S, S.X[0], S.X[1], P + F_W2, P + F_B2, 100, 200);
-    layer(S, S.X[1], S.X[0], P + F_W3, P + F_B3, 200, 200);
-    layer(S, S.X[0], S.X[1], P + F_W4, P + F_B4, 200, 100);
+    layer(S, P + F_W2, P + F_B2, 100, 200);
+    layer(S, P + F_W3, P + F_B3, 200, 200);
+    layer(S, P + F_W4, P + F_B4, 200, 100);
     __syncthreads();
     // ---- layer 5 (100 -> 1), clamp at 0: 4 threads per row, then a fixed-order sum
     if (tid < kT) {
       const uint32_t rq = t * kT + tid;
       float acc = b5;
-      for (uint32_t k = 0; k < 100; ++k) acc = __fmaf_rn(S.w5[k], S.X[1][tid][k], acc);
+      for (uint32_t k = 0; k < 100; ++k) acc = __fmaf_rn(S.w5[k], S.X[tid][k], acc);
       if (rq < n) u_out[rq] = fmaxf(acc, 0.0f);
     }
   }
@@ -174,7 +191,7 @@ cudaError_t launch_mlp_f32(const uint16_t* feat, uint32_t n, const float* blob, 
   cudaError_t e = cudaFuncSetAttribute(k_mlp_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const uint32_t ntiles = (n + kT - 1) / kT;
-  const uint32_t grid = ntiles < (uint32_t)num_sms ? ntiles : (uint32_t)num_sms;
+  const uint32_t grid = ntiles < 2u * (uint32_t)num_sms ? ntiles : 2u * (uint32_t)num_sms;  // 2 CTAs per SM
   k_mlp_f32<<<grid, kThr, smem, s>>>(feat, n, blob, u);
   note_launch();
   return cudaGetLastError();

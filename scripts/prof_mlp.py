@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """rt_predict_mlp on config-2 features (random-init weights): CUDA-event ms per launch.
-Usage: python scripts/prof_mlp.py [reps]"""
+Usage: python scripts/prof_mlp.py [reps] [fp32|bf16]"""
 import os
 import sys
 
@@ -19,6 +19,7 @@ ctx = rt.Context(d["lexicon"], 0)
 feat = ctx.score(torch.from_numpy(d["data"]).to(dev), torch.from_numpy(d["offsets"].view(np.int32)).to(dev))
 ws, bs = rtgen.mlp_weights(12345)
 ctx.set_mlp(ws, bs)
+ctx.set_mlp_precision(sys.argv[2] if len(sys.argv) > 2 else "bf16")
 u = torch.empty(feat.shape[0], dtype=torch.float32, device=dev)
 for _ in range(3):
     ctx.predict_mlp(feat, u)
