@@ -15,8 +15,11 @@ namespace rtlm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr uint32_t kTile = kThreads * kItems;  // 4096 keys
+#ifndef KSORT_ITEMS
+#define KSORT_ITEMS 12
+#endif
+constexpr int kItems = KSORT_ITEMS;
+constexpr uint32_t kTile = kThreads * kItems;  // keys per tile
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxPass = 8;
 constexpr uint32_t kFlagA = 1u << 30;  // tile aggregate published
