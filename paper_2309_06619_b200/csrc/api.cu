@@ -805,7 +805,12 @@ rt_status rt_simulate(rt_ctx* c, const int64_t* d_arr, const uint16_t* d_len, co
       if (e != cudaSuccess) return cuda_fail(c, e, "long-trace rank sort");
     }
   }
-  e = rtlm::launch_replay(a, s);
+  uint32_t max_window = 1;
+  for (uint32_t k = 0; k < np; ++k) {
+    const uint32_t C = (uint32_t)h_profiles[k].C, m = (uint32_t)h_profiles[k].b10 * C / 10u;
+    max_window = std::max(max_window, h_profiles[k].consolidate ? std::max(m, C) : C);
+  }
+  e = rtlm::launch_replay(a, max_window, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_replay");
   return RT_OK;
 }

@@ -149,7 +149,7 @@ struct ReplayLaunch {
   const uint32_t* long_perm;  // traces > kMaxTrace: rank -> global index at [lo, lo + n) (NULL: none)
   uint32_t* long_rank;        //                      arrival index -> rank (workspace)
 };
-cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s);
+cudaError_t launch_replay(const ReplayLaunch& a, uint32_t max_window, cudaStream_t s);  // max_window: max(m, C) over the profiles
 cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,
                               const uint32_t* d_trace_off, uint32_t nt, const rt_profile* d_prof,
                               const uint16_t* d_trace_prof, rt_trace_util* out, cudaStream_t s);

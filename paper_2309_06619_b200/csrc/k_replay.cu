@@ -91,6 +91,10 @@ __global__ void __launch_bounds__(kRankThr) k_trace_rank(const uint64_t* __restr
   if (p < n) sidx_out[(size_t)t * kMaxTrace + p] = (uint16_t)i0;
 }
 
+// KCH = 32-element chunks of the largest window of the launch's profiles
+// (ceil(max(b10 * C / 10, C) / 32)): the window's per-lane arrays and loops
+// are sized for it at compile time
+template <uint32_t KCH>
 __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   ReplaySmem& sm = *reinterpret_cast<ReplaySmem*>(smem_raw);
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           // slot e / 32): rank, arrival index, u, length, deadline and arrival,
           // all loads issued together; each element learns its position in the
           // (u, rank) order, and the batch is the positions below cnt
-          constexpr uint32_t kCh = kMaxWindow / 32;
+          constexpr uint32_t kCh = KCH;
           const uint32_t nch = (take + 31u) >> 5;
           uint32_t re[kCh], pos[kCh], len_e[kCh], D_e[kCh];
           float ue[kCh];
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
             // position in the (u asc, rank asc) order, by shuffles over all elements
 #pragma unroll
             for (uint32_t k = 0; k < kCh; ++k) pos[k] = 0u;
-            if (nch == 1) {  // windows of <= 32 (m = 19 at C = 11)
+            if (kCh == 1 || nch == 1) {  // windows of <= 32 (m = 19 at C = 11)
               const uint32_t r0 = re[0] & 0xFFFFu;
               for (uint32_t x = 0; x < take; ++x) {
                 const float ux = __shfl_sync(0xFFFFFFFFu, ue[0], x);
@@ -799,14 +803,16 @@ cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_replay(const ReplayLaunch& a, cudaStream_t s) {
+cudaError_t launch_replay(const ReplayLaunch& a, uint32_t max_window, cudaStream_t s) {
   if (!a.nt) return cudaSuccess;
   const size_t smem = sizeof(ReplaySmem);
-  cudaError_t e = cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const uint32_t kch = (max_window + 31u) / 32u;
+  void (*kern)(ReplayLaunch) = kch <= 1 ? k_replay<1> : (kch <= 2 ? k_replay<2> : k_replay<4>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_trace_rank<<<a.nt, kRankThr, 0, s>>>(a.key, a.trace_off, a.sidx);
   note_launch();
-  k_replay<<<a.nt, 32, smem, s>>>(a);
+  kern<<<a.nt, 32, smem, s>>>(a);
   note_launch();
   if (a.long_perm) {  // some trace is longer than kMaxTrace (its rank order is already in long_perm)
     e = cudaFuncSetAttribute(k_replay_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LongSmem));
