@@ -23,6 +23,7 @@ of the same workload, same metric/unit (the task's reference arm).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -503,7 +504,9 @@ def native(args):
                                    + ("; each slot's step replayed from one CUDA graph" if args.graphs else ""),
                        "l2": f"pipelined: {depth} distinct inputs of ~100 MB each (> 126 MB L2) in turn; "
                              "latency leg: 256 MB buffer written between steps",
-                       "parallelism": f"replicas{world}"},
+                       "parallelism": f"replicas{world}",
+                       "lexicon_sha256": hashlib.sha256(d2["lexicon"]).hexdigest(),
+                       "seed": "rtgen ROOT_SEED + 2 (counter-based; gid range rank * n ..)"},
             "latency": {"ms_per_step": round(sum_ms / args.steps, 4), "score_key_ms": round(score_ms, 4),
                         "schedule_ms": round(sum(t_step) / len(t_step) - score_ms, 4),
                         "note": "one batch at a time, L2 flushed between steps"},

@@ -282,8 +282,8 @@ rt_status rt_simulate(rt_ctx* ctx, const int64_t* d_arrival_us, const uint16_t* 
 
 /* Richer replay statistics (NEXT-4; tables; SPEC
  * S:523-546) from per-task end times (rt_simulate's d_end_us): per trace t in
- * [0, nt) (tasks h_trace_off[t] .. h_trace_off[t+1], HOST offsets, <= 1024 per
- * trace), d_report[t] = {max response, nearest-rank p95 response, makespan,
+ * [0, nt) (tasks h_trace_off[t] .. h_trace_off[t+1], HOST offsets, <= 65536 per
+ * trace; traces over 1024 tasks are sorted by a radix sort each), d_report[t] = {max response, nearest-rank p95 response, makespan,
  * n} (rt_trace_summary).  Throughput = n / makespan (completions per unit time). */
 rt_status rt_trace_report(rt_ctx* ctx, const int64_t* d_arrival_us, const int64_t* d_end_us,
                           const uint32_t* h_trace_off, uint32_t nt, rt_trace_summary* d_report, rt_stream stream);

@@ -733,12 +733,15 @@ static rt_status upload_profiles(rt_ctx* c, const rt_profile* h_profiles, uint32
   return stage_copy(c, c->st_prof, c->d_prof, h_profiles, np * sizeof(rt_profile), s);
 }
 
-static rt_status check_trace_off(rt_ctx* c, const uint32_t* h_trace_off, uint32_t nt) {
+static rt_status check_trace_off(rt_ctx* c, const uint32_t* h_trace_off, uint32_t nt, uint32_t* longest) {
   if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
+  uint32_t lg = 0;
   for (uint32_t t = 0; t < nt; ++t) {
     if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
-    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
+    lg = std::max(lg, h_trace_off[t + 1] - h_trace_off[t]);
   }
+  if (lg > rtlm::kMaxLongTrace) return fail(c, RT_EINVAL, "trace longer than 65536");
+  *longest = lg;
   return RT_OK;
 }
 
@@ -911,18 +914,27 @@ rt_status rt_trace_report(rt_ctx* c, const int64_t* d_arrival_us, const int64_t*
   if (!c) return RT_EINVAL;
   if (!nt) return RT_OK;
   if (!d_arrival_us || !d_end_us || !h_trace_off || !d_report) return fail(c, RT_EINVAL, "null argument");
-  if (h_trace_off[0] != 0) return fail(c, RT_EINVAL, "h_trace_off[0] must be 0");
-  for (uint32_t t = 0; t < nt; ++t) {
-    if (h_trace_off[t + 1] < h_trace_off[t]) return fail(c, RT_EINVAL, "h_trace_off must be non-decreasing");
-    if (h_trace_off[t + 1] - h_trace_off[t] > rtlm::kMaxTrace) return fail(c, RT_EINVAL, "trace longer than 1024");
-  }
+  uint32_t longest = 0;
+  rt_status st = check_trace_off(c, h_trace_off, nt, &longest);
+  if (st != RT_OK) return st;
   DeviceGuard g(c->device);
   if (capturing(cs(stream))) c->captured = true;  // see retire()
   cudaStream_t s = cs(stream);
-  rt_status st = upload_offsets(c, h_trace_off, nt + 1, s);
+  st = upload_offsets(c, h_trace_off, nt + 1, s);
   if (st != RT_OK) return st;
   cudaError_t e = rtlm::launch_trace_report(d_arrival_us, d_end_us, c->d_off, nt, d_report, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_trace_report");
+  if (longest > rtlm::kMaxTrace) {  // long traces: key sort + one-CTA pick each
+    st = ensure_ws(c, rtlm::trace_long_workspace(longest), s);
+    if (st != RT_OK) return st;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t lo = h_trace_off[t], m = h_trace_off[t + 1] - lo;
+      if (m <= rtlm::kMaxTrace) continue;
+      e = rtlm::launch_trace_long(d_arrival_us, d_end_us, nullptr, nullptr, lo, m, nullptr, nullptr, t,
+                                  d_report + t, nullptr, c->ws, s);
+      if (e != cudaSuccess) return cuda_fail(c, e, "long-trace report");
+    }
+  }
   return RT_OK;
 }
 
@@ -936,7 +948,8 @@ rt_status rt_trace_utilization(rt_ctx* c, const uint16_t* d_len, const uint64_t*
     rt_status st = check_profile(c, &h_profiles[k], true);
     if (st != RT_OK) return st;
   }
-  rt_status st = check_trace_off(c, h_trace_off, nt);
+  uint32_t longest = 0;
+  rt_status st = check_trace_off(c, h_trace_off, nt, &longest);
   if (st != RT_OK) return st;
   if (h_trace_off[nt] && (!d_len || !d_key || !d_end_us)) return fail(c, RT_EINVAL, "null task array");
   DeviceGuard g(c->device);
@@ -948,6 +961,18 @@ rt_status rt_trace_utilization(rt_ctx* c, const uint16_t* d_len, const uint64_t*
   if (st != RT_OK) return st;
   cudaError_t e = rtlm::launch_trace_util(d_len, d_key, d_end_us, c->d_off, nt, c->d_prof, d_trace_prof, d_util, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "k_trace_util");
+  if (longest > rtlm::kMaxTrace) {
+    st = ensure_ws(c, rtlm::trace_long_workspace(longest), s);
+    if (st != RT_OK) return st;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t lo = h_trace_off[t], m = h_trace_off[t + 1] - lo;
+      if (m <= rtlm::kMaxTrace) continue;
+      // arrival is not needed for the utilization keys: pass end_us in its place
+      e = rtlm::launch_trace_long(d_end_us, d_end_us, d_len, d_key, lo, m, c->d_prof, d_trace_prof, t, nullptr,
+                                  d_util + t, c->ws, s);
+      if (e != cudaSuccess) return cuda_fail(c, e, "long-trace utilization");
+    }
+  }
   return RT_OK;
 }
 

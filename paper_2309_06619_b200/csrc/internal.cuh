@@ -153,6 +153,13 @@ cudaError_t launch_replay(const ReplayLaunch& a, uint32_t max_window, cudaStream
 cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,
                               const uint32_t* d_trace_off, uint32_t nt, const rt_profile* d_prof,
                               const uint16_t* d_trace_prof, rt_trace_util* out, cudaStream_t s);
+// traces longer than kMaxTrace (one call per trace, after the short-trace launch):
+// exactly one of rep / util non-null
+size_t trace_long_workspace(uint32_t n);
+cudaError_t launch_trace_long(const int64_t* arrival, const int64_t* end_us, const uint16_t* len,
+                              const uint64_t* key, uint32_t lo, uint32_t n, const rt_profile* d_prof,
+                              const uint16_t* d_trace_prof, uint32_t t, rt_trace_summary* rep, rt_trace_util* util,
+                              void* ws, cudaStream_t s);
 cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, const uint32_t* d_trace_off,
                                 uint32_t nt, rt_trace_summary* out, cudaStream_t s);
 // K8 (NEXT-2): offline profiling (k_offline.cu)

@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(32) k_trace_report(const int64_t* __restrict__
   __shared__ int64_t resp[kMaxTrace];
   const uint32_t t = blockIdx.x, lane = threadIdx.x;
   const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
+  if (n > kMaxTrace) return;  // long traces: launch_trace_report_long
   if (n == 0) {
     if (lane == 0) out[t] = rt_trace_summary{0, 0, 0, 0u, 0u};
     return;
@@ -728,6 +729,7 @@ __global__ void __launch_bounds__(32) k_trace_util(const uint16_t* __restrict__ 
   __shared__ uint16_t sl[kMaxTrace];
   const uint32_t t = blockIdx.x, lane = threadIdx.x;
   const uint32_t lo = trace_off[t], n = trace_off[t + 1] - lo;
+  if (n > kMaxTrace) return;  // long traces: launch_trace_util_long
   const rt_profile& p = profiles[trace_prof ? trace_prof[t] : 0];
   uint32_t npow = 32;
   while (npow < n) npow <<= 1;
@@ -784,6 +786,88 @@ __global__ void __launch_bounds__(32) k_trace_util(const uint16_t* __restrict__ 
   if (lane == 0) out[t] = rt_trace_util{gbusy, cbusy, gcnt, ccnt};
 }
 
+
+// ---- NEXT-4 for long traces (> kMaxTrace tasks): sort keys built per trace,
+// ordered by one radix sort (K3, descending), then a one-CTA pass.
+// report: key = response end - r (>= 0); util: GPU-class key = end << 16 | len
+// (the first element of each equal-end group in descending order carries the
+// batch's max len), CPU-class tasks key 0 (sort last).
+__global__ void k_long_keys(const int64_t* __restrict__ arrival, const int64_t* __restrict__ end_us,
+                            const uint16_t* __restrict__ len, const uint64_t* __restrict__ key, uint32_t n,
+                            int util, uint64_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (!util) out[i] = (uint64_t)(end_us[i] - arrival[i]);
+    else out[i] = (key[i] >> 63) ? 0ull : (((uint64_t)end_us[i] << 16) | len[i]);
+  }
+}
+
+__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((threadIdx.x & 31u) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int64_t t = 0;
+  for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// one CTA (1024 threads): max / p95 response from the sorted order, makespan
+__global__ void __launch_bounds__(1024) k_long_report(const int64_t* __restrict__ arrival,
+                                                      const int64_t* __restrict__ end_us, uint32_t lo, uint32_t n,
+                                                      const uint32_t* __restrict__ perm, const uint64_t* __restrict__ k,
+                                                      rt_trace_summary* __restrict__ out) {
+  __shared__ int64_t sh[32];
+  int64_t mx_end = INT64_MIN, mn_r = INT64_MAX;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    mx_end = max(mx_end, end_us[lo + i]);
+    mn_r = min(mn_r, arrival[lo + i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx_end = max(mx_end, __shfl_xor_sync(0xFFFFFFFFu, mx_end, o));
+    mn_r = min(mn_r, __shfl_xor_sync(0xFFFFFFFFu, mn_r, o));
+  }
+  __shared__ int64_t smx[32], smn[32];
+  if ((threadIdx.x & 31u) == 0) { smx[threadIdx.x >> 5] = mx_end; smn[threadIdx.x >> 5] = mn_r; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) { mx_end = max(mx_end, smx[w]); mn_r = min(mn_r, smn[w]); }
+    const uint32_t p = (95u * n + 99u) / 100u;  // ceil(0.95 n), nearest rank (ascending)
+    const int64_t rmax = (int64_t)k[perm[0] - lo], rp95 = (int64_t)k[perm[n - p] - lo];
+    *out = rt_trace_summary{rmax, rp95, mx_end - mn_r, n, 0u};
+  }
+  (void)sh;
+}
+
+// one CTA: GPU busy = sum over equal-end groups (batches) of setup + base + eta * max len;
+// CPU busy = sum over CPU-class tasks of gamma * (base + eta * len)
+__global__ void __launch_bounds__(1024) k_long_util(const uint16_t* __restrict__ len, const uint64_t* __restrict__ key,
+                                                    uint32_t lo, uint32_t n, const rt_profile* __restrict__ profiles,
+                                                    const uint16_t* __restrict__ trace_prof, uint32_t t,
+                                                    const uint32_t* __restrict__ perm,
+                                                    const uint64_t* __restrict__ k, rt_trace_util* __restrict__ out) {
+  __shared__ int64_t sh[32];
+  const rt_profile& p = profiles[trace_prof ? trace_prof[t] : 0];
+  int64_t cb = 0, gb = 0, cc = 0, gc = 0;
+  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint32_t i = perm[j] - lo;  // j-th in descending (end, len); CPU-class keys 0 at the end
+    const uint64_t kj = k[i];
+    if (key[lo + i] >> 63) {
+      cb += (int64_t)p.gamma * (p.base_us + p.eta_us * (int64_t)len[lo + i]);
+      ++cc;
+    } else if (j == 0 || (k[perm[j - 1] - lo] >> 16) != (kj >> 16)) {  // first (max len) of its end group
+      gb += p.setup_us + p.base_us + p.eta_us * (int64_t)(kj & 0xFFFFu);
+      ++gc;
+    }
+  }
+  cb = block_sum64(cb, sh);
+  gb = block_sum64(gb, sh);
+  cc = block_sum64(cc, sh);
+  gc = block_sum64(gc, sh);
+  if (threadIdx.x == 0) *out = rt_trace_util{gb, cb, (uint32_t)gc, (uint32_t)cc};
+}
+
 }  // namespace
 
 cudaError_t launch_trace_util(const uint16_t* len, const uint64_t* key, const int64_t* end_us,
@@ -801,6 +885,29 @@ cudaError_t launch_trace_report(const int64_t* arrival, const int64_t* end_us, c
   k_trace_report<<<nt, 32, 0, s>>>(arrival, end_us, d_trace_off, out);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_trace_long(const int64_t* arrival, const int64_t* end_us, const uint16_t* len,
+                              const uint64_t* key, uint32_t lo, uint32_t n, const rt_profile* d_prof,
+                              const uint16_t* d_trace_prof, uint32_t t, rt_trace_summary* rep, rt_trace_util* util,
+                              void* ws, cudaStream_t s) {
+  char* p = static_cast<char*>(ws);
+  uint64_t* k = reinterpret_cast<uint64_t*>(p);
+  uint32_t* perm = reinterpret_cast<uint32_t*>(p + (((size_t)n * 8 + 255) & ~size_t(255)));
+  void* rws = p + (((size_t)n * 8 + 255) & ~size_t(255)) + (((size_t)n * 4 + 255) & ~size_t(255));
+  k_long_keys<<<(n + 255) / 256, 256, 0, s>>>(arrival + lo, end_us + lo, len ? len + lo : nullptr,
+                                               key ? key + lo : nullptr, n, util ? 1 : 0, k);
+  note_launch();
+  cudaError_t e = radix_sort_desc(k, lo, n, perm, 1, rws, s);
+  if (e != cudaSuccess) return e;
+  if (util) k_long_util<<<1, 1024, 0, s>>>(len, key, lo, n, d_prof, d_trace_prof, t, perm, k, util);
+  else k_long_report<<<1, 1024, 0, s>>>(arrival, end_us, lo, n, perm, k, rep);
+  note_launch();
+  return cudaGetLastError();
+}
+
+size_t trace_long_workspace(uint32_t n) {
+  return (((size_t)n * 8 + 255) & ~size_t(255)) + (((size_t)n * 4 + 255) & ~size_t(255)) + radix_sort_workspace(n);
 }
 
 cudaError_t launch_replay(const ReplayLaunch& a, uint32_t max_window, cudaStream_t s) {

@@ -150,3 +150,48 @@ def test_trace_utilization_parity(ctx):
     assert (out.cpu().numpy() == 0).all()
     with pytest.raises(rt.RtlmError):
         ctx.trace_utilization(None, z, z, np.array([0, 1]), d["profiles"][0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("offload", [1, 0])
+def test_trace_report_and_utilization_long_traces(ctx, offload):
+    """NEXT-4 on traces beyond the 1024-task short path: two full paper ramps
+    (11 280 tasks) beside 1000-task traces; report and utilization
+    exact against the oracle (sorted responses / the event loop's accumulators)."""
+    from oracle.offline import trace_report
+    lex = oracle.Lexicon(configs.read_lexicon())
+    dl = configs.traces(3, range(700, 702), 11280, lambda t: t % 4)
+    ds = configs.traces(3, range(710, 713), 1000, lambda t: (t + 2) % 4)
+    for dd in (dl, ds):
+        for p in dd["profiles"]:
+            p["offload"] = offload
+    cat = {kk: np.concatenate([dl[kk], ds[kk]]) for kk in ("arrival_us", "true_len", "trace_prof")}
+    toff = np.concatenate([dl["trace_off"], dl["trace_off"][-1] + ds["trace_off"][1:]]).astype(np.uint32)
+    profs = dl["profiles"]
+    u, k, D = [], [], []
+    for dd in (dl, ds):
+        f = oracle.rule_gen(lex, dd["data"], dd["offsets"])
+        for t in range(len(dd["trace_off"]) - 1):
+            lo, hi = int(dd["trace_off"][t]), int(dd["trace_off"][t + 1])
+            lm = int(dd["trace_prof"][t])
+            ut = oracle.predict(f[lo:hi], dd["regressors"][lm])
+            kt, Dt = oracle.key(ut, f[lo:hi], profs[lm], r_us=dd["arrival_us"][lo:hi])
+            u.append(ut), k.append(kt), D.append(Dt)
+    u, k, D = np.concatenate(u), np.concatenate(k), np.concatenate(D)
+    _, end, ut = oracle.simulate(cat["arrival_us"], cat["true_len"], u, k, D, toff, profs, cat["trace_prof"],
+                                 want_end=True, want_util=True)
+    rep = ctx.trace_report(torch.from_numpy(cat["arrival_us"]).to(DEV), torch.from_numpy(end).to(DEV), toff)
+    rep = rep.cpu().numpy()
+    want = trace_report(cat["arrival_us"], end, toff)
+    assert (rep[:, 0] == want["max_resp_us"]).all()
+    assert (rep[:, 1] == want["p95_resp_us"]).all()
+    assert (rep[:, 2] == want["makespan_us"]).all()
+    assert ((rep[:, 3] & 0xFFFFFFFF) == want["n"]).all() and want["n"][0] == 11280
+    got = ctx.trace_utilization(torch.from_numpy(cat["true_len"].view(np.int16)).to(DEV),
+                                torch.from_numpy(k.view(np.int64)).to(DEV), torch.from_numpy(end).to(DEV),
+                                toff, profs, torch.from_numpy(cat["trace_prof"].astype(np.uint16).view(np.int16)).to(DEV))
+    got = got.cpu().numpy()
+    assert (got[:, 0] == ut["gpu_busy_us"]).all()
+    assert (got[:, 1] == ut["cpu_busy_us"]).all()
+    assert ((got[:, 2] & 0xFFFFFFFF) == ut["gpu_batches"]).all()
+    assert ((got[:, 2] >> 32) == ut["cpu_tasks"]).all()
