@@ -132,7 +132,9 @@ typedef struct {
  * *out is still created so the message can be read; destroy it). */
 rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** out);
 rt_status rt_destroy(rt_ctx* ctx);
-/* Message of the last non-OK status on this context (never NULL). */
+/* Message of the last non-OK status on this context, or, with ctx == NULL,
+ * of the calling thread's last non-OK status on any context (thread-local;
+ * e.g. after rt_create failed before a context existed).  Never NULL. */
 const char* rt_last_error(const rt_ctx* ctx);
 /* Reads and clears the sticky flags (synchronises the device). */
 rt_status rt_get_flags(rt_ctx* ctx, uint32_t* flags);

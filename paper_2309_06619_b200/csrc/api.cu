@@ -60,7 +60,10 @@ namespace {
 
 using rtlm::LexEntry;
 
+thread_local std::string t_err;  // the calling thread's last error (rt_last_error(NULL))
+
 rt_status fail(rt_ctx* c, rt_status st, const std::string& msg) {
+  t_err = msg;
   if (c) c->err = msg;
   return st;
 }
@@ -468,7 +471,7 @@ rt_status rt_destroy(rt_ctx* c) {
   return RT_OK;
 }
 
-const char* rt_last_error(const rt_ctx* c) { return c ? c->err.c_str() : "null context"; }
+const char* rt_last_error(const rt_ctx* c) { return c ? c->err.c_str() : t_err.c_str(); }
 
 uint32_t rt_lexicon_size(const rt_ctx* c) { return c ? c->n_entries : 0; }
 
