@@ -374,6 +374,7 @@ struct __align__(16) WarpBuf {
 
 struct Smem4 {
   uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000; punct kind << 24
+  uint32_t clit[8];                    // token codes of the 7 clitics (R-CLITIC), see clitic_kind
   uint32_t fa[kPunct + 8];             // token code -> machine attributes (fsm_attr)
   uint8_t tO[16 * 32], tP[128 * 4];    // O-part and P-part transition tables
   WarpBuf w[kW4];
@@ -388,12 +389,27 @@ __device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uin
   return lo;
 }
 
+// The seven clitics of R-CLITIC in a fixed order: n't 're 've 'll 's 'm 'd.
+// A clitic token's lemma (R-LEMMA: n't -> not; the others are too short or
+// end in no suffix) and so its lexicon code depend only on which clitic it is:
+// the codes are looked up once per CTA (Smem4::clit).
+__host__ __device__ __forceinline__ uint32_t clitic_bytes(uint32_t kind) {
+  switch (kind) {
+    case 0: return 'n' | ('\'' << 8) | ('t' << 16);
+    case 1: return '\'' | ('r' << 8) | ('e' << 16);
+    case 2: return '\'' | ('v' << 8) | ('e' << 16);
+    case 3: return '\'' | ('l' << 8) | ('l' << 16);
+    case 4: return '\'' | ('s' << 8);
+    case 5: return '\'' | ('m' << 8);
+    default: return '\'' | ('d' << 8);
+  }
+}
+
 // Word token(s) of the run of n bytes at stage byte x: one clitic split
-// (R-CLITIC), then the lemma (R-LEMMA) and code of the stem and of the
-// clitic; returns the token count.  The stem lookup runs on every lane, the
-// clitic lookup only if some lane of the warp has one.
-__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L, uint32_t& c0,
-                                              uint32_t& c1) {
+// (R-CLITIC), then the lemma (R-LEMMA) and code of the stem; the clitic's code
+// comes from the per-CTA table; returns the token count.
+__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L,
+                                              const uint32_t* clit, uint32_t& c0, uint32_t& c1) {
   const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
   const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
                  w4 = B.stage[a0 + 4];
@@ -409,17 +425,14 @@ __device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint
   const uint32_t t3 = R & 0xFFFFFFu;
   const uint32_t l1 = t3 & 0xFFu, l2 = (t3 >> 8) & 0xFFu, l3 = t3 >> 16, lo16 = t3 & 0xFFFFu;
   const bool c2 = n > 2u && l2 == '\'' && (l1 == 's' || l1 == 'm' || l1 == 'd');
-  const bool c3 = n > 3u && ((l3 == 'n' && l2 == '\'' && l1 == 't') ||
-                             (l3 == '\'' && (lo16 == (('r' << 8) | 'e') || lo16 == (('v' << 8) | 'e') ||
-                                             lo16 == (('l' << 8) | 'l'))));
+  const bool nt = l3 == 'n' && l2 == '\'' && l1 == 't';
+  const bool re = lo16 == (('r' << 8) | 'e'), ve = lo16 == (('v' << 8) | 'e'), ll = lo16 == (('l' << 8) | 'l');
+  const bool c3 = n > 3u && (nt || (l3 == '\'' && (re || ve || ll)));
   const uint32_t cut = c3 ? 3u : (c2 ? 2u : 0u);
   const uint32_t s3 = __funnelshift_r(R, R2, 8u * cut) & 0xFFFFFFu;  // last three stem bytes
   c0 = word_code(L, n - cut, o0, o1, o2, o3, s3);
-  if (!__any_sync(__activemask(), cut != 0u)) return 1;
-  // clitic bytes b[n-cut..n-1] -> little-endian key
-  const uint32_t ck = cut == 3u ? __byte_perm(t3, 0, 0x4012) : __byte_perm(t3, 0, 0x4401);
-  const uint32_t e1 = word_code(L, cut, ck, 0u, 0u, 0u, cut == 3u ? t3 : (t3 & 0xFFFFu));
-  c1 = e1;
+  const uint32_t kind = c3 ? (nt ? 0u : re ? 1u : ve ? 2u : 3u) : (l1 == 's' ? 4u : l1 == 'm' ? 5u : 6u);
+  c1 = clit[kind];
   return cut ? 2u : 1u;
 }
 
@@ -638,6 +651,13 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
   }
   __syncthreads();
   const Lex L{s_keys, s_slots, a.lex.entries, a.lex.bits, a.lex.seed};
+  if (tid < 7) {
+    const uint32_t cb = clitic_bytes(tid), len = tid < 4 ? 3u : 2u;
+    const uint32_t s3 = len == 3 ? (((cb & 0xFFu) << 16) | (cb & 0xFF00u) | ((cb >> 16) & 0xFFu))
+                                 : (((cb & 0xFFu) << 8) | ((cb >> 8) & 0xFFu));
+    S.clit[tid] = word_code(L, len, cb, 0u, 0u, 0u, s3);
+  }
+  __syncthreads();
   WarpBuf& B = S.w[wid];
   const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
   const uint32_t ntasks = (a.n + 31) / 32;
@@ -839,17 +859,14 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               kind = S.lut[c] >> 24;
             }
           }
-          if (isrun) ntk = stage_run(B, x, n, L, at0, at1);
+          if (isrun) ntk = stage_run(B, x, n, L, S.clit, at0, at1);
         }
-        uint32_t ti = ntk;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ti, o);
-          if (lane >= (uint32_t)o) ti += t;
-        }
-        const uint32_t nt = __shfl_sync(0xFFFFFFFFu, ti, 31);
+        // token positions: ntk is 0, 1 or 2 (a clitic split), so two ballots replace a scan
+        const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, ntk != 0u), b2 = __ballot_sync(0xFFFFFFFFu, ntk == 2u);
+        const uint32_t ltm = (1u << lane) - 1u;
+        const uint32_t nt = __popc(b1) + __popc(b2);
         if (ntk) {
-          const uint32_t t0 = (uint32_t)tokbase + ti - ntk;
+          const uint32_t t0 = (uint32_t)tokbase + __popc(b1 & ltm) + __popc(b2 & ltm);
           B.ring[t0 & (kRing - 1)] = (uint16_t)((kind == K_W ? at0 : kPunct + kind - 1u) | (rq << 11));
           if (ntk == 2) B.ring[(t0 + 1) & (kRing - 1)] = (uint16_t)(at1 | (rq << 11));
         }
