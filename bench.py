@@ -393,7 +393,7 @@ def native(args):
     # SMs at depth 6 -> 0.665 ms/batch vs 0.858 with all-SM scoring per slot stream.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     if split_streams:
-        score_ctas = max(1, (nsm * 27) // 40) if depth > 1 else nsm
+        score_ctas = max(1, (nsm * 27 + 39) // 40) if depth > 1 else nsm
     else:
         score_ctas = max(1, nsm - depth) if depth > 1 else nsm
     if os.environ.get("RTLM_SCORE_CTAS"):

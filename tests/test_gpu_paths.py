@@ -83,7 +83,7 @@ def test_bench_pipeline_launch_configuration(lex_v1, mode):
     seg = np.asarray([0, n], U32)
     ctxs = [rt.Context(d["lexicon"], 0) for d in ds]
     for c in ctxs:
-        c.set_sm_limit((nsm * 27) // 40 if mode == "split" else max(1, nsm - depth))
+        c.set_sm_limit((nsm * 27 + 39) // 40 if mode == "split" else max(1, nsm - depth))
     data = [dev(d["data"]) for d in ds]
     off = [dev(d["offsets"]) for d in ds]
     streams = [torch.cuda.Stream(DEV) for _ in range(depth)]
