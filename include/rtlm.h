@@ -174,13 +174,17 @@ rt_status rt_predict(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, const rt_r
  * layers, identity output, u = max(0, output).  Inputs are the six rule scores
  * feat[i][0..5] = {S, Y, M, V, O, P}.  Weights are HOST fp32, row-major
  * [out][in]: w[0] 100x6, w[1] 200x100, w[2] 200x200, w[3] 100x200, w[4] 1x100;
- * b[l] has `out` entries.  Two precisions (rt_set_mlp_precision):
+ * b[l] has `out` entries.  Three precisions (rt_set_mlp_precision):
  *   RT_MLP_FP32 (default): every multiply-add in binary32 on the CUDA cores,
  *     out[j] = fma chain over k in index order from b[j] (the paper's model is
  *     fp32); error vs the fp64 oracle within fp32 rounding;
  *   RT_MLP_BF16 (opt-in fast mode): layers 2-4 on the tensor cores (tcgen05,
  *     BF16 operands, FP32 accumulation), layers 1 and 5 in fp32;
- *     |u - u_fp64| <= 2^-5 x the oracle's |W|,|b|,|x| pass (DESIGN.md §7 K7). */
+ *     |u - u_fp64| <= 2^-5 x the oracle's |W|,|b|,|x| pass (DESIGN.md §7 K7);
+ *   RT_MLP_TF32X3: layers 2-4 on the tensor cores with fp32 accuracy — every
+ *     operand split x = hi + lo (two TF32 numbers, |x - hi - lo| <= 2^-22 |x|),
+ *     products hi.hi + hi.lo + lo.hi accumulated in fp32 in TMEM; same error
+ *     bound as RT_MLP_FP32 (1024 x 2^-24 x the |.| pass), not the same bits. */
 typedef struct {
   const float* w[5];
   const float* b[5];
@@ -194,8 +198,9 @@ rt_status rt_set_mlp(rt_ctx* ctx, const rt_mlp* mlp);
 rt_status rt_predict_mlp(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, float* d_u, rt_stream stream);
 #define RT_MLP_FP32 0
 #define RT_MLP_BF16 1
-/* Selects the arithmetic of rt_predict_mlp for this context (RT_MLP_FP32 or
- * RT_MLP_BF16; RT_EINVAL otherwise).  Takes effect for later calls. */
+#define RT_MLP_TF32X3 2
+/* Selects the arithmetic of rt_predict_mlp for this context (RT_MLP_FP32,
+ * RT_MLP_BF16 or RT_MLP_TF32X3; RT_EINVAL otherwise).  Takes effect for later calls. */
 rt_status rt_set_mlp_precision(rt_ctx* ctx, int precision);
 
 /* ---------------------------------------------------------------- (2c) offline profiling (NEXT-2) */

@@ -272,9 +272,9 @@ class Context:
         self._check(self._L.rt_set_mlp(self._h, ctypes.byref(m)))
 
     def set_mlp_precision(self, precision: str) -> None:
-        """rt_set_mlp_precision: "fp32" (default, CUDA-core binary32) or "bf16"
-        (tcgen05 tensor cores, opt-in fast mode)."""
-        self._check(self._L.rt_set_mlp_precision(self._h, {"fp32": 0, "bf16": 1}[precision]))
+        """rt_set_mlp_precision: "fp32" (default, CUDA-core binary32), "tf32x3"
+        (tcgen05 3xTF32, fp32-accurate) or "bf16" (tcgen05, opt-in fast mode)."""
+        self._check(self._L.rt_set_mlp_precision(self._h, {"fp32": 0, "bf16": 1, "tf32x3": 2}[precision]))
 
     def predict_mlp(self, feat, u=None):
         """rt_predict_mlp: feat uint16-as-int16 [n, 8] -> u float32 [n]."""

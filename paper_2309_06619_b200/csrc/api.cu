@@ -29,6 +29,7 @@ struct rt_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint8_t* d_mlp = nullptr;  // packed MLP weights (rt_set_mlp): bf16 tensor-core blob
   float* d_mlp32 = nullptr;  // fp32 blob (k_mlp_f32)
+  uint8_t* d_mlptf = nullptr;  // hi / lo tf32 blob (k_mlp_tf32)
   int mlp_precision = RT_MLP_FP32;
   void* io = nullptr;        // device buffers of rt_score_schedule_host
   size_t io_size = 0;
@@ -455,6 +456,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_prof);
     cudaFree(c->d_mlp);
     cudaFree(c->d_mlp32);
+    cudaFree(c->d_mlptf);
     cudaFree(c->io);
     cudaFree(c->kbuf);
     for (void* p : c->captured_stage) cudaFreeHost(p);
@@ -580,12 +582,20 @@ rt_status rt_set_mlp(rt_ctx* c, const rt_mlp* mlp) {
     if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("mlp weights: ") + cudaGetErrorString(e));
   }
   RT_CUDA(c, cudaMemcpy(c->d_mlp32, blob32.data(), rtlm::mlp_f32_blob_bytes(), cudaMemcpyHostToDevice));
+  std::vector<uint8_t> blobtf(rtlm::mlp_tf32_blob_bytes());
+  rtlm::mlp_tf32_pack(mlp->w, mlp->b, blobtf.data());
+  if (!c->d_mlptf) {
+    cudaError_t e = cudaMalloc(&c->d_mlptf, blobtf.size());
+    if (e != cudaSuccess) return fail(c, RT_ENOMEM, std::string("mlp weights: ") + cudaGetErrorString(e));
+  }
+  RT_CUDA(c, cudaMemcpy(c->d_mlptf, blobtf.data(), blobtf.size(), cudaMemcpyHostToDevice));
   return RT_OK;
 }
 
 rt_status rt_set_mlp_precision(rt_ctx* c, int precision) {
   if (!c) return RT_EINVAL;
-  if (precision != RT_MLP_FP32 && precision != RT_MLP_BF16) return fail(c, RT_EINVAL, "unknown MLP precision");
+  if (precision != RT_MLP_FP32 && precision != RT_MLP_BF16 && precision != RT_MLP_TF32X3)
+    return fail(c, RT_EINVAL, "unknown MLP precision");
   c->mlp_precision = precision;
   return RT_OK;
 }
@@ -598,10 +608,19 @@ rt_status rt_predict_mlp(rt_ctx* c, const uint16_t* d_feat, uint32_t n, float* d
   if (reinterpret_cast<uintptr_t>(d_feat) & 15u) return fail(c, RT_EINVAL, "d_feat must be 16-byte aligned");
   DeviceGuard g(c->device);
   if (capturing(cs(stream))) c->captured = true;  // see retire()
-  cudaError_t e = c->mlp_precision == RT_MLP_BF16
-                      ? rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream))
-                      : rtlm::launch_mlp_f32(d_feat, n, c->d_mlp32, d_u, persistent_ctas(c), cs(stream));
-  if (e != cudaSuccess) return cuda_fail(c, e, c->mlp_precision == RT_MLP_BF16 ? "k_mlp" : "k_mlp_f32");
+  cudaError_t e;
+  const char* what;
+  if (c->mlp_precision == RT_MLP_BF16) {
+    e = rtlm::launch_mlp(d_feat, n, c->d_mlp, d_u, persistent_ctas(c), cs(stream));
+    what = "k_mlp";
+  } else if (c->mlp_precision == RT_MLP_TF32X3) {
+    e = rtlm::launch_mlp_tf32(d_feat, n, c->d_mlptf, d_u, persistent_ctas(c), cs(stream));
+    what = "k_mlp_tf32";
+  } else {
+    e = rtlm::launch_mlp_f32(d_feat, n, c->d_mlp32, d_u, persistent_ctas(c), cs(stream));
+    what = "k_mlp_f32";
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, what);
   return RT_OK;
 }
 

@@ -176,6 +176,11 @@ size_t mlp_f32_blob_bytes();
 void mlp_f32_pack(const float* const w[5], const float* const b[5], float* blob);
 cudaError_t launch_mlp_f32(const uint16_t* feat, uint32_t n, const float* blob, float* u, int num_sms,
                            cudaStream_t s);
+// K7 3xTF32 mode (k_mlp_tf32.cu): layers 2-4 as hi.hi + hi.lo + lo.hi tcgen05 kind::tf32 products
+size_t mlp_tf32_blob_bytes();
+void mlp_tf32_pack(const float* const w[5], const float* const b[5], uint8_t* blob);
+cudaError_t launch_mlp_tf32(const uint16_t* feat, uint32_t n, const uint8_t* blob, float* u, int num_sms,
+                            cudaStream_t s);
 cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* group_of, uint32_t ngroups,
                                 int64_t* sums, cudaStream_t s);
 

@@ -32,3 +32,5 @@ for _ in range(reps):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 print("mlp ms min", f"{min(ts):.4f}", "median", f"{sorted(ts)[len(ts) // 2]:.4f}")
+if os.environ.get("KTF_TRACE"):
+    print("phase cycles", [int(x) for x in u[:16].cpu().tolist()])

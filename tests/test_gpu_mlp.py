@@ -9,6 +9,11 @@ the same sum over absolute values, so over the 606 FMAs that feed one output
 like a length model whose partial sums all add) that bound is relative, and
 north_star's "predicted lengths within 1e-5 relative" is asserted directly.
 
+tf32x3 (k_mlp_tf32): layers 2-4 on tcgen05 kind::tf32 with every operand split
+into two tf32 numbers (hi + lo, residual <= 2^-22) and three products per
+multiply; per product the error is <= 3 * 2^-22 = 12 unit roundoffs of |a||b|,
+so the same 1024 * 2^-24 bound holds with room (606 + 3 * 12 roundoffs).
+
 bf16 (opt-in, k_mlp on tcgen05): layers 2-4 round their weights and input
 activations to bf16 (unit roundoff 2^-8): six roundings perturb every partial
 sum by at most ~6 * 2^-8 of the same sum over absolute values, so
@@ -66,33 +71,39 @@ def _length_model(seed):
     return [w.astype(np.float32) for w in ws], [b.astype(np.float32) for b in bs]
 
 
-@pytest.mark.parametrize("n", [1, 63, 64, 65, 1000, 40000])
-def test_mlp_fp32_random_weights(ctx, n):
+FP32_MODES = ["fp32", "tf32x3"]
+
+
+@pytest.mark.parametrize("mode", FP32_MODES)
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 127, 128, 129, 1000, 40000])
+def test_mlp_fp32_random_weights(ctx, n, mode):
     ws, bs = mlp_weights(7)
     f = _feat(n, n)
-    g = _run(ctx, f, ws, bs)
+    g = _run(ctx, f, ws, bs, mode)
     want = mlp_predict(f, ws, bs)
     bound = TOL_FP32 * mlp_abs_pass(f, ws, bs)
     err = np.abs(g.astype(np.float64) - want)
     assert (err <= bound).all(), (np.max(err / bound), np.argmax(err / bound))
 
 
+@pytest.mark.parametrize("mode", FP32_MODES)
 @pytest.mark.parametrize("n", [129, 50000])
-def test_mlp_fp32_within_1e5_relative(ctx, n):
+def test_mlp_fp32_within_1e5_relative(ctx, n, mode):
     ws, bs = _length_model(11)
     f = _feat(n, 5 + n)
-    g = _run(ctx, f, ws, bs).astype(np.float64)
+    g = _run(ctx, f, ws, bs, mode).astype(np.float64)
     want = mlp_predict(f, ws, bs)
     assert (want > 5.0).all() and (want < 500.0).all()
     rel = np.abs(g - want) / want
     assert rel.max() <= 1e-5, rel.max()
 
 
-def test_mlp_fp32_on_rule_features(ctx):
+@pytest.mark.parametrize("mode", FP32_MODES)
+def test_mlp_fp32_on_rule_features(ctx, mode):
     d = configs.config2(n=3000, gid0=777)
     f = oracle.rule_gen(oracle.Lexicon(configs.read_lexicon()), d["data"], d["offsets"])
     for ws, bs in (mlp_weights(21), _length_model(21)):
-        g = _run(ctx, f, ws, bs)
+        g = _run(ctx, f, ws, bs, mode)
         err = np.abs(g.astype(np.float64) - mlp_predict(f, ws, bs))
         assert (err <= TOL_FP32 * mlp_abs_pass(f, ws, bs)).all()
 
@@ -124,7 +135,7 @@ def _zero():
             [np.zeros(o, np.float32) for o in DIMS[1:]])
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3", "bf16"])
 def test_mlp_exact_networks(ctx, precision):
     # zero network -> 0; a one-path network routing feature 4 with
     # gain g -> g * f4, exact when every value is a bf16 number (integers < 256: 8 bits)
