@@ -33,4 +33,4 @@ for _ in range(reps):
     ts.append(a.elapsed_time(b))
 print("mlp ms min", f"{min(ts):.4f}", "median", f"{sorted(ts)[len(ts) // 2]:.4f}")
 if os.environ.get("KTF_TRACE"):
-    print("phase cycles", [int(x) for x in u[:16].cpu().tolist()])
+    print("trace", [int(x) for x in u[:16].cpu().tolist()])
