@@ -545,12 +545,15 @@ def native(args):
 def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_ranks, flush, peaks):
     """NEXT-1: u = m_theta(feat) for the config-2 queue (features from rt_score),
     random-init weights (no trained model exists here; the cost does not depend
-    on the values), in both precisions: fp32 (default; CUDA-core binary32 FMA
-    chains, k_mlp_f32) and bf16 (opt-in; tcgen05 tensor cores, k_mlp).
-    Algorithmic 2 * 80 700 FLOP per request.  Rooflines: fp32 against the
-    CUDA-core FMA peak (148 SMs x 128 FP32 lanes x 2 FLOP x the SM clock,
-    derived: the profiling guide and MEASURED_PEAKS.json give no fp32 number);
-    bf16 against MEASURED_PEAKS.json bf16_tflops."""
+    on the values), in three precisions: fp32 (default; CUDA-core binary32 FMA
+    chains, k_mlp_f32), tf32x3 (fp32-accurate on tcgen05: three TF32 products
+    per multiply, k_mlp_tf32) and bf16 (opt-in; tcgen05, k_mlp).  Algorithmic
+    2 * 80 700 FLOP per request.  Rooflines: fp32 against the CUDA-core FMA
+    peak (148 SMs x 128 FP32 lanes x 2 FLOP x the SM clock, derived: the
+    profiling guide and MEASURED_PEAKS.json give no fp32 number); tf32x3
+    against the emulated-fp32 peak = the tf32 peak / 3, the tf32 peak being
+    MEASURED_PEAKS.json bf16_tflops x 1.1 / 2.25 (the guide's nominal tf32 :
+    bf16 ratio); bf16 against MEASURED_PEAKS.json bf16_tflops."""
     import torch
     import rtgen
     feat = ctx.score(data, off)
@@ -562,7 +565,7 @@ def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_r
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     out = {"metric": "M requests/s (u = m_theta(feat), MLP 6-100-200-200-100-1)", "unit": "Mreq/s",
            "alg_flops_per_launch": flops}
-    for prec in ("fp32", "bf16"):
+    for prec in ("fp32", "tf32x3", "bf16"):
         ctx.set_mlp_precision(prec)
         for _ in range(args.warmup):
             ctx.predict_mlp(feat, u)
@@ -586,6 +589,14 @@ def mlp_leg(args, rt, ctx, data, off, n, dev, stream, world, barrier, max_over_r
                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                     "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FP32 FMA/clk x 2 x {mhz:.0f} MHz"}
             dtype = "fp32 CUDA cores (binary32 FMA chains in index order)"
+        elif prec == "tf32x3":
+            bf16 = float(peaks.get("bf16_tflops", 2250.0))
+            peak = bf16 * 1.1 / 2.25 / 3
+            roof = {"bound": "tensor", "kernel": "k_mlp_tf32", "achieved": round(achieved, 1), "peak": round(peak, 1),
+                    "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "peak_source": ("MEASURED_PEAKS.json bf16_tflops" if "bf16_tflops" in peaks else "nominal bf16")
+                    + " x 1.1/2.25 (tf32, guide ratio) / 3 (three tf32 products per fp32 multiply)"}
+            dtype = "fp32-accurate: 3xTF32 on tcgen05 (hi/lo split operands), fp32 accumulate in TMEM"
         else:
             peak = float(peaks.get("bf16_tflops", 2250.0))
             roof = {"bound": "tensor", "kernel": "k_mlp", "achieved": round(achieved, 1), "peak": peak,

@@ -309,13 +309,11 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_tf32(const uint16_t* __restrict
       store_hl(grp, 1, row, (float)(f.z & 0xFFFFu), (float)(f.z >> 16), 1.0f, 0.0f);
       release_group(bars, G);
     };
-    uint4 fnext = make_uint4(0, 0, 0, 0);
     if (q == 0 && my_tiles > 0) stage_feat(load_feat(blockIdx.x), 0);
     for (uint32_t i = 0; i < my_tiles; ++i) {
       const uint32_t t = blockIdx.x + i * gridDim.x;
       const uint32_t Gt = i * kGroups;
       const uint32_t ph = i & 1u;
-      if (q == 0) fnext = load_feat(t + gridDim.x);
       mbar_wait(bars + 8 * (B_DONE + 0), ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       epilogue(smem, bars, tmem_row + TM_Y, G1, 100, Gt + 1, row, q);
@@ -325,8 +323,9 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_tf32(const uint16_t* __restrict
       mbar_wait(bars + 8 * (B_DONE + 2), ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       epilogue(smem, bars, tmem_row + TM_Y, G3, 200, Gt + 1 + G1 + G2, row, q);
-      // the next tile's layer-1 input goes ahead of this tile's layer 5
-      if (q == 0 && i + 1 < my_tiles) stage_feat(fnext, Gt + kGroups);
+      // the next tile's layer-1 input goes ahead of this tile's layer 5 (loaded here: an outstanding global load
+      // would hold up every release_group fence before it)
+      if (q == 0 && i + 1 < my_tiles) stage_feat(load_feat(t + gridDim.x), Gt + kGroups);
       mbar_wait(bars + 8 * (B_DONE + 3), ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // ---- layer 5 (100 -> 1): w5 . relu(D4) + b5, fp32 FMA chains over columns 25q .. 25q + 24
