@@ -859,7 +859,11 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
               kind = S.lut[c] >> 24;
             }
           }
+#ifdef KS_NOPROBE
+          if (isrun) { ntk = 1; at0 = x; }
+#else
           if (isrun) ntk = stage_run(B, x, n, L, S.clit, at0, at1);
+#endif
         }
         // token positions: ntk is 0, 1 or 2 (a clitic split), so two ballots replace a scan
         const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, ntk != 0u), b2 = __ballot_sync(0xFFFFFFFFu, ntk == 2u);
@@ -874,7 +878,9 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
         tokbase += (int32_t)nt;
         // a rule round every kRound tokens, and after the last event of the task
         if ((last_chunk && e0 + 32 >= nev) || tokbase - tokdone >= kRound) {
+#ifndef KS_NORULES  // KS_NORULES / KS_NOPROBE: ablation builds for profiling only (wrong results)
           rules_round(B, S.fa, S.tO, S.tP, tokdone, tokbase, lane);
+#endif
           tokdone = tokbase;
         }
       }
