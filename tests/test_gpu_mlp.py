@@ -162,3 +162,27 @@ def test_mlp_api_errors(ctx):
         c.set_mlp_precision("fp16")
     with pytest.raises(rt.RtlmError, match="precision"):
         c._check(c._L.rt_set_mlp_precision(c._h, 7))
+
+
+@pytest.mark.parametrize("mode", ["fp32", "tf32x3", "bf16"])
+def test_mlp_full_config2_sampled(ctx, mode):
+    # BASELINE's full size (config 2: 2^20 requests) in the bench's launch configuration (one
+    # rt_predict_mlp over the whole queue, all SMs): the features come from the GPU scorer (bit-exact
+    # against the oracle in test_gpu_parity), the oracle recomputes 2048 sampled rows one by one
+    d = configs.config2()
+    data = torch.from_numpy(d["data"]).to(DEV)
+    off = torch.from_numpy(d["offsets"].view(np.int32)).to(DEV)
+    feat = ctx.score(data, off)
+    ws, bs = mlp_weights(12345)
+    ctx.set_mlp(ws, bs)
+    ctx.set_mlp_precision(mode)
+    u = ctx.predict_mlp(feat).cpu().numpy().astype(np.float64)
+    ctx.set_mlp_precision("fp32")
+    n = feat.shape[0]
+    assert u.shape == (n,) and n == 1 << 20
+    rng = np.random.default_rng(99)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 2040), [0, 1, 127, 128, n - 129, n - 128, n - 2, n - 1]]))
+    f = feat.cpu().numpy().view(np.uint16)[idx]
+    want, absp = mlp_predict(f, ws, bs), mlp_abs_pass(f, ws, bs)
+    tol = TOL_BF16 if mode == "bf16" else TOL_FP32
+    assert (np.abs(u[idx] - want) <= tol * absp).all()
