@@ -135,7 +135,11 @@ __device__ __forceinline__ uint32_t word_code(const Lex& L, uint32_t len, uint32
   o1 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 32, 0));
   o2 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 64, 0));
   o3 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 96, 0));
+#ifdef KS_NOLOOKUP
+  return (o0 ^ o1 ^ o2 ^ o3) & 0x3FFu;
+#else
   return lookup(L, o0, o1, o2, o3);
+#endif
 }
 
 // ------------------------------------------------------------ rule FSM
