@@ -19,6 +19,7 @@ struct rt_ctx {
   uint16_t* d_slots = nullptr;
   uint32_t n_entries = 0, bits = 0, seed = 0;
   uint32_t* d_flags = nullptr;
+  uint16_t* d_tok = nullptr;  // scoring token buffers (one per persistent warp)
   void* ws = nullptr;
   size_t ws_size = 0;
   uint32_t* d_off = nullptr;  // device copy of segment / trace offsets
@@ -436,6 +437,7 @@ rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** o
   RT_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   RT_CUDA(c, cudaMalloc(&c->d_flags, 4 * sizeof(uint32_t)));  // [0] flags, [2] scoring work counter
   RT_CUDA(c, cudaMemset(c->d_flags, 0, 4 * sizeof(uint32_t)));
+  RT_CUDA(c, cudaMalloc(&c->d_tok, rtlm::score_scratch_bytes(c->num_sms)));
   RT_CUDA(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RT_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -451,6 +453,7 @@ rt_status rt_destroy(rt_ctx* c) {
     cudaFree(c->d_keys);
     cudaFree(c->d_slots);
     cudaFree(c->d_flags);
+    cudaFree(c->d_tok);
     cudaFree(c->ws);
     cudaFree(c->d_off);
     cudaFree(c->d_prof);
@@ -531,6 +534,7 @@ static rt_status score_common(rt_ctx* c, const uint8_t* d_bytes, const uint32_t*
   a.D_out = d_D_out;
   a.flags = c->d_flags;
   a.work = c->d_flags + 2;
+  a.tokbuf = c->d_tok;
   a.num_sms = persistent_ctas(c);
   cudaError_t e = rtlm::launch_score(a, cs(stream));
   if (e != cudaSuccess) return cuda_fail(c, e, "k_score");

@@ -84,8 +84,10 @@ struct ScoreLaunch {
   uint32_t* D_out;
   uint32_t* flags;
   uint32_t* work;  // device counter (scoring work queue), zeroed by the launcher
+  uint16_t* tokbuf;  // per-warp token buffers (score_scratch_bytes(num_sms))
   int num_sms;
 };
+size_t score_scratch_bytes(int ctas);
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s);
 cudaError_t launch_predict(const uint16_t* feat, uint32_t n, const rt_regressor& reg, float* u, cudaStream_t s);
 cudaError_t launch_key(const float* u, const uint16_t* feat, const int64_t* arrival, const uint32_t* D_in,

@@ -13,6 +13,8 @@
 // that decides an integer is binary32 with explicit round-to-nearest
 // intrinsics (R-FP).  Warps whose offsets decrease use the per-lane byte FSM
 // (Rules::byte), which implements the same rules sequentially.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace rtlm {
@@ -412,16 +414,16 @@ __host__ __device__ __forceinline__ uint32_t clitic_bytes(uint32_t kind) {
 // Word token(s) of the run of n bytes at stage byte x: one clitic split
 // (R-CLITIC), then the lemma (R-LEMMA) and code of the stem; the clitic's code
 // comes from the per-CTA table; returns the token count.
-__device__ __forceinline__ uint32_t stage_run(const WarpBuf& B, uint32_t x, uint32_t n, const Lex& L,
+__device__ __forceinline__ uint32_t stage_run(const uint32_t* stage, uint32_t x, uint32_t n, const Lex& L,
                                               const uint32_t* clit, uint32_t& c0, uint32_t& c1) {
   const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
-  const uint32_t w0 = B.stage[a0], w1 = B.stage[a0 + 1], w2 = B.stage[a0 + 2], w3 = B.stage[a0 + 3],
-                 w4 = B.stage[a0 + 4];
+  const uint32_t w0 = stage[a0], w1 = stage[a0 + 1], w2 = stage[a0 + 2], w3 = stage[a0 + 3],
+                 w4 = stage[a0 + 4];
   const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
   const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
   const uint32_t tb8 = x + n - 8;  // >= 8
   const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
-  const uint32_t v0 = B.stage[ta], v1 = B.stage[ta + 1], v2 = B.stage[ta + 2];
+  const uint32_t v0 = stage[ta], v1 = stage[ta + 1], v2 = stage[ta + 2];
   // last 8 bytes, newest first: R = b[n-1] b[n-2] b[n-3] b[n-4] (low to high), R2 = b[n-5] .. b[n-8]
   // (bytes before the run are garbage; every test below is guarded by the length)
   const uint32_t R = __byte_perm(__funnelshift_r(v1, v2, tsh), 0, 0x0123) | 0x20202020u;
@@ -866,7 +868,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
 #ifdef KS_NOPROBE
           if (isrun) { ntk = 1; at0 = x; }
 #else
-          if (isrun) ntk = stage_run(B, x, n, L, S.clit, at0, at1);
+          if (isrun) ntk = stage_run(B.stage, x, n, L, S.clit, at0, at1);
 #endif
         }
         // token positions: ntk is 0, 1 or 2 (a clitic split), so two ballots replace a scan
@@ -921,6 +923,511 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
   }
 }
 
+// ============================================================ K1 v6 (round 2): pools of tasks
+// Two phases per warp, both with (almost) every lane busy:
+//  (A) tokenize: up to kPoolTasks warp tasks (32 requests each) are streamed
+//      exactly as in k_score4 (classify, events, one lane per event), but a
+//      token's code goes to a per-warp token buffer in global memory (u16,
+//      kTokCap tokens; the pool's tokens are contiguous there) instead of a
+//      shared-memory ring, and each request's first token index is recorded.
+//      Runs without an apostrophe in their last three bytes (no clitic split
+//      possible, R-CLITIC) take a short path: the lemma (R-LEMMA) from the last
+//      four bytes and the length, then the two-choice probe; runs with one
+//      take stage_run (the exact clitic split) under a warp-uniform branch.
+//  (B) rules: the pool's requests are cut into 32 contiguous ranges of about
+//      equal token count (request granularity, so no request is shared by two
+//      lanes); every lane runs the sequential R-RULES machine of rules_round
+//      over its tokens, one token per iteration, reading them from the global
+//      buffer (L1/L2-resident: written a few microseconds earlier by the same
+//      warp).  A request's counts live in registers until its last token
+//      (16-bit fields: a pool holds <= kTokCap < 2^16 tokens) and then go to
+//      shared memory; the epilogue (u, key) runs lane-parallel per pool.
+// Tasks whose bytes exceed kTokCap (tokens <= bytes) and tasks with decreasing
+// offsets use the per-lane byte FSM.
+constexpr uint32_t kPoolTasks = 16;
+constexpr uint32_t kPoolReq = kPoolTasks * 32;
+constexpr uint32_t kTokCap = 16384;   // tokens per warp buffer
+constexpr uint32_t kTokPad = 64;      // read-ahead slack
+// per-warp global scratch: kTokCap + kTokPad tokens, then kPoolReq count records (16 B)
+constexpr size_t kWarpScratch = (kTokCap + kTokPad) * 2 + kPoolReq * 16;
+constexpr uint32_t kNoTok = 0xFFFFu;
+
+// token attributes for the v6 machine (Smem6::fa by token code):
+//   bit 0 VAGUE, bit 16 MULTIPOS (V | Y << 16 in one add), bits 1..10 entry id,
+//   bit 11 PREP, bit 12 NOUN, bit 13 END (. ! ?), bit 14 '?', bits 17..21
+//   O-class, bits 22..23 P-class, bits 24..31 senses - 1
+enum : uint32_t { G_VAGUE = 1u << 0, G_MULTI = 1u << 16, G_PREP = 1u << 11, G_NOUN = 1u << 12, G_END = 1u << 13,
+                  G_Q = 1u << 14 };
+
+__host__ __device__ __forceinline__ uint32_t fsm_attr6(uint32_t code, uint32_t at) {
+  if (code > kPunct) {
+    const uint32_t pk = code - kPunct;
+    if (pk == PK_COMMA) return (OC_PUNCT << 17) | (PC_COMMA << 22);
+    if (pk == PK_END) return (OC_END << 17) | (PC_PUNCT << 22) | G_END;
+    if (pk == PK_Q) return (OC_Q << 17) | (PC_PUNCT << 22) | G_END | G_Q;
+    return (OC_PUNCT << 17) | (PC_PUNCT << 22);
+  }
+  if (code == 0u) return PC_WORD << 22;
+  uint32_t f = 0;
+  f |= (at & A_VAGUE) ? G_VAGUE : 0u;
+  f |= (at & A_MULTIPOS) ? G_MULTI : 0u;
+  f |= (at & A_PREP) ? G_PREP : 0u;
+  f |= (at & A_NOUN) ? G_NOUN : 0u;
+  const uint32_t oc = ((at & A_OPENER) ? 1u : 0u) | ((at & A_WHAT) ? 2u : 0u) | ((at & A_CAUSE) ? 4u : 0u) |
+                      ((at & A_BROAD) ? 8u : 0u);
+  f |= oc << 17;
+  f |= ((at & A_COORD) ? PC_COORD : PC_WORD) << 22;
+  f |= ((at >> A_ID_SHIFT) & 0x3FFu) << 1;
+  f |= ((at >> A_SEM_SHIFT) & A_SEM_MASK) << 24;
+  return f;
+}
+
+struct __align__(16) WarpBuf6 {
+  union {
+    struct {
+      uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
+      uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
+      uint32_t sp[kChunk / 32 + 2];
+      uint32_t rs[32];
+      uint16_t ev[kChunk + 2];
+    } t;                                     // phase A
+    struct {
+      uint16_t ids[kPoolReq + 1];            // requests with tokens, in order
+      uint16_t ends[kPoolReq + 1];           // their end token index
+    } q;                                     // phase B
+  };
+  uint16_t nd[kPoolReq];                     // dropped bytes per request (<= task bytes <= kTokCap)
+  uint16_t tbeg[kPoolReq + 2];               // first token of each request in the pool buffer
+  uint32_t task[kPoolTasks];
+};
+
+struct Smem6 {
+  uint32_t lut[256];
+  uint32_t clit[8];
+  uint32_t fa[kPunct + 8];
+  uint8_t tO[16 * 32], tP[128 * 4];
+  WarpBuf6 w[kW4];
+};
+
+// Tokenize one warp task (requests r0 .. r0+rcnt-1, bytes [B0, B1)) into the
+// pool: tokens appended at gt[tok ..]; request lr0 + i's first token index in
+// tbeg.  A request's first token index is counted at the chunk holding its
+// first byte: the tokens before the chunk + the events of the chunk before
+// that byte (+ one per clitic split among them); requests without tokens get
+// the index of the next token.
+__device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6& S, WarpBuf6& B, const Lex& L,
+                                              uint16_t* gt, uint32_t& tok, uint32_t lr0, uint32_t rcnt,
+                                              uint32_t s_r, uint32_t e_r, bool rv, uint32_t lane,
+                                              uint32_t total_bytes) {
+  auto& T = B.t;
+  const uint8_t* st8 = reinterpret_cast<const uint8_t*>(T.stage);
+  const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
+  const uint32_t B1 = __shfl_sync(0xFFFFFFFFu, e_r, rcnt - 1);
+  T.rs[lane] = s_r;
+  B.nd[lr0 + lane] = 0;
+  uint32_t tb = 0xFFFFFFFFu;          // this lane's request: first token index (pool)
+  uint32_t prevW = 0;
+  int32_t pend_start = -1;
+  const uint32_t base = B0 & ~15u;
+  uint4 qprev = make_uint4(0, 0, 0, 0);
+  if (lane < 4) T.stage[lane] = 0;
+  __syncwarp();
+  for (uint32_t cb = base; cb < B1; cb += kChunk) {
+    // ---- (1) stage + classify 16 bytes per lane
+    const uint32_t g = cb + lane * 16u;
+    uint4 q;
+    if (g + 16u <= total_bytes) q = ld_nc_v4(a.bytes + g);
+    else {
+      uint32_t w4[4] = {0, 0, 0, 0};
+      for (uint32_t j = 0; j < 16u; ++j)
+        if (g + j < total_bytes) w4[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
+      q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    *reinterpret_cast<uint4*>(&T.stage[4 + lane * 4]) = qprev;
+    *reinterpret_cast<uint4*>(&T.stage[4 + kChunk / 4 + lane * 4]) = q;
+    qprev = q;
+    if (lane < kChunk / 32 + 1) T.mk[lane] = 0;
+    __syncwarp();
+    const bool here = rv && s_r >= cb && s_r < cb + kChunk;  // this lane's request starts in the chunk
+    if (here && s_r < B1) atomicOr(&T.mk[(s_r - cb) >> 5], 1u << ((s_r - cb) & 31u));
+    uint32_t accA = 0, accB = 0;
+    {
+      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t byte = (wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu;
+          const uint32_t c = S.lut[byte] << i;
+          if (j == 0) accA += c; else accB += c;
+        }
+    }
+    uint32_t vmask = 0xFFFFu;
+    if (g < B0) vmask &= B0 - g >= 16u ? 0u : (0xFFFFu << (B0 - g)) & 0xFFFFu;
+    if (g + 16u > B1) vmask &= B1 <= g ? 0u : (0xFFFFu >> (g + 16u - B1));
+    const uint32_t W16 = ((accA & 0xFFu) | ((accB & 0xFFu) << 8)) & vmask;
+    const uint32_t P16 = (((accA >> 8) & 0xFFu) | (((accB >> 8) & 0xFFu) << 8)) & vmask;
+    const uint32_t X16 = (((accA >> 16) & 0xFFu) | (((accB >> 16) & 0xFFu) << 8)) & vmask;
+    const uint32_t Wn = __shfl_down_sync(0xFFFFFFFFu, W16, 1);
+    if (!(lane & 1u)) T.wm[lane >> 1] = W16 | (Wn << 16);
+    if (lane == 0) T.wm[kChunk / 32] = 0;
+    __syncwarp();
+    // ---- (2) events: run starts and punctuation bytes, in byte order
+    if (lane < kChunk / 32 + 2) T.sp[lane] = lane < kChunk / 32 ? (~T.wm[lane] | T.mk[lane]) : 0xFFFFFFFFu;
+    const uint32_t mk16 = (T.mk[lane >> 1] >> (16u * (lane & 1u))) & 0xFFFFu;
+    const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W16, 1);
+    const uint32_t pw = lane ? (Wp >> 15) & 1u : prevW;
+    uint32_t R16 = (W16 & ~((W16 << 1) | pw)) | (W16 & mk16);
+    const bool last_chunk = cb + kChunk >= B1;
+    const bool defer = !last_chunk && ((__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u);
+    const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R16 != 0u);
+    const bool pend_here = pend_start >= 0 && (!defer || b_r);  // the carried run ends in this chunk
+    int32_t new_pend = -1;
+    if (defer && b_r) {  // the last run start of the chunk is carried into the next chunk
+      const uint32_t L2 = 31 - __clz(b_r);
+      const uint32_t top = __shfl_sync(0xFFFFFFFFu, R16, L2);
+      const uint32_t bit = 31 - __clz(top);
+      new_pend = (int32_t)(cb + L2 * 16u + bit);
+      if (lane == L2) R16 &= ~(1u << bit);
+    }
+    const uint32_t E16 = R16 | P16;
+    uint32_t incl = __popc(E16);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    const uint32_t ph = pend_here ? 1u : 0u;
+    const uint32_t nev = __shfl_sync(0xFFFFFFFFu, incl, 31) + ph;
+    const uint32_t excl = incl - __popc(E16) + ph;  // events before this lane's bytes
+    {
+      uint32_t k = excl, e = E16;
+      while (e) {
+        const uint32_t bit = __ffs(e) - 1;
+        e &= e - 1u;
+        T.ev[k++] = (uint16_t)(lane * 16u + bit);
+      }
+    }
+    if (lane == 0 && ph) T.ev[0] = 0xFFFFu;
+    // first event index of this lane's request (starting in the chunk)
+    uint32_t fe = 0xFFFFFFFFu;
+    {
+      const uint32_t off = s_r - cb, Lr = (off >> 4) & 31u;
+      const uint32_t exL = __shfl_sync(0xFFFFFFFFu, excl, Lr), EL = __shfl_sync(0xFFFFFFFFu, E16, Lr);
+      if (here) {
+        fe = exL + __popc(EL & ((1u << (off & 15u)) - 1u));
+        tb = tok + fe;
+      }
+    }
+    // the carried run: [pend_start, first stop of the chunk)
+    uint32_t cx = 0, cn = 0;
+    if (pend_here) {
+      const uint32_t ps = (uint32_t)pend_start;
+      uint32_t stop = 0;
+      for (uint32_t w = 0;; ++w) {
+        const uint32_t sm = T.sp[w];
+        if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
+      }
+      cn = cb + stop - ps;
+      if (ps + kChunk >= cb) {
+        cx = 16 + kChunk + ps - cb;
+      } else {
+        // longer than a chunk: its tokens depend only on its last 6 bytes (any
+        // stem is > 16 bytes, no lemma) -> stage them as a 24-byte run
+        const uint32_t pad = 16 + 2 * kChunk + 8;
+        uint8_t* stw = reinterpret_cast<uint8_t*>(T.stage);
+        if (lane < 8u) stw[pad + lane] = __ldg(a.bytes + ps + cn - 8 + lane);
+        cx = pad + 8 - 24;
+        cn = 24;
+      }
+    }
+    __syncwarp();
+    // ---- (3) tokens, 32 events at a time (branch-free; punctuation lanes
+    // compute a discarded word path)
+    for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
+      const uint32_t k = e0 + lane;
+      const bool valid = k < nev;
+      const uint32_t pe = valid ? T.ev[k] : 0u;
+      const bool carried = pe == 0xFFFFu;
+      const uint32_t p = pe & 511u;
+      const uint32_t lc = S.lut[st8[16 + kChunk + p]];
+      const bool isw = carried || (lc & 1u);
+      const uint32_t qq = p + 1, qw = qq >> 5, qb = qq & 31u;
+      const uint32_t st = __funnelshift_r(T.sp[qw], T.sp[qw + 1], qb);  // stops after p (sp[16], sp[17]: all ones)
+      uint32_t n = __ffs(st);
+      if (__any_sync(0xFFFFFFFFu, st == 0u && valid && isw && !carried)) {  // run of > 32 bytes (rare)
+        if (st == 0u) {
+          n = 33u - qb;
+          for (uint32_t w = qw + 2;; ++w) {
+            const uint32_t stop = T.sp[w];
+            if (stop) { n += __ffs(stop) - 1; break; }
+            n += 32u;
+          }
+        }
+      }
+      const uint32_t x = carried ? cx : 16 + kChunk + p;
+      n = carried ? cn : n;
+      // last four bytes of the run (lowercased): b[n-4] | b[n-3] << 8 | b[n-2] << 16 | b[n-1] << 24
+      uint32_t te = x + n - 4u;
+      uint32_t Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
+      // R-CLITIC needs an apostrophe at b[n-3] or b[n-2]: exact split for those lanes only
+      const bool apl = valid && isw && n > 2u && (__vcmpeq4(Tl, 0x27272727u) & 0x00FFFF00u) != 0u;
+      uint32_t ns = n, c1 = 0, cut = 0;
+      bool nt3 = false;
+      if (__any_sync(0xFFFFFFFFu, apl)) {
+        if (apl) {
+          constexpr uint32_t NT = 'n' | ('\'' << 8) | ('t' << 16);
+          const uint32_t l1 = Tl >> 24, l2 = (Tl >> 16) & 0xFFu, l3 = (Tl >> 8) & 0xFFu, h16 = Tl >> 16;
+          const bool c2 = l2 == '\'' && (l1 == 's' || l1 == 'm' || l1 == 'd');
+          const bool nt = (Tl >> 8) == NT;
+          const bool re = h16 == ('r' | ('e' << 8)), ve = h16 == ('v' | ('e' << 8)), ll = h16 == ('l' | ('l' << 8));
+          const bool c3 = n > 3u && (nt || (l3 == '\'' && (re || ve || ll)));
+          cut = c3 ? 3u : (c2 ? 2u : 0u);
+          const uint32_t kind = c3 ? (nt ? 0u : re ? 1u : ve ? 2u : 3u) : (l1 == 's' ? 4u : l1 == 'm' ? 5u : 6u);
+          c1 = S.clit[kind];
+          ns = n - cut;
+          if (cut) {  // the stem's last four bytes
+            te = x + ns - 4u;
+            Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
+          }
+          nt3 = ns == 3u && (Tl >> 8) == NT;  // the word n't: lemma "not" (R-LEMMA)
+        }
+      }
+      // R-LEMMA of the (stem) word: first rule wins (ing > ed / es > s)
+      const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
+      const uint32_t w0 = T.stage[a0], w1 = T.stage[a0 + 1], w2 = T.stage[a0 + 2], w3 = T.stage[a0 + 3],
+                     w4 = T.stage[a0 + 4];
+      uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
+      uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
+      o0 = nt3 ? ('n' | ('o' << 8) | ('t' << 16)) : o0;
+      const uint32_t t2 = Tl >> 16, t3 = Tl >> 8, b1 = Tl >> 24;
+      uint32_t strip = (ns >= 3u && b1 == 's' && (t2 & 0xFFu) != 's') ? 1u : 0u;
+      strip = (ns >= 4u && (t2 == ('e' | ('d' << 8)) || t2 == ('e' | ('s' << 8)))) ? 2u : strip;
+      strip = (ns >= 5u && t3 == ('i' | ('n' << 8) | ('g' << 16))) ? 3u : strip;
+      const uint32_t ll = ns - strip;
+      const int32_t shl = ll > 16u ? 0 : 8 * (int32_t)ll;
+      o0 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl, 0));
+      o1 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 32, 0));
+      o2 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 64, 0));
+      o3 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 96, 0));
+      const uint32_t cw = lookup(L, o0, o1, o2, o3);
+      const uint32_t c0 = isw ? cw : kPunct + (lc >> 24) - 1u;
+      // token positions: one token per event, two for a clitic split
+      const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, valid && cut != 0u);
+      if (valid) {
+        const uint32_t t0 = tok + lane + __popc(b2 & ((1u << lane) - 1u));
+        gt[t0] = (uint16_t)c0;
+        if (cut) gt[t0 + 1] = (uint16_t)c1;
+      }
+      if (b2) {  // requests whose first event follows a split start one token later
+        uint32_t m = b2;
+        while (m) {
+          const uint32_t c = __ffs(m) - 1;
+          m &= m - 1u;
+          if (fe != 0xFFFFFFFFu && fe > e0 + c) ++tb;
+        }
+      }
+      tok += min(32u, nev - e0) + __popc(b2);
+    }
+    if (__any_sync(0xFFFFFFFFu, X16 != 0u)) {  // dropped bytes (rare): count per request
+      uint32_t xm = X16;
+      while (xm) {
+        const uint32_t bit = __ffs(xm) - 1;
+        xm &= xm - 1u;
+        atomicAdd(reinterpret_cast<uint32_t*>(&B.nd[(lr0 + req_of(T.rs, rcnt, g + bit)) & ~1u]),
+                  1u << (16u * ((lr0 + req_of(T.rs, rcnt, g + bit)) & 1u)));
+      }
+    }
+    if (pend_here) pend_start = -1;
+    if (new_pend >= 0) pend_start = new_pend;
+    prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
+    __syncwarp();
+  }
+  B.tbeg[lr0 + lane] = (uint16_t)(tb == 0xFFFFFFFFu ? tok : tb);
+  __syncwarp();
+}
+
+// R-RULES over the pool's tokens: lane = a contiguous range of whole requests
+// of about T/32 tokens; the machine of rules_round (O-part / P-part tables,
+// S-part in registers), restarted at every request start.  Requests without
+// tokens are compacted away first; a request's counts go to its 16-byte record
+// in the warp's global scratch when its last token has been read.  Branch-free
+// per token: lanes past their range run the machine on ignored tokens.
+__device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const uint16_t* gt, uint4* gcnt, uint32_t R,
+                                           uint32_t T, uint32_t lane) {
+  if (lane == 0) B.tbeg[R] = (uint16_t)T;
+  __syncwarp();
+  auto& Q = B.q;
+  uint32_t nne = 0;
+  for (uint32_t b = 0; b < R; b += 32) {
+    const uint32_t r = b + lane;
+    const uint32_t e = B.tbeg[r + 1];
+    const bool ne = e > B.tbeg[r];
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, ne);
+    if (ne) {
+      const uint32_t pos = nne + __popc(m & ((1u << lane) - 1u));
+      Q.ids[pos] = (uint16_t)r;
+      Q.ends[pos] = (uint16_t)e;
+    }
+    nne += __popc(m);
+  }
+  if (lane == 0) { Q.ids[nne] = 0; Q.ends[nne] = (uint16_t)T; }
+  __syncwarp();
+  // this lane's entries [ja, jend): from the first entry starting at or after lane * T / 32
+  uint32_t ja = 0;
+  if (lane) {
+    const uint32_t target = (uint32_t)(((uint64_t)T * lane + 31u) >> 5);
+    uint32_t lo = 0, hi = nne;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (Q.ends[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    ja = min(lo + 1, nne);
+  }
+  uint32_t jend = __shfl_down_sync(0xFFFFFFFFu, ja, 1);
+  if (lane == 31) jend = nne;
+  uint32_t idx = ja ? Q.ends[ja - 1] : 0u;
+  const uint32_t stop = jend ? Q.ends[jend - 1] : 0u;
+  uint32_t j = ja;
+  uint32_t r = Q.ids[j], nxt = Q.ends[j];
+  const uint16_t* tp = gt + idx;
+  uint32_t tk0 = tp[0], tk1 = tp[1];
+  uint32_t c1 = 0, cq = 0, cop = 0, M = 0;
+  uint32_t nf = kNoNoun10, so = 0, sp = 0, n2 = 0;
+  while (__any_sync(0xFFFFFFFFu, idx < stop)) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const bool act = idx < stop;
+      const uint32_t t = tk0;
+      tk0 = tk1;
+      tk1 = tp[2];
+      tp += act ? 1 : 0;
+      const uint32_t a = S.fa[t];
+      c1 += a & (G_VAGUE | G_MULTI);
+      M += a >> 24;
+      const uint32_t vo = S.tO[(so << 5) | ((a >> 17) & 31u)];
+      const uint32_t vp = S.tP[(sp << 2) | ((a >> 22) & 3u)];
+      so = vo & 15u;
+      sp = vp & 127u;
+      const uint32_t sinc = (a >> 11) & n2;  // PREP after a second distinct noun (PREP tested first)
+      const uint32_t id = (a >> 1) & 0x3FFu;
+      const bool noun = (a & G_NOUN) != 0u, first = noun && nf == kNoNoun10;
+      n2 |= (noun && !first && id != nf) ? 1u : 0u;
+      nf = first ? id : nf;
+      const bool end = (a & G_END) != 0u;
+      nf = end ? kNoNoun10 : nf;
+      n2 = end ? 0u : n2;
+      cq += ((a >> 14) & 1u) | (sinc << 16);
+      cop += (vo >> 4) | ((vp >> 7) << 16);
+      idx += act ? 1u : 0u;
+      const bool fin = act && idx == nxt;  // last token of request r: store, fresh context
+      if (fin) gcnt[r] = make_uint4(c1, cq, cop, M);
+      const uint32_t keep = fin ? 0u : 1u;
+      c1 *= keep; cq *= keep; cop *= keep; M *= keep;
+      so *= keep; sp *= keep; n2 *= keep;
+      nf = fin ? kNoNoun10 : nf;
+      j += fin ? 1u : 0u;
+      if (fin) { r = Q.ids[j]; nxt = Q.ends[j]; }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work, uint16_t* tokbuf) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Smem6& S = *reinterpret_cast<Smem6*>(smem_raw);
+  uint8_t* tail_mem = smem_raw + ((sizeof(Smem6) + 15) & ~size_t(15));
+  uint4* s_keys = reinterpret_cast<uint4*>(tail_mem);
+  const uint32_t key_bytes = (a.lex.n_entries + 1u) * 16u;
+  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + key_bytes);
+  const uint32_t nslots = 1u << a.lex.bits;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+  {
+    for (uint32_t i = tid; i <= a.lex.n_entries; i += kT4) s_keys[i] = a.lex.keys[i];
+    for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
+    for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i) | (punct_kind(i) << 24);
+    for (uint32_t i = tid; i < kPunct + 8; i += kT4)
+      S.fa[i] = fsm_attr6(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
+    for (uint32_t i = tid; i < 16 * 32; i += kT4) S.tO[i] = (uint8_t)o_step(i >> 5, i & 31u);
+    for (uint32_t i = tid; i < 128 * 4; i += kT4) S.tP[i] = (uint8_t)p_step(i >> 2, i & 3u);
+  }
+  __syncthreads();
+  const Lex L{s_keys, s_slots, a.lex.entries, a.lex.bits, a.lex.seed};
+  if (tid < 7) {
+    const uint32_t cb = clitic_bytes(tid), len = tid < 4 ? 3u : 2u;
+    const uint32_t s3 = len == 3 ? (((cb & 0xFFu) << 16) | (cb & 0xFF00u) | ((cb >> 16) & 0xFFu))
+                                 : (((cb & 0xFFu) << 8) | ((cb >> 8) & 0xFFu));
+    S.clit[tid] = word_code(L, len, cb, 0u, 0u, 0u, s3);
+  }
+  __syncthreads();
+  WarpBuf6& B = S.w[wid];
+  uint8_t* wscr = reinterpret_cast<uint8_t*>(tokbuf) + (size_t)(blockIdx.x * kW4 + wid) * kWarpScratch;
+  uint16_t* gt = reinterpret_cast<uint16_t*>(wscr);
+  uint4* gcnt = reinterpret_cast<uint4*>(wscr + (kTokCap + kTokPad) * 2);
+  const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
+  const uint32_t ntasks = (a.n + 31) / 32;
+  uint32_t pending = 0xFFFFFFFFu;
+  bool done = false;
+  while (!done) {
+    // ---- (A) fill a pool
+    uint32_t np = 0, tok = 0;
+    for (;;) {
+      uint32_t task;
+      if (pending != 0xFFFFFFFFu) {
+        task = pending;
+        pending = 0xFFFFFFFFu;
+      } else {
+        task = 0;
+        if (lane == 0) task = atomicAdd(work, 1u);
+        task = __shfl_sync(0xFFFFFFFFu, task, 0);
+        if (task >= ntasks) { done = true; break; }
+      }
+      const uint32_t r0 = task * 32, rcnt = min(32u, a.n - r0);
+      const uint32_t r = r0 + lane;
+      const bool rv = lane < rcnt;
+      const uint32_t s_r = rv ? a.offsets[r] : 0u;
+      const uint32_t e_r = rv ? a.offsets[r + 1] : 0u;
+      const bool bad = rv && e_r < s_r;
+      const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
+      const uint32_t B1 = __shfl_sync(0xFFFFFFFFu, e_r, rcnt - 1);
+      if (__any_sync(0xFFFFFFFFu, bad) || B1 - B0 > kTokCap) {
+        // decreasing offsets, or more bytes than a pool buffer holds: per-lane byte FSM
+        if (bad) atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
+        if (rv) fsm_request(a, L, r, s_r, bad ? s_r : e_r);
+        continue;
+      }
+      if (tok + (B1 - B0) > kTokCap) { pending = task; break; }  // tokens <= bytes
+      if (lane == 0) B.task[np] = task;
+      tokenize_task(a, S, B, L, gt, tok, np * 32, rcnt, s_r, e_r, rv, lane, total_bytes);
+      if (++np == kPoolTasks) break;
+    }
+    if (np == 0) continue;
+    // ---- (B) rules, (C) epilogue
+    const uint32_t R = np * 32;
+    rules_pool(S, B, gt, gcnt, R, tok, lane);
+    for (uint32_t lr = lane; lr < R; lr += 32) {
+      const uint32_t gr = B.task[lr >> 5] * 32 + (lr & 31u);
+      if (gr >= a.n) continue;
+      const uint32_t ntk = (uint32_t)B.tbeg[lr + 1] - (uint32_t)B.tbeg[lr];
+      const uint4 c = ntk ? gcnt[lr] : make_uint4(0, 0, 0, 0);
+      const uint32_t q = c.y & 0xFFFFu;
+      const uint32_t Pt = (c.z >> 16) + (q > 1u ? q - 1u : 0u);
+      const uint32_t raw[8] = {c.y >> 16, c.x >> 16, c.w, c.x & 0xFFFFu, c.z & 0xFFFFu, Pt,
+                               ntk, B.nd[lr]};
+      uint32_t f[8];
+      bool sat = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        sat |= raw[k] > 65535u;
+        f[k] = min(raw[k], 65535u);
+      }
+      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
+      epilogue(a, gr, f);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_predict(const uint16_t* __restrict__ feat, uint32_t n, rt_regressor reg, float* __restrict__ u) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -942,18 +1449,31 @@ __global__ void k_key(const float* __restrict__ u, const uint16_t* __restrict__ 
 }  // namespace
 
 
+size_t score_scratch_bytes(int ctas) { return (size_t)ctas * kW4 * kWarpScratch; }
+
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + (size_t(a.lex.n_entries) + 1) * 16 +
-                      (size_t(1) << a.lex.bits) * 2;
-  cudaError_t e = cudaFuncSetAttribute(k_score4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.work, 0, sizeof(uint32_t), s);
+  cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const uint32_t ntasks = (a.n + 31) / 32;
   uint32_t grid = (uint32_t)a.num_sms;
   if (grid * kW4 > ntasks) grid = (ntasks + kW4 - 1) / kW4;
-  k_score4<<<grid, kT4, smem, s>>>(a, a.work);
+  const size_t lex_bytes = (size_t(a.lex.n_entries) + 1) * 16 + (size_t(1) << a.lex.bits) * 2;
+  static const int legacy = [] {
+    const char* v = getenv("RTLM_KSCORE");
+    return v && v[0] == '4';
+  }();
+  if (legacy || !a.tokbuf) {
+    const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + lex_bytes;
+    e = cudaFuncSetAttribute(k_score4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_score4<<<grid, kT4, smem, s>>>(a, a.work);
+  } else {
+    const size_t smem = ((sizeof(Smem6) + 15) & ~size_t(15)) + lex_bytes;
+    e = cudaFuncSetAttribute(k_score6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_score6<<<grid, kT4, smem, s>>>(a, a.work, a.tokbuf);
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -372,6 +372,45 @@ def test_score_stream_boundaries(ctx_v1, lex_v1):
     assert len(bad) == 0, [(int(i), got[i].tolist(), want[i].tolist()) for i in bad[:5]]
 
 
+def test_score_pool_boundaries(ctx_v1, lex_v1):
+    """K1 tokenizes whole warp tasks (32 requests) into a per-warp pool of up to
+    16 tasks / 16384 tokens before the rule pass: tasks of 2-16 KB fill a pool
+    after a few tasks (the next task waits for the following pool), tasks above
+    16 KB take the per-lane byte path, and empty requests sit between, before
+    and after requests with tokens (also at pool ends)."""
+    d = configs.config2(n=6000, gid0=99)
+    data, off = d["data"], d["offsets"]
+    reqs = [bytes(data[off[i]:off[i + 1]]) for i in range(len(off) - 1)]
+    rng = np.random.default_rng(17)
+    t, k = [], 0
+    while k < len(reqs) - 40:
+        kind = rng.integers(0, 4)
+        if kind == 0:  # a task of ~2-16 KB: 32 requests of 1-7 generator requests each
+            for _ in range(32):
+                m = int(rng.integers(1, 8))
+                t.append(b" ".join(reqs[k:k + m]))
+                k += m
+        elif kind == 1:  # empty requests around short ones
+            for _ in range(32):
+                t.append(b"" if rng.random() < 0.5 else reqs[k])
+                k += 1
+        elif kind == 2:  # one task above 16 KB (byte path) or just below it
+            big = int(rng.integers(14000, 19000))
+            chunk = b" ".join(reqs[k:k + 260])[:big]
+            k += 260
+            t += [chunk[i * len(chunk) // 32:(i + 1) * len(chunk) // 32] for i in range(32)]
+        else:
+            t += reqs[k:k + 32]
+            k += 32
+    t += [b""] * 40
+    data2, off2 = rtgen.pack_texts(t)
+    feat = ctx_v1.score(dev(data2), dev(off2))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex_v1, data2, off2)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), got[i].tolist(), want[i].tolist()) for i in bad[:5]]
+
+
 def test_score_decreasing_offsets(ctx_v1, lex_v1):
     """Offsets that decrease: those requests score as empty and set the flag; the
     other requests of the same warp task (per-lane FSM path) still match."""
