@@ -16,7 +16,7 @@ struct rt_ctx {
   uint32_t sm_limit = 0;  // rt_set_sm_limit (0: one CTA per SM)
   rtlm::LexEntry* d_entries = nullptr;
   uint4* d_keys = nullptr;
-  uint16_t* d_slots = nullptr;
+  uint32_t* d_slots = nullptr;
   uint32_t n_entries = 0, bits = 0, seed = 0;
   uint32_t* d_flags = nullptr;
   uint16_t* d_tok = nullptr;  // scoring token buffers (one per persistent warp)
@@ -283,7 +283,7 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
     keys[k + 1] = uint4{w[0], w[1], w[2], w[3]};
   }
   // cuckoo placement (two slots per key); a new seed if an insertion cycles
-  std::vector<uint16_t> slots;
+  std::vector<uint32_t> slots;
   uint32_t seed = 0;
   for (;; ++seed) {
     slots.assign(1u << bits, 0);
@@ -295,12 +295,12 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
         const uint4& q = keys[cur];
         const uint32_t x = rtlm::lex_mix(q.x, q.y, q.z, q.w, seed);
         const uint32_t s1 = rtlm::lex_slot1(x, bits), s2 = rtlm::lex_slot2(x, bits);
-        if (!slots[s1]) { slots[s1] = (uint16_t)cur; placed = true; }
-        else if (!slots[s2]) { slots[s2] = (uint16_t)cur; placed = true; }
+        if (!slots[s1]) { slots[s1] = cur; placed = true; }
+        else if (!slots[s2]) { slots[s2] = cur; placed = true; }
         else {  // evict the occupant of the slot that is not where we came from
           const uint32_t s = (kick & 1) ? s2 : s1;
           const uint32_t ev = slots[s];
-          slots[s] = (uint16_t)cur;
+          slots[s] = cur;
           cur = ev;
         }
       }
@@ -309,15 +309,22 @@ rt_status upload_lexicon(rt_ctx* c, const char* text, size_t len) {
     if (ok) break;
     if (seed > 1000) return fail(c, RT_ELEXICON, "lexicon hash table could not be built");
   }
+  // each occupied slot also carries the top 21 bits of its key's hash (the
+  // device compares one key: the one whose fingerprint matches)
+  for (uint32_t& v : slots) {
+    if (!v) continue;
+    const uint4& q = keys[v];
+    v |= (rtlm::lex_mix(q.x, q.y, q.z, q.w, seed) >> 11) << 11;
+  }
   c->n_entries = n;
   c->bits = bits;
   c->seed = seed;
   RT_CUDA(c, cudaMalloc(&c->d_entries, std::max<size_t>(1, n) * sizeof(LexEntry)));
   RT_CUDA(c, cudaMalloc(&c->d_keys, keys.size() * sizeof(uint4)));
-  RT_CUDA(c, cudaMalloc(&c->d_slots, slots.size() * sizeof(uint16_t)));
+  RT_CUDA(c, cudaMalloc(&c->d_slots, slots.size() * sizeof(uint32_t)));
   if (n) RT_CUDA(c, cudaMemcpy(c->d_entries, ent.data(), n * sizeof(LexEntry), cudaMemcpyHostToDevice));
   RT_CUDA(c, cudaMemcpy(c->d_keys, keys.data(), keys.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-  RT_CUDA(c, cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  RT_CUDA(c, cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
   return RT_OK;
 }
 

@@ -36,7 +36,8 @@ struct LexEntry {
 struct DevLexicon {
   const LexEntry* entries;  // n_entries (global; attributes)
   const uint4* keys;        // n_entries + 1: keys[0] = 0, keys[i] = zero-padded lemma of entry i - 1
-  const uint16_t* slots;    // 1 << bits; 0 = empty, else entry index + 1 (a key sits at one of its two slots)
+  const uint32_t* slots;    // 1 << bits; 0 = empty, else entry index + 1 | fingerprint << 11 (lex_fp of the key);
+                            // a key sits at one of its two slots
   uint32_t n_entries;
   uint32_t bits;
   uint32_t seed;
@@ -49,6 +50,7 @@ __host__ __device__ __forceinline__ uint32_t lex_mix(uint32_t w0, uint32_t w1, u
   uint32_t x = (w0 * 0x9E3779B1u) ^ (w1 * 0x85EBCA77u) ^ (w2 * 0xC2B2AE3Du) ^ (w3 * 0x27D4EB2Fu) ^ seed;
   return x ^ (x >> 15);
 }
+__host__ __device__ __forceinline__ uint32_t lex_fp(uint32_t x) { return x >> 11; }
 __host__ __device__ __forceinline__ uint32_t lex_slot1(uint32_t x, uint32_t bits) { return (x * 0x2C1B3C6Du) >> (32 - bits); }
 __host__ __device__ __forceinline__ uint32_t lex_slot2(uint32_t x, uint32_t bits) { return (x * 0x297A2D39u) >> (32 - bits); }
 

@@ -75,19 +75,28 @@ __device__ __forceinline__ uint64_t priority_key(float u, uint32_t D_us, int64_t
 // encodes the length), keys[0] = 0 so an empty slot never matches a lemma.
 struct Lex {
   const uint4* keys;        // shared memory
-  const uint16_t* slots;    // shared memory
+  const uint32_t* slots;    // shared memory
   const LexEntry* e;        // global (attributes, byte-FSM path only)
   uint32_t bits, seed;
 };
 
-// token code (entry index + 1, 0 = not in the lexicon) of a zero-padded lemma
+// token code (entry index + 1, 0 = not in the lexicon) of a zero-padded lemma:
+// the slot whose fingerprint matches names the one key compared (a second
+// compare only when both fingerprints match and the first key differs)
 __device__ __forceinline__ uint32_t lookup(const Lex& L, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
-  const uint32_t x = lex_mix(w0, w1, w2, w3, L.seed);
-  const uint32_t s1 = L.slots[lex_slot1(x, L.bits)], s2 = L.slots[lex_slot2(x, L.bits)];
-  const uint4 k1 = L.keys[s1], k2 = L.keys[s2];
-  const bool m1 = ((k1.x ^ w0) | (k1.y ^ w1) | (k1.z ^ w2) | (k1.w ^ w3)) == 0u;
-  const bool m2 = ((k2.x ^ w0) | (k2.y ^ w1) | (k2.z ^ w2) | (k2.w ^ w3)) == 0u;
-  return m1 ? s1 : (m2 ? s2 : 0u);
+  const uint32_t x = lex_mix(w0, w1, w2, w3, L.seed), fp = lex_fp(x);
+  const uint32_t v1 = L.slots[lex_slot1(x, L.bits)], v2 = L.slots[lex_slot2(x, L.bits)];
+  const bool f1 = (v1 >> 11) == fp, f2 = (v2 >> 11) == fp;
+  const uint32_t c = f1 ? (v1 & 0x7FFu) : (f2 ? (v2 & 0x7FFu) : 0u);
+  const uint4 k = L.keys[c];
+  const bool m = ((k.x ^ w0) | (k.y ^ w1) | (k.z ^ w2) | (k.w ^ w3)) == 0u;
+  uint32_t code = m ? c : 0u;
+  if (__builtin_expect(f1 && f2 && !m, 0)) {
+    const uint32_t c2 = v2 & 0x7FFu;
+    const uint4 k2 = L.keys[c2];
+    code = ((k2.x ^ w0) | (k2.y ^ w1) | (k2.z ^ w2) | (k2.w ^ w3)) == 0u ? c2 : 0u;
+  }
+  return code;
 }
 
 __device__ __forceinline__ uint32_t probe(const Lex& L, uint64_t k0, uint64_t k1, uint32_t len) {
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work
   uint8_t* tail_mem = smem_raw + ((sizeof(Smem4) + 15) & ~size_t(15));
   uint4* s_keys = reinterpret_cast<uint4*>(tail_mem);
   const uint32_t key_bytes = (a.lex.n_entries + 1u) * 16u;
-  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + key_bytes);
+  uint32_t* s_slots = reinterpret_cast<uint32_t*>(tail_mem + key_bytes);
   const uint32_t nslots = 1u << a.lex.bits;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
   {
@@ -952,34 +961,28 @@ constexpr uint32_t kTokPad = 64;      // read-ahead slack
 constexpr size_t kWarpScratch = (kTokCap + kTokPad) * 2 + kPoolReq * 16;
 constexpr uint32_t kNoTok = 0xFFFFu;
 
-// token attributes for the v6 machine (Smem6::fa by token code):
-//   bit 0 VAGUE, bit 16 MULTIPOS (V | Y << 16 in one add), bits 1..10 entry id,
-//   bit 11 PREP, bit 12 NOUN, bit 13 END (. ! ?), bit 14 '?', bits 17..21
-//   O-class, bits 22..23 P-class, bits 24..31 senses - 1
-enum : uint32_t { G_VAGUE = 1u << 0, G_MULTI = 1u << 16, G_PREP = 1u << 11, G_NOUN = 1u << 12, G_END = 1u << 13,
-                  G_Q = 1u << 14 };
-
-__host__ __device__ __forceinline__ uint32_t fsm_attr6(uint32_t code, uint32_t at) {
+// Token attributes for the v6 machine (Smem6::fa by token code), two words
+// so that every field is one or two instructions away:
+//   x = O-class * 4 | (senses - 1) << 8 | noun id << 16 (0xFFFF: not a noun)
+//   y = VAGUE | P-class * 4 | '?' << 8 | END << 12 | MULTIPOS << 16 | PREP << 24
+//       (y & 0x10001 is added to the V | Y counter; (y >> 8) masked by 0x1 or
+//       0x10001 -- "a second distinct noun seen" -- to the q | S counter)
+__host__ __device__ __forceinline__ uint2 fsm_attr6(uint32_t code, uint32_t at) {
+  constexpr uint32_t NONE = 0xFFFFu;
   if (code > kPunct) {
     const uint32_t pk = code - kPunct;
-    if (pk == PK_COMMA) return (OC_PUNCT << 17) | (PC_COMMA << 22);
-    if (pk == PK_END) return (OC_END << 17) | (PC_PUNCT << 22) | G_END;
-    if (pk == PK_Q) return (OC_Q << 17) | (PC_PUNCT << 22) | G_END | G_Q;
-    return (OC_PUNCT << 17) | (PC_PUNCT << 22);
+    if (pk == PK_COMMA) return make_uint2((OC_PUNCT * 4) | (NONE << 16), PC_COMMA * 4);
+    if (pk == PK_END) return make_uint2((OC_END * 4) | (NONE << 16), (PC_PUNCT * 4) | (1u << 12));
+    if (pk == PK_Q) return make_uint2((OC_Q * 4) | (NONE << 16), (PC_PUNCT * 4) | (1u << 12) | (1u << 8));
+    return make_uint2((OC_PUNCT * 4) | (NONE << 16), PC_PUNCT * 4);
   }
-  if (code == 0u) return PC_WORD << 22;
-  uint32_t f = 0;
-  f |= (at & A_VAGUE) ? G_VAGUE : 0u;
-  f |= (at & A_MULTIPOS) ? G_MULTI : 0u;
-  f |= (at & A_PREP) ? G_PREP : 0u;
-  f |= (at & A_NOUN) ? G_NOUN : 0u;
+  if (code == 0u) return make_uint2(NONE << 16, PC_WORD * 4);
   const uint32_t oc = ((at & A_OPENER) ? 1u : 0u) | ((at & A_WHAT) ? 2u : 0u) | ((at & A_CAUSE) ? 4u : 0u) |
                       ((at & A_BROAD) ? 8u : 0u);
-  f |= oc << 17;
-  f |= ((at & A_COORD) ? PC_COORD : PC_WORD) << 22;
-  f |= ((at >> A_ID_SHIFT) & 0x3FFu) << 1;
-  f |= ((at >> A_SEM_SHIFT) & A_SEM_MASK) << 24;
-  return f;
+  const uint32_t nid = (at & A_NOUN) ? ((at >> A_ID_SHIFT) & 0x3FFu) : NONE;
+  return make_uint2((oc * 4) | (((at >> A_SEM_SHIFT) & A_SEM_MASK) << 8) | (nid << 16),
+                    ((at & A_VAGUE) ? 1u : 0u) | (((at & A_COORD) ? PC_COORD : PC_WORD) * 4) |
+                        ((at & A_MULTIPOS) ? 0x10000u : 0u) | ((at & A_PREP) ? 0x1000000u : 0u));
 }
 
 struct __align__(16) WarpBuf6 {
@@ -1004,10 +1007,33 @@ struct __align__(16) WarpBuf6 {
 struct Smem6 {
   uint32_t lut[256];
   uint32_t clit[8];
-  uint32_t fa[kPunct + 8];
-  uint8_t tO[16 * 32], tP[128 * 4];
+  uint2 cl3[8], cl2[8];                // clitic patterns (last 3 / 2 bytes) -> token code, see clitic_hash3/2
+  uint4 lmask[18];                     // lemma byte masks for lengths 0..16 (17: none)
+  uint2 fa[kPunct + 8];                // rule-machine attributes by token code (fsm_attr6)
+  uint32_t tO[16 * 32], tP[128 * 4];   // transitions: next row byte offset | increment << 16
   WarpBuf6 w[kW4];
 };
+
+// Perfect hashes of the R-CLITIC patterns (lowercased little-endian bytes):
+// n't 're 've 'll -> slots 5 6 1 4 of 8; 's 'm 'd -> slots 0 5 6 of 8.
+__host__ __device__ __forceinline__ uint32_t clitic_hash3(uint32_t h) { return (h * 0x165667B1u) >> 29; }
+__host__ __device__ __forceinline__ uint32_t clitic_hash2(uint32_t h) { return (h * 0x9E3779B1u) >> 29; }
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 
 // Tokenize one warp task (requests r0 .. r0+rcnt-1, bytes [B0, B1)) into the
 // pool: tokens appended at gt[tok ..]; request lr0 + i's first token index in
@@ -1170,46 +1196,31 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       // last four bytes of the run (lowercased): b[n-4] | b[n-3] << 8 | b[n-2] << 16 | b[n-1] << 24
       uint32_t te = x + n - 4u;
       uint32_t Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
-      // R-CLITIC needs an apostrophe at b[n-3] or b[n-2]: exact split for those lanes only
-      const bool apl = valid && isw && n > 2u && (__vcmpeq4(Tl, 0x27272727u) & 0x00FFFF00u) != 0u;
-      uint32_t ns = n, c1 = 0, cut = 0;
-      bool nt3 = false;
-      if (__any_sync(0xFFFFFFFFu, apl)) {
-        if (apl) {
-          constexpr uint32_t NT = 'n' | ('\'' << 8) | ('t' << 16);
-          const uint32_t l1 = Tl >> 24, l2 = (Tl >> 16) & 0xFFu, l3 = (Tl >> 8) & 0xFFu, h16 = Tl >> 16;
-          const bool c2 = l2 == '\'' && (l1 == 's' || l1 == 'm' || l1 == 'd');
-          const bool nt = (Tl >> 8) == NT;
-          const bool re = h16 == ('r' | ('e' << 8)), ve = h16 == ('v' | ('e' << 8)), ll = h16 == ('l' | ('l' << 8));
-          const bool c3 = n > 3u && (nt || (l3 == '\'' && (re || ve || ll)));
-          cut = c3 ? 3u : (c2 ? 2u : 0u);
-          const uint32_t kind = c3 ? (nt ? 0u : re ? 1u : ve ? 2u : 3u) : (l1 == 's' ? 4u : l1 == 'm' ? 5u : 6u);
-          c1 = S.clit[kind];
-          ns = n - cut;
-          if (cut) {  // the stem's last four bytes
-            te = x + ns - 4u;
-            Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
-          }
-          nt3 = ns == 3u && (Tl >> 8) == NT;  // the word n't: lemma "not" (R-LEMMA)
-        }
-      }
+      // R-CLITIC: the run's last three / two bytes against the seven clitics
+      // (perfect hashes, branch-free); the stem keeps n - cut bytes
+      constexpr uint32_t NT = 'n' | ('\'' << 8) | ('t' << 16);
+      const uint32_t h3 = Tl >> 8, h2 = Tl >> 16;
+      const uint2 e3 = S.cl3[clitic_hash3(h3)], e2 = S.cl2[clitic_hash2(h2)];
+      const bool m3 = isw && n > 3u && e3.x == h3, m2 = isw && n > 2u && e2.x == h2;
+      const uint32_t cut = m3 ? 3u : (m2 ? 2u : 0u);
+      const uint32_t c1 = m3 ? e3.y : e2.y;
+      const uint32_t ns = n - cut;
+      te = x + ns - 4u;  // the stem's last four bytes
+      Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
+      const bool nt3 = ns == 3u && (Tl >> 8) == NT;  // the word n't: lemma "not" (R-LEMMA)
       // R-LEMMA of the (stem) word: first rule wins (ing > ed / es > s)
       const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
       const uint32_t w0 = T.stage[a0], w1 = T.stage[a0 + 1], w2 = T.stage[a0 + 2], w3 = T.stage[a0 + 3],
                      w4 = T.stage[a0 + 4];
-      uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
-      uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
-      o0 = nt3 ? ('n' | ('o' << 8) | ('t' << 16)) : o0;
       const uint32_t t2 = Tl >> 16, t3 = Tl >> 8, b1 = Tl >> 24;
       uint32_t strip = (ns >= 3u && b1 == 's' && (t2 & 0xFFu) != 's') ? 1u : 0u;
       strip = (ns >= 4u && (t2 == ('e' | ('d' << 8)) || t2 == ('e' | ('s' << 8)))) ? 2u : strip;
       strip = (ns >= 5u && t3 == ('i' | ('n' << 8) | ('g' << 16))) ? 3u : strip;
-      const uint32_t ll = ns - strip;
-      const int32_t shl = ll > 16u ? 0 : 8 * (int32_t)ll;
-      o0 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl, 0));
-      o1 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 32, 0));
-      o2 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 64, 0));
-      o3 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(shl - 96, 0));
+      const uint4 mk = S.lmask[min(ns - strip, 17u)];  // lemma bytes kept (none above 16)
+      const uint32_t o0 = nt3 ? ('n' | ('o' << 8) | ('t' << 16)) : ((__funnelshift_r(w0, w1, sh) | 0x20202020u) & mk.x);
+      const uint32_t o1 = (__funnelshift_r(w1, w2, sh) | 0x20202020u) & mk.y;
+      const uint32_t o2 = (__funnelshift_r(w2, w3, sh) | 0x20202020u) & mk.z;
+      const uint32_t o3 = (__funnelshift_r(w3, w4, sh) | 0x20202020u) & mk.w;
       const uint32_t cw = lookup(L, o0, o1, o2, o3);
       const uint32_t c0 = isw ? cw : kPunct + (lc >> 24) - 1u;
       // token positions: one token per event, two for a clitic split
@@ -1292,8 +1303,11 @@ __device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const ui
   uint32_t r = Q.ids[j], nxt = Q.ends[j];
   const uint16_t* tp = gt + idx;
   uint32_t tk0 = tp[0], tk1 = tp[1];
-  uint32_t c1 = 0, cq = 0, cop = 0, M = 0;
-  uint32_t nf = kNoNoun10, so = 0, sp = 0, n2 = 0;
+  const uint32_t fa_s = (uint32_t)__cvta_generic_to_shared(S.fa);
+  const uint32_t tO_s = (uint32_t)__cvta_generic_to_shared(S.tO), tP_s = (uint32_t)__cvta_generic_to_shared(S.tP);
+  uint32_t c1 = 0, cq = 0, co = 0, cp = 0, M = 0;   // V | Y<<16, q | S<<16, O, P, M of request r
+  uint32_t ro = 0, rp = 0;                          // O-part / P-part state (row byte offsets)
+  uint32_t nf = 0xFFFFu, n2m = 1u;                 // first noun id of the sentence; 0x10001 once a second one is seen
   while (__any_sync(0xFFFFFFFFu, idx < stop)) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -1302,30 +1316,30 @@ __device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const ui
       tk0 = tk1;
       tk1 = tp[2];
       tp += act ? 1 : 0;
-      const uint32_t a = S.fa[t];
-      c1 += a & (G_VAGUE | G_MULTI);
-      M += a >> 24;
-      const uint32_t vo = S.tO[(so << 5) | ((a >> 17) & 31u)];
-      const uint32_t vp = S.tP[(sp << 2) | ((a >> 22) & 3u)];
-      so = vo & 15u;
-      sp = vp & 127u;
-      const uint32_t sinc = (a >> 11) & n2;  // PREP after a second distinct noun (PREP tested first)
-      const uint32_t id = (a >> 1) & 0x3FFu;
-      const bool noun = (a & G_NOUN) != 0u, first = noun && nf == kNoNoun10;
-      n2 |= (noun && !first && id != nf) ? 1u : 0u;
-      nf = first ? id : nf;
-      const bool end = (a & G_END) != 0u;
-      nf = end ? kNoNoun10 : nf;
-      n2 = end ? 0u : n2;
-      cq += ((a >> 14) & 1u) | (sinc << 16);
-      cop += (vo >> 4) | ((vp >> 7) << 16);
+      const uint2 a = lds64(fa_s + t * 8u);
+      c1 += a.y & 0x10001u;
+      cq += (a.y >> 8) & n2m;  // '?', and PREP after a second distinct noun of the sentence (tested first)
+      M += (a.x >> 8) & 0xFFu;
+      const uint32_t vo = lds32(tO_s + ro + (a.x & 0xFFu));
+      const uint32_t vp = lds32(tP_s + rp + (a.y & 0xCu));
+      ro = vo & 0xFFFFu;
+      rp = vp & 0xFFFFu;
+      co += vo >> 16;
+      cp += vp >> 16;
+      const uint32_t nid = a.x >> 16;
+      n2m = (nid != 0xFFFFu && nf != 0xFFFFu && nid != nf) ? 0x10001u : n2m;
+      nf = nf == 0xFFFFu ? nid : nf;
+      const bool end = (a.y & 0x1000u) != 0u;  // sentence end: fresh S-part
+      nf = end ? 0xFFFFu : nf;
+      n2m = end ? 1u : n2m;
       idx += act ? 1u : 0u;
       const bool fin = act && idx == nxt;  // last token of request r: store, fresh context
-      if (fin) gcnt[r] = make_uint4(c1, cq, cop, M);
+      if (fin) gcnt[r] = make_uint4(c1, cq, co | (cp << 16), M);
       const uint32_t keep = fin ? 0u : 1u;
-      c1 *= keep; cq *= keep; cop *= keep; M *= keep;
-      so *= keep; sp *= keep; n2 *= keep;
-      nf = fin ? kNoNoun10 : nf;
+      c1 *= keep; cq *= keep; co *= keep; cp *= keep; M *= keep;
+      ro *= keep; rp *= keep;
+      nf = fin ? 0xFFFFu : nf;
+      n2m = fin ? 1u : n2m;
       j += fin ? 1u : 0u;
       if (fin) { r = Q.ids[j]; nxt = Q.ends[j]; }
     }
@@ -1339,7 +1353,7 @@ __global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work
   uint8_t* tail_mem = smem_raw + ((sizeof(Smem6) + 15) & ~size_t(15));
   uint4* s_keys = reinterpret_cast<uint4*>(tail_mem);
   const uint32_t key_bytes = (a.lex.n_entries + 1u) * 16u;
-  uint16_t* s_slots = reinterpret_cast<uint16_t*>(tail_mem + key_bytes);
+  uint32_t* s_slots = reinterpret_cast<uint32_t*>(tail_mem + key_bytes);
   const uint32_t nslots = 1u << a.lex.bits;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
   {
@@ -1348,8 +1362,24 @@ __global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work
     for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i) | (punct_kind(i) << 24);
     for (uint32_t i = tid; i < kPunct + 8; i += kT4)
       S.fa[i] = fsm_attr6(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
-    for (uint32_t i = tid; i < 16 * 32; i += kT4) S.tO[i] = (uint8_t)o_step(i >> 5, i & 31u);
-    for (uint32_t i = tid; i < 128 * 4; i += kT4) S.tP[i] = (uint8_t)p_step(i >> 2, i & 3u);
+    for (uint32_t i = tid; i < 16 * 32; i += kT4) {
+      const uint32_t v = o_step(i >> 5, i & 31u);
+      S.tO[i] = (v & 15u) * 128u | ((v >> 4) << 16);
+    }
+    for (uint32_t i = tid; i < 128 * 4; i += kT4) {
+      const uint32_t v = p_step(i >> 2, i & 3u);
+      S.tP[i] = (v & 127u) * 16u | ((v >> 7) << 16);
+    }
+    for (uint32_t i = tid; i < 18; i += kT4) {
+      const uint32_t sh = i > 16u ? 0u : 8u * i;
+      S.lmask[i] = make_uint4(__funnelshift_lc(0xFFFFFFFFu, 0u, sh), __funnelshift_lc(0xFFFFFFFFu, 0u, sh > 32u ? sh - 32u : 0u),
+                              __funnelshift_lc(0xFFFFFFFFu, 0u, sh > 64u ? sh - 64u : 0u),
+                              __funnelshift_lc(0xFFFFFFFFu, 0u, sh > 96u ? sh - 96u : 0u));
+    }
+    for (uint32_t i = tid; i < 8; i += kT4) {
+      S.cl3[i] = make_uint2(0xFFFFFFFFu, 0u);
+      S.cl2[i] = make_uint2(0xFFFFFFFFu, 0u);
+    }
   }
   __syncthreads();
   const Lex L{s_keys, s_slots, a.lex.entries, a.lex.bits, a.lex.seed};
@@ -1357,7 +1387,10 @@ __global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work
     const uint32_t cb = clitic_bytes(tid), len = tid < 4 ? 3u : 2u;
     const uint32_t s3 = len == 3 ? (((cb & 0xFFu) << 16) | (cb & 0xFF00u) | ((cb >> 16) & 0xFFu))
                                  : (((cb & 0xFFu) << 8) | ((cb >> 8) & 0xFFu));
-    S.clit[tid] = word_code(L, len, cb, 0u, 0u, 0u, s3);
+    const uint32_t code = word_code(L, len, cb, 0u, 0u, 0u, s3);
+    S.clit[tid] = code;
+    if (len == 3) S.cl3[clitic_hash3(cb)] = make_uint2(cb, code);
+    else S.cl2[clitic_hash2(cb)] = make_uint2(cb, code);
   }
   __syncthreads();
   WarpBuf6& B = S.w[wid];
@@ -1458,7 +1491,7 @@ cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   const uint32_t ntasks = (a.n + 31) / 32;
   uint32_t grid = (uint32_t)a.num_sms;
   if (grid * kW4 > ntasks) grid = (ntasks + kW4 - 1) / kW4;
-  const size_t lex_bytes = (size_t(a.lex.n_entries) + 1) * 16 + (size_t(1) << a.lex.bits) * 2;
+  const size_t lex_bytes = (size_t(a.lex.n_entries) + 1) * 16 + (size_t(1) << a.lex.bits) * 4;
   static const int legacy = [] {
     const char* v = getenv("RTLM_KSCORE");
     return v && v[0] == '4';
