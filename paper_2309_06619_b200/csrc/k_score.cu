@@ -2,19 +2,19 @@
 // scorers) fused with K2 (weighted-rule regression, deadline, priority key,
 // offload class).  §8(a) rows a1-a4.
 //
-// Design (DESIGN.md §7 K1): persistent CTAs of 32 warps; every warp streams
-// the bytes of 32 consecutive requests (a task from a global work counter) in
-// 512-byte chunks: byte classes and word-run starts as bit masks, one lane per
-// token event (run -> clitic split, lemma, lexicon probe), and the six rules
-// as per-token predicates evaluated one token per lane with ballots (see the
-// K1 v4 block).  The epilogue computes u and the key in registers and writes
-// 4 B + 8 B (+ optional 16 B feature row) per request.  The lexicon (<= 1024
-// lemmas) lives in shared memory as an open-addressing table.  All arithmetic
-// that decides an integer is binary32 with explicit round-to-nearest
-// intrinsics (R-FP).  Warps whose offsets decrease use the per-lane byte FSM
-// (Rules::byte), which implements the same rules sequentially.
-#include <cstdlib>
-
+// Design (DESIGN.md §7 K1, kernel k_score6): persistent CTAs of 32 warps.  A
+// warp takes warp tasks of 32 consecutive requests from a global work counter
+// and tokenizes up to 16 of them into a per-warp token buffer (a pool): 512-byte
+// chunks staged in shared memory, byte classes and word-run starts as bit
+// masks, one lane per token event (run -> clitic split, lemma, two-choice
+// lexicon probe).  Then every lane runs the sequential rule machine over a
+// contiguous range of whole requests of the pool, and the epilogue computes u
+// and the key per request and writes 4 B + 8 B (+ optional 16 B feature row).
+// The lexicon (<= 1024 lemmas) lives in shared memory as a fingerprinted
+// two-choice table.  All arithmetic that decides an integer is binary32 with
+// explicit round-to-nearest intrinsics (R-FP).  Tasks with decreasing offsets
+// or more bytes than a pool buffer use the per-lane byte FSM (Rules::byte),
+// which implements the same rules sequentially.
 #include "internal.cuh"
 
 namespace rtlm {
@@ -146,11 +146,7 @@ __device__ __forceinline__ uint32_t word_code(const Lex& L, uint32_t len, uint32
   o1 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 32, 0));
   o2 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 64, 0));
   o3 &= __funnelshift_lc(0xFFFFFFFFu, 0u, (uint32_t)max(sh - 96, 0));
-#ifdef KS_NOLOOKUP
-  return (o0 ^ o1 ^ o2 ^ o3) & 0x3FFu;
-#else
   return lookup(L, o0, o1, o2, o3);
-#endif
 }
 
 // ------------------------------------------------------------ rule FSM
@@ -268,17 +264,6 @@ struct Rules {
     else ++nd;                                    // X: dropped, counted
   }
 
-  static __device__ __forceinline__ void finish_acc(const uint32_t* a9, uint32_t f[8], bool& sat) {
-    unsigned long long Pt = (unsigned long long)a9[5] + (a9[8] > 1 ? a9[8] - 1 : 0);
-    uint64_t raw[8] = {a9[0], a9[1], a9[2], a9[3], a9[4], Pt, a9[6], a9[7]};
-    sat = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      sat |= raw[k] > 65535ull;
-      f[k] = raw[k] > 65535ull ? 65535u : (uint32_t)raw[k];
-    }
-  }
-
   __device__ __forceinline__ void finish(const Lex& L, uint32_t f[8], bool& sat) {
     if (wlen) end_run(L);
     unsigned long long Pt = (unsigned long long)P + (nq > 1 ? nq - 1 : 0);
@@ -332,68 +317,16 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
   }
 }
 
-// ============================================================ K1 v4 (warp streams)
-// One warp owns 32 consecutive requests (taken from a global work counter) and
-// streams their bytes in 512-byte chunks; no CTA-wide barriers.
-//  (1) classify: each lane classifies its 16 staged bytes through a per-lane
-//      replicated class table -> word / punctuation / dropped bit masks;
-//  (2) events: word-run starts (a run never crosses a request start) and
-//      punctuation bytes, compacted in byte order; a run reaching the chunk end
-//      is carried into the next chunk;
-//  (3) tokens: lane per event -- punctuation kind, or the run's clitic split
-//      (R-CLITIC), lemma (R-LEMMA) and lexicon probe -> 1 or 2 tokens written
-//      in order into a small ring;
-//  (4) rules (R-RULES, in the oracle's sentence formulation O2): lane per
-//      token.  Every rule is a predicate on the token, its three predecessors
-//      and "last earlier token with property X" positions (request start,
-//      sentence end, word, first word, noun, first noun, second distinct
-//      noun, punctuation) obtained with ballots, so the counters become
-//      per-token contributions summed per request (segmented warp scan).
-// Warps whose offsets are not non-decreasing use the per-lane byte FSM.
-#ifndef KSCORE_THREADS
-#define KSCORE_THREADS 1024
-#endif
-constexpr uint32_t kT4 = KSCORE_THREADS;      // threads per CTA (32 warps)
+// ============================================================ K1 (shared pieces)
+constexpr uint32_t kT4 = 1024;                // threads per CTA (32 warps)
 constexpr uint32_t kW4 = kT4 / 32;
 constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
-constexpr uint32_t kRing = 1024;              // token ring per warp
-constexpr int32_t kRound = 896;               // tokens buffered before a rule round (+ <= 64 per event batch)
 
-enum : uint32_t { K_W = 1, K_COMMA = 2, K_END = 3, K_Q = 4, K_OTH = 5 };
-
-// Token in the ring (u16): bits 0..10 a code -- 0 a word outside the
+// Token codes (u16 in the per-warp token buffer): 0 a word outside the
 // lexicon, 1..1024 a word with lexicon entry code-1, kPunct + PK_* a
-// punctuation token -- and bits 11..15 the request within the warp task.
-// Smem4::attr maps a code to the entry's attributes (0 for punctuation and
-// for entries without flags or senses).
+// punctuation token.
 enum : uint32_t { PK_COMMA = 1, PK_END = 2, PK_Q = 3, PK_OTH = 4 };
 constexpr uint32_t kPunct = 1024;
-constexpr uint32_t kNoReq = 0xFFFFFFFFu;
-
-// FSM context of the open sentence, carried from one rule round to the next
-struct FsmCtx {
-  uint32_t req, nf, so, sp, n2;  // request, first noun id, O-part state, P-part state, NOUN2
-};
-
-struct __align__(16) WarpBuf {
-  uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
-  uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
-  uint32_t sp[kChunk / 32 + 2];        // run stops: ~wm | mk (words 16, 17: all ones)
-  uint16_t ev[kChunk + 1];             // event: byte in chunk | request << 9 (0xFFFF: carried run)
-  uint32_t rs[32];                     // request starts (absolute byte offsets)
-  uint16_t ring[kRing];                // tokens (code | request << 11)
-  uint32_t ss[kRing / 32];             // sentence starts of a rule round (bit i: token tdone + i)
-  uint32_t acc[32][9];                 // S Y M V O P ntok nd nq
-  FsmCtx cx;
-};
-
-struct Smem4 {
-  uint32_t lut[256];                   // class bits per byte: W 0x1, P 0x100, X 0x10000; punct kind << 24
-  uint32_t clit[8];                    // token codes of the 7 clitics (R-CLITIC), see clitic_kind
-  uint32_t fa[kPunct + 8];             // token code -> machine attributes (fsm_attr)
-  uint8_t tO[16 * 32], tP[128 * 4];    // O-part and P-part transition tables
-  WarpBuf w[kW4];
-};
 
 // request index of absolute byte position pos: last i < cnt with rs[i] <= pos
 __device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uint32_t pos) {
@@ -407,7 +340,7 @@ __device__ __forceinline__ uint32_t req_of(const uint32_t* rs, uint32_t cnt, uin
 // The seven clitics of R-CLITIC in a fixed order: n't 're 've 'll 's 'm 'd.
 // A clitic token's lemma (R-LEMMA: n't -> not; the others are too short or
 // end in no suffix) and so its lexicon code depend only on which clitic it is:
-// the codes are looked up once per CTA (Smem4::clit).
+// the codes are looked up once per CTA (Smem6::clit, Smem6::cl3 / cl2).
 __host__ __device__ __forceinline__ uint32_t clitic_bytes(uint32_t kind) {
   switch (kind) {
     case 0: return 'n' | ('\'' << 8) | ('t' << 16);
@@ -418,37 +351,6 @@ __host__ __device__ __forceinline__ uint32_t clitic_bytes(uint32_t kind) {
     case 5: return '\'' | ('m' << 8);
     default: return '\'' | ('d' << 8);
   }
-}
-
-// Word token(s) of the run of n bytes at stage byte x: one clitic split
-// (R-CLITIC), then the lemma (R-LEMMA) and code of the stem; the clitic's code
-// comes from the per-CTA table; returns the token count.
-__device__ __forceinline__ uint32_t stage_run(const uint32_t* stage, uint32_t x, uint32_t n, const Lex& L,
-                                              const uint32_t* clit, uint32_t& c0, uint32_t& c1) {
-  const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
-  const uint32_t w0 = stage[a0], w1 = stage[a0 + 1], w2 = stage[a0 + 2], w3 = stage[a0 + 3],
-                 w4 = stage[a0 + 4];
-  const uint32_t o0 = __funnelshift_r(w0, w1, sh) | 0x20202020u, o1 = __funnelshift_r(w1, w2, sh) | 0x20202020u;
-  const uint32_t o2 = __funnelshift_r(w2, w3, sh) | 0x20202020u, o3 = __funnelshift_r(w3, w4, sh) | 0x20202020u;
-  const uint32_t tb8 = x + n - 8;  // >= 8
-  const uint32_t ta = tb8 >> 2, tsh = (tb8 & 3u) * 8u;
-  const uint32_t v0 = stage[ta], v1 = stage[ta + 1], v2 = stage[ta + 2];
-  // last 8 bytes, newest first: R = b[n-1] b[n-2] b[n-3] b[n-4] (low to high), R2 = b[n-5] .. b[n-8]
-  // (bytes before the run are garbage; every test below is guarded by the length)
-  const uint32_t R = __byte_perm(__funnelshift_r(v1, v2, tsh), 0, 0x0123) | 0x20202020u;
-  const uint32_t R2 = __byte_perm(__funnelshift_r(v0, v1, tsh), 0, 0x0123) | 0x20202020u;
-  const uint32_t t3 = R & 0xFFFFFFu;
-  const uint32_t l1 = t3 & 0xFFu, l2 = (t3 >> 8) & 0xFFu, l3 = t3 >> 16, lo16 = t3 & 0xFFFFu;
-  const bool c2 = n > 2u && l2 == '\'' && (l1 == 's' || l1 == 'm' || l1 == 'd');
-  const bool nt = l3 == 'n' && l2 == '\'' && l1 == 't';
-  const bool re = lo16 == (('r' << 8) | 'e'), ve = lo16 == (('v' << 8) | 'e'), ll = lo16 == (('l' << 8) | 'l');
-  const bool c3 = n > 3u && (nt || (l3 == '\'' && (re || ve || ll)));
-  const uint32_t cut = c3 ? 3u : (c2 ? 2u : 0u);
-  const uint32_t s3 = __funnelshift_r(R, R2, 8u * cut) & 0xFFFFFFu;  // last three stem bytes
-  c0 = word_code(L, n - cut, o0, o1, o2, o3, s3);
-  const uint32_t kind = c3 ? (nt ? 0u : re ? 1u : ve ? 2u : 3u) : (l1 == 's' ? 4u : l1 == 'm' ? 5u : 6u);
-  c1 = clit[kind];
-  return cut ? 2u : 1u;
 }
 
 // one request by the per-lane byte FSM (fallback path; kept out of line)
@@ -464,61 +366,22 @@ __device__ __noinline__ void fsm_request(const ScoreLaunch& a, const Lex& L, uin
 }
 
 
-// ---- R-RULES as a per-lane finite-state machine over the ring's tokens (O2
-// in the sequential form of Rules::on_word / on_punct).  The machine's
-// context is the same as at a request start at every sentence start (the
-// token after . ! ?, or a request's first token), so a rule round cuts its
-// tokens [tdone, tavail) into 32 runs of whole sentences of about equal length
-// (boundaries at the sentence starts nearest to lane*avail/32); lane 0
-// continues the open sentence of the previous round (carried context B.cx),
-// and the lane that reaches tavail carries its context on.  Counters go to
-// the per-request accumulators at request changes and at the end of a run.
-//
-// The machine is three independent parts (each rule reads only its own
-// part's context):
+// ---- R-RULES as a finite-state machine (O2 in the sequential form of
+// Rules::on_word / on_punct).  The machine's context equals the fresh one at
+// every request start, and the counts are sums per request.  Three
+// independent parts (each rule reads only its own part's context):
 //  * O-part (open-endedness): context SWORD (a word seen in the sentence),
 //    BROAD (last word BROAD), wcd (what-countdown 0..3) -> 16 states; token
 //    class: word with flags {OPENER, WHAT, CAUSE, BROAD} (0..15), '?' (16),
-//    '.' '!' (17), other punctuation (18).  Table Smem4::tO[state*32+class] =
-//    next state | O increment << 4.
+//    '.' '!' (17), other punctuation (18); o_step = next state | O increment << 4.
 //  * P-part (multi-part): context PW, PC, P2W (previous two token kinds),
 //    CPEND (coordinator after a word), WSC (word since the last comma), chain
 //    (0..2) -> 7 bits; token class: word (0), COORD word (1), comma (2), other
-//    punctuation (3).  Table Smem4::tP[state*4+class] = next | P inc << 7.
+//    punctuation (3); p_step = next | P increment << 7.
 //  * S-part (structural): first noun id of the sentence and NOUN2 (a second
 //    distinct noun seen), in registers.
-// Token attributes for the machine (Smem4::fa, by token code):
-//   bit 0 VAGUE, bits 1..10 entry id, bit 11 MULTIPOS, bit 22 '?'   (V, Y, q: packed-count fields)
-//   bits 12..16 O-class, bits 17..18 P-class, bit 19 PREP, bit 20 NOUN, bit 21 END (. ! ?)
-//   bits 24..31 senses - 1
-enum : uint32_t { FA_VAGUE = 1u << 0, FA_MULTI = 1u << 11, FA_Q = 1u << 22, FA_PREP = 1u << 19,
-                  FA_NOUN = 1u << 20, FA_END = 1u << 21 };
 enum : uint32_t { OC_Q = 16, OC_END = 17, OC_PUNCT = 18 };
 enum : uint32_t { PC_WORD = 0, PC_COORD = 1, PC_COMMA = 2, PC_PUNCT = 3 };
-constexpr uint32_t kNoNoun10 = 0xFFFFu;
-
-__host__ __device__ __forceinline__ uint32_t fsm_attr(uint32_t code, uint32_t at) {
-  if (code > kPunct) {
-    const uint32_t pk = code - kPunct;
-    if (pk == PK_COMMA) return (OC_PUNCT << 12) | (PC_COMMA << 17);
-    if (pk == PK_END) return (OC_END << 12) | (PC_PUNCT << 17) | FA_END;
-    if (pk == PK_Q) return (OC_Q << 12) | (PC_PUNCT << 17) | FA_END | FA_Q;
-    return (OC_PUNCT << 12) | (PC_PUNCT << 17);
-  }
-  if (code == 0u) return (0u << 12) | (PC_WORD << 17);
-  uint32_t f = 0;
-  f |= (at & A_VAGUE) ? FA_VAGUE : 0u;
-  f |= (at & A_MULTIPOS) ? FA_MULTI : 0u;
-  f |= (at & A_PREP) ? FA_PREP : 0u;
-  f |= (at & A_NOUN) ? FA_NOUN : 0u;
-  const uint32_t oc = ((at & A_OPENER) ? 1u : 0u) | ((at & A_WHAT) ? 2u : 0u) | ((at & A_CAUSE) ? 4u : 0u) |
-                      ((at & A_BROAD) ? 8u : 0u);
-  f |= oc << 12;
-  f |= ((at & A_COORD) ? PC_COORD : PC_WORD) << 17;
-  f |= ((at >> A_ID_SHIFT) & 0x3FFu) << 1;
-  f |= ((at >> A_SEM_SHIFT) & A_SEM_MASK) << 24;
-  return f;
-}
 
 // O-part transition (Rules::on_word / on_punct restricted to SENT_WORD, LAST_BROAD, what_cd)
 __host__ __device__ __forceinline__ uint32_t o_step(uint32_t st, uint32_t cls) {
@@ -550,407 +413,26 @@ __host__ __device__ __forceinline__ uint32_t p_step(uint32_t st, uint32_t cls) {
   return (pw << 2) | (wsc << 4);
 }
 
-__device__ __forceinline__ bool tok_is_end(uint32_t t) {  // . ! or ?
-  return ((t & 0x7FFu) - (kPunct + PK_END)) < 2u;
-}
-
-// packed counts of one request within one run (<= 959 tokens): c1 = V | Y << 11 | q << 22,
-// c2 = S | O << 11 | P << 22, M, and ntok = tokens since the run / request start
-__device__ __forceinline__ void flush_counts(uint32_t* a, uint32_t c1, uint32_t c2, uint32_t M, uint32_t n) {
-  atomicAdd(&a[0], c2 & 0x7FFu);
-  atomicAdd(&a[1], (c1 >> 11) & 0x7FFu);
-  const uint32_t old = atomicAdd(&a[2], M);     // M < 2^18 per run
-  if (old + M >= 0x40000000u) atomicMin(&a[2], 0x40000000u);  // stays < 2^31; saturates to 65535 later
-  atomicAdd(&a[3], c1 & 0x7FFu);
-  atomicAdd(&a[4], (c2 >> 11) & 0x7FFu);
-  atomicAdd(&a[5], c2 >> 22);
-  atomicAdd(&a[6], n);
-  atomicAdd(&a[8], c1 >> 22);
-}
-
-__device__ __forceinline__ void rules_round(WarpBuf& B, const uint32_t* fa_of, const uint8_t* tO, const uint8_t* tP,
-                                            int32_t tdone, int32_t tavail, uint32_t lane) {
-  const int32_t avail = tavail - tdone;
-  if (avail <= 0) return;
-  // sentence starts of the round as a bit mask
-  const int32_t nw = (avail + 31) >> 5;
-  for (int32_t j = 0; j < nw; ++j) {
-    const int32_t T = tdone + j * 32 + (int32_t)lane;
-    bool st = false;
-    if (T < tavail) {
-      if (T == 0) {
-        st = true;
-      } else {
-        const uint32_t t = B.ring[T & (kRing - 1)], pv = B.ring[(T - 1) & (kRing - 1)];
-        st = ((t ^ pv) >> 11) != 0u || tok_is_end(pv);
-      }
-    }
-    const uint32_t b = __ballot_sync(0xFFFFFFFFu, st);
-    if (lane == 0) B.ss[j] = b;
-  }
-  __syncwarp();
-  // this lane's run [s, e): from the sentence start nearest to lane*avail/32
-  int32_t s = 0;
-  if (lane) {
-    const int32_t nom = (int32_t)(((uint32_t)avail * lane) >> 5);
-    int32_t w = nom >> 5;
-    uint32_t m = B.ss[w] & (0xFFFFFFFFu << (nom & 31));
-    while (!m && ++w < nw) m = B.ss[w];
-    const int32_t up = m ? w * 32 + (int32_t)__ffs(m) - 1 : avail;      // first start >= nom
-    w = nom >> 5;
-    m = B.ss[w] & (0xFFFFFFFFu >> (31 - (nom & 31)));
-    while (!m && --w >= 0) m = B.ss[w];
-    const int32_t dn = m ? w * 32 + 31 - (int32_t)__clz(m) : -1;      // last start <= nom
-    s = (dn >= 0 && nom - dn < up - nom) ? dn : up;
-  }
-  int32_t e = __shfl_down_sync(0xFFFFFFFFu, s, 1);
-  if (lane == 31) e = avail;
-  FsmCtx c;
-  if (lane == 0) c = B.cx;
-  else c = FsmCtx{kNoReq, kNoNoun10, 0u, 0u, 0u};
-  uint32_t c1 = 0, c2 = 0, M = 0;
-  int32_t i0 = s;  // first token of the current request in this run
-  for (int32_t i = s; i < e; ++i) {
-    const uint32_t t = B.ring[(tdone + i) & (kRing - 1)];
-    const uint32_t r = t >> 11;
-    if (r != c.req) {  // request start: flush, fresh context
-      if (c.req != kNoReq) flush_counts(B.acc[c.req], c1, c2, M, (uint32_t)(i - i0));
-      c1 = c2 = M = 0;
-      i0 = i;
-      c = FsmCtx{r, kNoNoun10, 0u, 0u, 0u};
-    }
-    const uint32_t a = fa_of[t & 0x7FFu];
-    c1 += a & (FA_VAGUE | FA_MULTI | FA_Q);
-    M += a >> 24;
-    const uint32_t vo = tO[(c.so << 5) | ((a >> 12) & 31u)];
-    const uint32_t vp = tP[(c.sp << 2) | ((a >> 17) & 3u)];
-    c.so = vo & 15u;
-    c.sp = vp & 127u;
-    // S-part: PREP after a second distinct noun of the sentence (PREP tested first)
-    const uint32_t sinc = (a >> 19) & c.n2;
-    {
-      const uint32_t id = (a >> 1) & 0x3FFu;
-      const bool noun = (a & FA_NOUN) != 0u, first = noun && c.nf == kNoNoun10;
-      c.n2 |= (noun && !first && id != c.nf) ? 1u : 0u;
-      c.nf = first ? id : c.nf;
-      const bool end = (a & FA_END) != 0u;  // sentence end: fresh S-part
-      c.nf = end ? kNoNoun10 : c.nf;
-      c.n2 = end ? 0u : c.n2;
-    }
-    c2 += sinc | ((vo >> 4) << 11) | ((vp >> 7) << 22);
-  }
-  if (s < e) {
-    flush_counts(B.acc[c.req], c1, c2, M, (uint32_t)(e - i0));
-    if (e == avail) B.cx = c;
-  }
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(kT4, 1) k_score4(ScoreLaunch a, uint32_t* work) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  Smem4& S = *reinterpret_cast<Smem4*>(smem_raw);
-  uint8_t* tail_mem = smem_raw + ((sizeof(Smem4) + 15) & ~size_t(15));
-  uint4* s_keys = reinterpret_cast<uint4*>(tail_mem);
-  const uint32_t key_bytes = (a.lex.n_entries + 1u) * 16u;
-  uint32_t* s_slots = reinterpret_cast<uint32_t*>(tail_mem + key_bytes);
-  const uint32_t nslots = 1u << a.lex.bits;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
-  {
-    for (uint32_t i = tid; i <= a.lex.n_entries; i += kT4) s_keys[i] = a.lex.keys[i];
-    for (uint32_t i = tid; i < nslots; i += kT4) s_slots[i] = a.lex.slots[i];
-    for (uint32_t i = tid; i < 256; i += kT4) S.lut[i] = class_bits(i) | (punct_kind(i) << 24);
-    for (uint32_t i = tid; i < kPunct + 8; i += kT4)
-      S.fa[i] = fsm_attr(i, (i >= 1u && i <= a.lex.n_entries) ? a.lex.entries[i - 1].attr : 0u);
-    for (uint32_t i = tid; i < 16 * 32; i += kT4) S.tO[i] = (uint8_t)o_step(i >> 5, i & 31u);
-    for (uint32_t i = tid; i < 128 * 4; i += kT4) S.tP[i] = (uint8_t)p_step(i >> 2, i & 3u);
-  }
-  __syncthreads();
-  const Lex L{s_keys, s_slots, a.lex.entries, a.lex.bits, a.lex.seed};
-  if (tid < 7) {
-    const uint32_t cb = clitic_bytes(tid), len = tid < 4 ? 3u : 2u;
-    const uint32_t s3 = len == 3 ? (((cb & 0xFFu) << 16) | (cb & 0xFF00u) | ((cb >> 16) & 0xFFu))
-                                 : (((cb & 0xFFu) << 8) | ((cb >> 8) & 0xFFu));
-    S.clit[tid] = word_code(L, len, cb, 0u, 0u, 0u, s3);
-  }
-  __syncthreads();
-  WarpBuf& B = S.w[wid];
-  const uint32_t total_bytes = a.n ? a.offsets[a.n] : 0u;
-  const uint32_t ntasks = (a.n + 31) / 32;
-  const uint8_t* st8 = reinterpret_cast<const uint8_t*>(B.stage);
-  if (lane < 4) B.stage[lane] = 0;
-
-  for (;;) {
-    uint32_t task = 0;
-    if (lane == 0) task = atomicAdd(work, 1u);
-    task = __shfl_sync(0xFFFFFFFFu, task, 0);
-    if (task >= ntasks) break;
-    const uint32_t r0 = task * 32, rcnt = min(32u, a.n - r0);
-    const uint32_t r = r0 + lane;
-    const bool rv = lane < rcnt;
-    const uint32_t s_r = rv ? a.offsets[r] : 0u;
-    const uint32_t e_r = rv ? a.offsets[r + 1] : 0u;
-    const bool bad = rv && e_r < s_r;
-    if (__any_sync(0xFFFFFFFFu, bad)) {
-      // offsets not non-decreasing: per-lane byte FSM (requests with e < s are empty)
-      if (bad) atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
-      if (rv) fsm_request(a, L, r, s_r, bad ? s_r : e_r);
-      continue;
-    }
-    // request of a byte = (# request starts at or before it) - 1; a popcount of the
-    // start marks when no two requests start at the same byte (no empty request
-    // in the middle), else a search of the starts
-    const uint32_t s_prev = __shfl_up_sync(0xFFFFFFFFu, s_r, 1);
-    const bool uniq_starts = !__any_sync(0xFFFFFFFFu, rv && lane > 0 && s_r == s_prev);
-    const uint32_t B0 = __shfl_sync(0xFFFFFFFFu, s_r, 0);
-    const uint32_t B1 = __shfl_sync(0xFFFFFFFFu, e_r, rcnt - 1);
-    B.rs[lane] = s_r;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) B.acc[lane][k] = 0;
-    if (lane == 0) B.cx = FsmCtx{kNoReq, kNoNoun10, 0u, 0u, 0u};
-    int32_t tokbase = 0;
-    uint32_t prevW = 0;                 // W bit of the byte before the chunk
-    int32_t pend_start = -1;            // absolute start of a run carried from earlier chunks
-    uint32_t pend_rq = 0;               // its request (within the task)
-    const uint32_t base = B0 & ~15u;
-    uint4 qprev = make_uint4(0, 0, 0, 0);
-    int32_t tokdone = 0;                // tokens already through the rules
-    __syncwarp();
-    for (uint32_t cb = base; cb < B1; cb += kChunk) {
-      // ---- (1) stage + classify 16 bytes per lane
-      const uint32_t g = cb + lane * 16u;
-      uint4 q;
-      if (g + 16u <= total_bytes) q = ld_nc_v4(a.bytes + g);
-      else {
-        uint32_t w4[4] = {0, 0, 0, 0};
-        for (uint32_t j = 0; j < 16u; ++j)
-          if (g + j < total_bytes) w4[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
-        q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-      }
-      *reinterpret_cast<uint4*>(&B.stage[4 + lane * 4]) = qprev;
-      *reinterpret_cast<uint4*>(&B.stage[4 + kChunk / 4 + lane * 4]) = q;
-      qprev = q;
-      if (lane < kChunk / 32 + 1) B.mk[lane] = 0;
-      __syncwarp();
-      if (rv && s_r >= cb && s_r < cb + kChunk && s_r < B1)
-        atomicOr(&B.mk[(s_r - cb) >> 5], 1u << ((s_r - cb) & 31u));
-      uint32_t accA = 0, accB = 0;
-      {
-        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t byte = (wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu;
-            const uint32_t c = S.lut[byte] << i;
-            if (j == 0) accA += c; else accB += c;
-          }
-      }
-      // in-range bytes of this lane: [B0, B1)
-      uint32_t vmask = 0xFFFFu;
-      if (g < B0) vmask &= B0 - g >= 16u ? 0u : (0xFFFFu << (B0 - g)) & 0xFFFFu;
-      if (g + 16u > B1) vmask &= B1 <= g ? 0u : (0xFFFFu >> (g + 16u - B1));
-      const uint32_t W16 = ((accA & 0xFFu) | ((accB & 0xFFu) << 8)) & vmask;
-      const uint32_t P16 = (((accA >> 8) & 0xFFu) | (((accB >> 8) & 0xFFu) << 8)) & vmask;
-      const uint32_t X16 = (((accA >> 16) & 0xFFu) | (((accB >> 16) & 0xFFu) << 8)) & vmask;
-      const uint32_t Wn = __shfl_down_sync(0xFFFFFFFFu, W16, 1);
-      if (!(lane & 1u)) B.wm[lane >> 1] = W16 | (Wn << 16);
-      if (lane == 0) B.wm[kChunk / 32] = 0;
-      __syncwarp();
-      // ---- (2) events
-      if (lane < kChunk / 32 + 2) B.sp[lane] = lane < kChunk / 32 ? (~B.wm[lane] | B.mk[lane]) : 0xFFFFFFFFu;
-      const uint32_t mk16 = (B.mk[lane >> 1] >> (16u * (lane & 1u))) & 0xFFFFu;
-      const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W16, 1);
-      const uint32_t pw = lane ? (Wp >> 15) & 1u : prevW;
-      uint32_t R16 = (W16 & ~((W16 << 1) | pw)) | (W16 & mk16);
-      // a run reaching the chunk end continues in the next chunk
-      const bool last_chunk = cb + kChunk >= B1;
-      const bool defer = !last_chunk && ((__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u);
-      const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R16 != 0u);
-      bool pend_here = false;  // the carried run ends in this chunk
-      int32_t new_pend = -1;
-      uint32_t new_pend_rq = 0;
-      if (defer) {
-        if (b_r) {
-          const uint32_t L2 = 31 - __clz(b_r);
-          const uint32_t top = __shfl_sync(0xFFFFFFFFu, R16, L2);
-          const uint32_t bit = 31 - __clz(top);
-          new_pend = (int32_t)(cb + L2 * 16u + bit);
-          new_pend_rq = __popc(__ballot_sync(0xFFFFFFFFu, rv && s_r <= (uint32_t)new_pend)) - 1u;
-          if (lane == L2) R16 &= ~(1u << bit);
-          pend_here = pend_start >= 0;
-        }  // else: the carried run spans the whole chunk
-      } else {
-        pend_here = pend_start >= 0;
-      }
-      const uint32_t E16 = R16 | P16;
-      const uint32_t cnt = __popc(E16);
-      // one scan for the event count (low half) and the request-start count (high half)
-      const uint32_t cm = cnt | ((uint32_t)__popc(mk16) << 16);
-      uint32_t incl = cm;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= (uint32_t)o) incl += t;
-      }
-      const uint32_t ph = pend_here ? 1u : 0u;
-      const uint32_t nev = (__shfl_sync(0xFFFFFFFFu, incl, 31) & 0xFFFFu) + ph;
-      const uint32_t base_rq = __popc(__ballot_sync(0xFFFFFFFFu, rv && s_r < cb));  // requests started earlier
-      if (E16) {
-        uint32_t k = ((incl - cm) & 0xFFFFu) + ph;
-        uint32_t e = E16;
-        if (uniq_starts) {
-          const uint32_t rq0 = base_rq + ((incl - cm) >> 16) - 1u;  // + starts in this lane up to the byte
-          while (e) {
-            const uint32_t bit = __ffs(e) - 1;
-            e &= e - 1u;
-            B.ev[k++] = (uint16_t)((lane * 16u + bit) | ((rq0 + __popc(mk16 & ((2u << bit) - 1u))) << 9));
-          }
-        } else {
-          uint32_t rq = req_of(B.rs, rcnt, g);  // request at this lane's first byte, advanced per event
-          while (e) {
-            const uint32_t bit = __ffs(e) - 1;
-            e &= e - 1u;
-            while (rq + 1 < rcnt && B.rs[rq + 1] <= g + bit) ++rq;
-            B.ev[k++] = (uint16_t)((lane * 16u + bit) | (rq << 9));
-          }
-        }
-      }
-      if (lane == 0 && ph) B.ev[0] = 0xFFFFu;
-      __syncwarp();
-      // ---- (3) tokens, 32 events at a time, then (4) rules
-      // (at least one pass, so that the last chunk always flushes the rules)
-      for (uint32_t e0 = 0; e0 < max(nev, 1u); e0 += 32) {
-        const uint32_t k = e0 + lane;
-        uint32_t ntk = 0, at0 = 0, at1 = 0, kind = K_W, rq = 0;
-        if (k < nev) {
-          const uint32_t pe = B.ev[k];
-          uint32_t x = 0, n = 0;
-          bool isrun = false;
-          if (pe == 0xFFFFu) {
-            // carried run: [pend_start, stop) with stop the first non-word byte or request start here
-            const uint32_t ps = (uint32_t)pend_start;
-            uint32_t stop = 0;
-            for (uint32_t w = 0;; ++w) {
-              const uint32_t sm = B.sp[w];
-              if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
-            }
-            n = cb + stop - ps;
-            rq = pend_rq;
-            isrun = true;
-            if (ps + kChunk >= cb) {
-              x = 16 + kChunk + ps - cb;
-            } else {
-              // longer than a chunk (> 512 bytes): its tokens depend only on its last
-              // 6 bytes (any stem is > 16 bytes, no lemma) -> stage them as a 24-byte run
-              const uint32_t pad = 16 + 2 * kChunk + 8;  // in the stage's tail padding
-              uint8_t* st = reinterpret_cast<uint8_t*>(B.stage);
-              for (uint32_t j = 0; j < 8u; ++j) st[pad + j] = __ldg(a.bytes + ps + n - 8 + j);
-              x = pad + 8 - 24;
-              n = 24;
-            }
-          } else {
-            const uint32_t p = pe & 511u;
-            const uint32_t c = st8[16 + kChunk + p];
-            rq = pe >> 9;
-            if ((B.wm[p >> 5] >> (p & 31u)) & 1u) {
-              // run length: up to the first non-word byte or request start (two stop
-              // words cover runs of <= 32 bytes; sp[16], sp[17] stop at the chunk end)
-              const uint32_t qq = p + 1, qw = qq >> 5, qb = qq & 31u;
-              const uint64_t st2 = ((uint64_t)B.sp[qw] | ((uint64_t)B.sp[qw + 1] << 32)) >> qb;
-              if (st2) {
-                n = (uint32_t)__ffsll((long long)st2);
-              } else {
-                n = 65u - qb;
-                for (uint32_t w = qw + 2;; ++w) {
-                  const uint32_t stop = B.sp[w];
-                  if (stop) { n += __ffs(stop) - 1; break; }
-                  n += 32u;
-                }
-              }
-              x = 16 + kChunk + p;
-              isrun = true;
-            } else {
-              ntk = 1;
-              kind = S.lut[c] >> 24;
-            }
-          }
-#ifdef KS_NOPROBE
-          if (isrun) { ntk = 1; at0 = x; }
-#else
-          if (isrun) ntk = stage_run(B.stage, x, n, L, S.clit, at0, at1);
-#endif
-        }
-        // token positions: ntk is 0, 1 or 2 (a clitic split), so two ballots replace a scan
-        const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, ntk != 0u), b2 = __ballot_sync(0xFFFFFFFFu, ntk == 2u);
-        const uint32_t ltm = (1u << lane) - 1u;
-        const uint32_t nt = __popc(b1) + __popc(b2);
-        if (ntk) {
-          const uint32_t t0 = (uint32_t)tokbase + __popc(b1 & ltm) + __popc(b2 & ltm);
-          B.ring[t0 & (kRing - 1)] = (uint16_t)((kind == K_W ? at0 : kPunct + kind - 1u) | (rq << 11));
-          if (ntk == 2) B.ring[(t0 + 1) & (kRing - 1)] = (uint16_t)(at1 | (rq << 11));
-        }
-        __syncwarp();
-        tokbase += (int32_t)nt;
-        // a rule round every kRound tokens, and after the last event of the task
-        if ((last_chunk && e0 + 32 >= nev) || tokbase - tokdone >= kRound) {
-#ifndef KS_NORULES  // KS_NORULES / KS_NOPROBE: ablation builds for profiling only (wrong results)
-          rules_round(B, S.fa, S.tO, S.tP, tokdone, tokbase, lane);
-#endif
-          tokdone = tokbase;
-        }
-      }
-      // dropped bytes (rare): count per request
-      if (__any_sync(0xFFFFFFFFu, X16 != 0u)) {
-        uint32_t xm = X16;
-        while (xm) {
-          const uint32_t bit = __ffs(xm) - 1;
-          xm &= xm - 1u;
-          atomicAdd(&B.acc[req_of(B.rs, rcnt, g + bit)][7], 1u);
-        }
-      }
-      if (pend_here) pend_start = -1;
-      if (defer && b_r) {
-        pend_start = new_pend;
-        pend_rq = new_pend_rq;
-      }
-      prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
-      __syncwarp();
-    }
-    // ---- epilogue: lane = request
-    if (rv) {
-      const uint32_t* ac = B.acc[lane];
-      uint32_t a9[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) a9[k] = ac[k];
-      uint32_t f[8];
-      bool sat;
-      Rules::finish_acc(a9, f, sat);
-      if (sat) atomicOr(a.flags, RT_FLAG_SATURATED);
-      epilogue(a, r, f);
-    }
-    __syncwarp();
-  }
-}
-
 // ============================================================ K1 v6 (round 2): pools of tasks
 // Two phases per warp, both with (almost) every lane busy:
 //  (A) tokenize: up to kPoolTasks warp tasks (32 requests each) are streamed
-//      exactly as in k_score4 (classify, events, one lane per event), but a
-//      token's code goes to a per-warp token buffer in global memory (u16,
-//      kTokCap tokens; the pool's tokens are contiguous there) instead of a
-//      shared-memory ring, and each request's first token index is recorded.
-//      Runs without an apostrophe in their last three bytes (no clitic split
-//      possible, R-CLITIC) take a short path: the lemma (R-LEMMA) from the last
-//      four bytes and the length, then the two-choice probe; runs with one
-//      take stage_run (the exact clitic split) under a warp-uniform branch.
-//  (B) rules: the pool's requests are cut into 32 contiguous ranges of about
-//      equal token count (request granularity, so no request is shared by two
-//      lanes); every lane runs the sequential R-RULES machine of rules_round
-//      over its tokens, one token per iteration, reading them from the global
-//      buffer (L1/L2-resident: written a few microseconds earlier by the same
+//      (classify, events, one lane per event); a token's code goes to a
+//      per-warp token buffer in global memory (u16, kTokCap tokens; the pool's
+//      tokens are contiguous there) and each request's first token index is
+//      recorded.  The event path is branch-free: the clitic split (R-CLITIC)
+//      by perfect hashes of the run's last three / two bytes, the lemma
+//      (R-LEMMA) from the stem's last four bytes and its length, masks from a
+//      table, then the fingerprinted two-choice probe; punctuation lanes run
+//      the same instructions and keep their punctuation code.
+//  (B) rules: the pool's requests with tokens are cut into 32 contiguous
+//      ranges of about equal token count (request granularity, so no request
+//      is shared by two lanes); every lane runs the sequential R-RULES
+//      machine over its tokens, one token per step, reading them from the
+//      global buffer (L1/L2-resident: written microseconds earlier by the same
 //      warp).  A request's counts live in registers until its last token
 //      (16-bit fields: a pool holds <= kTokCap < 2^16 tokens) and then go to
-//      shared memory; the epilogue (u, key) runs lane-parallel per pool.
+//      its 16-byte record in the warp's scratch; the epilogue (u, key) runs
+//      lane-parallel per pool.
 // Tasks whose bytes exceed kTokCap (tokens <= bytes) and tasks with decreasing
 // offsets use the per-lane byte FSM.
 constexpr uint32_t kPoolTasks = 16;
@@ -959,7 +441,6 @@ constexpr uint32_t kTokCap = 16384;   // tokens per warp buffer
 constexpr uint32_t kTokPad = 64;      // read-ahead slack
 // per-warp global scratch: kTokCap + kTokPad tokens, then kPoolReq count records (16 B)
 constexpr size_t kWarpScratch = (kTokCap + kTokPad) * 2 + kPoolReq * 16;
-constexpr uint32_t kNoTok = 0xFFFFu;
 
 // Token attributes for the v6 machine (Smem6::fa by token code), two words
 // so that every field is one or two instructions away:
@@ -1027,11 +508,6 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
   uint2 v;
   asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-  uint4 v;
-  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
 
@@ -1492,21 +968,11 @@ cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   uint32_t grid = (uint32_t)a.num_sms;
   if (grid * kW4 > ntasks) grid = (ntasks + kW4 - 1) / kW4;
   const size_t lex_bytes = (size_t(a.lex.n_entries) + 1) * 16 + (size_t(1) << a.lex.bits) * 4;
-  static const int legacy = [] {
-    const char* v = getenv("RTLM_KSCORE");
-    return v && v[0] == '4';
-  }();
-  if (legacy || !a.tokbuf) {
-    const size_t smem = ((sizeof(Smem4) + 15) & ~size_t(15)) + lex_bytes;
-    e = cudaFuncSetAttribute(k_score4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_score4<<<grid, kT4, smem, s>>>(a, a.work);
-  } else {
-    const size_t smem = ((sizeof(Smem6) + 15) & ~size_t(15)) + lex_bytes;
-    e = cudaFuncSetAttribute(k_score6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_score6<<<grid, kT4, smem, s>>>(a, a.work, a.tokbuf);
-  }
+  if (!a.tokbuf) return cudaErrorInvalidValue;
+  const size_t smem = ((sizeof(Smem6) + 15) & ~size_t(15)) + lex_bytes;
+  e = cudaFuncSetAttribute(k_score6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_score6<<<grid, kT4, smem, s>>>(a, a.work, a.tokbuf);
   note_launch();
   return cudaGetLastError();
 }
