@@ -320,7 +320,8 @@ __device__ __forceinline__ void epilogue(const ScoreLaunch& a, uint32_t r, const
 // ============================================================ K1 (shared pieces)
 constexpr uint32_t kT4 = 1024;                // threads per CTA (32 warps)
 constexpr uint32_t kW4 = kT4 / 32;
-constexpr uint32_t kChunk = 512;              // bytes per warp chunk (16 per lane)
+constexpr uint32_t kChunk = 1024;             // bytes per warp chunk (32 per lane)
+constexpr uint32_t kCB = 64;                  // stage byte of the chunk's first byte (32 B pad, previous chunk's last 32 B)
 
 // Token codes (u16 in the per-warp token buffer): 0 a word outside the
 // lexicon, 1..1024 a word with lexicon entry code-1, kPunct + PK_* a
@@ -435,7 +436,7 @@ __host__ __device__ __forceinline__ uint32_t p_step(uint32_t st, uint32_t cls) {
 //      lane-parallel per pool.
 // Tasks whose bytes exceed kTokCap (tokens <= bytes) and tasks with decreasing
 // offsets use the per-lane byte FSM.
-constexpr uint32_t kPoolTasks = 16;
+constexpr uint32_t kPoolTasks = 8;
 constexpr uint32_t kPoolReq = kPoolTasks * 32;
 constexpr uint32_t kTokCap = 16384;   // tokens per warp buffer
 constexpr uint32_t kTokPad = 64;      // read-ahead slack
@@ -469,8 +470,8 @@ __host__ __device__ __forceinline__ uint2 fsm_attr6(uint32_t code, uint32_t at) 
 struct __align__(16) WarpBuf6 {
   union {
     struct {
-      uint32_t stage[4 + 2 * kChunk / 4 + 8];  // 16 B pad | previous chunk | chunk | 32 B pad
-      uint32_t wm[kChunk / 32 + 1], mk[kChunk / 32 + 1];
+      uint32_t stage[(kCB + kChunk + 32) / 4 + 4];  // 32 B pad | previous chunk's last 32 B | chunk | pad
+      uint32_t mk[kChunk / 32 + 1];
       uint32_t sp[kChunk / 32 + 2];
       uint32_t rs[32];
       uint16_t ev[kChunk + 2];
@@ -531,69 +532,73 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
   uint32_t prevW = 0;
   int32_t pend_start = -1;
   const uint32_t base = B0 & ~15u;
-  uint4 qprev = make_uint4(0, 0, 0, 0);
-  if (lane < 4) T.stage[lane] = 0;
+  uint4 qa = make_uint4(0, 0, 0, 0), qb = qa;  // this lane's 32 bytes of the current chunk
+  if (lane < 8) T.stage[lane] = 0;
   __syncwarp();
   for (uint32_t cb = base; cb < B1; cb += kChunk) {
-    // ---- (1) stage + classify 16 bytes per lane
-    const uint32_t g = cb + lane * 16u;
-    uint4 q;
-    if (g + 16u <= total_bytes) q = ld_nc_v4(a.bytes + g);
-    else {
-      uint32_t w4[4] = {0, 0, 0, 0};
-      for (uint32_t j = 0; j < 16u; ++j)
-        if (g + j < total_bytes) w4[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
-      q = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    // ---- (1) stage + classify 32 bytes per lane (the previous chunk keeps its
+    // last 32 bytes at stage bytes 32..63, where a carried run's bytes are)
+    if (lane == 31) {
+      *reinterpret_cast<uint4*>(&T.stage[8]) = qa;
+      *reinterpret_cast<uint4*>(&T.stage[12]) = qb;
     }
-    *reinterpret_cast<uint4*>(&T.stage[4 + lane * 4]) = qprev;
-    *reinterpret_cast<uint4*>(&T.stage[4 + kChunk / 4 + lane * 4]) = q;
-    qprev = q;
-    if (lane < kChunk / 32 + 1) T.mk[lane] = 0;
+    const uint32_t g = cb + lane * 32u;
+    if (g + 32u <= total_bytes) {
+      qa = ld_nc_v4(a.bytes + g);
+      qb = ld_nc_v4(a.bytes + g + 16u);
+    } else {
+      uint32_t w8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t j = 0; j < 32u; ++j)
+        if (g + j < total_bytes) w8[j >> 2] |= (uint32_t)a.bytes[g + j] << (8 * (j & 3u));
+      qa = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+      qb = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+    }
+    __syncwarp();
+    *reinterpret_cast<uint4*>(&T.stage[kCB / 4 + lane * 8]) = qa;
+    *reinterpret_cast<uint4*>(&T.stage[kCB / 4 + lane * 8 + 4]) = qb;
+    T.mk[lane] = 0;
+    if (lane == 0) T.mk[32] = 0;
     __syncwarp();
     const bool here = rv && s_r >= cb && s_r < cb + kChunk;  // this lane's request starts in the chunk
     if (here && s_r < B1) atomicOr(&T.mk[(s_r - cb) >> 5], 1u << ((s_r - cb) & 31u));
-    uint32_t accA = 0, accB = 0;
+    uint32_t acc[4] = {0, 0, 0, 0};
     {
-      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+      const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t byte = (wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu;
-          const uint32_t c = S.lut[byte] << i;
-          if (j == 0) accA += c; else accB += c;
-        }
+        for (int i = 0; i < 8; ++i) acc[j] += S.lut[(wv[j * 2 + (i >> 2)] >> (8 * (i & 3))) & 0xFFu] << i;
     }
-    uint32_t vmask = 0xFFFFu;
-    if (g < B0) vmask &= B0 - g >= 16u ? 0u : (0xFFFFu << (B0 - g)) & 0xFFFFu;
-    if (g + 16u > B1) vmask &= B1 <= g ? 0u : (0xFFFFu >> (g + 16u - B1));
-    const uint32_t W16 = ((accA & 0xFFu) | ((accB & 0xFFu) << 8)) & vmask;
-    const uint32_t P16 = (((accA >> 8) & 0xFFu) | (((accB >> 8) & 0xFFu) << 8)) & vmask;
-    const uint32_t X16 = (((accA >> 16) & 0xFFu) | (((accB >> 16) & 0xFFu) << 8)) & vmask;
-    const uint32_t Wn = __shfl_down_sync(0xFFFFFFFFu, W16, 1);
-    if (!(lane & 1u)) T.wm[lane >> 1] = W16 | (Wn << 16);
-    if (lane == 0) T.wm[kChunk / 32] = 0;
+    uint32_t vmask = 0xFFFFFFFFu;
+    if (g < B0) vmask &= B0 - g >= 32u ? 0u : (0xFFFFFFFFu << (B0 - g));
+    if (g + 32u > B1) vmask &= B1 <= g ? 0u : (0xFFFFFFFFu >> (g + 32u - B1));
+    const uint32_t W32 = ((acc[0] & 0xFFu) | ((acc[1] & 0xFFu) << 8) | ((acc[2] & 0xFFu) << 16) | (acc[3] << 24)) & vmask;
+    const uint32_t P32 = (((acc[0] >> 8) & 0xFFu) | (acc[1] & 0xFF00u) | ((acc[2] & 0xFF00u) << 8) |
+                          ((acc[3] & 0xFF00u) << 16)) & vmask;
+    const uint32_t X32 = (((acc[0] >> 16) & 0xFFu) | ((acc[1] >> 8) & 0xFF00u) | (acc[2] & 0xFF0000u) |
+                          ((acc[3] & 0xFF0000u) << 8)) & vmask;
     __syncwarp();
     // ---- (2) events: run starts and punctuation bytes, in byte order
-    if (lane < kChunk / 32 + 2) T.sp[lane] = lane < kChunk / 32 ? (~T.wm[lane] | T.mk[lane]) : 0xFFFFFFFFu;
-    const uint32_t mk16 = (T.mk[lane >> 1] >> (16u * (lane & 1u))) & 0xFFFFu;
-    const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W16, 1);
-    const uint32_t pw = lane ? (Wp >> 15) & 1u : prevW;
-    uint32_t R16 = (W16 & ~((W16 << 1) | pw)) | (W16 & mk16);
+    const uint32_t mk32 = T.mk[lane];
+    T.sp[lane] = ~W32 | mk32;  // run stops: a non-word byte or a request start
+    if (lane < 2) T.sp[32 + lane] = 0xFFFFFFFFu;
+    const uint32_t Wp = __shfl_up_sync(0xFFFFFFFFu, W32, 1);
+    const uint32_t pw = lane ? (Wp >> 31) : prevW;
+    uint32_t R32 = (W32 & ~((W32 << 1) | pw)) | (W32 & mk32);
     const bool last_chunk = cb + kChunk >= B1;
-    const bool defer = !last_chunk && ((__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u);
-    const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R16 != 0u);
+    const bool defer = !last_chunk && (__shfl_sync(0xFFFFFFFFu, W32, 31) >> 31);
+    const uint32_t b_r = __ballot_sync(0xFFFFFFFFu, R32 != 0u);
     const bool pend_here = pend_start >= 0 && (!defer || b_r);  // the carried run ends in this chunk
     int32_t new_pend = -1;
     if (defer && b_r) {  // the last run start of the chunk is carried into the next chunk
       const uint32_t L2 = 31 - __clz(b_r);
-      const uint32_t top = __shfl_sync(0xFFFFFFFFu, R16, L2);
+      const uint32_t top = __shfl_sync(0xFFFFFFFFu, R32, L2);
       const uint32_t bit = 31 - __clz(top);
-      new_pend = (int32_t)(cb + L2 * 16u + bit);
-      if (lane == L2) R16 &= ~(1u << bit);
+      new_pend = (int32_t)(cb + L2 * 32u + bit);
+      if (lane == L2) R32 &= ~(1u << bit);
     }
-    const uint32_t E16 = R16 | P16;
-    uint32_t incl = __popc(E16);
+    const uint32_t E32 = R32 | P32;
+    uint32_t incl = __popc(E32);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -601,26 +606,27 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
     }
     const uint32_t ph = pend_here ? 1u : 0u;
     const uint32_t nev = __shfl_sync(0xFFFFFFFFu, incl, 31) + ph;
-    const uint32_t excl = incl - __popc(E16) + ph;  // events before this lane's bytes
+    const uint32_t excl = incl - __popc(E32) + ph;  // events before this lane's bytes
     {
-      uint32_t k = excl, e = E16;
+      uint32_t k = excl, e = E32;
       while (e) {
         const uint32_t bit = __ffs(e) - 1;
         e &= e - 1u;
-        T.ev[k++] = (uint16_t)(lane * 16u + bit);
+        T.ev[k++] = (uint16_t)(lane * 32u + bit);
       }
     }
     if (lane == 0 && ph) T.ev[0] = 0xFFFFu;
     // first event index of this lane's request (starting in the chunk)
     uint32_t fe = 0xFFFFFFFFu;
     {
-      const uint32_t off = s_r - cb, Lr = (off >> 4) & 31u;
-      const uint32_t exL = __shfl_sync(0xFFFFFFFFu, excl, Lr), EL = __shfl_sync(0xFFFFFFFFu, E16, Lr);
+      const uint32_t off = s_r - cb, Lr = (off >> 5) & 31u;
+      const uint32_t exL = __shfl_sync(0xFFFFFFFFu, excl, Lr), EL = __shfl_sync(0xFFFFFFFFu, E32, Lr);
       if (here) {
-        fe = exL + __popc(EL & ((1u << (off & 15u)) - 1u));
+        fe = exL + __popc(EL & ((1u << (off & 31u)) - 1u));
         tb = tok + fe;
       }
     }
+    __syncwarp();
     // the carried run: [pend_start, first stop of the chunk)
     uint32_t cx = 0, cn = 0;
     if (pend_here) {
@@ -631,19 +637,15 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
         if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
       }
       cn = cb + stop - ps;
-      if (ps + kChunk >= cb) {
-        cx = 16 + kChunk + ps - cb;
+      if (ps + 32u >= cb) {
+        cx = kCB + ps - cb;  // starts in the previous chunk's last 32 bytes
       } else {
-        // longer than a chunk: its tokens depend only on its last 6 bytes (any
-        // stem is > 16 bytes, no lemma) -> stage them as a 24-byte run
-        const uint32_t pad = 16 + 2 * kChunk + 8;
-        uint8_t* stw = reinterpret_cast<uint8_t*>(T.stage);
-        if (lane < 8u) stw[pad + lane] = __ldg(a.bytes + ps + cn - 8 + lane);
-        cx = pad + 8 - 24;
-        cn = 24;
+        // longer than 32 bytes: its tokens depend only on its last 6 bytes (any
+        // stem is > 16 bytes, no lemma) -> the 24-byte run that ends where it ends
+        cx = kCB + stop - 24u;
+        cn = 24u;
       }
     }
-    __syncwarp();
     // ---- (3) tokens, 32 events at a time (branch-free; punctuation lanes
     // compute a discarded word path)
     for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
@@ -651,8 +653,8 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       const bool valid = k < nev;
       const uint32_t pe = valid ? T.ev[k] : 0u;
       const bool carried = pe == 0xFFFFu;
-      const uint32_t p = pe & 511u;
-      const uint32_t lc = S.lut[st8[16 + kChunk + p]];
+      const uint32_t p = pe & 1023u;
+      const uint32_t lc = S.lut[st8[kCB + p]];
       const bool isw = carried || (lc & 1u);
       const uint32_t qq = p + 1, qw = qq >> 5, qb = qq & 31u;
       const uint32_t st = __funnelshift_r(T.sp[qw], T.sp[qw + 1], qb);  // stops after p (sp[16], sp[17]: all ones)
@@ -667,7 +669,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
           }
         }
       }
-      const uint32_t x = carried ? cx : 16 + kChunk + p;
+      const uint32_t x = carried ? cx : kCB + p;
       n = carried ? cn : n;
       // last four bytes of the run (lowercased): b[n-4] | b[n-3] << 8 | b[n-2] << 16 | b[n-1] << 24
       uint32_t te = x + n - 4u;
@@ -716,8 +718,8 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       }
       tok += min(32u, nev - e0) + __popc(b2);
     }
-    if (__any_sync(0xFFFFFFFFu, X16 != 0u)) {  // dropped bytes (rare): count per request
-      uint32_t xm = X16;
+    if (__any_sync(0xFFFFFFFFu, X32 != 0u)) {  // dropped bytes (rare): count per request
+      uint32_t xm = X32;
       while (xm) {
         const uint32_t bit = __ffs(xm) - 1;
         xm &= xm - 1u;
@@ -727,7 +729,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
     }
     if (pend_here) pend_start = -1;
     if (new_pend >= 0) pend_start = new_pend;
-    prevW = (__shfl_sync(0xFFFFFFFFu, W16, 31) >> 15) & 1u;
+    prevW = __shfl_sync(0xFFFFFFFFu, W32, 31) >> 31;
     __syncwarp();
   }
   B.tbeg[lr0 + lane] = (uint16_t)(tb == 0xFFFFFFFFu ? tok : tb);
