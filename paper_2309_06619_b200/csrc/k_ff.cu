@@ -32,7 +32,6 @@ constexpr uint32_t kEnd = 0xFFFFFFFFu;
 constexpr uint64_t kInf = 0xFFFFFFFFFFFFFFFFull;
 
 __device__ __forceinline__ float kk_u(uint64_t k) { return __uint_as_float((uint32_t)(k >> 32) & 0x7FFFFFFFu); }
-__device__ __forceinline__ uint32_t kk_p(uint64_t k) { return (uint32_t)k; }
 
 struct FF {
   // inputs

@@ -51,7 +51,6 @@ constexpr uint32_t kStages = KTF_STAGES;   // weight ring: one stage = the chunk
 constexpr uint32_t kA = KTF_AGROUPS;       // A-group ring
 constexpr uint32_t N1 = 112, N2 = 208, N3 = 208, N4 = 112;
 constexpr uint32_t S1 = 1, S2 = 13, S3 = 26, S4 = 26;  // k-steps (K = 8, 104, 208, 208)
-constexpr uint32_t kSteps = S1 + S2 + S3 + S4;          // per tile
 constexpr uint32_t kChunkMax = 2 * 64 * 208;           // bytes of one weight stage (2 k-steps, hi + lo) at N = 208
 constexpr uint32_t G1 = 7, G2 = 13, G3 = 13;           // A groups of the layer 1 / 2 / 3 outputs
 constexpr uint32_t kGroups = 1 + G1 + G2 + G3;         // per tile
@@ -81,10 +80,6 @@ __device__ __forceinline__ constexpr uint32_t idesc_tf32(uint32_t m, uint32_t n)
   // D f32, A / B tf32 (format 2), both K-major, N >> 3, M >> 4
   return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
-               ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
 // warp-collective forms for the MMA warp: every lane runs the loop with identical (uniform) operands, one
 // elected lane issues
 __device__ __forceinline__ void mma_tf32_w(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -96,9 +91,6 @@ __device__ __forceinline__ void mma_tf32_w(uint32_t tmem, uint64_t da, uint64_t 
 __device__ __forceinline__ void commit_w(uint32_t mbar) {
   asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0]; }" ::"r"(mbar));
-}
-__device__ __forceinline__ void commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"((uint64_t)mbar));
 }
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));

@@ -817,7 +817,6 @@ __global__ void __launch_bounds__(1024) k_long_report(const int64_t* __restrict_
                                                       const int64_t* __restrict__ end_us, uint32_t lo, uint32_t n,
                                                       const uint32_t* __restrict__ perm, const uint64_t* __restrict__ k,
                                                       rt_trace_summary* __restrict__ out) {
-  __shared__ int64_t sh[32];
   int64_t mx_end = INT64_MIN, mn_r = INT64_MAX;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     mx_end = max(mx_end, end_us[lo + i]);
@@ -837,7 +836,6 @@ __global__ void __launch_bounds__(1024) k_long_report(const int64_t* __restrict_
     const int64_t rmax = (int64_t)k[perm[0] - lo], rp95 = (int64_t)k[perm[n - p] - lo];
     *out = rt_trace_summary{rmax, rp95, mx_end - mn_r, n, 0u};
   }
-  (void)sh;
 }
 
 // one CTA: GPU busy = sum over equal-end groups (batches) of setup + base + eta * max len;

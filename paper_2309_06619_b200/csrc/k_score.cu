@@ -671,20 +671,20 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       }
       const uint32_t x = carried ? cx : kCB + p;
       n = carried ? cn : n;
-      // last four bytes of the run (lowercased): b[n-4] | b[n-3] << 8 | b[n-2] << 16 | b[n-1] << 24
-      uint32_t te = x + n - 4u;
-      uint32_t Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
+      // last eight bytes of the run (lowercased): Th = b[n-4] | .. | b[n-1] << 24, Tlo = b[n-8] .. b[n-5]
+      const uint32_t te = x + n - 8u, ta = te >> 2, tsh = (te & 3u) * 8u;
+      const uint32_t v0 = T.stage[ta], v1 = T.stage[ta + 1], v2 = T.stage[ta + 2];
+      const uint32_t Tlo = __funnelshift_r(v0, v1, tsh) | 0x20202020u, Th = __funnelshift_r(v1, v2, tsh) | 0x20202020u;
       // R-CLITIC: the run's last three / two bytes against the seven clitics
       // (perfect hashes, branch-free); the stem keeps n - cut bytes
       constexpr uint32_t NT = 'n' | ('\'' << 8) | ('t' << 16);
-      const uint32_t h3 = Tl >> 8, h2 = Tl >> 16;
+      const uint32_t h3 = Th >> 8, h2 = Th >> 16;
       const uint2 e3 = S.cl3[clitic_hash3(h3)], e2 = S.cl2[clitic_hash2(h2)];
       const bool m3 = isw && n > 3u && e3.x == h3, m2 = isw && n > 2u && e2.x == h2;
       const uint32_t cut = m3 ? 3u : (m2 ? 2u : 0u);
       const uint32_t c1 = m3 ? e3.y : e2.y;
       const uint32_t ns = n - cut;
-      te = x + ns - 4u;  // the stem's last four bytes
-      Tl = __funnelshift_r(T.stage[te >> 2], T.stage[(te >> 2) + 1], (te & 3u) * 8u) | 0x20202020u;
+      const uint32_t Tl = __funnelshift_rc(Tlo, Th, 8u * (4u - cut));  // the stem's last four bytes
       const bool nt3 = ns == 3u && (Tl >> 8) == NT;  // the word n't: lemma "not" (R-LEMMA)
       // R-LEMMA of the (stem) word: first rule wins (ing > ed / es > s)
       const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
