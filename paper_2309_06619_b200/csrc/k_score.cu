@@ -660,12 +660,17 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       const uint32_t st = __funnelshift_r(T.sp[qw], T.sp[qw + 1], qb);  // stops after p (sp[16], sp[17]: all ones)
       uint32_t n = __ffs(st);
       if (__any_sync(0xFFFFFFFFu, st == 0u && valid && isw && !carried)) {  // run of > 32 bytes (rare)
-        if (st == 0u) {
-          n = 33u - qb;
-          for (uint32_t w = qw + 2;; ++w) {
-            const uint32_t stop = T.sp[w];
-            if (stop) { n += __ffs(stop) - 1; break; }
-            n += 32u;
+        if (st == 0u) {  // st held bits qq .. qq+31: the rest of word qw+1, then whole words
+          const uint32_t hi = T.sp[qw + 1] >> qb;
+          if (hi) {
+            n = 32u + __ffs(hi);
+          } else {
+            n = 65u - qb;
+            for (uint32_t w = qw + 2;; ++w) {
+              const uint32_t stop = T.sp[w];
+              if (stop) { n += __ffs(stop) - 1; break; }
+              n += 32u;
+            }
           }
         }
       }

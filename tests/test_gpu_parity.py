@@ -353,8 +353,8 @@ def test_score_stream_boundaries(ctx_v1, lex_v1):
     longer than one and two chunks, requests splitting a word, and requests with
     thousands of tokens (many 32-token rule batches, carries across chunks)."""
     t = []
-    for pad in range(500, 516):  # a word (with clitic) straddling the first chunk boundary
-        t.append("a" * pad + " don't stop.")
+    for pad in list(range(500, 516)) + list(range(985, 1000)) + list(range(1012, 1030)):
+        t.append("a" * pad + " don't stop.")  # a word (with clitic) straddling a chunk boundary
     t += ["x" * 600 + "n't", "y" * 1100 + "'s and stuff", "history" * 100, "Why" + "z" * 530 + "?",
           "q" * 511 + " " + "r" * 513 + "'ll"]
     t += ["ab", "cd", "n't", "s", "'s", "", "", "ing", "edges"]  # adjacent requests split words
@@ -409,6 +409,55 @@ def test_score_pool_boundaries(ctx_v1, lex_v1):
     got, want = host(feat, np.uint16), oracle.rule_gen(lex_v1, data2, off2)
     bad = np.nonzero((got != want).any(1))[0]
     assert len(bad) == 0, [(int(i), got[i].tolist(), want[i].tolist()) for i in bad[:5]]
+
+
+def test_score_chunk_boundaries_random_runs(ctx_v1, lex_v1):
+    """K1 stages 1 KB chunks after the previous chunk's last 32 bytes: runs of
+    1-48 bytes (lexicon words with suffixes and clitics, upper case, digits)
+    at every offset around the chunk boundaries, including runs that started
+    more than 32 bytes before a chunk (carried as the 24-byte run ending where
+    they end) and runs that end exactly at a chunk end."""
+    rng = np.random.default_rng(23)
+    stems = ["history", "stuff", "bank", "john", "what", "why", "and", "or", "flies", "like", "art", "poverty",
+             "x" * 14, "y" * 16, "z" * 20, "abcdefghijklmnopqrstuvwxyzabcdefghij", "a"]
+    tails = ["", "s", "es", "ed", "ing", "'s", "n't", "'ll", "'re", "'ve", "'m", "'d", "s's", "ing's"]
+    t = []
+    for _ in range(96 * 32):
+        parts = []
+        for _ in range(int(rng.integers(1, 40))):
+            w = rng.choice(stems) + rng.choice(tails)
+            if rng.random() < 0.1:
+                w = w.upper()
+            if rng.random() < 0.05:
+                w = w * int(rng.integers(2, 5))  # long runs
+            parts.append(w)
+            parts.append(rng.choice([" ", "  ", ", ", ". ", "? ", "", "\t"]))
+        t.append("".join(parts)[: int(rng.integers(0, 400))])
+    data, off = rtgen.pack_texts(t)
+    feat = ctx_v1.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex_v1, data, off)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), bytes(data[off[i]:off[i + 1]])[:80], got[i].tolist(), want[i].tolist())
+                           for i in bad[:5]]
+
+
+def test_score_runs_longer_than_32_bytes(ctx_v1, lex_v1):
+    """A run's length comes from a 32-bit window of the stop mask; runs of
+    28-72 bytes (plain, with a suffix, with a clitic) at every byte alignment,
+    so their ends fall in every bit of the following stop words."""
+    t = []
+    for L in range(28, 73):
+        for pre in range(0, 33):
+            for tail in ("", "ing", "'s", "n't"):
+                t.append(" " * pre + "b" * L + tail + " and stuff.")
+    data, off = rtgen.pack_texts(t)
+    feat = ctx_v1.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex_v1, data, off)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert len(bad) == 0, [(int(i), bytes(data[off[i]:off[i + 1]])[:80], got[i].tolist(), want[i].tolist())
+                           for i in bad[:5]]
 
 
 def test_score_decreasing_offsets(ctx_v1, lex_v1):
