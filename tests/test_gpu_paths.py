@@ -300,6 +300,24 @@ def test_lexicon_1024_long_lemmas():
         rt.Context(text + "vague:\nqqqqqqqqqqqqqq\n", 0)
 
 
+def test_senses_saturation_in_the_pool_path():
+    """M (sum of senses - 1) saturates at 65535 and sets RT_FLAG_SATURATED for a
+    request small enough for the pool path (not the byte FSM): 300 words of 255
+    senses = 76 200; its neighbours in the same warp task stay exact."""
+    text = "polysemy:\nbat\t255\nbank\t3\n"
+    lex = oracle.Lexicon(text)
+    ctx = rt.Context(text, 0)
+    t = ["bat " * 300, "bats and banks", "bat " * 257 + "bank", "bat " * 259, ""] + ["bank bat"] * 40
+    data, off = rtgen.pack_texts(t)
+    ctx.flags()
+    feat = ctx.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex, data, off)
+    assert (got == want).all(), [(i, got[i].tolist(), want[i].tolist()) for i in np.nonzero((got != want).any(1))[0][:5]]
+    assert want[0, 2] == 65535 and want[2, 2] == 257 * 254 + 2 and want[3, 2] == 65535
+    assert ctx.flags() & 1
+
+
 # ------------------------------------------------------------------ argument checks launch nothing
 def test_schedule_argument_checks_launch_nothing(ctx_v1):
     n = 5000
