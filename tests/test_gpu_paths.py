@@ -318,6 +318,28 @@ def test_senses_saturation_in_the_pool_path():
     assert ctx.flags() & 1
 
 
+@pytest.mark.parametrize("order", [0, 1])
+def test_lexicon_fingerprint_collision(order):
+    """The probe compares only the key whose slot fingerprint matches; when both
+    slots' fingerprints match and the first key differs it compares the second.
+    "dvpczvzzu" and "wnhunduzd" share a 21-bit fingerprint and their first slot
+    (seed 0, 64 slots; found by a search over the library's published hash,
+    lex_mix / lex_slot1 in csrc/internal.cuh): the word inserted second sits in
+    its second slot, behind the other word's matching fingerprint."""
+    a, b = "dvpczvzzu", "wnhunduzd"
+    first, second = (b, a) if order == 0 else (a, b)
+    text = f"vague:\n{first}\npolysemy:\n{second}\t3\n"
+    lex = oracle.Lexicon(text)
+    ctx = rt.Context(text, 0)
+    t = [f"{second}", f"{first}", f"{second} {first} {second.upper()}", f"{second}s and {first}'s", "other"] * 8
+    data, off = rtgen.pack_texts(t)
+    feat = ctx.score(dev(data), dev(off))
+    torch.cuda.synchronize()
+    got, want = host(feat, np.uint16), oracle.rule_gen(lex, data, off)
+    assert (got == want).all(), [(i, got[i].tolist(), want[i].tolist()) for i in np.nonzero((got != want).any(1))[0][:5]]
+    assert want[1, 3] == 1 and want[0, 2] == 2 and want[2, 2] == 4  # the first word VAGUE, the second 3 senses
+
+
 # ------------------------------------------------------------------ argument checks launch nothing
 def test_schedule_argument_checks_launch_nothing(ctx_v1):
     n = 5000
