@@ -387,14 +387,15 @@ def native(args):
         return t0.elapsed_time(t1)
 
     # SM partition: the persistent scoring kernel (one at a time, on the scoring
-    # stream) gets ~54 % of the SMs; the slots' schedules (GPU-class consolidation
+    # stream) gets ~47 % of the SMs; the slots' schedules (GPU-class consolidation
     # kernels and the one-SM CPU-class list-scheduling chains) run concurrently on
-    # the rest.  Measured with k_score6 (profiles/notes/r02_schedule_pipeline.md):
-    # 148 / 124 / 100 / 88 / 76 / 64 scoring CTAs at depth 6 -> 0.786 / 0.672 /
-    # 0.654 / 0.625 / 0.618 / 0.695 ms per batch.
+    # the rest.  Measured with the final k_score6 (profiles/notes/r02_schedule_pipeline.md),
+    # depth 6, 60 steps: 96 / 88 / 80 / 76 / 74 / 72 / 70 / 68 / 66 / 64 scoring CTAs
+    # -> 0.625 / 0.610 / 0.608 / 0.605 / 0.604 / 0.601 / 0.587 / 0.589 / 0.603 /
+    # 0.622 ms per batch.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     if split_streams:
-        score_ctas = max(1, (nsm * 20 + 36) // 37) if depth > 1 else nsm
+        score_ctas = max(1, (nsm * 70 + 74) // 148) if depth > 1 else nsm
     else:
         score_ctas = max(1, nsm - depth) if depth > 1 else nsm
     if os.environ.get("RTLM_SCORE_CTAS"):
