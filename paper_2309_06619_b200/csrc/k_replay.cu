@@ -16,15 +16,17 @@
 namespace rtlm {
 namespace {
 
+// Arrival times are read from global memory (L1 / L2): 5.7 KB of shared memory
+// per trace, so 32 one-warp CTAs (the per-SM maximum) fit on an SM and a
+// config-3 launch (4096 traces) runs in one wave on 148 SMs.
 struct ReplaySmem {
-  int64_t r[kMaxTrace];      // arrival times
   uint16_t sidx[kMaxTrace];  // rank -> arrival index
   uint16_t rank[kMaxTrace];  // arrival index -> rank
   uint32_t ready_gpu[32], ready_cpu[32], wait_arr[32];
   int64_t core_free[kMaxCores];
   uint32_t W[kMaxWindow];
   float Su[kMaxWindow];
-};  // ~14.6 KB: u, D and lengths are read from global memory (L2) when needed
+};  // 5.7 KB: arrival times, u, D and lengths are read from global memory (L1 / L2)
 
 __device__ __forceinline__ int64_t warp_min64(int64_t v) {
 #pragma unroll
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     ncpu_l += (uint32_t)(a.key[lo + j] >> 63);
   }
   const uint32_t ncpu = __reduce_add_sync(0xFFFFFFFFu, ncpu_l);
-  for (uint32_t i = lane; i < n; i += 32) sm.r[i] = a.arrival[lo + i];
+  const int64_t* __restrict__ g_r = a.arrival + lo;
   const uint16_t* g_len = a.len + lo;
   const float* g_u = a.u + lo;
   const uint32_t* g_D = a.D + lo;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
 
   const uint32_t C = (uint32_t)p.C, m = (uint32_t)p.b10 * C / 10u, cores = (uint32_t)p.cores;
   const int64_t gpu_fixed = p.setup_us + p.base_us;
-  int64_t now = sm.r[0], gpu_free = 0;
+  int64_t now = __ldg(g_r + (0)), gpu_free = 0;
   uint32_t next = 0, done = 0;
   uint32_t cpu_ready = 0, gpu_ready = 0;  // ready-set sizes (warp-uniform)
   bool have_oldest = false;                // oldest_r = arrival of the oldest waiting GPU-class task
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   const uint32_t lt = (1u << lane) - 1u;
   // the next 32 arrival times, one per lane (index next + lane), reloaded only
   // when `next` advances: events that admit nothing read no arrival times
-  int64_t rw = lane < n ? sm.r[lane] : INT64_MAX;
+  int64_t rw = lane < n ? __ldg(g_r + (lane)) : INT64_MAX;
 
   for (;;) {
     // ---- admit arrivals <= now (arrival order is non-decreasing)
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       }
       if (cnt) {
         next += cnt;
-        rw = next + lane < n ? sm.r[next + lane] : INT64_MAX;
+        rw = next + lane < n ? __ldg(g_r + (next + lane)) : INT64_MAX;
       }
       if (cnt < 32) break;
     }
@@ -190,8 +192,8 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       if (lane == 0) {
         sm.core_free[c] = end;
         sm.ready_cpu[wl] = word & (word - 1u);
-        resp += end - sm.r[i];
-        misses += end > sm.r[i] + (int64_t)g_D[i];
+        resp += end - __ldg(g_r + (i));
+        misses += end > __ldg(g_r + (i)) + (int64_t)g_D[i];
         if (a.end_us) a.end_us[lo + i] = end;
       }
       ++done;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
           const uint32_t anyw = __ballot_sync(0xFFFFFFFFu, aw != 0);
           const uint32_t owl = __ffs(anyw) - 1;
           const uint32_t oword = __shfl_sync(0xFFFFFFFFu, aw, owl);
-          oldest_r = sm.r[owl * 32 + (__ffs(oword) - 1)];
+          oldest_r = __ldg(g_r + (owl * 32 + (__ffs(oword) - 1)));
           have_oldest = true;
         }
         const bool flush = (oldest_r <= now - p.xi_us) || next == n;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
               ue[k] = g_u[i];
               len_e[k] = g_len[i];
               D_e[k] = g_D[i];
-              r_e[k] = sm.r[i];
+              r_e[k] = __ldg(g_r + (i));
               pos[k] = e;
               re[k] |= i << 16;  // rank (low 16 bits) | arrival index (high)
             }
