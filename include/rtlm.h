@@ -129,7 +129,11 @@ typedef struct {
  * R-LEX: sections vague/polysemy/pos/wh/coord/prep; entries are single word
  * tokens lemmatized at load; <= 1024 distinct lemmas of <= 16 bytes).
  * Returns RT_ELEXICON on a parse error (message via rt_last_error(*out) --
- * *out is still created so the message can be read; destroy it). */
+ * *out is still created so the message can be read; destroy it).
+ * Device memory owned by the context: the lexicon tables, and the scoring
+ * scratch of rt_score / rt_score_key (one token buffer of 16 448 u16 tokens +
+ * 256 count records of 16 B per persistent warp: 32 warps x SM count x 37 KB,
+ * ~175 MB on 148 SMs), allocated here so that scoring never allocates. */
 rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** out);
 rt_status rt_destroy(rt_ctx* ctx);
 /* Message of the last non-OK status on this context, or, with ctx == NULL,
