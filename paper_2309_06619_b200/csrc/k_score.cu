@@ -17,6 +17,15 @@
 // which implements the same rules sequentially.
 #include "internal.cuh"
 
+// RTLM_CHECK builds (scripts/build_variant.sh with EXTRA_NVCC=-DRTLM_CHECK): bounds
+// of every computed shared / scratch index in k_score6 are checked, a violation
+// traps (the call then fails with a CUDA error)
+#ifdef RTLM_CHECK
+#define KS_CHECK(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define KS_CHECK(c) do { } while (0)
+#endif
+
 namespace rtlm {
 
 namespace {
@@ -88,6 +97,7 @@ __device__ __forceinline__ uint32_t lookup(const Lex& L, uint32_t w0, uint32_t w
   const uint32_t v1 = L.slots[lex_slot1(x, L.bits)], v2 = L.slots[lex_slot2(x, L.bits)];
   const bool f1 = (v1 >> 11) == fp, f2 = (v2 >> 11) == fp;
   const uint32_t c = f1 ? (v1 & 0x7FFu) : (f2 ? (v2 & 0x7FFu) : 0u);
+  KS_CHECK(c <= 1024u);
   const uint4 k = L.keys[c];
   const bool m = ((k.x ^ w0) | (k.y ^ w1) | (k.z ^ w2) | (k.w ^ w3)) == 0u;
   uint32_t code = m ? c : 0u;
@@ -612,6 +622,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       while (e) {
         const uint32_t bit = __ffs(e) - 1;
         e &= e - 1u;
+        KS_CHECK(k < kChunk + 2u);
         T.ev[k++] = (uint16_t)(lane * 32u + bit);
       }
     }
@@ -633,6 +644,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       const uint32_t ps = (uint32_t)pend_start;
       uint32_t stop = 0;
       for (uint32_t w = 0;; ++w) {
+        KS_CHECK(w < kChunk / 32 + 2u);
         const uint32_t sm = T.sp[w];
         if (sm) { stop = w * 32 + __ffs(sm) - 1; break; }
       }
@@ -651,12 +663,14 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
     for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
       const uint32_t k = e0 + lane;
       const bool valid = k < nev;
+      KS_CHECK(!valid || k < kChunk + 2u);
       const uint32_t pe = valid ? T.ev[k] : 0u;
       const bool carried = pe == 0xFFFFu;
       const uint32_t p = pe & 1023u;
       const uint32_t lc = S.lut[st8[kCB + p]];
       const bool isw = carried || (lc & 1u);
       const uint32_t qq = p + 1, qw = qq >> 5, qb = qq & 31u;
+      KS_CHECK(qw + 1u < kChunk / 32 + 2u);
       const uint32_t st = __funnelshift_r(T.sp[qw], T.sp[qw + 1], qb);  // stops after p (sp[16], sp[17]: all ones)
       uint32_t n = __ffs(st);
       if (__any_sync(0xFFFFFFFFu, st == 0u && valid && isw && !carried)) {  // run of > 32 bytes (rare)
@@ -667,6 +681,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
           } else {
             n = 65u - qb;
             for (uint32_t w = qw + 2;; ++w) {
+              KS_CHECK(w < kChunk / 32 + 2u);
               const uint32_t stop = T.sp[w];
               if (stop) { n += __ffs(stop) - 1; break; }
               n += 32u;
@@ -678,6 +693,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       n = carried ? cn : n;
       // last eight bytes of the run (lowercased): Th = b[n-4] | .. | b[n-1] << 24, Tlo = b[n-8] .. b[n-5]
       const uint32_t te = x + n - 8u, ta = te >> 2, tsh = (te & 3u) * 8u;
+      KS_CHECK(ta + 2u < sizeof(T.stage) / 4);
       const uint32_t v0 = T.stage[ta], v1 = T.stage[ta + 1], v2 = T.stage[ta + 2];
       const uint32_t Tlo = __funnelshift_r(v0, v1, tsh) | 0x20202020u, Th = __funnelshift_r(v1, v2, tsh) | 0x20202020u;
       // R-CLITIC: the run's last three / two bytes against the seven clitics
@@ -693,6 +709,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       const bool nt3 = ns == 3u && (Tl >> 8) == NT;  // the word n't: lemma "not" (R-LEMMA)
       // R-LEMMA of the (stem) word: first rule wins (ing > ed / es > s)
       const uint32_t a0 = x >> 2, sh = (x & 3u) * 8u;
+      KS_CHECK(a0 + 4u < sizeof(T.stage) / 4);
       const uint32_t w0 = T.stage[a0], w1 = T.stage[a0 + 1], w2 = T.stage[a0 + 2], w3 = T.stage[a0 + 3],
                      w4 = T.stage[a0 + 4];
       const uint32_t t2 = Tl >> 16, t3 = Tl >> 8, b1 = Tl >> 24;
@@ -710,6 +727,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
       const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, valid && cut != 0u);
       if (valid) {
         const uint32_t t0 = tok + lane + __popc(b2 & ((1u << lane) - 1u));
+        KS_CHECK(t0 + 1u < kTokCap + kTokPad);
         gt[t0] = (uint16_t)c0;
         if (cut) gt[t0 + 1] = (uint16_t)c1;
       }
@@ -737,6 +755,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
     prevW = __shfl_sync(0xFFFFFFFFu, W32, 31) >> 31;
     __syncwarp();
   }
+  KS_CHECK(lr0 + lane < kPoolReq && tok <= kTokCap && (tb == 0xFFFFFFFFu || tb <= tok));
   B.tbeg[lr0 + lane] = (uint16_t)(tb == 0xFFFFFFFFu ? tok : tb);
   __syncwarp();
 }
@@ -765,6 +784,7 @@ __device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const ui
     }
     nne += __popc(m);
   }
+  KS_CHECK(nne <= kPoolReq && R <= kPoolReq);
   if (lane == 0) { Q.ids[nne] = 0; Q.ends[nne] = (uint16_t)T; }
   __syncwarp();
   // this lane's entries [ja, jend): from the first entry starting at or after lane * T / 32
@@ -785,6 +805,7 @@ __device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const ui
   uint32_t j = ja;
   uint32_t r = Q.ids[j], nxt = Q.ends[j];
   const uint16_t* tp = gt + idx;
+  KS_CHECK(idx <= stop && stop <= T && ja <= jend && jend <= nne);
   uint32_t tk0 = tp[0], tk1 = tp[1];
   const uint32_t fa_s = (uint32_t)__cvta_generic_to_shared(S.fa);
   const uint32_t tO_s = (uint32_t)__cvta_generic_to_shared(S.tO), tP_s = (uint32_t)__cvta_generic_to_shared(S.tP);
@@ -824,6 +845,7 @@ __device__ __forceinline__ void rules_pool(const Smem6& S, WarpBuf6& B, const ui
       nf = fin ? 0xFFFFu : nf;
       n2m = fin ? 1u : n2m;
       j += fin ? 1u : 0u;
+      KS_CHECK(j <= nne && idx <= T + 1u);
       if (fin) { r = Q.ids[j]; nxt = Q.ends[j]; }
     }
   }
