@@ -159,7 +159,10 @@ rt_status rt_set_sm_limit(rt_ctx* ctx, uint32_t max_ctas);
 
 /* RuleGen(J) (Eq. 1; Table 1; Listing 1; R-TOK,
  * R-CLITIC, R-LEMMA, R-RULES).  Request i is bytes d_bytes[d_offsets[i] ..
- * d_offsets[i+1]).  d_offsets: n+1 non-decreasing u32.  Output feat[i][0..7] =
+ * d_offsets[i+1]).  d_offsets: n+1 non-decreasing u32; d_bytes holds
+ * d_offsets[n] bytes (with offsets that decrease somewhere, RT_FLAG_BAD_OFFSETS
+ * is set, requests with end < start score as empty and the others of their
+ * 32-request group are clamped to [0, d_offsets[n])).  Output feat[i][0..7] =
  * {S, Y, M, V, O, P, ntok, ndropped} (u16, saturating; row = 16 bytes).
  * n == 0 is a no-op. */
 rt_status rt_score(rt_ctx* ctx, const uint8_t* d_bytes, const uint32_t* d_offsets, uint32_t n, uint16_t* d_feat,

@@ -931,7 +931,8 @@ __global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work
       if (__any_sync(0xFFFFFFFFu, bad) || B1 - B0 > kTokCap) {
         // decreasing offsets, or more bytes than a pool buffer holds: per-lane byte FSM
         if (bad) atomicOr(a.flags, RT_FLAG_BAD_OFFSETS);
-        if (rv) fsm_request(a, L, r, s_r, bad ? s_r : e_r);
+        // (offsets that are not non-decreasing: reads stay inside [0, offsets[n]))
+        if (rv) fsm_request(a, L, r, min(s_r, total_bytes), bad ? min(s_r, total_bytes) : min(e_r, total_bytes));
         continue;
       }
       if (tok + (B1 - B0) > kTokCap) { pending = task; break; }  // tokens <= bytes
