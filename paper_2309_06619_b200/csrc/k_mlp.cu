@@ -97,6 +97,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// ReLU + round-to-nearest bf16 + pack in one instruction (max(x, 0) then RN
+// equals RN then max for every finite x)
+__device__ __forceinline__ uint32_t pack_bf16_relu(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
 
 // hidden-layer epilogue: TMEM row -> + bias -> ReLU -> bf16 -> the next A operand;
 // the kQ threads of a row take every kQ-th 16-column group
@@ -105,8 +112,7 @@ __device__ __forceinline__ void store_group(const uint32_t (&r)[16], const float
   uint32_t p[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    p[j] = pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + bias[c0 + 2 * j], 0.0f),
-                     fmaxf(__uint_as_float(r[2 * j + 1]) + bias[c0 + 2 * j + 1], 0.0f));
+    p[j] = pack_bf16_relu(__uint_as_float(r[2 * j]) + bias[c0 + 2 * j], __uint_as_float(r[2 * j + 1]) + bias[c0 + 2 * j + 1]);
   *reinterpret_cast<uint4*>(sA + ((c0 / 8) * kT + row) * 16) = make_uint4(p[0], p[1], p[2], p[3]);
   *reinterpret_cast<uint4*>(sA + ((c0 / 8 + 1) * kT + row) * 16) = make_uint4(p[4], p[5], p[6], p[7]);
 }
