@@ -618,6 +618,7 @@ def offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks)
     0.9-quantile + max of u (tau, u_max).  Algorithmic bytes: 20 B/record (fit),
     the sort's 5 passes x 24 B/record for the quantile."""
     import torch
+    import rtgen
     feat = ctx.score(data, off)
     y = torch.from_numpy(d2["true_len"].astype(np.float32)).to(dev)
     u = torch.rand(n, device=dev) * 100
@@ -637,10 +638,25 @@ def offline_leg(args, ctx, data, off, n, d2, dev, stream, world, max_over_ranks)
 
     fit_ms = timed(lambda: ctx.fit_rule(feat, y))
     q_ms = timed(lambda: ctx.quantile(u, 0.9))
+    # MLP training (rt_train_mlp, Adam, lr 1e-4 as P:620): one epoch over the
+    # 65 536-record training sample of the calibration in batches of
+    # 256; the paper trains 100 epochs at ~3 s per epoch on its board
+    ntr = min(n, 65536)
+    ws, bs = rtgen.mlp_weights(2024)
+    ctx.set_mlp(ws, bs)
+    ft, yt = feat[:ntr], y[:ntr]
+    t0 = time.perf_counter()
+    ctx.train_mlp(ft, yt, 1, 256, 1e-4, 7)
+    ep_s = time.perf_counter() - t0
+    flops = 3 * 2 * (6 * 100 + 100 * 200 + 200 * 200 + 200 * 100 + 100) * ntr  # forward + 2 backward GEMMs
     return {"fit_ms": round(fit_ms, 4), "fit_Mrec_per_s": round(world * n / (fit_ms / 1e3) / 1e6, 1),
             "fit_GBps": round(20 * n / (fit_ms / 1e3) / 1e9, 1),
             "quantile_ms": round(q_ms, 4), "quantile_Mrec_per_s": round(world * n / (q_ms / 1e3) / 1e6, 1),
-            "records_per_gpu": n}
+            "records_per_gpu": n,
+            "train_mlp": {"epoch_s": round(ep_s, 4), "records": ntr, "batch": 256, "lr": 1e-4,
+                          "records_per_s": round(ntr / ep_s, 1), "TFLOPs": round(flops / ep_s / 1e12, 3),
+                          "note": "wall clock of one rt_train_mlp epoch (it synchronizes): 256 Adam steps of ~22 "
+                                  "launches each, fp32 CUDA-core GEMMs"}}
 
 
 def run_traces_once(ctx, d, dev, profile_overrides=None):

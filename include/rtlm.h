@@ -203,6 +203,28 @@ rt_status rt_set_mlp(rt_ctx* ctx, const rt_mlp* mlp);
 /* u[i] = m_theta(feat[i]) for i < n (d_feat as produced by rt_score).
  * RT_EINVAL if no model was set. n == 0 is a no-op. */
 rt_status rt_predict_mlp(rt_ctx* ctx, const uint16_t* d_feat, uint32_t n, float* d_u, rt_stream stream);
+
+/* NEXT-2, optional part of the offline profiling (Alg. 1: "Minimize
+ * L_MSE <- ||m_theta(r_J) - l_J||^2"; "train the model with a learning
+ * rate of 1e-4"; "for 100 epochs"): trains this
+ * context's MLP from the weights of the last rt_set_mlp (or rt_train_mlp) by
+ * mini-batch Adam (beta1 0.9, beta2 0.999, eps 1e-8) on mean((z - y)^2), z the
+ * raw network output for the six rule scores of d_feat rows (u16 [n][8], as
+ * rt_score writes them), y = d_y[n] (fp32 output lengths).  R-TRAIN: epoch e
+ * visits rows (a_e * i + b_e) mod n, i = 0 .. n-1, in batches of `batch`
+ * (the last one partial), with (a_e, b_e) from SplitMix64(seed + e) (a_e made
+ * coprime with n), one Adam step per batch.  h_losses[e] (host, `epochs`
+ * doubles) = the epoch's squared errors (forward passes before each step)
+ * summed / n.  fp32 on the CUDA cores, every sum in a fixed order
+ * (deterministic).  On return the context's MLP (all precisions) holds the
+ * trained weights.  Allocates its buffers (not graph-capturable) and
+ * synchronizes `stream`.  RT_EINVAL: no model set, n == 0, NULL pointers,
+ * batch outside [1, 65536], lr not positive; epochs == 0 is a no-op. */
+rt_status rt_train_mlp(rt_ctx* ctx, const uint16_t* d_feat, const float* d_y, uint32_t n, uint32_t epochs,
+                       uint32_t batch, float lr, uint64_t seed, double* h_losses, rt_stream stream);
+/* Copies the context's current MLP weights (fp32, layout of rt_mlp) into the
+ * caller's arrays w[l] ([out][in]) and b[l] ([out]). */
+rt_status rt_get_mlp(rt_ctx* ctx, float* const w[5], float* const b[5]);
 #define RT_MLP_FP32 0
 #define RT_MLP_BF16 1
 #define RT_MLP_TF32X3 2

@@ -27,7 +27,7 @@ EXPORTS = ["rt_create", "rt_destroy", "rt_last_error", "rt_get_flags", "rt_abi_v
            "rt_score", "rt_predict", "rt_key", "rt_score_key", "rt_schedule", "rt_simulate", "rt_reduce_stats", "rt_launch_count",
            "rt_set_mlp", "rt_predict_mlp", "rt_set_mlp_precision", "rt_fit_rule", "rt_quantile", "rt_trace_report",
            "rt_trace_utilization", "rt_set_sm_limit", "rt_score_schedule_host",
-           "rt_schedule_deadlines"]
+           "rt_schedule_deadlines", "rt_train_mlp", "rt_get_mlp"]
 NO_BATCH = 0xFFFFFFFF
 
 
@@ -128,6 +128,10 @@ def load_library(path: str = LIB_PATH):
     L.rt_set_mlp.argtypes = [V, ctypes.POINTER(Mlp)]
     L.rt_predict_mlp.restype = I32
     L.rt_predict_mlp.argtypes = [V, P, U32, P, V]
+    L.rt_train_mlp.restype = I32
+    L.rt_train_mlp.argtypes = [V, P, P, U32, U32, U32, ctypes.c_float, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double), V]
+    L.rt_get_mlp.restype = I32
+    L.rt_get_mlp.argtypes = [V, ctypes.POINTER(P * 5), ctypes.POINTER(P * 5)]
     L.rt_set_mlp_precision.restype = I32
     L.rt_set_mlp_precision.argtypes = [V, ctypes.c_int]
     L.rt_fit_rule.restype = I32
@@ -270,6 +274,27 @@ class Context:
             m.w[l] = ws[l].ctypes.data
             m.b[l] = bs[l].ctypes.data
         self._check(self._L.rt_set_mlp(self._h, ctypes.byref(m)))
+
+    def train_mlp(self, feat, y, epochs: int, batch: int, lr: float, seed: int = 0):
+        """rt_train_mlp (NEXT-2): Adam on the MSE of the context's MLP (from the weights
+        of set_mlp) over feat uint16-as-int16 [n, 8] and y float32 [n]; returns the
+        per-epoch losses (numpy float64).  Synchronizes the current stream."""
+        torch = _torch()
+        n = feat.shape[0]
+        losses = np.zeros(max(int(epochs), 1), np.float64)
+        self._check(self._L.rt_train_mlp(self._h, _ptr(feat, torch.int16, "feat"), _ptr(y, torch.float32, "y"), n,
+                                         int(epochs), int(batch), float(lr), int(seed),
+                                         losses.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), self._stream()))
+        return losses[:int(epochs)]
+
+    def get_mlp(self):
+        """rt_get_mlp: the context's current MLP weights -> (weights, biases), fp32 numpy."""
+        ws = [np.zeros((MLP_DIMS[l + 1], MLP_DIMS[l]), np.float32) for l in range(5)]
+        bs = [np.zeros(MLP_DIMS[l + 1], np.float32) for l in range(5)]
+        pw = (ctypes.c_void_p * 5)(*[w.ctypes.data for w in ws])
+        pb = (ctypes.c_void_p * 5)(*[b.ctypes.data for b in bs])
+        self._check(self._L.rt_get_mlp(self._h, ctypes.byref(pw), ctypes.byref(pb)))
+        return ws, bs
 
     def set_mlp_precision(self, precision: str) -> None:
         """rt_set_mlp_precision: "fp32" (default, CUDA-core binary32), "tf32x3"

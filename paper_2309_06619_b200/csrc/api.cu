@@ -32,6 +32,7 @@ struct rt_ctx {
   float* d_mlp32 = nullptr;  // fp32 blob (k_mlp_f32)
   uint8_t* d_mlptf = nullptr;  // hi / lo tf32 blob (k_mlp_tf32)
   int mlp_precision = RT_MLP_FP32;
+  std::vector<float> mlp_host;  // the current weights, fp32, flat: W0 b0 W1 b1 .. W4 b4 (rt_set_mlp / rt_train_mlp)
   void* io = nullptr;        // device buffers of rt_score_schedule_host
   size_t io_size = 0;
   uint64_t* kbuf = nullptr;  // keys of rt_schedule_deadlines
@@ -61,6 +62,8 @@ void note_launch(unsigned k) { g_launches.fetch_add(k, std::memory_order_relaxed
 namespace {
 
 using rtlm::LexEntry;
+
+constexpr uint32_t kMlpDims[6] = {6, 100, 200, 200, 100, 1};  // m_theta
 
 thread_local std::string t_err;  // the calling thread's last error (rt_last_error(NULL))
 
@@ -579,6 +582,15 @@ rt_status rt_set_mlp(rt_ctx* c, const rt_mlp* mlp) {
   for (int l = 0; l < 5; ++l)
     if (!mlp->w[l] || !mlp->b[l]) return fail(c, RT_EINVAL, "null MLP weight or bias");
   DeviceGuard g(c->device);
+  {  // host copy of the weights (the starting point of rt_train_mlp, rt_get_mlp)
+    std::vector<float> flat;
+    for (int l = 0; l < 5; ++l) {
+      const size_t nw = (size_t)kMlpDims[l + 1] * kMlpDims[l];
+      flat.insert(flat.end(), mlp->w[l], mlp->w[l] + nw);
+      flat.insert(flat.end(), mlp->b[l], mlp->b[l] + kMlpDims[l + 1]);
+    }
+    c->mlp_host.swap(flat);
+  }
   std::vector<uint8_t> blob(rtlm::mlp_blob_bytes());
   rtlm::mlp_pack(mlp->w, mlp->b, blob.data());
   if (!c->d_mlp) {
@@ -1010,3 +1022,126 @@ rt_status rt_trace_utilization(rt_ctx* c, const uint16_t* d_len, const uint64_t*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- NEXT-2: training (k_train.cu)
+namespace {
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// R-TRAIN: epoch e visits the requests in the order i -> (a * i + b) mod n
+void epoch_perm(uint32_t n, uint64_t seed, uint32_t e, uint64_t& a, uint64_t& b) {
+  const uint64_t h = splitmix64(seed + e);
+  a = 1 + h % n;
+  auto gcd = [](uint64_t x, uint64_t y) { while (y) { const uint64_t t = x % y; x = y; y = t; } return x; };
+  while (gcd(a, n) != 1) ++a;
+  a %= n;
+  b = (h >> 32) % n;
+}
+}  // namespace
+
+rt_status rt_get_mlp(rt_ctx* c, float* const w[5], float* const b[5]) {
+  if (!c) return RT_EINVAL;
+  if (c->mlp_host.empty()) return fail(c, RT_EINVAL, "no MLP model (rt_set_mlp)");
+  size_t off = 0;
+  for (int l = 0; l < 5; ++l) {
+    const size_t nw = (size_t)kMlpDims[l + 1] * kMlpDims[l];
+    if (!w[l] || !b[l]) return fail(c, RT_EINVAL, "null MLP weight or bias");
+    std::memcpy(w[l], c->mlp_host.data() + off, nw * sizeof(float));
+    off += nw;
+    std::memcpy(b[l], c->mlp_host.data() + off, kMlpDims[l + 1] * sizeof(float));
+    off += kMlpDims[l + 1];
+  }
+  return RT_OK;
+}
+
+rt_status rt_train_mlp(rt_ctx* c, const uint16_t* d_feat, const float* d_y, uint32_t n, uint32_t epochs,
+                       uint32_t batch, float lr, uint64_t seed, double* h_losses, rt_stream stream) {
+  if (!c) return RT_EINVAL;
+  if (c->mlp_host.empty()) return fail(c, RT_EINVAL, "no MLP model to start from (rt_set_mlp)");
+  if (!epochs) return RT_OK;
+  if (!n || !d_feat || !d_y || !h_losses) return fail(c, RT_EINVAL, "null argument or n == 0");
+  if (batch == 0 || batch > 65536) return fail(c, RT_EINVAL, "batch must be in [1, 65536]");
+  if (!(lr > 0.0f) || !std::isfinite(lr)) return fail(c, RT_EINVAL, "lr must be positive and finite");
+  DeviceGuard g(c->device);
+  cudaStream_t s = cs(stream);
+  if (capturing(s)) return fail(c, RT_EINVAL, "rt_train_mlp cannot be captured into a CUDA graph");
+  const uint32_t bmax = std::min(batch, n);
+  const size_t np = c->mlp_host.size();
+  size_t lofs[5], off = 0;  // offset of W_l in the flat parameter array (b_l follows)
+  for (int l = 0; l < 5; ++l) {
+    lofs[l] = off;
+    off += (size_t)kMlpDims[l + 1] * kMlpDims[l] + kMlpDims[l + 1];
+  }
+  size_t act_ofs[6], acts = 0;  // activations of one batch: x, h1..h4, z
+  for (int l = 0; l < 6; ++l) {
+    act_ofs[l] = acts;
+    acts += (size_t)bmax * kMlpDims[l];
+  }
+  const size_t nbytes = (4 * np + acts + 2 * (size_t)bmax * 200 + bmax) * sizeof(float) + epochs * sizeof(double);
+  void* mem = nullptr;
+  if (cudaMalloc(&mem, nbytes) != cudaSuccess) return fail(c, RT_ENOMEM, "training buffers");
+  struct Free { void* p; ~Free() { cudaFree(p); } } fr{mem};
+  float* P = reinterpret_cast<float*>(mem);
+  float* G = P + np;
+  float* Mo = G + np;
+  float* Vo = Mo + np;
+  float* act = Vo + np;
+  float* D0 = act + acts;
+  float* D1 = D0 + (size_t)bmax * 200;
+  float* yb = D1 + (size_t)bmax * 200;
+  double* esq = reinterpret_cast<double*>(yb + bmax);
+  RT_CUDA(c, cudaMemcpyAsync(P, c->mlp_host.data(), np * sizeof(float), cudaMemcpyHostToDevice, s));
+  RT_CUDA(c, cudaMemsetAsync(Mo, 0, 2 * np * sizeof(float), s));
+  RT_CUDA(c, cudaMemsetAsync(esq, 0, epochs * sizeof(double), s));
+  uint64_t t = 0;
+  for (uint32_t e = 0; e < epochs; ++e) {
+    uint64_t pa, pb;
+    epoch_perm(n, seed, e, pa, pb);
+    for (uint32_t i0 = 0; i0 < n; i0 += bmax) {
+      const uint32_t B = std::min(bmax, n - i0);
+      RT_CUDA(c, rtlm::launch_gather(d_feat, d_y, n, pa, pb, i0, B, act + act_ofs[0], yb, s));
+      // forward: h_{l+1} = relu(h_l W_l^T + b_l), raw output z (no clamp: R-TRAIN)
+      for (int l = 0; l < 5; ++l) {
+        const uint32_t in = kMlpDims[l], out = kMlpDims[l + 1];
+        const float* W = P + lofs[l];
+        RT_CUDA(c, rtlm::launch_gemm(act + act_ofs[l], in, 1, W, 1, in, W + (size_t)out * in, act + act_ofs[l + 1],
+                                     out, B, out, in, l < 4 ? 1 : 0, s));
+      }
+      float* dZ = D0;
+      RT_CUDA(c, rtlm::launch_loss(act + act_ofs[5], yb, B, dZ, esq + e, s));
+      for (int l = 4; l >= 0; --l) {
+        const uint32_t in = kMlpDims[l], out = kMlpDims[l + 1];
+        float* gW = G + lofs[l];
+        // gW[o][i] = sum_m dZ[m][o] h_l[m][i];  gb[o] = sum_m dZ[m][o]
+        RT_CUDA(c, rtlm::launch_gemm(dZ, 1, out, act + act_ofs[l], in, 1, nullptr, gW, in, out, in, B, 0, s));
+        RT_CUDA(c, rtlm::launch_colsum(dZ, B, out, gW + (size_t)out * in, s));
+        if (l > 0) {  // dh_l[m][i] = sum_o dZ[m][o] W_l[o][i], then the ReLU derivative of h_l
+          float* dA = dZ == D0 ? D1 : D0;
+          RT_CUDA(c, rtlm::launch_gemm(dZ, out, 1, P + lofs[l], in, 1, nullptr, dA, in, B, in, out, 0, s));
+          RT_CUDA(c, rtlm::launch_relu_back(dA, act + act_ofs[l], (size_t)B * in, s));
+          dZ = dA;
+        }
+      }
+      ++t;
+      const float c1 = (float)(1.0 / (1.0 - std::pow(0.9, (double)t)));
+      const float c2 = (float)(1.0 / (1.0 - std::pow(0.999, (double)t)));
+      RT_CUDA(c, rtlm::launch_adam(P, G, Mo, Vo, (uint32_t)np, lr, c1, c2, s));
+    }
+  }
+  std::vector<float> trained(np);
+  std::vector<double> sq(epochs);
+  RT_CUDA(c, cudaMemcpyAsync(trained.data(), P, np * sizeof(float), cudaMemcpyDeviceToHost, s));
+  RT_CUDA(c, cudaMemcpyAsync(sq.data(), esq, epochs * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RT_CUDA(c, cudaStreamSynchronize(s));
+  for (uint32_t e = 0; e < epochs; ++e) h_losses[e] = sq[e] / n;
+  rt_mlp m{};
+  for (int l = 0; l < 5; ++l) {
+    m.w[l] = trained.data() + lofs[l];
+    m.b[l] = trained.data() + lofs[l] + (size_t)kMlpDims[l + 1] * kMlpDims[l];
+  }
+  return rt_set_mlp(c, &m);  // the packed inference blobs and the host copy follow the trained weights
+}

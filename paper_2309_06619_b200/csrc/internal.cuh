@@ -185,6 +185,17 @@ size_t mlp_tf32_blob_bytes();
 void mlp_tf32_pack(const float* const w[5], const float* const b[5], uint8_t* blob);
 cudaError_t launch_mlp_tf32(const uint16_t* feat, uint32_t n, const uint8_t* blob, float* u, int num_sms,
                             cudaStream_t s);
+// NEXT-2 training (k_train.cu)
+cudaError_t launch_gemm(const float* A, uint32_t sam, uint32_t sak, const float* B, uint32_t sbk, uint32_t sbn,
+                        const float* bias, float* C, uint32_t ldc, uint32_t M, uint32_t N, uint32_t K, int relu,
+                        cudaStream_t s);
+cudaError_t launch_gather(const uint16_t* feat, const float* y, uint32_t n, uint64_t a, uint64_t b, uint32_t i0,
+                          uint32_t bsz, float* x, float* yb, cudaStream_t s);
+cudaError_t launch_loss(const float* z, const float* yb, uint32_t bsz, float* dz, double* epoch_sq, cudaStream_t s);
+cudaError_t launch_colsum(const float* dZ, uint32_t M, uint32_t N, float* gb, cudaStream_t s);
+cudaError_t launch_relu_back(float* dA, const float* Aprev, size_t cnt, cudaStream_t s);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, uint32_t cnt, float lr, float c1, float c2,
+                        cudaStream_t s);
 cudaError_t launch_reduce_stats(const rt_trace_stats* st, uint32_t nt, const uint16_t* group_of, uint32_t ngroups,
                                 int64_t* sums, cudaStream_t s);
 

@@ -186,3 +186,76 @@ def test_mlp_full_config2_sampled(ctx, mode):
     want, absp = mlp_predict(f, ws, bs), mlp_abs_pass(f, ws, bs)
     tol = TOL_BF16 if mode == "bf16" else TOL_FP32
     assert (np.abs(u[idx] - want) <= tol * absp).all()
+
+
+# ---------------------------------------------------------------- NEXT-2: rt_train_mlp
+from oracle.mlp import mlp_train_adam  # noqa: E402
+
+
+def _train_case(n=300, seed=21):
+    rng = np.random.default_rng(seed)
+    f = _feat(n, seed, hi=12)
+    y = (5.0 + 2.0 * f[:, 3] + 1.5 * f[:, 1] + rng.normal(0, 1.0, n)).astype(np.float32)
+    ws, bs = mlp_weights(seed)
+    return f, y, [w.astype(np.float32) for w in ws], [b.astype(np.float32) for b in bs]
+
+
+def _gpu_train(ctx, f, y, ws, bs, epochs, batch, lr, seed):
+    ctx.set_mlp(ws, bs)
+    losses = ctx.train_mlp(torch.from_numpy(f.view(np.int16)).to(DEV), torch.from_numpy(y).to(DEV), epochs, batch, lr,
+                           seed)
+    w2, b2 = ctx.get_mlp()
+    return losses, w2, b2
+
+
+def test_train_matches_the_fp64_oracle(ctx):
+    """3 epochs of 300 rows in batches of 64 (the last one partial), lr 1e-3: the
+    fp32 training follows the fp64 oracle: per-epoch losses within 1e-4
+    relative; the trained networks' predictions within 1e-3 relative; each
+    parameter within 1e-3 lr + 1e-5 |w| (Adam moves a parameter by ~lr per step
+    whatever the gradient's scale, so fp32 / fp64 differences stay ~lr-relative;
+    a parameter whose gradient is at fp32 noise level may differ by up to 2 lr
+    per step -- allowed for at most 0.1 % of them)."""
+    f, y, ws, bs = _train_case()
+    epochs, batch, lr, seed = 3, 64, 1e-3, 11
+    losses, w2, b2 = _gpu_train(ctx, f, y, ws, bs, epochs, batch, lr, seed)
+    ow, ob, ol = mlp_train_adam(f, y.astype(np.float64), ws, bs, epochs, batch, lr, seed)
+    np.testing.assert_allclose(losses, ol, rtol=1e-4)
+    pg = mlp_predict(f, [w.astype(np.float64) for w in w2], [b.astype(np.float64) for b in b2])
+    po = mlp_predict(f, ow, ob)
+    assert np.all(np.abs(pg - po) <= 1e-3 * np.maximum(np.abs(po), 1.0))
+    steps = epochs * ((len(y) + batch - 1) // batch)
+    d = np.concatenate([np.abs(a - b).ravel() for a, b in zip(w2 + b2, ow + ob)])
+    w = np.concatenate([np.abs(b).ravel() for b in ow + ob])
+    close = d <= 1e-3 * lr + 1e-5 * w
+    assert close.mean() >= 0.999, close.mean()
+    assert d.max() <= 2 * lr * steps
+
+
+def test_train_is_deterministic_and_learns(ctx):
+    f, y, ws, bs = _train_case(n=1000, seed=5)
+    l1, w1, b1 = _gpu_train(ctx, f, y, ws, bs, 8, 128, 1e-3, 3)
+    l2, w2, b2 = _gpu_train(ctx, f, y, ws, bs, 8, 128, 1e-3, 3)
+    assert np.array_equal(l1, l2)
+    assert all(np.array_equal(a, b) for a, b in zip(w1 + b1, w2 + b2))
+    assert l1[-1] < 0.5 * l1[0], l1
+    # the trained model serves rt_predict_mlp (all precisions follow the trained weights)
+    u = ctx.predict_mlp(torch.from_numpy(f.view(np.int16)).to(DEV)).cpu().numpy()
+    ref = mlp_predict(f, [w.astype(np.float64) for w in w1], [b.astype(np.float64) for b in b1])
+    assert np.all(np.abs(u - ref) <= TOL_FP32 * mlp_abs_pass(f, w1, b1) + 1e-6)
+
+
+def test_train_argument_checks(ctx):
+    f, y, ws, bs = _train_case(n=10)
+    fd, yd = torch.from_numpy(f.view(np.int16)).to(DEV), torch.from_numpy(y).to(DEV)
+    fresh = rt.Context(configs.read_lexicon(), 0)
+    with pytest.raises(rt.RtlmError, match="no MLP model"):
+        fresh.train_mlp(fd, yd, 1, 4, 1e-3)
+    ctx.set_mlp(ws, bs)
+    with pytest.raises(rt.RtlmError, match="batch"):
+        ctx.train_mlp(fd, yd, 1, 0, 1e-3)
+    with pytest.raises(rt.RtlmError, match="lr"):
+        ctx.train_mlp(fd, yd, 1, 4, 0.0)
+    assert len(ctx.train_mlp(fd, yd, 0, 4, 1e-3)) == 0  # zero epochs: no-op
+    w2, b2 = ctx.get_mlp()
+    assert all(np.array_equal(a, b) for a, b in zip(ws + bs, w2 + b2))
