@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
   // the next 32 arrival times, one per lane (index next + lane), reloaded only
   // when `next` advances: events that admit nothing read no arrival times
   int64_t rw = lane < n ? __ldg(g_r + (lane)) : INT64_MAX;
+  int64_t next_arr = __shfl_sync(0xFFFFFFFFu, rw, 0);  // arrival time of task `next` (warp-uniform)
 
   for (;;) {
     // ---- admit arrivals <= now (arrival order is non-decreasing)
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
       if (cnt) {
         next += cnt;
         rw = next + lane < n ? __ldg(g_r + (next + lane)) : INT64_MAX;
+        next_arr = __shfl_sync(0xFFFFFFFFu, rw, 0);
       }
       if (cnt < 32) break;
     }
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(32) k_replay(ReplayLaunch a) {
     if (done >= n) break;
     // ---- next event time
     int64_t nxt = INT64_MAX;
-    if (next < n) nxt = __shfl_sync(0xFFFFFFFFu, rw, 0);
+    if (next < n) nxt = next_arr;
     if (gpu_free > now) nxt = min(nxt, gpu_free);
     const bool cpu_waiting = cpu_ready != 0;
     if (cpu_waiting) {
