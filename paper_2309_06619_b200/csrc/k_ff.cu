@@ -411,6 +411,55 @@ __global__ void __launch_bounds__(256) k_ff_vtab(FF f) {
   if ((threadIdx.x & 31u) == 0 && j < nwords * 32) f.passbm[j >> 5] = bal;
 }
 
+// k_ff_vtab with the chunk size CT = C known at compile time (the profiles'
+// C = 11 and 33): the chunk's u values in registers, both loops unrolled --
+// the same table entry for entry
+template <int CT>
+__global__ void __launch_bounds__(256) k_ff_vtab_t(FF f) {
+  __shared__ uint32_t t[256 + kMaxWindow];
+  const uint32_t NR = f.scal[2];
+  const uint32_t j0 = blockIdx.x * 256u;
+  const uint32_t nwords = (NR + 31) / 32 + 1;
+  if (j0 >= nwords * 32) return;  // block-uniform
+  const uint32_t j = j0 + threadIdx.x;
+  for (uint32_t i = threadIdx.x; i < 256 + CT; i += 256)
+    t[i] = j0 + i < NR ? __float_as_uint(kk_u(f.rseq[j0 + i])) + 1u : 0u;
+  __syncthreads();
+  uint32_t w[CT];
+#pragma unroll
+  for (int b = 0; b < CT; ++b) w[b] = t[threadIdx.x + b];
+  const float lam = f.lambda;
+  auto bad2 = [&](uint32_t lo1, uint32_t hi1) {  // u values + 1
+    return !(__uint_as_float(hi1 - 1u) <= __fmul_rn(lam, __uint_as_float(lo1 - 1u)));
+  };
+  int bad = 0;
+  uint32_t mx = 0;
+  bool passC = false;
+#pragma unroll
+  for (int c = 1; c <= CT; ++c) {
+    const bool full = j + c <= NR;
+    if (full) {
+      const uint32_t x = w[c - 1];
+      uint32_t pred = 0u, succ = 0xFFFFFFFFu;
+      bool dup = false;
+#pragma unroll
+      for (int b = 0; b + 1 < c; ++b) {
+        const uint32_t y = w[b];
+        pred = (y < x && y > pred) ? y : pred;
+        succ = (y > x && y < succ) ? y : succ;
+        dup |= y == x;
+      }
+      const bool hp = pred != 0u, hs = succ != 0xFFFFFFFFu;
+      if (!dup) bad += (hp && bad2(pred, x)) + (hs && bad2(x, succ)) - (hp && hs && bad2(pred, succ));
+      mx = x > mx ? x : mx;
+    }
+    if (j < NR) f.vt[(size_t)(c - 1) * f.vstride + j] = (full && bad == 0) ? __uint_as_float(mx - 1u) : __int_as_float(0x7f800000);
+    if (c == CT) passC = full && bad == 0;
+  }
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, passC);
+  if ((threadIdx.x & 31u) == 0 && j < nwords * 32) f.passbm[j >> 5] = bal;
+}
+
 __device__ __forceinline__ bool pass_at(const uint32_t* bm, uint32_t j) { return (bm[j >> 5] >> (j & 31u)) & 1u; }
 
 // compact failing positions (j + C <= NR and !pass)
@@ -999,7 +1048,9 @@ static cudaError_t launch_ff(const SchedLaunch& a, uint32_t q, uint32_t lo, uint
     note_launch(3);
   }
   const uint32_t npass = ((n + 31) / 32 + 1) * 32;
-  k_ff_vtab<<<(npass + 255) / 256, 256, 0, s>>>(f);
+  if (f.C == 11) k_ff_vtab_t<11><<<(npass + 255) / 256, 256, 0, s>>>(f);
+  else if (f.C == 33) k_ff_vtab_t<33><<<(npass + 255) / 256, 256, 0, s>>>(f);
+  else k_ff_vtab<<<(npass + 255) / 256, 256, 0, s>>>(f);
   const uint32_t fb = (n + 255) / 256;
   k_ff_failcount<<<fb, 256, 0, s>>>(f, blocksum);
   k_ff_blockscan<<<1, 1024, 0, s>>>(blocksum, fb, f.scal + 3);
