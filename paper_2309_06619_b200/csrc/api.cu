@@ -445,7 +445,7 @@ rt_status rt_create(int device, const char* lexicon_text, size_t len, rt_ctx** o
   if (device < 0 || device >= ndev) return fail(c, RT_EINVAL, "no such CUDA device");
   DeviceGuard g(device);
   RT_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-  RT_CUDA(c, cudaMalloc(&c->d_flags, 4 * sizeof(uint32_t)));  // [0] flags, [2] scoring work counter
+  RT_CUDA(c, cudaMalloc(&c->d_flags, 4 * sizeof(uint32_t)));  // [0] flags, [2] scoring work counter, [3] its CTA counter
   RT_CUDA(c, cudaMemset(c->d_flags, 0, 4 * sizeof(uint32_t)));
   RT_CUDA(c, cudaMalloc(&c->d_tok, rtlm::score_scratch_bytes(c->num_sms)));
   RT_CUDA(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));

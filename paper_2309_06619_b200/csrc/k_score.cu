@@ -965,6 +965,18 @@ __global__ void __launch_bounds__(kT4, 1) k_score6(ScoreLaunch a, uint32_t* work
     }
     __syncwarp();
   }
+  // the last CTA to finish resets the work counter (work[0]) and the CTA
+  // counter (work[1]) for the next launch, which stream order starts after this
+  // one has completed; a faulting launch leaves the context unusable anyway
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(work + 1, 1u) == gridDim.x - 1u) {
+      work[0] = 0u;
+      work[1] = 0u;
+      __threadfence();
+    }
+  }
 }
 
 __global__ void k_predict(const uint16_t* __restrict__ feat, uint32_t n, rt_regressor reg, float* __restrict__ u) {
@@ -992,8 +1004,7 @@ size_t score_scratch_bytes(int ctas) { return (size_t)ctas * kW4 * kWarpScratch;
 
 cudaError_t launch_score(const ScoreLaunch& a, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(a.work, 0, sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;  // a.work[0..1] are zero here: reset by the previous launch's last CTA
   const uint32_t ntasks = (a.n + 31) / 32;
   uint32_t grid = (uint32_t)a.num_sms;
   if (grid * kW4 > ntasks) grid = (ntasks + kW4 - 1) / kW4;
