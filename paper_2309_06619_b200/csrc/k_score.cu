@@ -761,7 +761,7 @@ __device__ __forceinline__ void tokenize_task(const ScoreLaunch& a, const Smem6&
 }
 
 // R-RULES over the pool's tokens: lane = a contiguous range of whole requests
-// of about T/32 tokens; the machine of rules_round (O-part / P-part tables,
+// of about T/32 tokens; the R-RULES machine (O-part / P-part tables,
 // S-part in registers), restarted at every request start.  Requests without
 // tokens are compacted away first; a request's counts go to its 16-byte record
 // in the warp's global scratch when its last token has been read.  Branch-free

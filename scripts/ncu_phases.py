@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Warp instructions and stall samples of k_score4 grouped by phase (k_score.cu line ranges), from
+"""Warp instructions and stall samples of round-1 k_score4 grouped by phase (its k_score.cu line ranges; for k_score6 use ncu_ranges.py), from
 `ncu -i X.ncu-rep --page source --csv --print-source cuda,sass > X.csv`.  usage: ncu_phases.py <csv>
 Lines of other files (inlined intrinsics, internal.cuh helpers) are reported per file."""
 import csv

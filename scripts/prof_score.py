@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Runs rt_score_key on the config-2 queue a few times (for ncu captures of k_score4)
+"""Runs rt_score_key on the config-2 queue a few times (for ncu captures of the scoring kernel, k_score6)
 and prints the CUDA-event time per launch.  Usage: python scripts/prof_score.py [reps]"""
 import os
 import sys
