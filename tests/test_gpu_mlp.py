@@ -259,3 +259,13 @@ def test_train_argument_checks(ctx):
     assert len(ctx.train_mlp(fd, yd, 0, 4, 1e-3)) == 0  # zero epochs: no-op
     w2, b2 = ctx.get_mlp()
     assert all(np.array_equal(a, b) for a, b in zip(ws + bs, w2 + b2))
+
+
+def test_train_tiny_sets(ctx):
+    """n = 1 (one row, the identity permutation) and batch > n (one partial batch per
+    epoch) against the fp64 oracle."""
+    for n, batch in ((1, 4), (7, 64)):
+        f, y, ws, bs = _train_case(n=n, seed=40 + n)
+        losses, w2, b2 = _gpu_train(ctx, f, y, ws, bs, 4, batch, 1e-3, 9)
+        _, _, ol = mlp_train_adam(f, y.astype(np.float64), ws, bs, 4, batch, 1e-3, 9)
+        np.testing.assert_allclose(losses, ol, rtol=1e-4)

@@ -460,6 +460,23 @@ def test_score_runs_longer_than_32_bytes(ctx_v1, lex_v1):
                            for i in bad[:5]]
 
 
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_score_few_ctas_many_pools(lex_v1, ctas):
+    """rt_set_sm_limit(1 / 3): 32 / 96 warps take all 1 563 tasks of a 50 001-request
+    queue, so every warp fills dozens of 8-task pools in turn (the pool loop, the
+    pending task carried into the next pool, the self-resetting work counter
+    over repeated launches)."""
+    ctx = rt.Context(configs.read_lexicon(), 0)
+    ctx.set_sm_limit(ctas)
+    d = configs.config2(n=50001, gid0=31337)
+    want = oracle.rule_gen(lex_v1, d["data"], d["offsets"])
+    for _ in range(2):
+        feat = ctx.score(dev(d["data"]), dev(d["offsets"]))
+        torch.cuda.synchronize()
+        got = host(feat, np.uint16)
+        assert (got == want).all()
+
+
 def test_score_decreasing_offsets(ctx_v1, lex_v1):
     """Offsets that decrease: those requests score as empty and set the flag; the
     other requests of the same warp task (per-lane FSM path) still match."""
