@@ -518,18 +518,34 @@ __global__ void k_ff_failwrite(FF f, const uint32_t* blockoff) {
 // leaves L unchanged) iff the chunk passes its λ chain and
 // u(min L) > λ·u(max chunk) -- i.e. !(u0 <= λ·vt[c-1][j]) with u0 = u(min L)
 // (+inf when L is empty).  ffwd() checks 32 consecutive rounds per warp step.
+constexpr uint32_t kFfwdDepth = 4;
 __device__ __forceinline__ uint32_t ffwd(const FF& f, uint32_t lc, float u0, uint32_t& j, uint32_t NR) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t c = f.C - lc;
+  const float* vt = f.vt + (size_t)(c - 1) * f.vstride;
+  const auto pass = [&](uint32_t jk) { return (jk + c <= NR) && !(u0 <= __fmul_rn(f.lambda, __ldg(vt + jk))); };
   uint32_t total = 0;
-  for (;;) {
-    const uint32_t jk = j + lane * c;
-    const bool ok = (jk + c <= NR) && !(u0 <= __fmul_rn(f.lambda, f.vt[(size_t)(c - 1) * f.vstride + jk]));
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
+  {  // most stretches inside an excursion are short: one batch of 32 rounds first
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pass(j + lane * c));
     const uint32_t k = (bal == 0xFFFFFFFFu) ? 32u : (uint32_t)(__ffs(~bal) - 1);
     j += k * c;
     total += k;
     if (k < 32) return total;
+  }
+  // long stretch: four batches (128 rounds) in flight per step, so that one
+  // L2 round trip covers 128 rounds instead of 32
+  for (;;) {
+    bool ok[kFfwdDepth];
+#pragma unroll
+    for (uint32_t u = 0; u < kFfwdDepth; ++u) ok[u] = pass(j + (u * 32u + lane) * c);
+#pragma unroll
+    for (uint32_t u = 0; u < kFfwdDepth; ++u) {
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok[u]);
+      const uint32_t k = (bal == 0xFFFFFFFFu) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+      j += k * c;
+      total += k;
+      if (k < 32) return total;
+    }
   }
 }
 
