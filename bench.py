@@ -37,6 +37,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# The pipelined step runs 2 x depth + 1 streams (slot streams, the library's
+# CPU-class fork streams, the scoring stream).  With the default 8 hardware
+# work queues, streams share queues and their kernels wait on each other in
+# submission order (false dependencies): the schedules of different batches
+# then ran one after another (0.45 -> 0.25 ms per batch for schedules alone,
+# pipelined step 0.59 -> 0.45 ms with 32 queues, profiles/notes/r02_schedule_pipeline.md).
+# Read when the CUDA context is created, so it is set before torch touches CUDA.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 METRIC = "M requests scored+scheduled/s"
 UNIT = "Mreq/s"
 
@@ -60,7 +69,7 @@ def parse():
                          "all-reduce, MAX-over-ranks timing, rank-0 JSON line) without any kernel; for tests")
     ap.add_argument("--no-config5", action="store_true", help="skip config 5 (rate/deadline x ablation sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--depth", type=int, default=6, help="batches in flight (contexts / streams / distinct inputs)")
+    ap.add_argument("--depth", type=int, default=8, help="batches in flight (contexts / streams / distinct inputs)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay one CUDA graph per batch slot instead of issuing the pipelined step call by call")
     return ap.parse_args()
@@ -387,15 +396,16 @@ def native(args):
         return t0.elapsed_time(t1)
 
     # SM partition: the persistent scoring kernel (one at a time, on the scoring
-    # stream) gets ~47 % of the SMs; the slots' schedules (GPU-class consolidation
+    # stream) gets ~2/3 of the SMs; the slots' schedules (GPU-class consolidation
     # kernels and the one-SM CPU-class list-scheduling chains) run concurrently on
-    # the rest.  Measured with the final k_score6 (profiles/notes/r02_schedule_pipeline.md),
-    # depth 6, 60 steps: 96 / 88 / 80 / 76 / 74 / 72 / 70 / 68 / 66 / 64 scoring CTAs
-    # -> 0.625 / 0.610 / 0.608 / 0.605 / 0.604 / 0.601 / 0.587 / 0.589 / 0.603 /
-    # 0.622 ms per batch.
+    # the rest.  Measured with k_score6 and 32 hardware queues
+    # (profiles/notes/r02_schedule_pipeline.md), 60 steps, two repetitions:
+    # 82 / 88 / 94 / 100 / 108 / 116 scoring CTAs -> depth 6: 0.493 / 0.467 /
+    # 0.461 / 0.462 / 0.469 / 0.479, depth 8: 0.493 / 0.465 / 0.460 / 0.454 /
+    # 0.462 / 0.472 ms per batch.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     if split_streams:
-        score_ctas = max(1, (nsm * 70 + 74) // 148) if depth > 1 else nsm
+        score_ctas = max(1, (nsm * 100 + 74) // 148) if depth > 1 else nsm
     else:
         score_ctas = max(1, nsm - depth) if depth > 1 else nsm
     if os.environ.get("RTLM_SCORE_CTAS"):
@@ -503,7 +513,8 @@ def native(args):
                                    f"scoring on {score_ctas} CTAs"
                                    + ("; scoring of every batch on one stream, each batch's schedule on its slot's "
                                       "stream (event-ordered)" if split_streams else "")
-                                   + ("; each slot's step replayed from one CUDA graph" if args.graphs else ""),
+                                   + ("; each slot's step replayed from one CUDA graph" if args.graphs else "")
+                                   + f"; CUDA_DEVICE_MAX_CONNECTIONS={os.environ.get('CUDA_DEVICE_MAX_CONNECTIONS')}",
                        "l2": f"pipelined: {depth} distinct inputs of ~100 MB each (> 126 MB L2) in turn; "
                              "latency leg: 256 MB buffer written between steps",
                        "parallelism": f"replicas{world}",

@@ -19,8 +19,9 @@ from rtgen import configs  # noqa: E402
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/pipe2.json"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 sc = int(sys.argv[3]) if len(sys.argv) > 3 else 70
+part = os.environ.get("PIPE_PART", "all")  # "schedule": the batches are scored once, only schedules are timed
 dev = torch.device("cuda", 0)
-depth, n = 6, 1 << 20
+depth, n = int(os.environ.get("PIPE_DEPTH", "6")), 1 << 20
 ds = [configs.config2(n=n, gid0=i * n) for i in range(depth)]
 ctxs = [rt.Context(d["lexicon"], 0) for d in ds]
 data = [torch.from_numpy(d["data"]).to(dev) for d in ds]
@@ -40,12 +41,15 @@ for c in ctxs:
 prof, reg = ds[0]["profile"], ds[0]["regressor"]
 
 
-def step(k):
+def step(k, score=None):
     sl = k % depth
-    with torch.cuda.stream(score_stream):
-        score_stream.wait_event(ev_sched[sl])
-        ctxs[sl].score_key(data[sl], off[sl], reg, prof, want_D=False, out=outs[sl])
-        ev_scored[sl].record(score_stream)
+    if score is None:
+        score = part != "schedule"
+    if score:
+        with torch.cuda.stream(score_stream):
+            score_stream.wait_event(ev_sched[sl])
+            ctxs[sl].score_key(data[sl], off[sl], reg, prof, want_D=False, out=outs[sl])
+            ev_scored[sl].record(score_stream)
     with torch.cuda.stream(streams[sl]):
         streams[sl].wait_event(ev_scored[sl])
         ctxs[sl].schedule(outs[sl]["key"], outs[sl]["u"], seg, prof, out=souts[sl])
@@ -53,7 +57,7 @@ def step(k):
 
 
 for k in range(2 * depth):
-    step(k)
+    step(k, True)
 torch.cuda.synchronize()
 import time  # noqa: E402
 for rep in range(3):  # host issue cost of `depth` steps (well under the launch-queue capacity), GPU idle at the start
@@ -63,6 +67,19 @@ for rep in range(3):  # host issue cost of `depth` steps (well under the launch-
     h1 = time.perf_counter()
     torch.cuda.synchronize()
     print(f"host issue: {(h1 - h0) * 1e3 / depth:.4f} ms per step")
+if os.environ.get("PIPE_HOST"):  # per-call host time of the issue loop (no profiler)
+    torch.cuda.synchronize()
+    hs = []
+    h0 = time.perf_counter()
+    for k in range(K):
+        a0 = time.perf_counter()
+        step(k)
+        hs.append((time.perf_counter() - a0) * 1e3)
+    h1 = time.perf_counter()
+    torch.cuda.synchronize()
+    h2 = time.perf_counter()
+    print(f"{part}: issue loop {(h1 - h0) * 1e3 / K:.4f} ms per step, to completion {(h2 - h0) * 1e3 / K:.4f}; "
+          f"per-call ms: " + " ".join(f"{x:.2f}" for x in hs))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as p:
     ev0.record()
@@ -79,6 +96,9 @@ p.export_chrome_trace(out)
 tr = json.load(open(out))
 ev = sorted((e for e in tr["traceEvents"] if e.get("cat") == "kernel"), key=lambda e: e["ts"])
 sco = [e for e in ev if "k_score6" in e["name"]]
+if not sco:
+    print(f"{part} depth {depth}: {ms:.4f} ms/batch")
+    sys.exit(0)
 t0, t1 = ev[0]["ts"], max(e["ts"] + e["dur"] for e in ev)
 busy = sum(e["dur"] for e in sco)
 gaps = [b["ts"] - (a["ts"] + a["dur"]) for a, b in zip(sco, sco[1:])]

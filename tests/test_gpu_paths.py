@@ -70,12 +70,12 @@ def test_bench_pipeline_launch_configuration(lex_v1, mode):
     """bench.py's pipelined requests leg in each of its launch forms: "split"
     (the default: every batch's scoring on one stream with the persistent
     kernel capped at ~2/3 of the SMs, each batch's schedule on its slot's stream,
-    ordered by events; depth 6), "slot" (score + schedule on the slot's stream,
+    ordered by events; depth 8), "slot" (score + schedule on the slot's stream,
     scoring capped at nsm - depth; depth 4) and "graphs" (slot form, each slot's
     step replayed from one CUDA graph).  Two waves of steps so that every slot
     runs while other slots' kernels are in flight; every batch against the oracle."""
     n = 1 << 20
-    depth = 6 if mode == "split" else 4
+    depth = 8 if mode == "split" else 4
     steps = 2 * depth
     nsm = torch.cuda.get_device_properties(DEV).multi_processor_count
     ds = [configs.config2(n=n, gid0=i * n) for i in range(depth)]
@@ -83,7 +83,7 @@ def test_bench_pipeline_launch_configuration(lex_v1, mode):
     seg = np.asarray([0, n], U32)
     ctxs = [rt.Context(d["lexicon"], 0) for d in ds]
     for c in ctxs:
-        c.set_sm_limit((nsm * 27 + 39) // 40 if mode == "split" else max(1, nsm - depth))
+        c.set_sm_limit((nsm * 100 + 74) // 148 if mode == "split" else max(1, nsm - depth))
     data = [dev(d["data"]) for d in ds]
     off = [dev(d["offsets"]) for d in ds]
     streams = [torch.cuda.Stream(DEV) for _ in range(depth)]
