@@ -490,7 +490,8 @@ def native(args):
     # ---------------- config 4 (strong: 2^26 requests split over the ranks)
     cfg4 = None
     if not args.no_config4:
-        cfg4 = config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush)
+        cfg4 = config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush,
+                           lambda: rt.Context(d2["lexicon"], local))
 
     # ---------------- cpu baseline (oracle, rank 0, N = 1)
     cpu = None
@@ -1019,11 +1020,15 @@ def config5_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_
             "b": {"mean_response_s": ab("b=", mean_resp), "miss_ratio": ab("b=", miss)}}
 
 
-def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush):
+def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_ranks, flush, make_ctx):
     """BASELINE configs[3]: 2^26 requests = 65536 traces x 1024, contiguous trace
     ranges per rank (strong scaling: the job is fixed, each rank takes 1/N of
     it), score_key per LM + replay + stats, one NCCL all-reduce of the per-LM
-    int64 sums (a8).  value = 2^26 requests / max-over-ranks step time."""
+    int64 sums (a8).  value = 2^26 requests / max-over-ranks step time.
+    The rank's blocks (8192 traces each) alternate between two contexts and
+    streams, so that one block's scoring (issue-bound, whole SMs) overlaps the
+    other's replay (latency-bound one-warp CTAs); the per-LM sums are
+    accumulated by both with atomics."""
     import torch
     from paper_2309_06619_b200 import dist as rdist
     t0 = time.time()
@@ -1045,16 +1050,34 @@ def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_
     n = sum(len(b["d"]["arrival_us"]) for b in blocks)
     nt = sum(len(b["d"]["trace_off"]) - 1 for b in blocks)
     sums = torch.zeros((4, 3), dtype=torch.int64, device=dev)
+    nstreams = max(1, int(os.environ.get("RTLM_C4_STREAMS", "2")))
+    ctxs = [ctx] + [make_ctx() for _ in range(nstreams - 1)]
+    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+    # scoring capped at half the SMs so that it leaves room for the other
+    # stream's replay: 48.0 ms (one stream) -> 47.4 (two) -> 46.3 / 46.0 (two,
+    # scoring on 100 / 74 CTAs) per 2^26 requests
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    c4_ctas = int(os.environ.get("RTLM_C4_SCORE_CTAS", str((nsm + 1) // 2 if nstreams > 1 else 0)))
+    for c in ctxs:
+        c.set_sm_limit(c4_ctas)
+    ev0 = torch.cuda.Event()
 
     def step():
         sums.zero_()
-        for b in blocks:
-            d, u, key, D, arr = b["d"], b["u"], b["key"], b["D"], b["arr"]
-            for f, r0, r1, gd, so in b["groups"]:
-                ctx.score_key(gd, so, d["regressors"][f], d["profiles"][f], arrival=arr[r0:r1],
-                              out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
-            ctx.simulate(arr, b["tl"], u, key, D, d["trace_off"], d["profiles"], b["tp"], stats=b["stats"])
-            ctx.reduce_stats(b["stats"], b["tp"], 4, sums=sums)
+        ev0.record(stream)
+        for i, b in enumerate(blocks):
+            c, st = ctxs[i % nstreams], streams[i % nstreams]
+            with torch.cuda.stream(st):
+                if i < nstreams:
+                    st.wait_event(ev0)
+                d, u, key, D, arr = b["d"], b["u"], b["key"], b["D"], b["arr"]
+                for f, r0, r1, gd, so in b["groups"]:
+                    c.score_key(gd, so, d["regressors"][f], d["profiles"][f], arrival=arr[r0:r1],
+                                out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
+                c.simulate(arr, b["tl"], u, key, D, d["trace_off"], d["profiles"], b["tp"], stats=b["stats"])
+                c.reduce_stats(b["stats"], b["tp"], 4, sums=sums)
+        for st in streams:
+            stream.wait_stream(st)
         rdist.allreduce_sums(sums)
 
     steps = max(1, min(args.steps, 5))
@@ -1072,11 +1095,14 @@ def config4_leg(args, ctx, configs, dev, stream, rank, world, barrier, max_over_
         ev_b.synchronize()
         ts.append(ev_a.elapsed_time(ev_b))
     ms = max_over_ranks(sum(ts)) / steps
+    for c in ctxs:
+        c.set_sm_limit(0)
     s = sums.cpu().numpy()
     total_req = 65536 * 1024
     return {"metric": "M requests scored+scheduled+replayed/s", "value": round(total_req / (ms / 1e3) / 1e6, 2),
             "unit": "Mreq/s", "traces_per_s": round(65536 / (ms / 1e3), 1), "ms_per_step": round(ms, 3),
             "scaling": "strong", "requests_per_gpu": n, "traces_per_gpu": nt, "host_gen_s": round(gen_s, 1),
+            "streams": nstreams, "score_ctas": c4_ctas or None,
             "workload": "config4: 65536 Poisson-ramp traces x 1024 requests (2^26) split over the ranks, 4 LMs, "
                         "tight, UP+C+O; one NCCL all-reduce of per-LM int64 sums",
             "mean_response_s_per_lm": [round(float(s[f, 0]) / max(1, s[f, 1]) / 1e6, 4) for f in range(4)],
