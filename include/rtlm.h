@@ -152,7 +152,13 @@ uint32_t rt_lexicon_size(const rt_ctx* ctx);
  * concurrently: rt_schedule forks a one-CTA list-scheduling kernel that holds
  * an SM for ~1 ms per 2^20-request queue, and a persistent kernel with one CTA
  * per SM would wait for that SM before it can complete.  No effect on
- * results.  RT_EINVAL if ctx is NULL. */
+ * results.  RT_EINVAL if ctx is NULL.
+ * Pipelining batches over many streams (each context's rt_schedule also forks
+ * onto one internal stream per context): CUDA maps streams onto
+ * CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8), and kernels of
+ * streams that share a queue wait for each other in submission order; set it
+ * to >= 2 x contexts + 1 (max 32) in the environment before the process
+ * creates its CUDA context (bench.py uses 32: DESIGN.md section 9). */
 rt_status rt_set_sm_limit(rt_ctx* ctx, uint32_t max_ctas);
 
 /* ---------------------------------------------------------------- (1) score */
