@@ -438,3 +438,57 @@ def test_replay_rejects_traces_over_65536(ctx_v1):
         ctx_v1.simulate(z, torch.zeros(n, dtype=torch.int16, device=DEV), torch.zeros(n, device=DEV), z,
                         torch.zeros(n, dtype=torch.int32, device=DEV), np.asarray([0, n], U32),
                         [configs.paper_lms()[0]], None)
+
+
+def test_config4_two_streams_match_one():
+    """bench.py's config-4 step: blocks alternate between two contexts and
+    streams (scoring capped at half the SMs), stats accumulated by both with
+    atomics.  Per-trace stats and per-LM sums equal the one-context serial run."""
+    from bench import _lm_groups
+    blocks = []
+    for blk in range(4):
+        d = configs.config4_shard(blk, 4, n_traces=512, per_trace=256, grouped=True)
+        blocks.append({"d": d, "groups": _lm_groups(d, DEV), "arr": dev(d["arrival_us"]), "tl": dev(d["true_len"]),
+                       "tp": dev(d["trace_prof"])})
+    lex = blocks[0]["d"]["lexicon"]
+    ctxs = [rt.Context(lex, 0), rt.Context(lex, 0)]
+    nsm = torch.cuda.get_device_properties(DEV).multi_processor_count
+
+    def run(nstreams):
+        streams = [torch.cuda.Stream(DEV) for _ in range(nstreams)]
+        for c in ctxs:
+            c.set_sm_limit((nsm + 1) // 2 if nstreams > 1 else 0)
+        sums = torch.zeros((4, 3), dtype=torch.int64, device=DEV)
+        ev0 = torch.cuda.Event()
+        ev0.record()
+        stats = []
+        for i, b in enumerate(blocks):
+            c, st = ctxs[i % nstreams], streams[i % nstreams]
+            d, arr = b["d"], b["arr"]
+            nb, ntb = len(d["arrival_us"]), len(d["trace_off"]) - 1
+            with torch.cuda.stream(st):
+                if i < nstreams:
+                    st.wait_event(ev0)
+                u = torch.empty(nb, dtype=torch.float32, device=DEV)
+                key = torch.empty(nb, dtype=torch.int64, device=DEV)
+                D = torch.empty(nb, dtype=torch.int32, device=DEV)
+                s = torch.empty((ntb, 2), dtype=torch.int64, device=DEV)
+                for f, r0, r1, gd, so in b["groups"]:
+                    c.score_key(gd, so, d["regressors"][f], d["profiles"][f], arrival=arr[r0:r1],
+                                out={"u": u[r0:r1], "key": key[r0:r1], "D": D[r0:r1]})
+                c.simulate(arr, b["tl"], u, key, D, d["trace_off"], d["profiles"], b["tp"], stats=s)
+                c.reduce_stats(s, b["tp"], 4, sums=sums)
+                stats.append(s)
+        for st in streams:
+            torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.set_sm_limit(0)
+        return [s.cpu().numpy() for s in stats], sums.cpu().numpy()
+
+    st1, s1 = run(1)
+    st2, s2 = run(2)
+    for a, b in zip(st1, st2):
+        assert (a == b).all()
+    assert (s1 == s2).all()
+    assert s1[:, 1].sum() == sum(len(b["d"]["arrival_us"]) for b in blocks)  # every request counted once
