@@ -247,11 +247,21 @@ __global__ void __launch_bounds__(256) k_ff_topk32(FF f) {
   if (p0 >= G) return;
   const uint32_t p1 = min(G, p0 + B1);
   uint64_t top = 0, thr = 0;
-  for (uint32_t pb = p0; pb < p1; pb += 32) {
-    const uint64_t x = pb + lane < p1 ? f.kk[pb + lane] : 0ull;
-    if (!__any_sync(0xFFFFFFFFu, x > thr)) continue;
-    top = merge32_desc(top, sort32_desc(x));
-    thr = __shfl_sync(0xFFFFFFFFu, top, K - 1);
+  // eight 32-key batches loaded at once (one L2 round trip instead of eight),
+  // then taken in order
+  for (uint32_t pg = p0; pg < p1; pg += 8 * 32) {
+    uint64_t xs[8];
+#pragma unroll
+    for (uint32_t t = 0; t < 8; ++t) {
+      const uint32_t i = pg + t * 32 + lane;
+      xs[t] = i < p1 ? __ldg(f.kk + i) : 0ull;
+    }
+#pragma unroll
+    for (uint32_t t = 0; t < 8; ++t) {
+      if (!__any_sync(0xFFFFFFFFu, xs[t] > thr)) continue;
+      top = merge32_desc(top, sort32_desc(xs[t]));
+      thr = __shfl_sync(0xFFFFFFFFu, top, K - 1);
+    }
   }
   f.summ[(size_t)c * KS + lane] = lane < K ? top : 0ull;
 }
@@ -312,8 +322,10 @@ __global__ void __launch_bounds__(128) k_ff_replay(FF f) {
     const uint32_t s = t * 32 + lane;
     h[t] = s < K ? f.heapH[(size_t)warp * KS + (K - 1 - s)] : kInf;
   }
+  uint64_t nxt = p0 + lane < p1 ? __ldg(f.kk + p0 + lane) : 0ull;  // the next batch, loaded one batch ahead
   for (uint32_t pb = p0; pb < p1; pb += 32) {
-    const uint64_t mine = pb + lane < p1 ? f.kk[pb + lane] : 0ull;
+    const uint64_t mine = nxt;
+    if (pb + 32 < p1) nxt = pb + 32 + lane < p1 ? __ldg(f.kk + pb + 32 + lane) : 0ull;
     const uint32_t cnt = min(32u, p1 - pb);
     // a key below the heap's minimum at the start of the batch is evicted at once
     // (the minimum only grows), so only the others go through the insertion
